@@ -1,0 +1,166 @@
+/*
+ * prgpu.h -- C ABI of libprgpu: the synchronous (and optional No-Sync-style
+ * asynchronous) fp64 PageRank pull iteration of arXiv 2109.09527 on one B200.
+ *
+ * Citations: "P:N" = PAPER.md line N (section / equation / algorithm named),
+ * "S:N" = SPEC.md line N, "Q-x" = a reading of the paper listed in DESIGN.md.
+ *
+ * What is computed (Eq.(1)):
+ *     pr(v) = (1-d)/n + d * sum_{(u,v) in E} pr(u)/outdeg(u)
+ * iterated from pr = 1/n (Alg.1) "while err > threshold" with
+ * err = the L1 (default; BASELINE configs) or L-inf norm of
+ * the change over one sweep, reset every sweep (Q-E).  Dangling vertices
+ * (outdeg 0) contribute nothing and nothing is redistributed (Alg.2 P:489-491;
+ * Q-D).  Self-loops and duplicate edges are removed when the graph is built
+ * (Q-L).
+ *
+ * Conventions for every call:
+ *  - Pointers may be device pointers or host pointers (pageable or pinned);
+ *    the library detects which with CUDA unified addressing and copies host
+ *    data inside the call.  Pointer arguments are never retained after return.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default
+ *    stream).  All device work of a call is ordered on that stream.
+ *  - Return values are PR_* status codes; on any status other than PR_OK and
+ *    PR_NOT_CONVERGED, pr_last_error() returns a message (thread-local, valid
+ *    until the next call from the same thread).  The library never aborts and
+ *    never throws across the ABI.
+ *  - One pr_graph is used by one stream at a time; distinct graphs are
+ *    independent.
+ */
+#ifndef PRGPU_H
+#define PRGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
+
+/* Status codes (mirror the CLI exit-code convention of SPEC S:483). */
+#define PR_OK             0   /* converged / success */
+#define PR_EINVAL         1   /* invalid argument (ids out of range, d not in (0,1), ...) */
+#define PR_NOT_CONVERGED  2   /* max_iter reached; ranks and iterations still written */
+#define PR_ESTATE         3   /* call not valid in the graph's state (e.g. reductions not built) */
+#define PR_ENOMEM        (-1) /* device or host allocation failed */
+#define PR_ECUDA         (-2) /* a CUDA runtime error; see pr_last_error() */
+
+/* pr_preprocess flags */
+#define PR_PRE_IDENTICAL  1u  /* identical in-neighbour groups (STIC-D, §3) */
+#define PR_PRE_CHAIN      2u  /* chains of in=1/out=1 vertices (STIC-D, §3; Q-C) */
+
+/* pr_run mode bits */
+#define PR_MODE_SYNC      0u  /* synchronous pull, double-buffered contribs (Alg.1) */
+#define PR_MODE_ASYNC     1u  /* in-place No-Sync-style sweeps (Alg.3; Q-Y) */
+#define PR_NORM_L1        0u  /* stop when sum_v |x_t(v)-x_{t-1}(v)| <= threshold (configs) */
+#define PR_NORM_LINF      2u  /* stop when max_v |x_t(v)-x_{t-1}(v)| <= threshold */
+#define PR_USE_REDUCTIONS 4u  /* compute one vertex per identical group, resolve chain
+                                 members from their head; needs pr_preprocess */
+#define PR_TIMING         8u  /* record CUDA events around every gather launch (bench) */
+
+/*
+ * pr_graph_create -- build the in-edge CSR and out-degrees on the device
+ * (§5.2 "converted later to Compressed Sparse Row (CSR) format";
+ * Alg.1 P:433 "CSR representation").
+ *   n      number of vertices, 1 <= n <= 2^31-1 (dense 0-based ids, Q-V)
+ *   m      number of raw edges, 0 <= m <= 2^31-1
+ *   src,dst  int32[m] raw edge list (src -> dst); duplicates and self-loops
+ *          allowed (removed here).  Host or device memory; read only.
+ *   out    receives the new graph (NULL on failure)
+ * Result: row_ptr int64[n+1], col_idx int32[E] (sources of each row sorted
+ * ascending), outdeg int32[n], all bit-exact functions of the edge set.
+ * Synchronises `stream` once (to learn E).
+ * Errors: PR_EINVAL for n/m out of range, NULL pointers with m > 0, or any id
+ * outside [0,n) (detected on the device; no graph is created).
+ */
+int pr_graph_create(int64_t n, int64_t m, const int32_t *src, const int32_t *dst,
+                    void *stream, pr_graph **out);
+
+/*
+ * pr_preprocess -- find the STIC-D work-saving structure (§3):
+ *   PR_PRE_IDENTICAL: rep[v] = min id of the class of vertices with the same
+ *       in-neighbour set; the empty in-set is one class (Q-G).
+ *   PR_PRE_CHAIN: chain vertex <=> in-degree 1 and out-degree 1; members are
+ *       the chain vertices at distance k >= 1 from a head h (chain(h) and not
+ *       chain(pred(h))); their source is rep(h); pure cycles are excluded (Q-C).
+ * Calling again replaces the previous result.  flags == 0 clears it.
+ * Synchronises `stream` a few times (counts).  Errors: PR_EINVAL (NULL g or
+ * unknown flag bits).
+ */
+int pr_preprocess(pr_graph *g, uint32_t flags, void *stream);
+
+/*
+ * pr_run -- iterate to convergence.
+ *   d          damping, 0 < d < 1 ("initialized to 0.85")
+ *   threshold  >= 0 (P:438 uses 1e-16 with L-inf; configs use 1e-10 / 1e-12 L1)
+ *   max_iter   >= 1; reaching it returns PR_NOT_CONVERGED with valid ranks
+ *   mode       PR_MODE_* | PR_NORM_* | PR_USE_REDUCTIONS | PR_TIMING
+ *   ranks      fp64[n] output in vertex-id order (host or device, caller-owned)
+ *   iters_out  (host, nullable) number of update sweeps including the final
+ *              one that met the stop test (Q-I)
+ *   final_delta_out (host, nullable) the stop-test norm of the last sweep
+ * Sync mode is deterministic (fixed-order reductions): identical inputs give
+ * bit-identical ranks and iteration counts.  Async mode is not deterministic;
+ * it reaches the same fixed point (Lemma 2).
+ * Errors: PR_EINVAL (bad d / threshold / max_iter / NULL ranks),
+ * PR_ESTATE (PR_USE_REDUCTIONS before pr_preprocess).
+ */
+int pr_run(pr_graph *g, double d, double threshold, int32_t max_iter, void *stream,
+           uint32_t mode, double *ranks, int32_t *iters_out, double *final_delta_out);
+
+/* pr_destroy -- release every device buffer of g.  NULL-safe. */
+void pr_destroy(pr_graph *g);
+
+/* pr_last_error -- message for the last failing call on this thread ("" if none). */
+const char *pr_last_error(void);
+
+/* ---- introspection (tests, bench) ------------------------------------- */
+
+/* Sizes: n, E (deduplicated edges), number of member vertices resolved by
+ * scatter in reduced mode (identical non-representatives + chain members),
+ * longest chain distance k.  Any output pointer may be NULL. */
+int pr_graph_info(const pr_graph *g, int64_t *n, int64_t *E, int64_t *n_members,
+                  int32_t *max_chain);
+
+/* Copy the canonical in-CSR into caller buffers (host or device):
+ * row_ptr int64[n+1], col_idx int32[E], outdeg int32[n].  Any may be NULL. */
+int pr_get_csr(const pr_graph *g, int64_t *row_ptr, int32_t *col_idx, int32_t *outdeg,
+               void *stream);
+
+/* Copy the reductions: rep int32[n] (identity if identical groups were not
+ * requested), chain_src int32[n] (rep(head) or -1), chain_k int32[n] (k or 0).
+ * PR_ESTATE before pr_preprocess.  Any may be NULL. */
+int pr_get_reductions(const pr_graph *g, int32_t *rep, int32_t *chain_src, int32_t *chain_k,
+                      void *stream);
+
+/* Per-sweep (L1, L-inf) deltas of the last pr_run: writes min(cap, iters)
+ * pairs into host buffer log[2*cap]; returns the number of pairs written
+ * (>= 0) or a negative PR_* code. */
+int pr_get_delta_log(const pr_graph *g, double *log, int32_t cap);
+
+/* Statistics of the last pr_run (and of the graph's lifetime). */
+typedef struct {
+    int32_t iterations;         /* sweeps performed (== *iters_out) */
+    int32_t status;             /* PR_OK or PR_NOT_CONVERGED */
+    double  delta_l1;           /* last sweep's L1 delta */
+    double  delta_linf;         /* last sweep's L-inf delta */
+    int64_t run_launches;       /* kernels launched by the last pr_run (incl. early-exit ones) */
+    int64_t total_launches;     /* kernels launched for this graph since pr_graph_create */
+    int32_t host_syncs;         /* stream synchronisations inside the last pr_run */
+    int32_t timed_iterations;   /* PR_TIMING: gather launches timed */
+    double  gather_ms;          /* PR_TIMING: summed CUDA-event time of those gather launches */
+    double  scatter_ms;         /* PR_TIMING: summed time of the member-scatter launches */
+    int64_t gather_rows;        /* rows one gather launch processes (n, or |R| reduced) */
+    int64_t gather_edges;       /* edges one gather launch processes */
+    int64_t scatter_members;    /* members one scatter launch processes (0 plain) */
+    int64_t n_contrib;          /* vertices with outdeg > 0 (size of the contrib vector) */
+    int64_t n_tasks;            /* row-block + hub-chunk tasks of the gather launch */
+} pr_run_stats;
+
+int pr_get_run_stats(const pr_graph *g, pr_run_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRGPU_H */

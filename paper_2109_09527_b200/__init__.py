@@ -1,0 +1,247 @@
+"""paper_2109_09527_b200 -- Python binding of libprgpu (include/prgpu.h).
+
+Argument marshalling only: every step of the PageRank path (ingest,
+preprocessing, the iteration) runs in libprgpu's CUDA kernels for sm_100a.
+There is no CPU fallback: importing this package on a machine without the
+built ``libprgpu.so`` raises immediately, and calls without a CUDA device fail
+with the library's own error.
+
+The names mirror the C ABI: :func:`pr_graph_create`, :func:`pr_preprocess`,
+:func:`pr_run`, :func:`pr_destroy` (+ introspection).  Buffers may be torch
+tensors (CUDA or CPU) or numpy arrays; the library accepts host or device
+pointers and copies host data inside the call.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libprgpu.so")
+
+PR_OK = 0
+PR_EINVAL = 1
+PR_NOT_CONVERGED = 2
+PR_ESTATE = 3
+PR_ENOMEM = -1
+PR_ECUDA = -2
+
+PR_PRE_IDENTICAL = 1
+PR_PRE_CHAIN = 2
+
+PR_MODE_SYNC = 0
+PR_MODE_ASYNC = 1
+PR_NORM_L1 = 0
+PR_NORM_LINF = 2
+PR_USE_REDUCTIONS = 4
+PR_TIMING = 8
+
+# every symbol include/prgpu.h declares (tests check the .so exports them)
+ABI_SYMBOLS = (
+    "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_last_error",
+    "pr_graph_info", "pr_get_csr", "pr_get_reductions", "pr_get_delta_log", "pr_get_run_stats",
+)
+
+
+class PRError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"libprgpu error {code}: {msg}")
+        self.code = code
+
+
+class pr_run_stats(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int32),
+        ("status", ctypes.c_int32),
+        ("delta_l1", ctypes.c_double),
+        ("delta_linf", ctypes.c_double),
+        ("run_launches", ctypes.c_int64),
+        ("total_launches", ctypes.c_int64),
+        ("host_syncs", ctypes.c_int32),
+        ("timed_iterations", ctypes.c_int32),
+        ("gather_ms", ctypes.c_double),
+        ("scatter_ms", ctypes.c_double),
+        ("gather_rows", ctypes.c_int64),
+        ("gather_edges", ctypes.c_int64),
+        ("scatter_members", ctypes.c_int64),
+        ("n_contrib", ctypes.c_int64),
+        ("n_tasks", ctypes.c_int64),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libprgpu.so not built at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    i64, i32, u32, dbl, p = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_double, ctypes.c_void_p
+    pp = ctypes.POINTER(ctypes.c_void_p)
+    lib.pr_graph_create.argtypes = [i64, i64, p, p, p, pp]
+    lib.pr_graph_create.restype = ctypes.c_int
+    lib.pr_preprocess.argtypes = [p, u32, p]
+    lib.pr_preprocess.restype = ctypes.c_int
+    lib.pr_run.argtypes = [p, dbl, dbl, i32, p, u32, p, ctypes.POINTER(i32), ctypes.POINTER(dbl)]
+    lib.pr_run.restype = ctypes.c_int
+    lib.pr_destroy.argtypes = [p]
+    lib.pr_destroy.restype = None
+    lib.pr_last_error.argtypes = []
+    lib.pr_last_error.restype = ctypes.c_char_p
+    lib.pr_graph_info.argtypes = [p, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    lib.pr_graph_info.restype = ctypes.c_int
+    lib.pr_get_csr.argtypes = [p, p, p, p, p]
+    lib.pr_get_csr.restype = ctypes.c_int
+    lib.pr_get_reductions.argtypes = [p, p, p, p, p]
+    lib.pr_get_reductions.restype = ctypes.c_int
+    lib.pr_get_delta_log.argtypes = [p, p, i32]
+    lib.pr_get_delta_log.restype = ctypes.c_int
+    lib.pr_get_run_stats.argtypes = [p, ctypes.POINTER(pr_run_stats)]
+    lib.pr_get_run_stats.restype = ctypes.c_int
+    return lib
+
+
+lib = _load()
+
+
+def _ptr(a) -> int | None:
+    """Address of a torch tensor / numpy array (contiguous), or None."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    if hasattr(a, "ctypes"):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    raise TypeError(type(a))
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except ImportError:
+            pass
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+def last_error() -> str:
+    return (lib.pr_last_error() or b"").decode()
+
+
+def _check(rc: int, ok=(PR_OK,)):
+    if rc not in ok:
+        raise PRError(rc, last_error())
+    return rc
+
+
+def pr_graph_create(n: int, src, dst, stream=None) -> ctypes.c_void_p:
+    """In-CSR + out-degrees on the device.  src/dst int32[m]."""
+    m = int(src.shape[0])
+    if int(dst.shape[0]) != m:
+        raise ValueError("src and dst lengths differ")
+    for a in (src, dst):
+        dt = str(getattr(a, "dtype", ""))
+        if "int32" not in dt:
+            raise TypeError(f"edge arrays must be int32, got {dt}")
+    out = ctypes.c_void_p()
+    _check(lib.pr_graph_create(n, m, _ptr(src) if m else None, _ptr(dst) if m else None,
+                               _stream(stream), ctypes.byref(out)))
+    return out
+
+
+def pr_preprocess(g, flags: int = PR_PRE_IDENTICAL | PR_PRE_CHAIN, stream=None) -> None:
+    _check(lib.pr_preprocess(g, flags, _stream(stream)))
+
+
+def pr_run(g, d: float, threshold: float, max_iter: int, ranks, stream=None, mode: int = 0):
+    """Iterate to convergence; returns (status, iterations, final_delta)."""
+    it = ctypes.c_int32(0)
+    fd = ctypes.c_double(0.0)
+    rc = _check(lib.pr_run(g, d, threshold, max_iter, _stream(stream), mode, _ptr(ranks),
+                           ctypes.byref(it), ctypes.byref(fd)), ok=(PR_OK, PR_NOT_CONVERGED))
+    return rc, it.value, fd.value
+
+
+def pr_destroy(g) -> None:
+    lib.pr_destroy(g)
+
+
+def pr_graph_info(g):
+    n, E, nm = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    mc = ctypes.c_int32()
+    _check(lib.pr_graph_info(g, ctypes.byref(n), ctypes.byref(E), ctypes.byref(nm), ctypes.byref(mc)))
+    return {"n": n.value, "E": E.value, "n_members": nm.value, "max_chain": mc.value}
+
+
+def pr_get_csr(g, row_ptr, col_idx, outdeg, stream=None) -> None:
+    _check(lib.pr_get_csr(g, _ptr(row_ptr), _ptr(col_idx), _ptr(outdeg), _stream(stream)))
+
+
+def pr_get_reductions(g, rep, chain_src, chain_k, stream=None) -> None:
+    _check(lib.pr_get_reductions(g, _ptr(rep), _ptr(chain_src), _ptr(chain_k), _stream(stream)))
+
+
+def pr_get_delta_log(g, cap: int):
+    import numpy as np
+    buf = np.zeros((max(cap, 1), 2), np.float64)
+    k = lib.pr_get_delta_log(g, buf.ctypes.data, cap)
+    if k < 0:
+        raise PRError(k, last_error())
+    return buf[:k]
+
+
+def pr_get_run_stats(g) -> dict:
+    st = pr_run_stats()
+    _check(lib.pr_get_run_stats(g, ctypes.byref(st)))
+    return st.as_dict()
+
+
+class Graph:
+    """RAII convenience wrapper around one pr_graph (still only marshalling)."""
+
+    def __init__(self, n: int, src, dst, stream=None):
+        self.n = n
+        self.handle = pr_graph_create(n, src, dst, stream)
+
+    def preprocess(self, flags: int = PR_PRE_IDENTICAL | PR_PRE_CHAIN, stream=None):
+        pr_preprocess(self.handle, flags, stream)
+        return self
+
+    def run(self, ranks, d=0.85, threshold=1e-10, max_iter=1000, mode=0, stream=None):
+        return pr_run(self.handle, d, threshold, max_iter, ranks, stream, mode)
+
+    def info(self):
+        return pr_graph_info(self.handle)
+
+    def stats(self):
+        return pr_get_run_stats(self.handle)
+
+    def delta_log(self, cap=4096):
+        return pr_get_delta_log(self.handle, cap)
+
+    def close(self):
+        if self.handle is not None:
+            pr_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,118 @@
+// common.cuh -- internal helpers of libprgpu (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/prgpu.h"
+
+namespace prgpu {
+
+void set_error(const char* fmt, ...);
+
+// Return PR_ECUDA from the enclosing int function on a CUDA error.
+#define PR_CUDA(call)                                                              \
+    do {                                                                           \
+        cudaError_t _e = (call);                                                   \
+        if (_e != cudaSuccess) {                                                   \
+            ::prgpu::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,          \
+                               cudaGetErrorString(_e));                            \
+            return _e == cudaErrorMemoryAllocation ? PR_ENOMEM : PR_ECUDA;         \
+        }                                                                          \
+    } while (0)
+
+#define PR_TRY(expr)                 \
+    do {                             \
+        int _s = (expr);             \
+        if (_s != PR_OK) return _s;  \
+    } while (0)
+
+// Every kernel launch goes through this so the library can count launches.
+#define PR_LAUNCH(ctx, kernel, grid, block, smem, ...)                                  \
+    do {                                                                                \
+        kernel<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);                 \
+        (ctx).launches += 1;                                                            \
+        cudaError_t _le = cudaGetLastError();                                           \
+        if (_le != cudaSuccess) {                                                       \
+            ::prgpu::set_error("launch %s: %s", #kernel, cudaGetErrorString(_le));      \
+            return PR_ECUDA;                                                            \
+        }                                                                               \
+    } while (0)
+
+struct Ctx {
+    cudaStream_t stream;
+    int num_sms;
+    int64_t launches;
+};
+
+// Stream-ordered allocation; all library memory comes from here.
+template <class T>
+int dalloc(T** p, size_t count, cudaStream_t s) {
+    *p = nullptr;
+    size_t bytes = count * sizeof(T) + 64;  // +64: vector tails may read past the end
+    cudaError_t e = cudaMallocAsync((void**)p, bytes, s);
+    if (e != cudaSuccess) {
+        set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
+        *p = nullptr;
+        return PR_ENOMEM;
+    }
+    return PR_OK;
+}
+template <class T>
+void dfree(T*& p, cudaStream_t s) {
+    if (p) cudaFreeAsync((void*)p, s);
+    p = nullptr;
+}
+
+constexpr int WARP = 32;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// ---- cache-hinted memory operations (sm_100a PTX) -------------------------
+// Streamed-once data (col_idx): no L1 allocation, L2 evict-first.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int4 ld_stream_i4(const int4* ptr, uint64_t pol) {
+    int4 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr), "l"(pol));
+    return r;
+}
+// Read-only gathers of the contrib vector within one synchronous sweep.
+__device__ __forceinline__ double ld_gather_f64(const double* ptr, uint64_t pol) {
+    double r;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+// Async (No-Sync) mode: the contrib vector is read and written in the same
+// launch, so loads/stores are relaxed gpu-scope atomics (never .nc).
+__device__ __forceinline__ double ld_relaxed_f64(const double* ptr) {
+    double r;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(r) : "l"(ptr));
+    return r;
+}
+__device__ __forceinline__ void st_relaxed_f64(double* ptr, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(ptr), "d"(v) : "memory");
+}
+
+}  // namespace prgpu

@@ -1,0 +1,379 @@
+// ingest.cu -- K-INGEST: raw edge list -> deduplicated in-CSR + out-degrees
+// (§5.2 "converted later to Compressed Sparse Row (CSR)
+// format"; SPEC S:69-77 build_csr; readings Q-L, Q-V in DESIGN.md), plus the
+// contrib relabelling and the row-block task lists of the gather engine.
+//
+// Pipeline (all hand-written kernels):
+//   pack    validate ids, drop self-loops, key = dst << b | src   (b = bits(n-1))
+//   sort    LSD radix sort of the keys on 2b bits (8-bit digits)  -> (dst, src) order
+//   unique  adjacent-different flags -> scan -> col_idx / row dst  (dedup)
+//   rows    in-degree histogram (run-aggregated atomics) -> scan -> row_ptr
+//   outdeg  histogram of src over the deduplicated edges
+#include "internal.h"
+#include "primitives.cuh"
+
+namespace prgpu {
+
+__global__ void k_pack(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m,
+                       int64_t n, int b, uint64_t* __restrict__ keys,
+                       unsigned long long* __restrict__ count, int* __restrict__ err) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = lanemask_lt();
+    const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < m; base += wstride) {
+        int64_t i = base + lane;
+        bool valid = i < m;
+        int32_t s = valid ? src[i] : 0, t = valid ? dst[i] : 0;
+        bool bad = valid && (s < 0 || (int64_t)s >= n || t < 0 || (int64_t)t >= n);
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1);
+        bool keep = valid && !bad && s != t;
+        uint32_t mask = __ballot_sync(0xffffffffu, keep);
+        unsigned long long wbase = 0;
+        if (lane == 0 && mask) wbase = atomicAdd(count, (unsigned long long)__popc(mask));
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        if (keep) keys[wbase + __popc(mask & lt)] = ((uint64_t)(uint32_t)t << b) | (uint32_t)s;
+    }
+}
+
+// In-degree histogram over the sorted unique dst array, one atomic per run of
+// equal dst within a thread's 16 consecutive positions (hub rows are long runs).
+__global__ void k_indeg(const uint32_t* __restrict__ udst, int64_t E, int32_t* __restrict__ indeg) {
+    constexpr int R = 16;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
+    for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * R; b0 < E; b0 += stride) {
+        int64_t e1 = min(E, b0 + R);
+        uint32_t cur = udst[b0];
+        int run = 1;
+        for (int64_t p = b0 + 1; p < e1; ++p) {
+            uint32_t d = udst[p];
+            if (d == cur) {
+                ++run;
+            } else {
+                atomicAdd(&indeg[cur], run);
+                cur = d;
+                run = 1;
+            }
+        }
+        atomicAdd(&indeg[cur], run);
+    }
+}
+
+__global__ void k_outdeg(const int32_t* __restrict__ col, int64_t E, int32_t* __restrict__ outdeg) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&outdeg[col[e]], 1);
+}
+
+struct UniqueGet {
+    const uint64_t* k;
+    __device__ int64_t operator()(int64_t i) const { return (i == 0 || k[i] != k[i - 1]) ? 1 : 0; }
+};
+struct UniqueEmit {
+    const uint64_t* k;
+    int32_t* col;
+    uint32_t* udst;
+    int b;
+    uint64_t mask;
+    __device__ void operator()(int64_t i, int64_t pos, int64_t v) const {
+        if (v) {
+            uint64_t key = k[i];
+            col[pos] = (int32_t)(key & mask);
+            udst[pos] = (uint32_t)(key >> b);
+        }
+    }
+};
+struct I32Get {
+    const int32_t* a;
+    int64_t n;
+    __device__ int64_t operator()(int64_t i) const { return i < n ? (int64_t)a[i] : 0; }
+};
+struct RowPtrEmit {
+    int64_t* row_ptr;
+    __device__ void operator()(int64_t i, int64_t pos, int64_t) const { row_ptr[i] = pos; }
+};
+
+int read_count(Ctx& ctx, const int64_t* dev, int64_t* host) {
+    PR_CUDA(cudaMemcpyAsync(host, dev, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    return PR_OK;
+}
+
+static unsigned grid_for(const Ctx& ctx, int64_t work, int nt) {
+    int64_t g = (work + nt - 1) / nt;
+    int64_t cap = (int64_t)ctx.num_sms * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
+    const int64_t n = g->n, m = g->m_raw;
+    const int b = bits_for((uint64_t)(n - 1));
+    cudaStream_t s = ctx.stream;
+
+    uint64_t* keys = nullptr;
+    uint64_t* keys_alt = nullptr;
+    int64_t* scratch = nullptr;  // [0] = kept count, [1] = error flag, [2] = E
+    PR_TRY(dalloc(&scratch, 4, s));
+    PR_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(int64_t), s));
+    int64_t kept = 0;
+    if (m > 0) {
+        PR_TRY(dalloc(&keys, (size_t)m, s));
+        PR_LAUNCH(ctx, k_pack, grid_for(ctx, m, 256), 256, 0, src, dst, m, n, b, keys,
+                  (unsigned long long*)scratch, (int*)(scratch + 1));
+        int64_t h[2];
+        PR_CUDA(cudaMemcpyAsync(h, scratch, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        if (h[1] != 0) {
+            dfree(keys, s);
+            dfree(scratch, s);
+            set_error("pr_graph_create: vertex id outside [0, n)");
+            return PR_EINVAL;
+        }
+        kept = h[0];
+    }
+
+    // sort by (dst, src) and deduplicate
+    uint32_t* udst = nullptr;
+    PR_TRY(dalloc(&g->col, (size_t)(kept > 0 ? kept : 1), s));
+    if (kept > 0) {
+        PR_TRY(dalloc(&keys_alt, (size_t)kept, s));
+        bool alt = false;
+        PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, kept, 0, 2 * b, &alt)));
+        const uint64_t* sorted = alt ? keys_alt : keys;
+        PR_TRY(dalloc(&udst, (size_t)kept, s));
+        PR_TRY((device_scan<int64_t>(ctx, kept, UniqueGet{sorted},
+                                     UniqueEmit{sorted, g->col, udst, b, (b ? ((1ull << b) - 1) : 0ull)},
+                                     scratch + 2)));
+        PR_TRY(read_count(ctx, scratch + 2, &g->E));
+        dfree(keys, s);
+        dfree(keys_alt, s);
+    } else {
+        g->E = 0;
+    }
+
+    // row_ptr from the in-degree histogram; outdeg from the sources
+    int32_t* indeg = nullptr;
+    PR_TRY(dalloc(&indeg, (size_t)n, s));
+    PR_TRY(dalloc(&g->row_ptr, (size_t)n + 1, s));
+    PR_TRY(dalloc(&g->outdeg, (size_t)n, s));
+    PR_CUDA(cudaMemsetAsync(indeg, 0, sizeof(int32_t) * (size_t)n, s));
+    PR_CUDA(cudaMemsetAsync(g->outdeg, 0, sizeof(int32_t) * (size_t)n, s));
+    if (g->E > 0) {
+        PR_LAUNCH(ctx, k_indeg, grid_for(ctx, (g->E + 15) / 16, 256), 256, 0, (const uint32_t*)udst, g->E, indeg);
+        PR_LAUNCH(ctx, k_outdeg, grid_for(ctx, g->E, 256), 256, 0, (const int32_t*)g->col, g->E, g->outdeg);
+    }
+    PR_TRY((device_scan<int64_t>(ctx, n + 1, I32Get{indeg, n}, RowPtrEmit{g->row_ptr}, (int64_t*)nullptr)));
+    dfree(indeg, s);
+    dfree(udst, s);
+    dfree(scratch, s);
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------- relabel --
+// The gather reads contrib values y(u) = x(u)/outdeg(u) only for sources u
+// (outdeg > 0).  They are stored compactly, ordered by (outdeg desc, id asc),
+// so the hottest contribs share sectors and the vector is ~44 % of n on R-MAT
+// (DESIGN.md "Data layout").  cidx[v] = position, or -1 for dangling v.
+struct NdGet {
+    const int32_t* od;
+    __device__ int64_t operator()(int64_t v) const { return od[v] > 0 ? 1 : 0; }
+};
+struct NdEmit {
+    const int32_t* od;
+    uint64_t* keys;
+    int b;
+    int32_t maxod;
+    __device__ void operator()(int64_t v, int64_t pos, int64_t f) const {
+        if (f) keys[pos] = ((uint64_t)(uint32_t)(maxod - od[v]) << b) | (uint64_t)v;
+    }
+};
+
+__global__ void k_max_i32(const int32_t* __restrict__ a, int64_t n, int* __restrict__ out) {
+    int mx = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        mx = max(mx, a[i]);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+__global__ void k_set_cidx(const uint64_t* __restrict__ sorted, int64_t cnt, uint64_t vmask, int32_t* __restrict__ cidx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        cidx[sorted[i] & vmask] = (int32_t)i;
+}
+
+__global__ void k_map_col(const int32_t* __restrict__ col, int64_t E, const int32_t* __restrict__ cidx,
+                          int32_t* __restrict__ out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] = cidx[col[e]];
+}
+
+int build_relabel(pr_graph* g, Ctx& ctx) {
+    cudaStream_t s = ctx.stream;
+    const int64_t n = g->n;
+    int64_t* scratch = nullptr;
+    PR_TRY(dalloc(&scratch, 2, s));
+    PR_CUDA(cudaMemsetAsync(scratch, 0, 2 * sizeof(int64_t), s));
+    PR_LAUNCH(ctx, k_max_i32, grid_for(ctx, n, 256), 256, 0, (const int32_t*)g->outdeg, n, (int*)(scratch + 1));
+    int64_t h[2];
+    PR_CUDA(cudaMemcpyAsync(h, scratch, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
+    const int32_t maxod = (int32_t)(h[1] & 0xffffffff);
+    const int b = bits_for((uint64_t)(n - 1));
+    const char* mode = getenv("PRGPU_RELABEL");
+    const bool by_degree = !(mode && mode[0] == 'i');  // "id": keep id order (ablation)
+
+    uint64_t* keys = nullptr;
+    uint64_t* keys_alt = nullptr;
+    PR_TRY(dalloc(&keys, (size_t)n, s));
+    PR_TRY((device_scan<int64_t>(ctx, n, NdGet{g->outdeg},
+                                 NdEmit{g->outdeg, keys, b, by_degree ? maxod : 0}, scratch)));
+    PR_TRY(read_count(ctx, scratch, &g->n_contrib));
+    const int64_t cnt = g->n_contrib;
+    PR_TRY(dalloc(&g->cidx, (size_t)n, s));
+    PR_CUDA(cudaMemsetAsync(g->cidx, 0xff, sizeof(int32_t) * (size_t)n, s));
+    const uint64_t* sorted = keys;
+    if (by_degree && cnt > 1) {
+        PR_TRY(dalloc(&keys_alt, (size_t)cnt, s));
+        bool alt = false;
+        PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, cnt, b,
+                                            b + bits_for((uint64_t)maxod), &alt)));
+        sorted = alt ? keys_alt : keys;
+    }
+    if (cnt > 0)
+        PR_LAUNCH(ctx, k_set_cidx, grid_for(ctx, cnt, 256), 256, 0, sorted, cnt,
+                  b ? ((1ull << b) - 1) : 0ull, g->cidx);
+    // plain view: all rows, relabelled sources
+    View& v = g->plain;
+    v.nrows = n;
+    v.nedges = g->E;
+    v.row_ptr = g->row_ptr;
+    v.owns_row_ptr = false;
+    v.vid = nullptr;
+    PR_TRY(dalloc(&v.col, (size_t)(g->E > 0 ? g->E : 1), s));
+    if (g->E > 0)
+        PR_LAUNCH(ctx, k_map_col, grid_for(ctx, g->E, 256), 256, 0, (const int32_t*)g->col, g->E,
+                  (const int32_t*)g->cidx, v.col);
+    dfree(keys, s);
+    dfree(keys_alt, s);
+    dfree(scratch, s);
+    return PR_OK;
+}
+
+// ------------------------------------------------------------ view tasks --
+// Row blocks: a non-hub row r starts a block iff r == 0, r-1 is a hub, or the
+// running weight P(r) (edges + ROW_W per row, hubs weigh 0) crosses a multiple
+// of CAP.  Hence a block holds < CAP/ROW_W + 1 rows and < CAP + LONG edges.
+// Hub rows (in-degree > LONG) become ceil(deg / HUB_CHUNK) chunk tasks.
+struct WGet {
+    const int64_t* rp;
+    __device__ int64_t operator()(int64_t r) const {
+        int64_t d = rp[r + 1] - rp[r];
+        return d > GT_LONG ? 0 : d + GT_ROW_W;
+    }
+};
+struct WEmit {
+    int64_t* P;
+    __device__ void operator()(int64_t r, int64_t pos, int64_t) const { P[r] = pos; }
+};
+struct StartGet {
+    const int64_t* rp;
+    const int64_t* P;
+    __device__ bool is_long(int64_t r) const { return rp[r + 1] - rp[r] > GT_LONG; }
+    __device__ int64_t operator()(int64_t r) const {
+        if (r == 0 || is_long(r) || is_long(r - 1)) return 1;
+        return (P[r] / GT_CAP) != (P[r - 1] / GT_CAP) ? 1 : 0;
+    }
+};
+struct StartEmit {
+    int64_t* starts;
+    __device__ void operator()(int64_t r, int64_t pos, int64_t f) const {
+        if (f) starts[pos] = r;
+    }
+};
+// per start: low 40 bits = number of tasks, high bits = 1 if hub
+struct TaskCountGet {
+    const int64_t* rp;
+    const int64_t* starts;
+    __device__ int64_t operator()(int64_t i) const {
+        int64_t r = starts[i];
+        int64_t d = rp[r + 1] - rp[r];
+        if (d > GT_LONG) return ((d + GT_HUB_CHUNK - 1) / GT_HUB_CHUNK) | (1ll << 40);
+        return 1;
+    }
+};
+struct TaskFillEmit {
+    const int64_t* rp;
+    const int64_t* starts;
+    int64_t nstarts;
+    int64_t nrows;
+    Task* tasks;
+    Hub* hubs;
+    __device__ void operator()(int64_t i, int64_t pos, int64_t v) const {
+        int64_t r = starts[i];
+        int64_t toff = pos & ((1ll << 40) - 1);
+        int64_t hid = pos >> 40;
+        if (v >> 40) {
+            int32_t nch = (int32_t)(v & ((1ll << 40) - 1));
+            hubs[hid].nchunks = nch;
+            hubs[hid].pad = 0;
+            hubs[hid].slot = toff;
+            for (int32_t j = 0; j < nch; ++j) tasks[toff + j] = Task{r, j, (int32_t)hid};
+        } else {
+            int64_t rend = i + 1 < nstarts ? starts[i + 1] : nrows;
+            tasks[toff] = Task{r, (int32_t)(rend - r), -1};
+        }
+    }
+};
+
+void free_view(View& v, cudaStream_t s) {
+    if (v.owns_row_ptr) dfree(v.row_ptr, s);
+    v.row_ptr = nullptr;
+    dfree(v.col, s);
+    dfree(v.vid, s);
+    dfree(v.tasks, s);
+    dfree(v.hubs, s);
+    dfree(v.hub_partial, s);
+    dfree(v.hub_delta, s);
+    dfree(v.hub_ticket, s);
+    v.nrows = v.nedges = v.ntasks = v.nhubs = v.hub_slots = 0;
+}
+
+int build_view_tasks(View& v, Ctx& ctx) {
+    cudaStream_t s = ctx.stream;
+    v.ntasks = 0;
+    v.nhubs = 0;
+    if (v.nrows == 0) return PR_OK;
+    int64_t* P = nullptr;
+    int64_t* starts = nullptr;
+    int64_t* scratch = nullptr;
+    PR_TRY(dalloc(&scratch, 2, s));
+    PR_TRY(dalloc(&P, (size_t)v.nrows, s));
+    PR_TRY((device_scan<int64_t>(ctx, v.nrows, WGet{v.row_ptr}, WEmit{P}, (int64_t*)nullptr)));
+    PR_TRY(dalloc(&starts, (size_t)v.nrows, s));
+    PR_TRY((device_scan<int64_t>(ctx, v.nrows, StartGet{v.row_ptr, P}, StartEmit{starts}, scratch)));
+    int64_t nstarts = 0;
+    PR_TRY(read_count(ctx, scratch, &nstarts));
+    // upper bound on tasks: nstarts + sum over hubs of chunks <= nstarts + E / HUB_CHUNK + 1
+    int64_t cap_tasks = nstarts + v.nedges / GT_HUB_CHUNK + 1;
+    int64_t cap_hubs = v.nedges / (GT_LONG + 1) + 1;
+    PR_TRY(dalloc(&v.tasks, (size_t)cap_tasks, s));
+    PR_TRY(dalloc(&v.hubs, (size_t)cap_hubs, s));
+    PR_TRY((device_scan<int64_t>(ctx, nstarts, TaskCountGet{v.row_ptr, starts},
+                                 TaskFillEmit{v.row_ptr, starts, nstarts, v.nrows, v.tasks, v.hubs}, scratch + 1)));
+    int64_t packed = 0;
+    PR_TRY(read_count(ctx, scratch + 1, &packed));
+    v.ntasks = packed & ((1ll << 40) - 1);
+    v.nhubs = packed >> 40;
+    v.hub_slots = v.ntasks;  // slot index == task index of the chunk
+    PR_TRY(dalloc(&v.hub_partial, (size_t)(v.ntasks > 0 ? v.ntasks : 1), s));
+    PR_TRY(dalloc(&v.hub_delta, (size_t)(v.nhubs > 0 ? v.nhubs : 1), s));
+    PR_TRY(dalloc(&v.hub_ticket, (size_t)(v.nhubs > 0 ? v.nhubs : 1), s));
+    PR_CUDA(cudaMemsetAsync(v.hub_ticket, 0, sizeof(uint32_t) * (size_t)(v.nhubs > 0 ? v.nhubs : 1), s));
+    PR_CUDA(cudaMemsetAsync(v.hub_delta, 0, sizeof(double) * (size_t)(v.nhubs > 0 ? v.nhubs : 1), s));
+    dfree(P, s);
+    dfree(starts, s);
+    dfree(scratch, s);
+    return PR_OK;
+}
+
+}  // namespace prgpu

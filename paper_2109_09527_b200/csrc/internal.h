@@ -1,0 +1,117 @@
+// internal.h -- library-private state of libprgpu.
+#pragma once
+#include "common.cuh"
+
+namespace prgpu {
+
+// Row-block engine tuning.
+constexpr int GT_NT = 256;                 // threads per CTA
+constexpr int GT_CAP = 2048;               // weight budget per row block (edges + ROW_W*rows)
+constexpr int GT_ROW_W = 4;                // per-row weight in edge units
+constexpr int GT_LONG = 1024;              // rows with in-degree > LONG become hub tasks
+constexpr int GT_MAXROWS = GT_CAP / GT_ROW_W + 1;
+constexpr int GT_VALS = GT_CAP + GT_LONG + 8;
+constexpr int GT_HUB_CHUNK = 8192;         // edges per hub-chunk task
+constexpr int GT_MIN_CTAS = 4;           // __launch_bounds__ min CTAs/SM of the gather (<= 64 regs)
+constexpr int GT_SHORT = 32;               // rows up to this length: one thread sums serially
+
+// A unit of work for one CTA.  b < 0: row block of rows [r0, r0 + a).
+// b >= 0: chunk a of hub b (the single row r0).
+struct Task {
+    int64_t r0;
+    int32_t a;
+    int32_t b;
+};
+
+struct Hub {
+    int32_t nchunks;
+    int32_t pad;
+    int64_t slot;  // first partial slot of this hub in View::hub_partial
+};
+
+// A set of rows over which the gather runs: all vertices (plain) or the
+// computed representatives R (reduced).  Rows are in increasing vertex id.
+struct View {
+    int64_t nrows = 0;
+    int64_t nedges = 0;
+    int64_t* row_ptr = nullptr;     // int64[nrows+1] (plain: aliases the canonical row_ptr)
+    int32_t* col = nullptr;         // int32[nedges] contrib indices (relabelled sources)
+    int32_t* vid = nullptr;         // int32[nrows] vertex id of each row (nullptr: identity)
+    bool owns_row_ptr = false;
+    Task* tasks = nullptr;
+    int64_t ntasks = 0;
+    Hub* hubs = nullptr;
+    int64_t nhubs = 0;
+    double* hub_partial = nullptr;  // [sum of nchunks]
+    double* hub_delta = nullptr;    // [nhubs] |delta| of each hub row (fixed-order reduce)
+    uint32_t* hub_ticket = nullptr; // [nhubs]
+    int64_t hub_slots = 0;
+};
+
+// Device-resident iteration state (one per graph).
+struct DevState {
+    int32_t done;
+    int32_t iters;
+    int32_t max_iter;
+    int32_t norm_linf;
+    double tau;
+    double l1;
+    double linf;
+    uint32_t ticket_gather;
+    uint32_t ticket_scatter;
+    int32_t status;
+    int32_t log_cap;
+};
+
+}  // namespace prgpu
+
+struct pr_graph {
+    int64_t n = 0;
+    int64_t m_raw = 0;
+    int64_t E = 0;
+    int num_sms = 0;
+    int device = 0;
+    // canonical in-CSR (bit-exact with the oracle)
+    int64_t* row_ptr = nullptr;
+    int32_t* col = nullptr;
+    int32_t* outdeg = nullptr;
+    // contrib relabelling: cidx[v] in [0, n_contrib) for outdeg(v) > 0, else -1
+    int32_t* cidx = nullptr;
+    int64_t n_contrib = 0;
+    prgpu::View plain;
+    // reductions
+    bool pre_done = false;
+    uint32_t pre_flags = 0;
+    int32_t* rep = nullptr;
+    int32_t* chain_src = nullptr;
+    int32_t* chain_k = nullptr;
+    int32_t max_chain = 0;
+    int64_t n_members = 0;
+    int32_t* mem_vid = nullptr;
+    int32_t* mem_src = nullptr;
+    int32_t* mem_k = nullptr;
+    prgpu::View reduced;
+    // iteration buffers (allocated lazily by pr_run)
+    double* x = nullptr;            // fp64[n] (used when the caller's ranks are on the host)
+    double* y[2] = {nullptr, nullptr};
+    double* cta_partial = nullptr;  // [2 * (gather grid + scatter grid)] (L1, Linf)
+    int64_t partial_cap = 0;
+    double* ab = nullptr;           // chain alpha/beta [2 * (max_chain+1)]
+    double* delta_log = nullptr;    // [2 * log_cap]
+    int32_t log_cap = 0;
+    prgpu::DevState* st = nullptr;
+    prgpu::DevState* st_host = nullptr;  // pinned
+    int64_t launches = 0;
+    pr_run_stats last{};
+};
+
+namespace prgpu {
+int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx);
+int build_relabel(pr_graph* g, Ctx& ctx);
+int build_view_tasks(View& v, Ctx& ctx);
+void free_view(View& v, cudaStream_t s);
+int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx);
+int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
+        Ctx& ctx, int32_t* iters_out, double* delta_out);
+int read_count(Ctx& ctx, const int64_t* dev, int64_t* host);
+}  // namespace prgpu

@@ -1,0 +1,394 @@
+// iterate.cu -- the PageRank iteration: K-INIT, K-GATHER (+ fused contrib and
+// fused Delta reduction), K-SCATTER (identical / chain members), loop control.
+//
+//   x_t(v) = (1-d)/n + d * sum_{u in in(v)} y_{t-1}(u),  y(u) = x(u)/outdeg(u)
+// (Eq.(1) P:329-332 in the "sum, then times d" form of Alg.2; Q-F).
+// Dangling u (outdeg 0) are never gathered (they have no out-edges), so they
+// contribute nothing (Alg.2; Q-D).  Delta_t is summed over all n
+// vertices (Q-R) and the loop runs "while err > threshold" (Q-S).
+#include <math.h>
+#include <vector>
+
+#include "internal.h"
+#include "rowengine.cuh"
+
+namespace prgpu {
+
+// ----------------------------------------------------------------- policy --
+template <bool ASYNC, bool VID>
+struct PRPolicy {
+    using T = double;
+    const double* y_in;
+    double* y_out;
+    double* x;
+    const int32_t* od;
+    const int32_t* cidx;
+    const int32_t* vid;
+    double c, d;
+    uint64_t pol_first, pol_last;
+
+    __device__ __forceinline__ void begin() {
+        pol_first = policy_evict_first();
+        pol_last = policy_evict_last();
+    }
+    __device__ __forceinline__ int4 ld_col(const int4* p) const { return ld_stream_i4(p, pol_first); }
+    __device__ __forceinline__ double load(int32_t u) const {
+        if (ASYNC) return ld_relaxed_f64(y_in + u);
+        return ld_gather_f64(y_in + u, pol_last);
+    }
+    // x_t(v) = c + d*S, fused contrib y_t(v) = x_t(v)/outdeg(v), returns |x_t(v) - x_{t-1}(v)|.
+    __device__ __forceinline__ double finalize(int64_t r, double s) const {
+        const int32_t v = VID ? vid[r] : (int32_t)r;
+        const double xn = __dadd_rn(c, __dmul_rn(d, s));
+        const double xo = x[v];
+        x[v] = xn;
+        const int32_t o = od[v];
+        if (o > 0) {
+            const double y = xn / (double)o;
+            if (ASYNC)
+                st_relaxed_f64(y_out + cidx[v], y);
+            else
+                y_out[cidx[v]] = y;
+        }
+        return fabs(xn - xo);
+    }
+};
+
+struct IterArgs {
+    DevState* st;
+    double* cta_partial;        // (L1, Linf) per CTA: gather CTAs first, then scatter CTAs
+    int64_t gather_ctas;
+    int64_t scatter_ctas;
+    const double* hub_delta;    // of the gather view
+    int64_t nhubs;
+    double* delta_log;
+};
+
+// Deterministic fixed-order reduction over all CTA partials and hub deltas,
+// then the stop test; executed by the last CTA of the iteration.
+__device__ void global_finalize(const IterArgs& ia, double* red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __threadfence();
+    double s = 0.0, mx = 0.0;
+    const int64_t nc = ia.gather_ctas + ia.scatter_ctas;
+    for (int64_t i = tid; i < nc; i += GT_NT) {
+        s += __ldcg(ia.cta_partial + 2 * i);
+        mx = fmax(mx, __ldcg(ia.cta_partial + 2 * i + 1));
+    }
+    for (int64_t i = tid; i < ia.nhubs; i += GT_NT) {
+        double v = __ldcg(ia.hub_delta + i);
+        s += v;
+        mx = fmax(mx, v);
+    }
+    s = warp_sum(s);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __syncthreads();
+    if (lane == 0) {
+        red[warp] = s;
+        red[GT_WARPS + warp] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double l1 = 0.0, li = 0.0;
+        for (int w = 0; w < GT_WARPS; ++w) {
+            l1 += red[w];
+            li = fmax(li, red[GT_WARPS + w]);
+        }
+        DevState* st = ia.st;
+        const int it = st->iters + 1;
+        st->iters = it;
+        st->l1 = l1;
+        st->linf = li;
+        if (it <= st->log_cap) {
+            ia.delta_log[2 * (it - 1)] = l1;
+            ia.delta_log[2 * (it - 1) + 1] = li;
+        }
+        const double dn = st->norm_linf ? li : l1;
+        if (dn <= st->tau) {
+            st->done = 1;
+            st->status = PR_OK;
+        } else if (it >= st->max_iter) {
+            st->done = 1;
+            st->status = PR_NOT_CONVERGED;
+        }
+        st->ticket_gather = 0u;
+        st->ticket_scatter = 0u;
+        __threadfence();
+    }
+}
+
+__device__ __forceinline__ void block_delta(double l1, double linf, double* red, double* out) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    l1 = warp_sum(l1);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) linf = fmax(linf, __shfl_xor_sync(0xffffffffu, linf, o));
+    __syncthreads();
+    if (lane == 0) {
+        red[warp] = l1;
+        red[GT_WARPS + warp] = linf;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < GT_WARPS; ++w) {
+            a += red[w];
+            b = fmax(b, red[GT_WARPS + w]);
+        }
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+template <bool ASYNC, bool VID>
+__global__ void __launch_bounds__(GT_NT, GT_MIN_CTAS) k_gather(PRPolicy<ASYNC, VID> p, EngineArgs a, IterArgs ia, int finalize) {
+    __shared__ EngineSmem sm;
+    if (ia.st->done) return;
+    p.begin();
+    double l1 = 0.0, linf = 0.0;
+    engine_run(p, a, sm, l1, linf);
+    block_delta(l1, linf, sm.red, ia.cta_partial + 2 * blockIdx.x);
+    if (!finalize) return;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        uint32_t t = atomicAdd(&ia.st->ticket_gather, 1u);
+        sm.flag = (t == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (sm.flag) global_finalize(ia, sm.red);
+}
+
+// Members (reduced mode): x_t(m) = alpha_k + beta_k * x_t(src), with
+// (alpha_0, beta_0) = (0, 1) an exact copy for identical members and
+// alpha_{k+1} = c + d alpha_k, beta_{k+1} = d beta_k for chain members at
+// distance k from their head (Q-C).  Runs after the gather of the same sweep.
+template <bool ASYNC>
+__global__ void __launch_bounds__(GT_NT) k_scatter(const int32_t* __restrict__ mvid, const int32_t* __restrict__ msrc,
+                                                   const int32_t* __restrict__ mk, int64_t nm, int64_t per_cta,
+                                                   const double* __restrict__ ab, double* x, double* y_out,
+                                                   const int32_t* __restrict__ od, const int32_t* __restrict__ cidx,
+                                                   IterArgs ia) {
+    __shared__ double red[2 * GT_WARPS];
+    __shared__ int flag;
+    if (ia.st->done) return;
+    const int64_t b = (int64_t)blockIdx.x * per_cta;
+    const int64_t e = min(nm, b + per_cta);
+    double l1 = 0.0, linf = 0.0;
+    for (int64_t i = b + threadIdx.x; i < e; i += GT_NT) {
+        const int32_t v = mvid[i], s = msrc[i], k = mk[i];
+        const double xs = x[s];
+        const double xn = __dadd_rn(ab[2 * k], __dmul_rn(ab[2 * k + 1], xs));
+        const double xo = x[v];
+        x[v] = xn;
+        const int32_t o = od[v];
+        if (o > 0) {
+            const double y = xn / (double)o;
+            if (ASYNC)
+                st_relaxed_f64(y_out + cidx[v], y);
+            else
+                y_out[cidx[v]] = y;
+        }
+        const double dl = fabs(xn - xo);
+        l1 += dl;
+        linf = fmax(linf, dl);
+    }
+    block_delta(l1, linf, red, ia.cta_partial + 2 * (ia.gather_ctas + blockIdx.x));
+    if (threadIdx.x == 0) {
+        __threadfence();
+        uint32_t t = atomicAdd(&ia.st->ticket_scatter, 1u);
+        flag = (t == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (flag) global_finalize(ia, red);
+}
+
+// x_0 = 1/n (Alg.1), y_0 = x_0/outdeg for sources.
+__global__ void k_init(double* __restrict__ x, double* __restrict__ y, const int32_t* __restrict__ od,
+                       const int32_t* __restrict__ cidx, int64_t n, double x0) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        x[v] = x0;
+        const int32_t o = od[v];
+        if (o > 0) y[cidx[v]] = x0 / (double)o;
+    }
+}
+
+// ------------------------------------------------------------------- host --
+static int gather_grid(const Ctx& ctx, int64_t ntasks, const void* kernel) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, GT_NT, 0);
+    if (per_sm < 1) per_sm = 1;
+    int64_t g = (int64_t)ctx.num_sms * per_sm;
+    if (g > ntasks) g = ntasks;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+template <bool ASYNC, bool VID>
+static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
+                         double c, double d, const IterArgs& ia, int grid, int finalize) {
+    PRPolicy<ASYNC, VID> p{y_in, y_out, x, g->outdeg, g->cidx, v.vid, c, d, 0, 0};
+    EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, v.col, v.hub_partial, v.hub_delta, v.hub_ticket};
+    PR_LAUNCH(ctx, (k_gather<ASYNC, VID>), grid, GT_NT, 0, p, a, ia, finalize);
+    return PR_OK;
+}
+
+static const void* gather_fn(bool async, bool vid) {
+    if (async) return vid ? (const void*)k_gather<true, true> : (const void*)k_gather<true, false>;
+    return vid ? (const void*)k_gather<false, true> : (const void*)k_gather<false, false>;
+}
+
+int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
+        int32_t* iters_out, double* delta_out) {
+    cudaStream_t s = ctx.stream;
+    const bool async = (mode & PR_MODE_ASYNC) != 0;
+    const bool reduced = (mode & PR_USE_REDUCTIONS) != 0;
+    const bool timing = (mode & PR_TIMING) != 0;
+    const int64_t n = g->n;
+    const View& v = reduced ? g->reduced : g->plain;
+    const int64_t nm = reduced ? g->n_members : 0;
+    const int64_t launches0 = ctx.launches;
+
+    // ranks on the device: iterate in place in the caller's buffer
+    cudaPointerAttributes at{};
+    bool ranks_dev = cudaPointerGetAttributes(&at, ranks) == cudaSuccess &&
+                     (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    double* x = ranks;
+    if (!ranks_dev) {
+        if (!g->x) PR_TRY(dalloc(&g->x, (size_t)n, s));
+        x = g->x;
+    }
+    const int64_t ny = g->n_contrib > 0 ? g->n_contrib : 1;
+    if (!g->y[0]) PR_TRY(dalloc(&g->y[0], (size_t)ny, s));
+    if (!g->y[1]) PR_TRY(dalloc(&g->y[1], (size_t)ny, s));
+
+    const int ggrid = gather_grid(ctx, v.ntasks, gather_fn(async, v.vid != nullptr));
+    const int64_t sgrid_cap = (int64_t)ctx.num_sms * 4;
+    int64_t sgrid = nm > 0 ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
+    if (sgrid > sgrid_cap) sgrid = sgrid_cap;
+    const int64_t sper = sgrid > 0 ? (nm + sgrid - 1) / sgrid : 0;
+    const int64_t need = 2 * ((int64_t)ggrid + sgrid);
+    if (g->partial_cap < need) {
+        dfree(g->cta_partial, s);
+        PR_TRY(dalloc(&g->cta_partial, (size_t)need, s));
+        g->partial_cap = need;
+    }
+    const int log_cap = max_iter < 4096 ? max_iter : 4096;
+    if (g->log_cap < log_cap) {
+        dfree(g->delta_log, s);
+        PR_TRY(dalloc(&g->delta_log, (size_t)(2 * log_cap), s));
+        g->log_cap = log_cap;
+    }
+    const double c = (1.0 - d) / (double)n;
+    if (reduced && nm > 0) {
+        std::vector<double> ab(2 * ((size_t)g->max_chain + 1));
+        ab[0] = 0.0;
+        ab[1] = 1.0;
+        for (int k = 1; k <= g->max_chain; ++k) {
+            ab[2 * k] = c + d * ab[2 * (k - 1)];
+            ab[2 * k + 1] = d * ab[2 * (k - 1) + 1];
+        }
+        dfree(g->ab, s);
+        PR_TRY(dalloc(&g->ab, ab.size(), s));
+        PR_CUDA(cudaMemcpyAsync(g->ab, ab.data(), ab.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    DevState* hs = g->st_host;
+    *hs = DevState{};
+    hs->max_iter = max_iter;
+    hs->norm_linf = (mode & PR_NORM_LINF) ? 1 : 0;
+    hs->tau = tau;
+    hs->log_cap = log_cap;
+    PR_CUDA(cudaMemcpyAsync(g->st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
+    PR_LAUNCH(ctx, k_init, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, x,
+              g->y[0], (const int32_t*)g->outdeg, (const int32_t*)g->cidx, n, 1.0 / (double)n);
+
+    IterArgs ia{g->st, g->cta_partial, (int64_t)ggrid, reduced ? sgrid : 0, v.hub_delta, v.nhubs, g->delta_log};
+    const bool gather_finalizes = !(reduced && sgrid > 0);
+
+    std::vector<cudaEvent_t> ev;
+    double gather_ms = 0.0, scatter_ms = 0.0;
+    int timed = 0;
+    int host_syncs = 0;
+    int64_t launched = 0;
+    int batch = 8;
+    while (true) {
+        int nb = batch;
+        if (launched + nb > max_iter) nb = (int)(max_iter - launched);
+        if (timing && (int)ev.size() < 4 * nb) {
+            size_t old = ev.size();
+            ev.resize(4 * nb);
+            for (size_t i = old; i < ev.size(); ++i) PR_CUDA(cudaEventCreate(&ev[i]));
+        }
+        for (int j = 0; j < nb; ++j) {
+            const int64_t it = launched + j;
+            const double* y_in = async ? g->y[0] : g->y[it & 1];
+            double* y_out = async ? g->y[0] : g->y[(it + 1) & 1];
+            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
+            {
+                int rc;
+                if (async)
+                    rc = v.vid ? launch_gather<true, true>(ctx, v, y_in, y_out, x, g, c, d, ia, ggrid, gather_finalizes)
+                               : launch_gather<true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, ggrid, gather_finalizes);
+                else
+                    rc = v.vid ? launch_gather<false, true>(ctx, v, y_in, y_out, x, g, c, d, ia, ggrid, gather_finalizes)
+                               : launch_gather<false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, ggrid, gather_finalizes);
+                if (rc != PR_OK) return rc;
+            }
+            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
+            if (!gather_finalizes) {
+                if (async)
+                    PR_LAUNCH(ctx, k_scatter<true>, (unsigned)sgrid, GT_NT, 0, (const int32_t*)g->mem_vid,
+                              (const int32_t*)g->mem_src, (const int32_t*)g->mem_k, nm, sper, (const double*)g->ab, x,
+                              y_out, (const int32_t*)g->outdeg, (const int32_t*)g->cidx, ia);
+                else
+                    PR_LAUNCH(ctx, k_scatter<false>, (unsigned)sgrid, GT_NT, 0, (const int32_t*)g->mem_vid,
+                              (const int32_t*)g->mem_src, (const int32_t*)g->mem_k, nm, sper, (const double*)g->ab, x,
+                              y_out, (const int32_t*)g->outdeg, (const int32_t*)g->cidx, ia);
+            }
+            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
+        }
+        PR_CUDA(cudaMemcpyAsync(hs, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        ++host_syncs;
+        if (timing) {
+            for (int j = 0; j < nb; ++j) {
+                if (launched + j >= hs->iters) break;
+                float a = 0.f, b2 = 0.f;
+                PR_CUDA(cudaEventElapsedTime(&a, ev[4 * j], ev[4 * j + 1]));
+                PR_CUDA(cudaEventElapsedTime(&b2, ev[4 * j + 1], ev[4 * j + 2]));
+                gather_ms += a;
+                scatter_ms += b2;
+                ++timed;
+            }
+        }
+        launched += nb;
+        if (hs->done || launched >= max_iter) break;
+        if (batch < 64) batch *= 2;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    if (!ranks_dev) {
+        PR_CUDA(cudaMemcpyAsync(ranks, x, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        ++host_syncs;
+    }
+    pr_run_stats& rs = g->last;
+    rs.iterations = hs->iters;
+    rs.status = hs->status;
+    rs.delta_l1 = hs->l1;
+    rs.delta_linf = hs->linf;
+    rs.run_launches = ctx.launches - launches0;
+    rs.host_syncs = host_syncs;
+    rs.timed_iterations = timed;
+    rs.gather_ms = gather_ms;
+    rs.scatter_ms = scatter_ms;
+    rs.gather_rows = v.nrows;
+    rs.gather_edges = v.nedges;
+    rs.scatter_members = nm;
+    rs.n_contrib = g->n_contrib;
+    rs.n_tasks = v.ntasks;
+    if (iters_out) *iters_out = hs->iters;
+    if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
+    return hs->status;
+}
+
+}  // namespace prgpu

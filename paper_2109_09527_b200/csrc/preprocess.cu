@@ -1,0 +1,376 @@
+// preprocess.cu -- K-PRE-IDENT, K-PRE-CHAIN and the reduced view (STIC-D
+// work-saving techniques cited in PAPER.md P:398 §3; readings Q-G, Q-C).
+//
+// Identical groups: v ~ w iff in(v) == in(w) as sets (after dedup); rep(v) =
+// min id of the class; the empty in-set is one class.
+//   1. row hash h(v) = mix(indeg) + sum_{u in in(v)} mix(u)  (row engine)
+//   2. stable radix sort of vertex ids by h  -> runs of equal hash, ids ascending
+//   3. exact verification of every member against the run's first vertex; on a
+//      hash collision the vertex scans its run for the first equal row.
+// Chains: chain(v) <=> indeg 1 and outdeg 1; pred(v) = the in-neighbour.
+//   Pointer jumping over chain vertices (next = pred while pred is a chain
+//   vertex) gives every vertex its head and distance k; vertices that never
+//   reach a head lie on pure cycles and are not members.
+#include "internal.h"
+#include "primitives.cuh"
+#include "rowengine.cuh"
+
+namespace prgpu {
+
+// ---------------------------------------------------------------- hashing --
+struct HashPolicy {
+    using T = uint64_t;
+    const int64_t* rp;
+    uint64_t* out;
+    __device__ __forceinline__ void begin() {}
+    __device__ __forceinline__ int4 ld_col(const int4* p) const { return __ldg(p); }
+    __device__ __forceinline__ uint64_t load(int32_t u) const {
+        return mix64((uint64_t)(uint32_t)u * 0x9E3779B97F4A7C15ULL + 0x2545F4914F6CDD1DULL);
+    }
+    __device__ __forceinline__ double finalize(int64_t r, uint64_t s) const {
+        out[r] = s + mix64((uint64_t)(rp[r + 1] - rp[r]) + 0xD6E8FEB86659FD93ULL);
+        return 0.0;
+    }
+};
+
+__global__ void __launch_bounds__(GT_NT) k_rowhash(HashPolicy p, EngineArgs a) {
+    __shared__ EngineSmem sm;
+    double l1 = 0.0, linf = 0.0;
+    engine_run(p, a, sm, l1, linf);
+}
+
+__global__ void k_iota(uint32_t* __restrict__ a, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+
+__device__ __forceinline__ bool same_row(const int64_t* rp, const int32_t* col, int32_t u, int32_t v) {
+    const int64_t du = rp[u + 1] - rp[u];
+    if (du != rp[v + 1] - rp[v]) return false;
+    const int32_t* a = col + rp[u];
+    const int32_t* b = col + rp[v];
+    for (int64_t k = 0; k < du; ++k)
+        if (a[k] != b[k]) return false;
+    return true;
+}
+
+struct RunGet {
+    const uint64_t* h;
+    __device__ int64_t operator()(int64_t i) const { return (i == 0 || h[i] != h[i - 1]) ? 1 : 0; }
+};
+struct RunEmit {
+    int32_t* rid;
+    int64_t* rstart;
+    __device__ void operator()(int64_t i, int64_t pos, int64_t f) const {
+        rid[i] = (int32_t)(pos + f - 1);
+        if (f) rstart[pos] = i;
+    }
+};
+
+__global__ void k_verify(const uint32_t* __restrict__ sv, const int32_t* __restrict__ rid,
+                         const int64_t* __restrict__ rstart, int64_t n, const int64_t* __restrict__ rp,
+                         const int32_t* __restrict__ col, int32_t* __restrict__ rep) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = (int32_t)sv[i];
+        const int64_t s = rstart[rid[i]];
+        int32_t r = v;
+        if (i != s) {
+            const int32_t w = (int32_t)sv[s];
+            if (same_row(rp, col, v, w)) {
+                r = w;
+            } else {  // hash collision: first equal row in the run (smallest id)
+                for (int64_t j = s + 1; j < i; ++j) {
+                    const int32_t u = (int32_t)sv[j];
+                    if (same_row(rp, col, v, u)) {
+                        r = u;
+                        break;
+                    }
+                }
+            }
+        }
+        rep[v] = r;
+    }
+}
+
+// ----------------------------------------------------------------- chains --
+__device__ __forceinline__ bool is_chain(const int64_t* rp, const int32_t* od, int32_t v) {
+    return rp[v + 1] - rp[v] == 1 && od[v] == 1;
+}
+
+struct ChainGet {
+    const int64_t* rp;
+    const int32_t* od;
+    __device__ int64_t operator()(int64_t v) const { return is_chain(rp, od, (int32_t)v) ? 1 : 0; }
+};
+struct ListEmit {
+    int32_t* list;
+    __device__ void operator()(int64_t v, int64_t pos, int64_t f) const {
+        if (f) list[pos] = (int32_t)v;
+    }
+};
+
+__global__ void k_chain_init(const int32_t* __restrict__ cl, int64_t C, const int64_t* __restrict__ rp,
+                             const int32_t* __restrict__ col, const int32_t* __restrict__ od,
+                             int32_t* __restrict__ nxt, int32_t* __restrict__ dist) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = cl[i];
+        const int32_t p = col[rp[v]];
+        if (is_chain(rp, od, p)) {
+            nxt[v] = p;
+            dist[v] = 1;
+        } else {
+            nxt[v] = v;  // head: root of its list
+            dist[v] = 0;
+        }
+    }
+}
+
+__global__ void k_chain_jump(const int32_t* __restrict__ cl, int64_t C, const int32_t* __restrict__ nxt,
+                             const int32_t* __restrict__ dist, int32_t* __restrict__ nxt2, int32_t* __restrict__ dist2) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = cl[i];
+        const int32_t u = nxt[v];
+        nxt2[v] = nxt[u];
+        dist2[v] = min(dist[v] + dist[u], 1 << 30);
+    }
+}
+
+__global__ void k_chain_finish(const int32_t* __restrict__ cl, int64_t C, const int32_t* __restrict__ nxt,
+                               const int32_t* __restrict__ dist, const int64_t* __restrict__ rp,
+                               const int32_t* __restrict__ col, const int32_t* __restrict__ od,
+                               const int32_t* __restrict__ rep, int32_t* __restrict__ csrc, int32_t* __restrict__ ck) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = cl[i];
+        const int32_t h = nxt[v];
+        const bool head = !is_chain(rp, od, col[rp[h]]);  // h is a chain vertex whose pred is not
+        if (head && dist[v] >= 1) {
+            csrc[v] = rep[h];
+            ck[v] = dist[v];
+        }
+    }
+}
+
+// ------------------------------------------------------- members / R view --
+struct MemberGet {
+    const int32_t* rep;
+    const int32_t* ck;
+    __device__ int64_t operator()(int64_t v) const { return (rep[v] != (int32_t)v || ck[v] > 0) ? 1 : 0; }
+};
+struct MemberEmit {
+    const int32_t* rep;
+    const int32_t* csrc;
+    const int32_t* ck;
+    int32_t* mvid;
+    int32_t* msrc;
+    int32_t* mk;
+    __device__ void operator()(int64_t v, int64_t pos, int64_t f) const {
+        if (!f) return;
+        mvid[pos] = (int32_t)v;
+        if (ck[v] > 0) {
+            msrc[pos] = csrc[v];
+            mk[pos] = ck[v];
+        } else {
+            msrc[pos] = rep[v];
+            mk[pos] = 0;
+        }
+    }
+};
+struct ComputedGet {
+    const int32_t* rep;
+    const int32_t* ck;
+    __device__ int64_t operator()(int64_t v) const { return (rep[v] == (int32_t)v && ck[v] == 0) ? 1 : 0; }
+};
+struct DegGet {
+    const int64_t* rp;
+    const int32_t* vid;
+    int64_t nr;
+    __device__ int64_t operator()(int64_t i) const {
+        if (i >= nr) return 0;
+        const int32_t v = vid[i];
+        return rp[v + 1] - rp[v];
+    }
+};
+struct PosEmit {
+    int64_t* out;
+    __device__ void operator()(int64_t i, int64_t pos, int64_t) const { out[i] = pos; }
+};
+
+__global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const int64_t* __restrict__ rp,
+                            const int32_t* __restrict__ col, const int64_t* __restrict__ rpR, int32_t* __restrict__ colR) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < nr; i += nw) {
+        const int32_t v = vid[i];
+        const int64_t s = rp[v], len = rp[v + 1] - s, o = rpR[i];
+        for (int64_t k = lane; k < len; k += 32) colR[o + k] = col[s + k];
+    }
+}
+
+static unsigned grid_of(const Ctx& ctx, int64_t work) {
+    int64_t g = (work + 255) / 256;
+    int64_t cap = (int64_t)ctx.num_sms * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+static void clear_reductions(pr_graph* g, cudaStream_t s) {
+    dfree(g->rep, s);
+    dfree(g->chain_src, s);
+    dfree(g->chain_k, s);
+    dfree(g->mem_vid, s);
+    dfree(g->mem_src, s);
+    dfree(g->mem_k, s);
+    free_view(g->reduced, s);
+    g->n_members = 0;
+    g->max_chain = 0;
+    g->pre_done = false;
+    g->pre_flags = 0;
+}
+
+static int find_identical(pr_graph* g, Ctx& ctx) {
+    cudaStream_t s = ctx.stream;
+    const int64_t n = g->n;
+    uint64_t* h = nullptr;
+    uint64_t* h2 = nullptr;
+    uint32_t* sv = nullptr;
+    uint32_t* sv2 = nullptr;
+    PR_TRY(dalloc(&h, (size_t)n, s));
+    PR_TRY(dalloc(&h2, (size_t)n, s));
+    PR_TRY(dalloc(&sv, (size_t)n, s));
+    PR_TRY(dalloc(&sv2, (size_t)n, s));
+    const View& v = g->plain;
+    {
+        HashPolicy p{g->row_ptr, h};
+        EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, g->col, v.hub_partial, v.hub_delta, v.hub_ticket};
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowhash, GT_NT, 0);
+        int64_t grid = (int64_t)ctx.num_sms * (per_sm > 0 ? per_sm : 1);
+        if (grid > v.ntasks) grid = v.ntasks;
+        if (grid < 1) grid = 1;
+        PR_LAUNCH(ctx, k_rowhash, (unsigned)grid, GT_NT, 0, p, a);
+    }
+    PR_LAUNCH(ctx, k_iota, grid_of(ctx, n), 256, 0, sv, n);
+    bool alt = false;
+    PR_TRY((radix_sort<uint64_t, true>(ctx, h, h2, sv, sv2, n, 0, 64, &alt)));
+    const uint64_t* hs = alt ? h2 : h;
+    const uint32_t* svs = alt ? sv2 : sv;
+    int32_t* rid = nullptr;
+    int64_t* rstart = nullptr;
+    PR_TRY(dalloc(&rid, (size_t)n, s));
+    PR_TRY(dalloc(&rstart, (size_t)n, s));
+    PR_TRY((device_scan<int64_t>(ctx, n, RunGet{hs}, RunEmit{rid, rstart}, (int64_t*)nullptr)));
+    PR_LAUNCH(ctx, k_verify, grid_of(ctx, n), 256, 0, svs, (const int32_t*)rid, (const int64_t*)rstart, n,
+              (const int64_t*)g->row_ptr, (const int32_t*)g->col, g->rep);
+    dfree(h, s);
+    dfree(h2, s);
+    dfree(sv, s);
+    dfree(sv2, s);
+    dfree(rid, s);
+    dfree(rstart, s);
+    return PR_OK;
+}
+
+__global__ void k_fill_i32(int32_t* a, int64_t n, int32_t v, int iota) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = iota ? (int32_t)i : v;
+}
+
+__global__ void k_max_chain(const int32_t* __restrict__ ck, int64_t n, int* __restrict__ out) {
+    int mx = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        mx = max(mx, ck[i]);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+static int find_chains(pr_graph* g, Ctx& ctx) {
+    cudaStream_t s = ctx.stream;
+    const int64_t n = g->n;
+    int64_t* cnt = nullptr;
+    int32_t* cl = nullptr;
+    PR_TRY(dalloc(&cnt, 1, s));
+    PR_TRY(dalloc(&cl, (size_t)n, s));
+    PR_TRY((device_scan<int64_t>(ctx, n, ChainGet{g->row_ptr, g->outdeg}, ListEmit{cl}, cnt)));
+    int64_t C = 0;
+    PR_TRY(read_count(ctx, cnt, &C));
+    if (C > 0) {
+        int32_t *nxt = nullptr, *dist = nullptr, *nxt2 = nullptr, *dist2 = nullptr;
+        PR_TRY(dalloc(&nxt, (size_t)n, s));
+        PR_TRY(dalloc(&dist, (size_t)n, s));
+        PR_TRY(dalloc(&nxt2, (size_t)n, s));
+        PR_TRY(dalloc(&dist2, (size_t)n, s));
+        PR_LAUNCH(ctx, k_chain_init, grid_of(ctx, C), 256, 0, (const int32_t*)cl, C, (const int64_t*)g->row_ptr,
+                  (const int32_t*)g->col, (const int32_t*)g->outdeg, nxt, dist);
+        const int rounds = bits_for((uint64_t)C) + 1;  // ceil(log2 C) + 1 >= enough for any path
+        for (int r = 0; r < rounds; ++r) {
+            PR_LAUNCH(ctx, k_chain_jump, grid_of(ctx, C), 256, 0, (const int32_t*)cl, C, (const int32_t*)nxt,
+                      (const int32_t*)dist, nxt2, dist2);
+            int32_t* t = nxt; nxt = nxt2; nxt2 = t;
+            t = dist; dist = dist2; dist2 = t;
+        }
+        PR_LAUNCH(ctx, k_chain_finish, grid_of(ctx, C), 256, 0, (const int32_t*)cl, C, (const int32_t*)nxt,
+                  (const int32_t*)dist, (const int64_t*)g->row_ptr, (const int32_t*)g->col,
+                  (const int32_t*)g->outdeg, (const int32_t*)g->rep, g->chain_src, g->chain_k);
+        dfree(nxt, s);
+        dfree(dist, s);
+        dfree(nxt2, s);
+        dfree(dist2, s);
+    }
+    dfree(cl, s);
+    dfree(cnt, s);
+    return PR_OK;
+}
+
+int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
+    cudaStream_t s = ctx.stream;
+    const int64_t n = g->n;
+    clear_reductions(g, s);
+    if (flags == 0) return PR_OK;
+    PR_TRY(dalloc(&g->rep, (size_t)n, s));
+    PR_TRY(dalloc(&g->chain_src, (size_t)n, s));
+    PR_TRY(dalloc(&g->chain_k, (size_t)n, s));
+    PR_LAUNCH(ctx, k_fill_i32, grid_of(ctx, n), 256, 0, g->chain_src, n, -1, 0);
+    PR_LAUNCH(ctx, k_fill_i32, grid_of(ctx, n), 256, 0, g->chain_k, n, 0, 0);
+    if (flags & PR_PRE_IDENTICAL)
+        PR_TRY(find_identical(g, ctx));
+    else
+        PR_LAUNCH(ctx, k_fill_i32, grid_of(ctx, n), 256, 0, g->rep, n, 0, 1);
+    if (flags & PR_PRE_CHAIN) PR_TRY(find_chains(g, ctx));
+
+    // members (scatter list) and the computed set R (reduced gather view)
+    int64_t* cnt = nullptr;
+    PR_TRY(dalloc(&cnt, 3, s));
+    PR_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(int64_t), s));
+    PR_LAUNCH(ctx, k_max_chain, grid_of(ctx, n), 256, 0, (const int32_t*)g->chain_k, n, (int*)(cnt + 2));
+    PR_TRY(dalloc(&g->mem_vid, (size_t)n, s));
+    PR_TRY(dalloc(&g->mem_src, (size_t)n, s));
+    PR_TRY(dalloc(&g->mem_k, (size_t)n, s));
+    PR_TRY((device_scan<int64_t>(ctx, n, MemberGet{g->rep, g->chain_k},
+                                 MemberEmit{g->rep, g->chain_src, g->chain_k, g->mem_vid, g->mem_src, g->mem_k}, cnt)));
+    View& R = g->reduced;
+    PR_TRY(dalloc(&R.vid, (size_t)n, s));
+    PR_TRY((device_scan<int64_t>(ctx, n, ComputedGet{g->rep, g->chain_k}, ListEmit{R.vid}, cnt + 1)));
+    int64_t h[3];
+    PR_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
+    g->n_members = h[0];
+    R.nrows = h[1];
+    g->max_chain = (int32_t)(h[2] & 0xffffffff);
+    PR_TRY(dalloc(&R.row_ptr, (size_t)R.nrows + 1, s));
+    R.owns_row_ptr = true;
+    PR_TRY((device_scan<int64_t>(ctx, R.nrows + 1, DegGet{g->row_ptr, R.vid, R.nrows}, PosEmit{R.row_ptr}, cnt)));
+    PR_TRY(read_count(ctx, cnt, &R.nedges));
+    PR_TRY(dalloc(&R.col, (size_t)(R.nedges > 0 ? R.nedges : 1), s));
+    if (R.nrows > 0)
+        PR_LAUNCH(ctx, k_copy_rows, grid_of(ctx, R.nrows * 32), 256, 0, (const int32_t*)R.vid, R.nrows,
+                  (const int64_t*)g->row_ptr, (const int32_t*)g->plain.col, (const int64_t*)R.row_ptr, R.col);
+    PR_TRY(build_view_tasks(R, ctx));
+    dfree(cnt, s);
+    g->pre_done = true;
+    g->pre_flags = flags;
+    return PR_OK;
+}
+
+}  // namespace prgpu

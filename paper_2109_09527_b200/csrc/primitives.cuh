@@ -1,0 +1,281 @@
+// primitives.cuh -- hand-written device-wide scan, stream compaction and LSD
+// radix sort used by graph ingest and preprocessing (no CUB / Thrust).
+//
+// Design: "reduce-then-scan" with a fixed number G of CTAs, each owning one
+// contiguous range of the input, so every result is a deterministic function
+// of the input (no decoupled look-back, no atomics on the data path).
+#pragma once
+#include "common.cuh"
+
+namespace prgpu {
+
+constexpr int SCAN_NT = 256;
+constexpr int SCAN_IPT = 8;
+constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
+
+// Block-wide exclusive sum over one value per thread; returns the exclusive
+// prefix and writes the block total to *total (all threads see it).
+template <class T>
+__device__ __forceinline__ T block_exclusive_sum(T v, T* total, T* smem_warp /*[33]*/) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    T x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) smem_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        T w = lane < nwarps ? smem_warp[lane] : T(0);
+        T ws = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T y = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += y;
+        }
+        if (lane < nwarps) smem_warp[lane] = ws - w;  // exclusive warp offsets
+        if (lane == nwarps - 1) smem_warp[32] = ws;   // block total
+    }
+    __syncthreads();
+    T res = smem_warp[warp] + x - v;
+    *total = smem_warp[32];
+    __syncthreads();
+    return res;
+}
+
+template <class T>
+__device__ __forceinline__ T block_sum(T v, T* smem_warp) {
+    T tot;
+    block_exclusive_sum(v, &tot, smem_warp);
+    return tot;
+}
+
+template <class T, class Get>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_reduce(Get get, int64_t n, int64_t per_cta, T* partial) {
+    __shared__ T sw[33];
+    const int64_t b = (int64_t)blockIdx.x * per_cta;
+    const int64_t e = min(n, b + per_cta);
+    T s = T(0);
+    for (int64_t i = b + threadIdx.x; i < e; i += SCAN_NT) s += get(i);
+    T tot = block_sum(s, sw);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+// Single CTA: in-place exclusive scan of partial[0..G); *total = sum.
+template <class T>
+__global__ void __launch_bounds__(1024) k_scan_partials(T* partial, int64_t G, T* total) {
+    __shared__ T sw[33];
+    T carry = T(0);
+    constexpr int IPT = 8;
+    for (int64_t base = 0; base < G; base += 1024 * IPT) {
+        T v[IPT];
+        T ts = T(0);
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            int64_t i = base + (int64_t)threadIdx.x * IPT + j;
+            v[j] = i < G ? partial[i] : T(0);
+            ts += v[j];
+        }
+        T tot;
+        T p = carry + block_exclusive_sum(ts, &tot, sw);
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            int64_t i = base + (int64_t)threadIdx.x * IPT + j;
+            if (i < G) partial[i] = p;
+            p += v[j];
+        }
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+template <class T, class Get, class Emit>
+__global__ void __launch_bounds__(SCAN_NT) k_scan_down(Get get, Emit emit, int64_t n, int64_t per_cta,
+                                                       const T* partial) {
+    __shared__ T sw[33];
+    const int64_t b = (int64_t)blockIdx.x * per_cta;
+    const int64_t e = min(n, b + per_cta);
+    T running = partial[blockIdx.x];
+    for (int64_t tb = b; tb < e; tb += SCAN_TILE) {
+        T v[SCAN_IPT];
+        T ts = T(0);
+#pragma unroll
+        for (int j = 0; j < SCAN_IPT; ++j) {
+            int64_t i = tb + (int64_t)threadIdx.x * SCAN_IPT + j;
+            v[j] = i < e ? get(i) : T(0);
+            ts += v[j];
+        }
+        T tile_total;
+        T p = running + block_exclusive_sum(ts, &tile_total, sw);
+#pragma unroll
+        for (int j = 0; j < SCAN_IPT; ++j) {
+            int64_t i = tb + (int64_t)threadIdx.x * SCAN_IPT + j;
+            if (i < e) emit(i, p, v[j]);
+            p += v[j];
+        }
+        running += tile_total;
+    }
+}
+
+inline int64_t scan_grid(const Ctx& ctx, int64_t n, int64_t tile) {
+    int64_t g = (n + tile - 1) / tile;
+    int64_t cap = (int64_t)ctx.num_sms * 8;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return g;
+}
+
+// Exclusive scan: emit(i, exclusive_prefix, get(i)) for every i in [0, n);
+// *total_dev (device, nullable) = sum of all get(i).
+template <class T, class Get, class Emit>
+int device_scan(Ctx& ctx, int64_t n, Get get, Emit emit, T* total_dev) {
+    if (n <= 0) {
+        if (total_dev) PR_CUDA(cudaMemsetAsync(total_dev, 0, sizeof(T), ctx.stream));
+        return PR_OK;
+    }
+    int64_t G = scan_grid(ctx, n, SCAN_TILE);
+    int64_t per = (n + G - 1) / G;
+    T* partial = nullptr;
+    PR_TRY(dalloc(&partial, (size_t)G, ctx.stream));
+    PR_LAUNCH(ctx, (k_scan_reduce<T, Get>), (unsigned)G, SCAN_NT, 0, get, n, per, partial);
+    PR_LAUNCH(ctx, (k_scan_partials<T>), 1, 1024, 0, partial, G, total_dev);
+    PR_LAUNCH(ctx, (k_scan_down<T, Get, Emit>), (unsigned)G, SCAN_NT, 0, get, emit, n, per,
+              (const T*)partial);
+    dfree(partial, ctx.stream);
+    return PR_OK;
+}
+
+// ------------------------------------------------------------ radix sort --
+constexpr int RS_NT = 256;
+constexpr int RS_WARPS = RS_NT / 32;
+constexpr int RS_ROUNDS = 8;                       // items per thread per tile
+constexpr int RS_TILE = RS_NT * RS_ROUNDS;         // 2048
+constexpr int RS_BITS = 8;
+constexpr int RS_BINS = 1 << RS_BITS;
+
+template <class K>
+__global__ void __launch_bounds__(RS_NT) k_rs_hist(const K* __restrict__ keys, int64_t n, int64_t per_cta,
+                                                   int shift, uint32_t* __restrict__ hist, int64_t G) {
+    __shared__ uint32_t cnt[RS_WARPS][RS_BINS];
+    for (int i = threadIdx.x; i < RS_WARPS * RS_BINS; i += RS_NT) (&cnt[0][0])[i] = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    const int64_t b = (int64_t)blockIdx.x * per_cta;
+    const int64_t e = min(n, b + per_cta);
+    for (int64_t i = b + threadIdx.x; i < e; i += RS_NT) {
+        uint32_t d = (uint32_t)(keys[i] >> shift) & (RS_BINS - 1);
+        atomicAdd(&cnt[warp][d], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < RS_BINS; d += RS_NT) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int w = 0; w < RS_WARPS; ++w) s += cnt[w][d];
+        hist[(int64_t)d * G + blockIdx.x] = s;
+    }
+}
+
+template <class K, bool HAS_V>
+__global__ void __launch_bounds__(RS_NT) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                      K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                      int64_t n, int64_t per_cta, int shift,
+                                                      const uint32_t* __restrict__ offs, int64_t G) {
+    __shared__ uint32_t base[RS_BINS];
+    __shared__ uint32_t wc[RS_WARPS][RS_BINS + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = lanemask_lt();
+    for (int d = threadIdx.x; d < RS_BINS; d += RS_NT) base[d] = offs[(int64_t)d * G + blockIdx.x];
+    const int64_t b = (int64_t)blockIdx.x * per_cta;
+    const int64_t e = min(n, b + per_cta);
+    for (int64_t tb = b; tb < e; tb += RS_TILE) {
+        for (int i = threadIdx.x; i < RS_WARPS * (RS_BINS + 1); i += RS_NT) (&wc[0][0])[i] = 0;
+        __syncthreads();
+        K k[RS_ROUNDS];
+        uint32_t v[RS_ROUNDS];
+        uint32_t dg[RS_ROUNDS];
+        uint32_t pos[RS_ROUNDS];
+        const int64_t s = tb + (int64_t)warp * (32 * RS_ROUNDS);
+#pragma unroll
+        for (int r = 0; r < RS_ROUNDS; ++r) {
+            int64_t i = s + r * 32 + lane;
+            bool valid = i < e;
+            k[r] = valid ? kin[i] : K(0);
+            if (HAS_V) v[r] = valid ? vin[i] : 0u;
+            uint32_t d = valid ? ((uint32_t)(k[r] >> shift) & (RS_BINS - 1)) : RS_BINS;
+            dg[r] = d;
+            uint32_t peers = __match_any_sync(0xffffffffu, d);
+            uint32_t rank = __popc(peers & lt);
+            pos[r] = wc[warp][d] + rank;
+            __syncwarp();
+            if ((peers & lt) == 0) wc[warp][d] += __popc(peers);
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int d = threadIdx.x; d < RS_BINS; d += RS_NT) {
+            uint32_t run = base[d];
+#pragma unroll
+            for (int w = 0; w < RS_WARPS; ++w) {
+                uint32_t c = wc[w][d];
+                wc[w][d] = run;
+                run += c;
+            }
+            base[d] = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < RS_ROUNDS; ++r) {
+            if (dg[r] < RS_BINS) {
+                uint32_t dst = wc[warp][dg[r]] + pos[r];
+                kout[dst] = k[r];
+                if (HAS_V) vout[dst] = v[r];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Stable LSD radix sort of keys[0..n) on bits [begin_bit, end_bit), carrying
+// optional uint32 values.  Uses keys_alt / vals_alt as ping-pong buffers.  On
+// return *in_alt tells which buffer holds the sorted result.
+template <class K, bool HAS_V>
+int radix_sort(Ctx& ctx, K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, int64_t n,
+               int begin_bit, int end_bit, bool* in_alt) {
+    *in_alt = false;
+    if (n <= 1 || end_bit <= begin_bit) return PR_OK;
+    int64_t G = (n + RS_TILE - 1) / RS_TILE;
+    int64_t cap = (int64_t)ctx.num_sms * 4;
+    if (G > cap) G = cap;
+    int64_t per = (n + G - 1) / G;
+    per = (per + RS_TILE - 1) / RS_TILE * RS_TILE;
+    G = (n + per - 1) / per;
+    uint32_t* hist = nullptr;
+    PR_TRY(dalloc(&hist, (size_t)(RS_BINS * G), ctx.stream));
+    K* kin = keys;
+    K* kout = keys_alt;
+    uint32_t* vin = vals;
+    uint32_t* vout = vals_alt;
+    bool alt = false;
+    for (int shift = begin_bit; shift < end_bit; shift += RS_BITS) {
+        PR_LAUNCH(ctx, (k_rs_hist<K>), (unsigned)G, RS_NT, 0, (const K*)kin, n, per, shift, hist, G);
+        PR_LAUNCH(ctx, (k_scan_partials<uint32_t>), 1, 1024, 0, hist, (int64_t)RS_BINS * G,
+                  (uint32_t*)nullptr);
+        PR_LAUNCH(ctx, (k_rs_scatter<K, HAS_V>), (unsigned)G, RS_NT, 0, (const K*)kin,
+                  (const uint32_t*)vin, kout, vout, n, per, shift, (const uint32_t*)hist, G);
+        K* tk = kin; kin = kout; kout = tk;
+        uint32_t* tv = vin; vin = vout; vout = tv;
+        alt = !alt;
+    }
+    dfree(hist, ctx.stream);
+    *in_alt = alt;
+    return PR_OK;
+}
+
+inline int bits_for(uint64_t maxval) {  // number of bits to represent values <= maxval
+    int b = 0;
+    while (b < 64 && (maxval >> b) != 0) ++b;
+    return b;
+}
+
+}  // namespace prgpu

@@ -1,0 +1,75 @@
+"""The C-ABI library loads and exports every symbol include/prgpu.h declares;
+host-side argument validation (no compute, no GPU needed)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "prgpu.h")
+
+
+def _declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(pr_[a-z_]+)\s*\(", txt)))
+
+
+def test_header_declares_the_four_calls():
+    d = _declared()
+    for name in ("pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy"):
+        assert name in d
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2109_09527_b200 as pr
+    out = subprocess.check_output(["nm", "-D", "--defined-only", pr.LIB_PATH]).decode()
+    exported = set(re.findall(r" T (pr_[a-z_]+)$", out, flags=re.M))
+    assert set(_declared()) <= exported
+    assert set(pr.ABI_SYMBOLS) == set(_declared())
+    for s in _declared():
+        assert hasattr(pr.lib, s)
+
+
+def test_library_is_sm100a():
+    import paper_2109_09527_b200 as pr
+    out = subprocess.check_output(["cuobjdump", "--list-elf", pr.LIB_PATH]).decode()
+    assert "sm_100a" in out
+
+
+def test_argument_validation_without_device():
+    import paper_2109_09527_b200 as pr
+    out = ctypes.c_void_p()
+    assert pr.lib.pr_graph_create(0, 0, None, None, None, ctypes.byref(out)) == pr.PR_EINVAL
+    assert "n=0" in pr.last_error()
+    assert pr.lib.pr_graph_create(1 << 31, 0, None, None, None, ctypes.byref(out)) == pr.PR_EINVAL
+    assert pr.lib.pr_graph_create(5, -1, None, None, None, ctypes.byref(out)) == pr.PR_EINVAL
+    assert pr.lib.pr_graph_create(5, 3, None, None, None, ctypes.byref(out)) == pr.PR_EINVAL
+    assert pr.lib.pr_graph_create(5, 0, None, None, None, None) == pr.PR_EINVAL
+    x = np.zeros(4)
+    it = ctypes.c_int32()
+    fd = ctypes.c_double()
+    assert pr.lib.pr_run(None, 0.85, 1e-10, 10, None, 0, x.ctypes.data, ctypes.byref(it), ctypes.byref(fd)) == pr.PR_EINVAL
+    assert pr.lib.pr_preprocess(None, 1, None) == pr.PR_EINVAL
+    pr.lib.pr_destroy(None)   # NULL-safe
+
+
+def test_binding_rejects_wrong_dtypes():
+    import paper_2109_09527_b200 as pr
+    with pytest.raises(TypeError):
+        pr.pr_graph_create(4, np.zeros(3, np.int64), np.zeros(3, np.int64))
+
+
+def test_no_cpu_fallback_in_product_package():
+    """The product package never imports the oracle or the generators."""
+    pkg = os.path.join(ROOT, "paper_2109_09527_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt
+                assert "oracle.c" not in txt and "liboracle" not in txt
+                assert "graphgen" not in txt
