@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py -- PageRank GTEPS/iteration + time-to-converge on R-MAT-24 (BASELINE.json).
+
+One *step* = the whole hot path over one synthetic
+graph already resident in HBM: pr_graph_create (ingest: radix sort, dedup,
+CSR, outdeg, relabel, row-block tasks) -> pr_preprocess (identical groups +
+chains) -> pr_run (sync pull iteration to the L1 threshold with the
+reductions, fused contrib + Delta, member scatter) -> pr_destroy.
+
+value = whole-job GTEPS = sum over ranks and steps of E * iterations / timed
+region (E = deduplicated edges).  Multi-GPU is "replicas only":
+each rank runs its own replica, scaling is weak.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4]
+       python bench.py --impl reference ...   (the CPU fp64 oracle, bounded sample)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PageRank GTEPS/iteration + time-to-converge on R-MAT-24; % of HBM peak"
+UNIT = "GTEPS"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", type=int, default=4, help="BASELINE.json config (1-based); 4 = R-MAT 24")
+    p.add_argument("--mode", choices=["reduced", "plain", "async"], default="reduced")
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def oracle_iters(cfg: int):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "config_iters.json")) as f:
+            rec = json.load(f)[str(cfg)]
+        return int(rec["reduced_iters"]), int(rec["plain_iters"])
+    except Exception:
+        return None, None
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            c = [x.strip() for x in line.split(",")]
+            if len(c) < 9:
+                continue
+            try:
+                sm.append(float(c[1]))
+                mx.append(float(c[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, c[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return ws, rank, local
+
+
+def max_over_ranks(v: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# --------------------------------------------------------------- reference --
+def cpu_sample(gen, iters_whole: int, sweeps: int, warm: int = 0):
+    """Bounded oracle sample: CSR build once + `sweeps` timed Jacobi sweeps on the
+    full graph, extrapolated to a whole job of `iters_whole` iterations."""
+    import oracle
+    t0 = time.perf_counter()
+    c = oracle.build_csr(gen.n, gen.src, gen.dst)
+    t_build = time.perf_counter() - t0
+    if warm:
+        oracle.pagerank(c, gen.d, 0.0, warm)
+    per = []
+    for _ in range(sweeps):
+        r = oracle.pagerank(c, gen.d, 0.0, 1)
+        per.append(r.seconds)
+    t_sweep = statistics.mean(per)
+    t_job = t_build + iters_whole * t_sweep
+    return {"E": c.E, "t_build": t_build, "t_sweep": t_sweep, "t_job": t_job,
+            "value": c.E * iters_whole / t_job / 1e9, "sweeps": sweeps}
+
+
+def run_reference(args, ws, rank):
+    import graphgen
+    if rank != 0:
+        return 0
+    gen = graphgen.make_config(args.config)
+    red_it, plain_it = oracle_iters(args.config)
+    iters = red_it or plain_it or 100
+    s = cpu_sample(gen, iters, sweeps=max(1, args.steps), warm=max(0, min(args.warmup, 1)))
+    sample = (f"oracle (single-threaded C, -O2) CSR build of the full {gen.name} edge list "
+              f"({gen.m} raw edges) timed once ({s['t_build']:.2f} s) + {s['sweeps']} timed Jacobi sweeps "
+              f"({s['t_sweep']:.3f} s each) on the full graph, extrapolated to the oracle's own iteration "
+              f"count for this workload ({iters}, tests/golden/config_iters.json); preprocessing not included")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(s["value"], 5), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(s["t_job"] * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": gen.name, "n": gen.n, "E": s["E"], "tau": gen.tau, "d": gen.d,
+                   "iterations": iters},
+        "cpu_baseline": {"value": round(s["value"], 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(s["value"], 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- ours --
+def main():
+    args = parse()
+    ws, rank, local = dist_init(args)
+    if args.impl == "reference":
+        rc = run_reference(args, ws, rank)
+        barrier(ws)
+        return rc
+    import numpy as np
+    import torch
+
+    import graphgen
+    import paper_2109_09527_b200 as pr
+
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    W = max(3, args.warmup)
+    K = max(1, args.steps)
+
+    gen = graphgen.make_config(args.config)
+    n, m = gen.n, gen.m
+    src_h = torch.from_numpy(gen.src).pin_memory()
+    dst_h = torch.from_numpy(gen.dst).pin_memory()
+    src_d = src_h.to(dev)
+    dst_d = dst_h.to(dev)
+    x_d = torch.empty(n, dtype=torch.float64, device=dev)
+    x_h = torch.empty(n, dtype=torch.float64).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+
+    mode = {"reduced": pr.PR_USE_REDUCTIONS, "plain": 0, "async": pr.PR_MODE_ASYNC}[args.mode]
+    flags = pr.PR_PRE_IDENTICAL | pr.PR_PRE_CHAIN if args.mode == "reduced" else 0
+
+    def step(src, dst, x, timing=True):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        evs[0].record(stream)
+        g = pr.Graph(n, src, dst)
+        evs[1].record(stream)
+        if flags:
+            g.preprocess(flags)
+        evs[2].record(stream)
+        st, it, fd = g.run(x, gen.d, gen.tau, gen.max_iter, mode=mode | (pr.PR_TIMING if timing else 0))
+        evs[3].record(stream)
+        stats = g.stats()
+        info = g.info()
+        g.close()
+        return {"iters": it, "status": st, "delta": fd, "stats": stats, "info": info, "ev": evs}
+
+    for _ in range(W):
+        step(src_d, dst_d, x_d)
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks.start()
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e_start.record(stream)
+    recs = [step(src_d, dst_d, x_d) for _ in range(K)]
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    t_ms = e_start.elapsed_time(e_end)
+    t_max = max_over_ranks(t_ms, ws, dev)
+    E = recs[0]["info"]["E"]
+    edges_iter = sum(E * r["iters"] for r in recs)
+    total_units = sum_over_ranks(float(edges_iter), ws, dev)
+    value = total_units / (t_max * 1e-3) / 1e9
+    phase = {k: statistics.median(r["ev"][i].elapsed_time(r["ev"][i + 1]) for r in recs)
+             for k, i in (("create_ms", 0), ("preprocess_ms", 1), ("run_ms", 2))}
+    st0 = recs[-1]["stats"]
+    launches = sum(r["stats"]["total_launches"] for r in recs)
+    launches = int(sum_over_ranks(float(launches), ws, dev))
+
+    # dominant kernel roofline: the gather launch (CUDA events on the launching stream)
+    hbm_peak, peak_src = load_peaks()
+    g_ms = sum(r["stats"]["gather_ms"] for r in recs) / max(1, sum(r["stats"]["timed_iterations"] for r in recs))
+    rows, edges = st0["gather_rows"], st0["gather_edges"]
+    g_bytes = 12 * edges + 8 * (rows + 1) + 16 * rows          # north_star byte model
+    achieved = g_bytes / (g_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "gather_traffic.json")
+    if os.path.exists(prof):
+        try:
+            pj = json.load(open(prof))
+            key = f"{gen.name}:{args.mode}"
+            if key in pj:
+                traffic = pj[key]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "kernel": f"k_gather ({args.mode})", "bytes_per_launch": g_bytes,
+                "launch_ms": round(g_ms, 5), "peak_source": peak_src,
+                "gteps_per_iteration": round(E / (g_ms * 1e-3) / 1e9, 2) if args.mode == "plain" else
+                round(edges / (g_ms * 1e-3) / 1e9, 2)}
+
+    # plain-mode gather roofline (the north_star 60 % target), one extra untimed run
+    extra = {}
+    if args.mode != "plain":
+        g = pr.Graph(n, src_d, dst_d)
+        g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=pr.PR_TIMING)
+        sp = g.stats()
+        pms = sp["gather_ms"] / max(1, sp["timed_iterations"])
+        pb = 12 * sp["gather_edges"] + 8 * (sp["gather_rows"] + 1) + 16 * sp["gather_rows"]
+        extra["plain_gather"] = {"launch_ms": round(pms, 5), "bytes_per_launch": pb,
+                                 "achieved_GBs": round(pb / (pms * 1e-3) / 1e9, 1),
+                                 "frac": round(pb / (pms * 1e-3) / 1e9 / hbm_peak, 4),
+                                 "gteps_per_iteration": round(E / (pms * 1e-3) / 1e9, 2),
+                                 "iterations": sp["iterations"]}
+        g.close()
+
+    # e2e: the same step through the same ABI calls with HOST (pinned) buffers
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(1):
+            step(src_h, dst_h, x_h, timing=False)
+        torch.cuda.synchronize()
+        barrier(ws)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        er = [step(src_h, dst_h, x_h, timing=False) for _ in range(max(1, args.e2e_steps))]
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier(ws)
+        te = max_over_ranks(a.elapsed_time(b), ws, dev)
+        eu = sum_over_ranks(float(sum(E * r["iters"] for r in er)), ws, dev)
+        e2e = {"value": round(eu / (te * 1e-3) / 1e9, 4), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * m, "d2h_bytes_per_step": 8 * n,
+               "ms_per_step": round(te / len(er), 3)}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        red_it, plain_it = oracle_iters(args.config)
+        iters = (red_it if args.mode == "reduced" else plain_it) or recs[0]["iters"]
+        s = cpu_sample(gen, iters, sweeps=2)
+        cpu = {"value": round(s["value"], 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": (f"oracle CSR build of the full {gen.name} edge list ({s['t_build']:.2f} s) + 2 Jacobi "
+                          f"sweeps on the full graph ({s['t_sweep']:.3f} s each), extrapolated to {iters} "
+                          f"iterations; host cores available: {os.cpu_count()}")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": round(t_max / K, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": gen.name, "n": n, "m_raw": m, "E": E, "d": gen.d, "tau": gen.tau,
+                       "norm": "L1", "mode": args.mode, "iterations": recs[0]["iters"],
+                       "parallelism": f"replicas{ws}", "l2": "inputs larger than L2 (edge list 8m bytes)",
+                       "time_to_converge_ms": round(phase["run_ms"], 3), "create_ms": round(phase["create_ms"], 3),
+                       "preprocess_ms": round(phase["preprocess_ms"], 3),
+                       "n_members": recs[0]["info"]["n_members"]},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    barrier(ws)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

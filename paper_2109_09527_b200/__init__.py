@@ -17,7 +17,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libprgpu.so")
+LIB_PATH = os.environ.get("PRGPU_LIB") or os.path.join(_HERE, "libprgpu.so")
 
 PR_OK = 0
 PR_EINVAL = 1

@@ -189,6 +189,7 @@ void pr_destroy(pr_graph* g) {
     dfree(g->col, s);
     dfree(g->outdeg, s);
     dfree(g->cidx, s);
+    dfree(g->zlist, s);
     free_view(g->plain, s);
     free_view(g->reduced, s);
     dfree(g->rep, s);

@@ -104,6 +104,18 @@ __device__ __forceinline__ double ld_gather_f64(const double* ptr, uint64_t pol)
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
     return r;
 }
+// Branch-free choice between a shared-memory copy (hot contribs) and the
+// global vector: one predicated load each, so the gathers of a round stay
+// independent (a C++ branch here serialises them).
+__device__ __forceinline__ double ld_hot_or_gather_f64(const double* gptr, uint32_t saddr, int hot, uint64_t pol) {
+    double r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %4, 0;\n\t"
+        "@p ld.shared.f64 %0, [%1];\n\t"
+        "@!p ld.global.nc.L2::cache_hint.f64 %0, [%2], %3;\n\t}"
+        : "=d"(r)
+        : "r"(saddr), "l"(gptr), "l"(pol), "r"(hot));
+    return r;
+}
 // Async (No-Sync) mode: the contrib vector is read and written in the same
 // launch, so loads/stores are relaxed gpu-scope atomics (never .nc).
 __device__ __forceinline__ double ld_relaxed_f64(const double* ptr) {

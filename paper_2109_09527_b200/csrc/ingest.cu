@@ -207,6 +207,37 @@ __global__ void k_map_col(const int32_t* __restrict__ col, int64_t E, const int3
         out[e] = cidx[col[e]];
 }
 
+struct ZeroInGet {
+    const int64_t* rp;
+    __device__ int64_t operator()(int64_t v) const { return rp[v + 1] == rp[v] ? 1 : 0; }
+};
+struct NonZeroInGet {
+    const int64_t* rp;
+    __device__ int64_t operator()(int64_t v) const { return rp[v + 1] != rp[v] ? 1 : 0; }
+};
+struct VListEmit {
+    int32_t* list;
+    __device__ void operator()(int64_t v, int64_t pos, int64_t f) const {
+        if (f) list[pos] = (int32_t)v;
+    }
+};
+// rows of in-degree > 0: vid[i] = v, row_ptr_view[i] = row_ptr[v]; the last
+// vertex also closes the view with row_ptr_view[nrows] = row_ptr[n] = E.
+struct NonZeroEmit {
+    const int64_t* rp;
+    int32_t* vid;
+    int64_t* rpv;
+    int64_t n;
+    int64_t nrows;
+    __device__ void operator()(int64_t v, int64_t pos, int64_t f) const {
+        if (f) {
+            vid[pos] = (int32_t)v;
+            rpv[pos] = rp[v];
+        }
+        if (v == n - 1) rpv[nrows] = rp[n];
+    }
+};
+
 int build_relabel(pr_graph* g, Ctx& ctx) {
     cudaStream_t s = ctx.stream;
     const int64_t n = g->n;
@@ -242,13 +273,25 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
     if (cnt > 0)
         PR_LAUNCH(ctx, k_set_cidx, grid_for(ctx, cnt, 256), 256, 0, sorted, cnt,
                   b ? ((1ull << b) - 1) : 0ull, g->cidx);
-    // plain view: all rows, relabelled sources
+    // zero in-degree vertices (written once, in sweep 1) and the plain view:
+    // the rows of in-degree > 0 (identity view when there are no empty rows)
     View& v = g->plain;
-    v.nrows = n;
+    PR_TRY(dalloc(&g->zlist, (size_t)n, s));
+    PR_TRY((device_scan<int64_t>(ctx, n, ZeroInGet{g->row_ptr}, VListEmit{g->zlist}, scratch)));
+    PR_TRY(read_count(ctx, scratch, &g->nz));
     v.nedges = g->E;
-    v.row_ptr = g->row_ptr;
     v.owns_row_ptr = false;
     v.vid = nullptr;
+    v.row_ptr = g->row_ptr;
+    v.nrows = n;
+    if (g->nz > 0) {
+        v.nrows = n - g->nz;
+        PR_TRY(dalloc(&v.vid, (size_t)(v.nrows > 0 ? v.nrows : 1), s));
+        PR_TRY(dalloc(&v.row_ptr, (size_t)v.nrows + 1, s));
+        v.owns_row_ptr = true;
+        PR_TRY((device_scan<int64_t>(ctx, n, NonZeroInGet{g->row_ptr},
+                                     NonZeroEmit{g->row_ptr, v.vid, v.row_ptr, n, v.nrows}, scratch)));
+    }
     PR_TRY(dalloc(&v.col, (size_t)(g->E > 0 ? g->E : 1), s));
     if (g->E > 0)
         PR_LAUNCH(ctx, k_map_col, grid_for(ctx, g->E, 256), 256, 0, (const int32_t*)g->col, g->E,
@@ -260,15 +303,16 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
 }
 
 // ------------------------------------------------------------ view tasks --
-// Row blocks: a non-hub row r starts a block iff r == 0, r-1 is a hub, or the
-// running weight P(r) (edges + ROW_W per row, hubs weigh 0) crosses a multiple
-// of CAP.  Hence a block holds < CAP/ROW_W + 1 rows and < CAP + LONG edges.
-// Hub rows (in-degree > LONG) become ceil(deg / HUB_CHUNK) chunk tasks.
+// Row blocks: a row r of in-degree <= WT_LONG starts a block iff r == 0, r-1
+// is a long row, or the running weight P(r) (edges + ROW_W per row; long rows
+// weigh 0) crosses a multiple of WT_CAP.  Hence a block has < WT_CAP/ROW_W + 1
+// rows and < WT_CAP + WT_LONG edges.  A long row (in-degree > WT_LONG) becomes
+// ceil(deg / WT_HCH) chunk tasks; rows with several chunks get a Hub record.
 struct WGet {
     const int64_t* rp;
     __device__ int64_t operator()(int64_t r) const {
         int64_t d = rp[r + 1] - rp[r];
-        return d > GT_LONG ? 0 : d + GT_ROW_W;
+        return d > WT_LONG ? 0 : d + WT_ROW_W;
     }
 };
 struct WEmit {
@@ -278,10 +322,10 @@ struct WEmit {
 struct StartGet {
     const int64_t* rp;
     const int64_t* P;
-    __device__ bool is_long(int64_t r) const { return rp[r + 1] - rp[r] > GT_LONG; }
+    __device__ bool is_long(int64_t r) const { return rp[r + 1] - rp[r] > WT_LONG; }
     __device__ int64_t operator()(int64_t r) const {
         if (r == 0 || is_long(r) || is_long(r - 1)) return 1;
-        return (P[r] / GT_CAP) != (P[r - 1] / GT_CAP) ? 1 : 0;
+        return (P[r] / WT_CAP) != (P[r - 1] / WT_CAP) ? 1 : 0;
     }
 };
 struct StartEmit {
@@ -290,14 +334,17 @@ struct StartEmit {
         if (f) starts[pos] = r;
     }
 };
-// per start: low 40 bits = number of tasks, high bits = 1 if hub
+// per start: low 40 bits = number of tasks, high bits = 1 if the row needs a Hub record
 struct TaskCountGet {
     const int64_t* rp;
     const int64_t* starts;
     __device__ int64_t operator()(int64_t i) const {
         int64_t r = starts[i];
         int64_t d = rp[r + 1] - rp[r];
-        if (d > GT_LONG) return ((d + GT_HUB_CHUNK - 1) / GT_HUB_CHUNK) | (1ll << 40);
+        if (d > WT_LONG) {
+            int64_t nch = (d + WT_HCH - 1) / WT_HCH;
+            return nch | (nch > 1 ? (1ll << 40) : 0ll);
+        }
         return 1;
     }
 };
@@ -309,18 +356,24 @@ struct TaskFillEmit {
     Task* tasks;
     Hub* hubs;
     __device__ void operator()(int64_t i, int64_t pos, int64_t v) const {
-        int64_t r = starts[i];
-        int64_t toff = pos & ((1ll << 40) - 1);
-        int64_t hid = pos >> 40;
-        if (v >> 40) {
-            int32_t nch = (int32_t)(v & ((1ll << 40) - 1));
-            hubs[hid].nchunks = nch;
-            hubs[hid].pad = 0;
-            hubs[hid].slot = toff;
-            for (int32_t j = 0; j < nch; ++j) tasks[toff + j] = Task{r, j, (int32_t)hid};
+        const int64_t r = starts[i];
+        const int64_t toff = pos & ((1ll << 40) - 1);
+        const int64_t hid = pos >> 40;
+        const int64_t rs = rp[r], d = rp[r + 1] - rs;
+        if (d > WT_LONG) {
+            const int32_t nch = (int32_t)(v & ((1ll << 40) - 1));
+            const bool hub = nch > 1;
+            if (hub) hubs[hid] = Hub{(int32_t)rs, nch, (int32_t)toff, 0};
+            for (int32_t j = 0; j < nch; ++j) {
+                const int64_t e0 = rs + (int64_t)j * WT_HCH;
+                const int64_t nnz = min((int64_t)WT_HCH, d - (int64_t)j * WT_HCH);
+                tasks[toff + j] = Task{(int32_t)e0, (int32_t)r, (int32_t)(0x80000000u | (uint32_t)nnz),
+                                       hub ? (int32_t)hid : -1};
+            }
         } else {
-            int64_t rend = i + 1 < nstarts ? starts[i + 1] : nrows;
-            tasks[toff] = Task{r, (int32_t)(rend - r), -1};
+            const int64_t rend = i + 1 < nstarts ? starts[i + 1] : nrows;
+            const int64_t nnz = rp[rend] - rs;
+            tasks[toff] = Task{(int32_t)rs, (int32_t)r, (int32_t)(((rend - r) << 16) | nnz), -1};
         }
     }
 };
@@ -354,8 +407,8 @@ int build_view_tasks(View& v, Ctx& ctx) {
     int64_t nstarts = 0;
     PR_TRY(read_count(ctx, scratch, &nstarts));
     // upper bound on tasks: nstarts + sum over hubs of chunks <= nstarts + E / HUB_CHUNK + 1
-    int64_t cap_tasks = nstarts + v.nedges / GT_HUB_CHUNK + 1;
-    int64_t cap_hubs = v.nedges / (GT_LONG + 1) + 1;
+    int64_t cap_tasks = nstarts + v.nedges / WT_HCH + 1;
+    int64_t cap_hubs = v.nedges / (WT_HCH + 1) + 1;
     PR_TRY(dalloc(&v.tasks, (size_t)cap_tasks, s));
     PR_TRY(dalloc(&v.hubs, (size_t)cap_hubs, s));
     PR_TRY((device_scan<int64_t>(ctx, nstarts, TaskCountGet{v.row_ptr, starts},

@@ -4,29 +4,48 @@
 
 namespace prgpu {
 
-// Row-block engine tuning.
-constexpr int GT_NT = 256;                 // threads per CTA
-constexpr int GT_CAP = 2048;               // weight budget per row block (edges + ROW_W*rows)
-constexpr int GT_ROW_W = 4;                // per-row weight in edge units
-constexpr int GT_LONG = 1024;              // rows with in-degree > LONG become hub tasks
-constexpr int GT_MAXROWS = GT_CAP / GT_ROW_W + 1;
-constexpr int GT_VALS = GT_CAP + GT_LONG + 8;
-constexpr int GT_HUB_CHUNK = 8192;         // edges per hub-chunk task
-constexpr int GT_MIN_CTAS = 4;           // __launch_bounds__ min CTAs/SM of the gather (<= 64 regs)
-constexpr int GT_SHORT = 32;               // rows up to this length: one thread sums serially
+// Warp-task engine tuning (see rowengine.cuh and DESIGN.md "K-GATHER").
+#ifndef PRGPU_NT
+#define PRGPU_NT 256
+#endif
+#ifndef PRGPU_MIN_CTAS
+#define PRGPU_MIN_CTAS 4
+#endif
+#ifndef PRGPU_HOT
+#define PRGPU_HOT 0
+#endif
+constexpr int GT_NT = PRGPU_NT;            // threads per CTA (independent warps)
+constexpr int GT_HOT_DEFAULT = PRGPU_HOT;  // max contribs staged in shared memory (0: off)
+constexpr int GT_MIN_CTAS = PRGPU_MIN_CTAS;  // __launch_bounds__ min CTAs/SM of the gather
+constexpr int WT_CAP = 384;                // weight budget per row-block task (edges + ROW_W*rows)
+constexpr int WT_ROW_W = 8;                // per-row weight in edge units
+constexpr int WT_LONG = 128;               // rows with in-degree > LONG become long-row tasks
+constexpr int WT_HCH = 4096;               // edges per long-row chunk task
+constexpr int WT_SHORT = 16;               // rows up to this length: one lane sums serially
+#ifndef PRGPU_WT_U
+#define PRGPU_WT_U 2
+#endif
+constexpr int WT_U = PRGPU_WT_U;           // int4 col loads per lane per round (4*U gathers)
+constexpr int WT_MAXE = WT_CAP + WT_LONG;  // a row block holds < MAXE edges
+constexpr int WT_MAXROWS = WT_CAP / WT_ROW_W + 1;
+constexpr int WT_VALS = WT_MAXE;
 
-// A unit of work for one CTA.  b < 0: row block of rows [r0, r0 + a).
-// b >= 0: chunk a of hub b (the single row r0).
+// A unit of work for one warp (16 bytes).
+//   info >= 0: row block, rows [r0, r0 + (info >> 16)), edges [e0, e0 + (info & 0xffff)).
+//   info <  0: chunk of one long row r0, edges [e0, e0 + (info & 0xffff));
+//              hub = index into View::hubs if the row has several chunks, else -1.
 struct Task {
-    int64_t r0;
-    int32_t a;
-    int32_t b;
+    int32_t e0;
+    int32_t r0;
+    int32_t info;
+    int32_t hub;
 };
 
 struct Hub {
+    int32_t row_e0;   // first edge of the row
     int32_t nchunks;
+    int32_t slot;     // first partial slot of this hub in View::hub_partial
     int32_t pad;
-    int64_t slot;  // first partial slot of this hub in View::hub_partial
 };
 
 // A set of rows over which the gather runs: all vertices (plain) or the
@@ -78,6 +97,10 @@ struct pr_graph {
     // contrib relabelling: cidx[v] in [0, n_contrib) for outdeg(v) > 0, else -1
     int32_t* cidx = nullptr;
     int64_t n_contrib = 0;
+    // vertices of in-degree 0: x_t = (1-d)/n for every t >= 1 exactly, so they
+    // are written once, in the first sweep, and excluded from the gather views
+    int32_t* zlist = nullptr;
+    int64_t nz = 0;
     prgpu::View plain;
     // reductions
     bool pre_done = false;

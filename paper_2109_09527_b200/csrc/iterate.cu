@@ -15,7 +15,11 @@
 namespace prgpu {
 
 // ----------------------------------------------------------------- policy --
-template <bool ASYNC, bool VID>
+// ASYNC: No-Sync in-place sweep (relaxed loads/stores of one contrib buffer).
+// VID:   rows of the view are vid[r] (else row r is vertex r).
+// HOT:   contribs with index < nhot (the highest out-degrees, DESIGN.md "Data
+//        layout") are read from a shared-memory copy staged at kernel start.
+template <bool ASYNC, bool VID, bool HOT>
 struct PRPolicy {
     using T = double;
     const double* y_in;
@@ -26,6 +30,9 @@ struct PRPolicy {
     const int32_t* vid;
     double c, d;
     uint64_t pol_first, pol_last;
+    const double* hot;
+    int32_t nhot;
+    uint32_t hot_s;  // shared-state-space address of hot[0]
 
     __device__ __forceinline__ void begin() {
         pol_first = policy_evict_first();
@@ -34,31 +41,44 @@ struct PRPolicy {
     __device__ __forceinline__ int4 ld_col(const int4* p) const { return ld_stream_i4(p, pol_first); }
     __device__ __forceinline__ double load(int32_t u) const {
         if (ASYNC) return ld_relaxed_f64(y_in + u);
+        if (HOT) return ld_hot_or_gather_f64(y_in + u, hot_s + 8u * (uint32_t)u, u < nhot, pol_last);
         return ld_gather_f64(y_in + u, pol_last);
     }
+    struct Pre {
+        double xo;
+        int32_t v, od, ci, pad;
+    };
+    // finalize operands, loaded before the row's gathers complete
+    __device__ __forceinline__ Pre prefetch(int64_t r) const {
+        Pre q;
+        q.v = VID ? vid[r] : (int32_t)r;
+        q.xo = x[q.v];
+        q.od = od[q.v];
+        q.ci = cidx[q.v];
+        q.pad = 0;
+        return q;
+    }
     // x_t(v) = c + d*S, fused contrib y_t(v) = x_t(v)/outdeg(v), returns |x_t(v) - x_{t-1}(v)|.
-    __device__ __forceinline__ double finalize(int64_t r, double s) const {
-        const int32_t v = VID ? vid[r] : (int32_t)r;
+    __device__ __forceinline__ double finalize(const Pre& q, double s) const {
         const double xn = __dadd_rn(c, __dmul_rn(d, s));
-        const double xo = x[v];
-        x[v] = xn;
-        const int32_t o = od[v];
-        if (o > 0) {
-            const double y = xn / (double)o;
+        x[q.v] = xn;
+        if (q.od > 0) {
+            const double y = xn / (double)q.od;
             if (ASYNC)
-                st_relaxed_f64(y_out + cidx[v], y);
+                st_relaxed_f64(y_out + q.ci, y);
             else
-                y_out[cidx[v]] = y;
+                y_out[q.ci] = y;
         }
-        return fabs(xn - xo);
+        return fabs(xn - q.xo);
     }
 };
 
 struct IterArgs {
     DevState* st;
-    double* cta_partial;        // (L1, Linf) per CTA: gather CTAs first, then scatter CTAs
+    double* cta_partial;        // (L1, Linf) per CTA: gather CTAs, scatter CTAs, zero-in CTAs
     int64_t gather_ctas;
     int64_t scatter_ctas;
+    int64_t zero_ctas;          // > 0 only in the first sweep
     const double* hub_delta;    // of the gather view
     int64_t nhubs;
     double* delta_log;
@@ -70,7 +90,7 @@ __device__ void global_finalize(const IterArgs& ia, double* red) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __threadfence();
     double s = 0.0, mx = 0.0;
-    const int64_t nc = ia.gather_ctas + ia.scatter_ctas;
+    const int64_t nc = ia.gather_ctas + ia.scatter_ctas + ia.zero_ctas;
     for (int64_t i = tid; i < nc; i += GT_NT) {
         s += __ldcg(ia.cta_partial + 2 * i);
         mx = fmax(mx, __ldcg(ia.cta_partial + 2 * i + 1));
@@ -140,10 +160,21 @@ __device__ __forceinline__ void block_delta(double l1, double linf, double* red,
     }
 }
 
-template <bool ASYNC, bool VID>
-__global__ void __launch_bounds__(GT_NT, GT_MIN_CTAS) k_gather(PRPolicy<ASYNC, VID> p, EngineArgs a, IterArgs ia, int finalize) {
-    __shared__ EngineSmem sm;
+template <bool ASYNC, bool VID, bool HOT>
+__global__ void __launch_bounds__(GT_NT, GT_MIN_CTAS)
+    k_gather(PRPolicy<ASYNC, VID, HOT> p, EngineArgs a, IterArgs ia, int finalize) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
     if (ia.st->done) return;
+    if (HOT) {  // stage the hottest contribs (cidx < nhot) of y_{t-1} in shared memory
+        double* hot = reinterpret_cast<double*>(smem_raw + sizeof(EngineSmem));
+        const double2* src = reinterpret_cast<const double2*>(p.y_in);
+        double2* dst = reinterpret_cast<double2*>(hot);
+        for (int i = threadIdx.x; i < p.nhot / 2; i += GT_NT) dst[i] = __ldg(src + i);
+        p.hot = hot;
+        p.hot_s = (uint32_t)__cvta_generic_to_shared(hot);
+        __syncthreads();
+    }
     p.begin();
     double l1 = 0.0, linf = 0.0;
     engine_run(p, a, sm, l1, linf);
@@ -202,6 +233,41 @@ __global__ void __launch_bounds__(GT_NT) k_scatter(const int32_t* __restrict__ m
     if (flag) global_finalize(ia, red);
 }
 
+// First sweep for the vertices of in-degree 0: Eq.(1) with an empty sum gives
+// x_t = (1-d)/n = c for every t >= 1, so they are written here once (x and
+// the contrib slot of y_out) and contribute |c - 1/n| to Delta_1 only; from
+// sweep 2 on their Delta is exactly 0 and no kernel touches them.
+__global__ void __launch_bounds__(GT_NT) k_zero(const int32_t* __restrict__ zl, int64_t nz, int64_t per_cta, double c,
+                                                double* x, double* y_out, const int32_t* __restrict__ od,
+                                                const int32_t* __restrict__ cidx, double* partial) {
+    __shared__ double red[2 * GT_WARPS];
+    const int64_t b = (int64_t)blockIdx.x * per_cta;
+    const int64_t e = min(nz, b + per_cta);
+    double l1 = 0.0, linf = 0.0;
+    for (int64_t i = b + threadIdx.x; i < e; i += GT_NT) {
+        const int32_t v = zl[i];
+        const double xo = x[v];
+        x[v] = c;
+        const int32_t o = od[v];
+        if (o > 0) y_out[cidx[v]] = c / (double)o;
+        const double dl = fabs(c - xo);
+        l1 += dl;
+        linf = fmax(linf, dl);
+    }
+    block_delta(l1, linf, red, partial + 2 * blockIdx.x);
+}
+
+// Sync mode: after sweep 1 also store the constant contribs of the in-degree-0
+// vertices into the other ping-pong buffer (read by sweep 3, 5, ...).
+__global__ void k_zero_y(const int32_t* __restrict__ zl, int64_t nz, double c, double* y,
+                         const int32_t* __restrict__ od, const int32_t* __restrict__ cidx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = zl[i];
+        const int32_t o = od[v];
+        if (o > 0) y[cidx[v]] = c / (double)o;
+    }
+}
+
 // x_0 = 1/n (Alg.1), y_0 = x_0/outdeg for sources.
 __global__ void k_init(double* __restrict__ x, double* __restrict__ y, const int32_t* __restrict__ od,
                        const int32_t* __restrict__ cidx, int64_t n, double x0) {
@@ -213,28 +279,76 @@ __global__ void k_init(double* __restrict__ x, double* __restrict__ y, const int
 }
 
 // ------------------------------------------------------------------- host --
-static int gather_grid(const Ctx& ctx, int64_t ntasks, const void* kernel) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, GT_NT, 0);
-    if (per_sm < 1) per_sm = 1;
-    int64_t g = (int64_t)ctx.num_sms * per_sm;
-    if (g > ntasks) g = ntasks;
-    if (g < 1) g = 1;
-    return (int)g;
-}
 
-template <bool ASYNC, bool VID>
-static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
-                         double c, double d, const IterArgs& ia, int grid, int finalize) {
-    PRPolicy<ASYNC, VID> p{y_in, y_out, x, g->outdeg, g->cidx, v.vid, c, d, 0, 0};
+struct GatherCfg {
+    bool async, vid, hot;
+    int nhot;
+    size_t smem;
+    int grid;
+};
+
+template <bool ASYNC, bool VID, bool HOT>
+static int launch_gather_t(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
+                           double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
+    PRPolicy<ASYNC, VID, HOT> p{y_in, y_out, x, g->outdeg, g->cidx, v.vid, c, d, 0, 0, nullptr, gc.nhot, 0u};
     EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, v.col, v.hub_partial, v.hub_delta, v.hub_ticket};
-    PR_LAUNCH(ctx, (k_gather<ASYNC, VID>), grid, GT_NT, 0, p, a, ia, finalize);
+    PR_LAUNCH(ctx, (k_gather<ASYNC, VID, HOT>), gc.grid, GT_NT, gc.smem, p, a, ia, finalize);
     return PR_OK;
 }
 
-static const void* gather_fn(bool async, bool vid) {
-    if (async) return vid ? (const void*)k_gather<true, true> : (const void*)k_gather<true, false>;
-    return vid ? (const void*)k_gather<false, true> : (const void*)k_gather<false, false>;
+static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
+                         double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
+    if (gc.async)
+        return gc.vid ? launch_gather_t<true, true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
+                      : launch_gather_t<true, false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
+    if (gc.hot)
+        return gc.vid ? launch_gather_t<false, true, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
+                      : launch_gather_t<false, false, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
+    return gc.vid ? launch_gather_t<false, true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
+                  : launch_gather_t<false, false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
+}
+
+static const void* gather_fn(const GatherCfg& gc) {
+    if (gc.async) return gc.vid ? (const void*)k_gather<true, true, false> : (const void*)k_gather<true, false, false>;
+    if (gc.hot) return gc.vid ? (const void*)k_gather<false, true, true> : (const void*)k_gather<false, false, true>;
+    return gc.vid ? (const void*)k_gather<false, true, false> : (const void*)k_gather<false, false, false>;
+}
+
+// Kernel variant, hot-cache size, dynamic shared memory and persistent grid.
+// The hot cache takes whatever shared memory the engine leaves (sync mode
+// only: in async mode the contribs change during the sweep).
+static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, GatherCfg* gc) {
+    gc->async = async;
+    gc->vid = v.vid != nullptr;
+    gc->hot = false;
+    gc->nhot = 0;
+    gc->smem = sizeof(EngineSmem);
+    const char* e = getenv("PRGPU_HOT");
+    int64_t hot_cap = e ? atoll(e) : (int64_t)GT_HOT_DEFAULT;
+    if (!async && hot_cap > 0 && g->n_contrib >= 1024) {
+        int dev = 0, optin = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        int64_t room = ((int64_t)optin - (int64_t)sizeof(EngineSmem) - 1024) / 8;
+        int64_t h = std::min<int64_t>(std::min<int64_t>(room, hot_cap), g->n_contrib);
+        h &= ~(int64_t)31;
+        if (h >= 1024) {
+            gc->hot = true;
+            gc->nhot = (int)h;
+            gc->smem = sizeof(EngineSmem) + (size_t)h * sizeof(double);
+        }
+    }
+    const void* fn = gather_fn(*gc);
+    PR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gc->smem));
+    int per_sm = 0;
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GT_NT, gc->smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)ctx.num_sms * per_sm;
+    int64_t warps_needed = (v.ntasks + GT_WARPS - 1) / GT_WARPS;
+    if (grid > warps_needed) grid = warps_needed;
+    if (grid < 1) grid = 1;
+    gc->grid = (int)grid;
+    return PR_OK;
 }
 
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
@@ -262,12 +376,18 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     if (!g->y[0]) PR_TRY(dalloc(&g->y[0], (size_t)ny, s));
     if (!g->y[1]) PR_TRY(dalloc(&g->y[1], (size_t)ny, s));
 
-    const int ggrid = gather_grid(ctx, v.ntasks, gather_fn(async, v.vid != nullptr));
+    GatherCfg gc;
+    PR_TRY(gather_config(ctx, v, g, async, &gc));
+    const int ggrid = gc.grid;
     const int64_t sgrid_cap = (int64_t)ctx.num_sms * 4;
     int64_t sgrid = nm > 0 ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
     if (sgrid > sgrid_cap) sgrid = sgrid_cap;
     const int64_t sper = sgrid > 0 ? (nm + sgrid - 1) / sgrid : 0;
-    const int64_t need = 2 * ((int64_t)ggrid + sgrid);
+    const int64_t nz = g->nz;
+    int64_t zgrid = nz > 0 ? (nz + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
+    if (zgrid > sgrid_cap) zgrid = sgrid_cap;
+    const int64_t zper = zgrid > 0 ? (nz + zgrid - 1) / zgrid : 0;
+    const int64_t need = 2 * ((int64_t)ggrid + sgrid + zgrid);
     if (g->partial_cap < need) {
         dfree(g->cta_partial, s);
         PR_TRY(dalloc(&g->cta_partial, (size_t)need, s));
@@ -302,7 +422,11 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     PR_LAUNCH(ctx, k_init, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, x,
               g->y[0], (const int32_t*)g->outdeg, (const int32_t*)g->cidx, n, 1.0 / (double)n);
 
-    IterArgs ia{g->st, g->cta_partial, (int64_t)ggrid, reduced ? sgrid : 0, v.hub_delta, v.nhubs, g->delta_log};
+    const int64_t sctas = reduced ? sgrid : 0;
+    IterArgs ia_rest{g->st, g->cta_partial, (int64_t)ggrid, sctas, 0, v.hub_delta, v.nhubs, g->delta_log};
+    IterArgs ia_first = ia_rest;
+    ia_first.zero_ctas = zgrid;
+    double* zero_partial = g->cta_partial + 2 * ((int64_t)ggrid + sctas);
     const bool gather_finalizes = !(reduced && sgrid > 0);
 
     std::vector<cudaEvent_t> ev;
@@ -323,15 +447,14 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
             const int64_t it = launched + j;
             const double* y_in = async ? g->y[0] : g->y[it & 1];
             double* y_out = async ? g->y[0] : g->y[(it + 1) & 1];
+            const IterArgs& ia = it == 0 ? ia_first : ia_rest;
+            if (it == 0 && zgrid > 0)
+                PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y_out,
+                          (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
             {
                 int rc;
-                if (async)
-                    rc = v.vid ? launch_gather<true, true>(ctx, v, y_in, y_out, x, g, c, d, ia, ggrid, gather_finalizes)
-                               : launch_gather<true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, ggrid, gather_finalizes);
-                else
-                    rc = v.vid ? launch_gather<false, true>(ctx, v, y_in, y_out, x, g, c, d, ia, ggrid, gather_finalizes)
-                               : launch_gather<false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, ggrid, gather_finalizes);
+                rc = launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, gather_finalizes);
                 if (rc != PR_OK) return rc;
             }
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
@@ -346,6 +469,10 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                               y_out, (const int32_t*)g->outdeg, (const int32_t*)g->cidx, ia);
             }
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
+            if (it == 0 && nz > 0 && !async)
+                PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256,
+                          0, (const int32_t*)g->zlist, nz, c, (double*)y_in, (const int32_t*)g->outdeg,
+                          (const int32_t*)g->cidx);
         }
         PR_CUDA(cudaMemcpyAsync(hs, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
         PR_CUDA(cudaStreamSynchronize(s));

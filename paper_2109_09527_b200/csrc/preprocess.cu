@@ -18,23 +18,41 @@
 namespace prgpu {
 
 // ---------------------------------------------------------------- hashing --
+constexpr uint64_t kDegSalt = 0xD6E8FEB86659FD93ULL;
+
 struct HashPolicy {
     using T = uint64_t;
-    const int64_t* rp;
+    const int64_t* rp;   // canonical row_ptr (by vertex id)
+    const int32_t* vid;  // view rows -> vertex ids (nullptr: identity)
     uint64_t* out;
     __device__ __forceinline__ void begin() {}
     __device__ __forceinline__ int4 ld_col(const int4* p) const { return __ldg(p); }
     __device__ __forceinline__ uint64_t load(int32_t u) const {
         return mix64((uint64_t)(uint32_t)u * 0x9E3779B97F4A7C15ULL + 0x2545F4914F6CDD1DULL);
     }
-    __device__ __forceinline__ double finalize(int64_t r, uint64_t s) const {
-        out[r] = s + mix64((uint64_t)(rp[r + 1] - rp[r]) + 0xD6E8FEB86659FD93ULL);
+    struct Pre {
+        int64_t v, deg;
+    };
+    __device__ __forceinline__ Pre prefetch(int64_t r) const {
+        const int64_t v = vid ? vid[r] : r;
+        return Pre{v, rp[v + 1] - rp[v]};
+    }
+    __device__ __forceinline__ double finalize(const Pre& q, uint64_t s) const {
+        out[q.v] = s + mix64((uint64_t)q.deg + kDegSalt);
         return 0.0;
     }
 };
 
+// Hash of the empty in-set, for the rows the plain view leaves out.
+__global__ void k_hash_empty(uint64_t* __restrict__ h, int64_t n) {
+    const uint64_t e = mix64(kDegSalt);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        h[i] = e;
+}
+
 __global__ void __launch_bounds__(GT_NT) k_rowhash(HashPolicy p, EngineArgs a) {
-    __shared__ EngineSmem sm;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
     double l1 = 0.0, linf = 0.0;
     engine_run(p, a, sm, l1, linf);
 }
@@ -151,10 +169,15 @@ __global__ void k_chain_finish(const int32_t* __restrict__ cl, int64_t C, const 
 }
 
 // ------------------------------------------------------- members / R view --
+// In-degree-0 vertices are excluded from both lists: they are written once,
+// in the first sweep (g->zlist), and are constant afterwards.
 struct MemberGet {
     const int32_t* rep;
     const int32_t* ck;
-    __device__ int64_t operator()(int64_t v) const { return (rep[v] != (int32_t)v || ck[v] > 0) ? 1 : 0; }
+    const int64_t* rp;
+    __device__ int64_t operator()(int64_t v) const {
+        return (rp[v + 1] > rp[v] && (rep[v] != (int32_t)v || ck[v] > 0)) ? 1 : 0;
+    }
 };
 struct MemberEmit {
     const int32_t* rep;
@@ -178,7 +201,10 @@ struct MemberEmit {
 struct ComputedGet {
     const int32_t* rep;
     const int32_t* ck;
-    __device__ int64_t operator()(int64_t v) const { return (rep[v] == (int32_t)v && ck[v] == 0) ? 1 : 0; }
+    const int64_t* rp;
+    __device__ int64_t operator()(int64_t v) const {
+        return (rp[v + 1] > rp[v] && rep[v] == (int32_t)v && ck[v] == 0) ? 1 : 0;
+    }
 };
 struct DegGet {
     const int64_t* rp;
@@ -242,14 +268,16 @@ static int find_identical(pr_graph* g, Ctx& ctx) {
     PR_TRY(dalloc(&sv2, (size_t)n, s));
     const View& v = g->plain;
     {
-        HashPolicy p{g->row_ptr, h};
+        if (v.vid) PR_LAUNCH(ctx, k_hash_empty, grid_of(ctx, n), 256, 0, h, n);
+        HashPolicy p{g->row_ptr, v.vid, h};
         EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, g->col, v.hub_partial, v.hub_delta, v.hub_ticket};
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowhash, GT_NT, 0);
+        cudaFuncSetAttribute(k_rowhash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EngineSmem));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowhash, GT_NT, sizeof(EngineSmem));
         int64_t grid = (int64_t)ctx.num_sms * (per_sm > 0 ? per_sm : 1);
         if (grid > v.ntasks) grid = v.ntasks;
         if (grid < 1) grid = 1;
-        PR_LAUNCH(ctx, k_rowhash, (unsigned)grid, GT_NT, 0, p, a);
+        PR_LAUNCH(ctx, k_rowhash, (unsigned)grid, GT_NT, sizeof(EngineSmem), p, a);
     }
     PR_LAUNCH(ctx, k_iota, grid_of(ctx, n), 256, 0, sv, n);
     bool alt = false;
@@ -347,11 +375,11 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
     PR_TRY(dalloc(&g->mem_vid, (size_t)n, s));
     PR_TRY(dalloc(&g->mem_src, (size_t)n, s));
     PR_TRY(dalloc(&g->mem_k, (size_t)n, s));
-    PR_TRY((device_scan<int64_t>(ctx, n, MemberGet{g->rep, g->chain_k},
+    PR_TRY((device_scan<int64_t>(ctx, n, MemberGet{g->rep, g->chain_k, g->row_ptr},
                                  MemberEmit{g->rep, g->chain_src, g->chain_k, g->mem_vid, g->mem_src, g->mem_k}, cnt)));
     View& R = g->reduced;
     PR_TRY(dalloc(&R.vid, (size_t)n, s));
-    PR_TRY((device_scan<int64_t>(ctx, n, ComputedGet{g->rep, g->chain_k}, ListEmit{R.vid}, cnt + 1)));
+    PR_TRY((device_scan<int64_t>(ctx, n, ComputedGet{g->rep, g->chain_k, g->row_ptr}, ListEmit{R.vid}, cnt + 1)));
     int64_t h[3];
     PR_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
     PR_CUDA(cudaStreamSynchronize(s));

@@ -1,29 +1,30 @@
-// rowengine.cuh -- the degree-aware row-block engine behind K-GATHER (and the
-// row-hash step of identical-group detection).
+// rowengine.cuh -- the degree-aware, warp-independent row engine behind
+// K-GATHER (and the row-hash step of identical-group detection).
 //
 // For every row r of a View it computes  S(r) = sum_{e in row r} load(col[e])
-// and calls  finalize(r, S(r)).  Work is cut into tasks (internal.h):
-//   * row block: consecutive rows with < CAP + LONG edges in total.  Phase A
-//     streams the block's col_idx range with 128-bit evict-first loads and
-//     gathers load(col) for every edge into shared memory (4 independent
-//     gathers per int4, U int4 per thread in flight).  Phase B: each lane owns
-//     rows (r = warp*32 + lane + k*NT); rows of length <= SHORT are summed
-//     serially by their lane, longer rows cooperatively by the owning warp
-//     (lane-strided partials + xor-shuffle tree).
-//   * hub chunk: HUB_CHUNK edges of one row with in-degree > LONG; each CTA
-//     reduces its chunk (fixed tree) into a partial slot; the CTA that takes
-//     the last ticket of the hub sums the partials in chunk order and
-//     finalizes the row.
+// and calls  finalize(r, S(r)).  The rows are cut into warp tasks (built by
+// build_view_tasks, ingest.cu); every warp of the grid walks its own static
+// list of tasks (task t -> global warp t mod #warps), with no CTA barrier:
+//   * row block  (info >= 0): consecutive rows with <= WT_MAXE edges, each of
+//     in-degree <= WT_LONG.  The warp issues the block's 128-bit col_idx loads
+//     and gathers at once (the edge range is in the descriptor), prefetches
+//     the finalize operands of its rows (x, outdeg, contrib slot) in the same
+//     wave, stages the gathered values in its private shared-memory slice,
+//     then sums rows: lengths <= WT_SHORT serially by the owning lane, longer
+//     ones cooperatively (lane-strided partials + xor tree).
+//   * long chunk (info < 0): up to WT_HCH edges of one row of in-degree >
+//     WT_LONG, reduced in registers (lane-strided, xor tree).  Single-chunk
+//     rows finalize directly; multi-chunk ("hub") rows write a partial slot
+//     and the warp taking the hub's last ticket sums the partials in chunk
+//     order and finalizes the row.
 // Every sum is taken in an order that depends only on the row's data, so the
-// results are deterministic run to run (not equal to the oracle's ascending
-// order; DESIGN.md Q-F).
+// results are deterministic (not the oracle's order, Q-F).
 #pragma once
 #include "internal.h"
 
 namespace prgpu {
 
 constexpr int GT_WARPS = GT_NT / 32;
-constexpr int GT_U = 4;  // int4 col loads in flight per thread in phase A
 
 struct EngineArgs {
     const Task* tasks;
@@ -36,9 +37,13 @@ struct EngineArgs {
     uint32_t* hub_ticket;
 };
 
+struct __align__(16) WarpSmem {
+    uint64_t vals[WT_VALS];
+    int32_t rp[WT_MAXROWS + 3];
+};
+
 struct __align__(16) EngineSmem {
-    uint64_t vals[GT_VALS];
-    int32_t rp[GT_MAXROWS + 1];
+    WarpSmem w[GT_WARPS];
     double red[2 * GT_WARPS];
     int flag;
 };
@@ -51,47 +56,52 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 template <class P>
-__device__ __forceinline__ void engine_rowblock(P& p, const EngineArgs& a, const Task tk, EngineSmem& sm,
+__device__ __forceinline__ void engine_rowblock(P& p, const EngineArgs& a, const Task tk, WarpSmem& ws,
                                                 double& l1, double& linf) {
     using T = typename P::T;
-    T* vals = reinterpret_cast<T*>(sm.vals);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    T* vals = reinterpret_cast<T*>(ws.vals);
+    const int lane = threadIdx.x & 31;
     const int64_t r0 = tk.r0;
-    const int nr = tk.a;
-    const int64_t e0 = a.row_ptr[r0];
-    for (int i = tid; i <= nr; i += GT_NT) sm.rp[i] = (int32_t)(a.row_ptr[r0 + i] - e0);
-    __syncthreads();
-    const int nnz = sm.rp[nr];
-    // ---- phase A: stream col_idx, gather into shared memory ----
+    const int nr = (tk.info >> 16) & 0x7fff;
+    const int nnz = tk.info & 0xffff;
+    const int64_t e0 = tk.e0;
+    // finalize operands of rows lane and lane+32 (independent of the gathers)
+    typename P::Pre pre0{}, pre1{};
+    if (lane < nr) pre0 = p.prefetch(r0 + lane);
+    if (lane + 32 < nr) pre1 = p.prefetch(r0 + lane + 32);
+    // row offsets relative to e0
+    for (int i = lane; i <= nr; i += 32) ws.rp[i] = (int32_t)(a.row_ptr[r0 + i] - e0);
+    // stream col_idx (aligned int4) and gather
     const int64_t a0 = e0 & ~(int64_t)3;
     const int lead = (int)(e0 - a0);
     const int n4 = (lead + nnz + 3) >> 2;
     const int4* c4 = reinterpret_cast<const int4*>(a.col + a0);
-    for (int q0 = 0; q0 < n4; q0 += GT_NT * GT_U) {
-        int4 cv[GT_U] = {};
+    for (int q0 = 0; q0 < n4; q0 += 32 * WT_U) {
+        int4 cv[WT_U];
 #pragma unroll
-        for (int u = 0; u < GT_U; ++u) {
-            int q = q0 + u * GT_NT + tid;
-            if (q < n4) cv[u] = p.ld_col(c4 + q);
+        for (int u = 0; u < WT_U; ++u) {
+            const int q = q0 + u * 32 + lane;
+            cv[u] = q < n4 ? p.ld_col(c4 + q) : make_int4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < GT_U; ++u) {
-            int q = q0 + u * GT_NT + tid;
-            int base = q * 4 - lead;
-            int cc[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+        for (int u = 0; u < WT_U; ++u) {
+            const int q = q0 + u * 32 + lane;
+            const int base = q * 4 - lead;
+            const int cc[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (q < n4 && base + j >= 0 && base + j < nnz) vals[base + j] = p.load(cc[j]);
         }
     }
-    __syncthreads();
-    // ---- phase B: per-row sums, finalize ----
-    for (int i0 = warp * 32; i0 < nr; i0 += GT_NT) {
-        const int i = i0 + lane;
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h;
+        if (32 * h >= nr) break;
         const bool valid = i < nr;
-        const int s = valid ? sm.rp[i] : 0;
-        const int len = valid ? sm.rp[i + 1] - s : 0;
-        const bool lng = len > GT_SHORT;
+        const int s = valid ? ws.rp[i] : 0;
+        const int len = valid ? ws.rp[i + 1] - s : 0;
+        const bool lng = len > WT_SHORT;
         T sum = T(0);
         if (valid && !lng) {
             T s0 = T(0), s1 = T(0);
@@ -115,82 +125,88 @@ __device__ __forceinline__ void engine_rowblock(P& p, const EngineArgs& a, const
             if (lane == src) sum = part;
         }
         if (valid) {
-            double dl = p.finalize(r0 + i, sum);
+            const double dl = p.finalize(h ? pre1 : pre0, sum);
             l1 += dl;
             linf = fmax(linf, dl);
         }
     }
-    __syncthreads();
+    __syncwarp();
 }
 
 template <class P>
-__device__ __forceinline__ void engine_hubchunk(P& p, const EngineArgs& a, const Task tk, EngineSmem& sm) {
+__device__ __forceinline__ void engine_longchunk(P& p, const EngineArgs& a, const Task tk, EngineSmem& sm,
+                                                 double& l1, double& linf) {
     using T = typename P::T;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const Hub h = a.hubs[tk.b];
+    const int lane = threadIdx.x & 31;
     const int64_t row = tk.r0;
-    const int64_t rs = a.row_ptr[row], re = a.row_ptr[row + 1];
-    const int64_t cs = rs + (int64_t)tk.a * GT_HUB_CHUNK;
-    const int64_t ce = min(re, cs + (int64_t)GT_HUB_CHUNK);
-    const int nnz = (int)(ce - cs);
-    const int64_t a0 = cs & ~(int64_t)3;
-    const int lead = (int)(cs - a0);
+    const int nnz = tk.info & 0xffff;
+    const int64_t e0 = tk.e0;
+    typename P::Pre pre{};
+    if (lane == 0 && tk.hub < 0) pre = p.prefetch(row);
+    const int64_t a0 = e0 & ~(int64_t)3;
+    const int lead = (int)(e0 - a0);
     const int n4 = (lead + nnz + 3) >> 2;
     const int4* c4 = reinterpret_cast<const int4*>(a.col + a0);
     T part = T(0);
-    for (int q0 = 0; q0 < n4; q0 += GT_NT * GT_U) {
-        int4 cv[GT_U] = {};
+    for (int q0 = 0; q0 < n4; q0 += 32 * WT_U) {
+        int4 cv[WT_U];
 #pragma unroll
-        for (int u = 0; u < GT_U; ++u) {
-            int q = q0 + u * GT_NT + tid;
-            if (q < n4) cv[u] = p.ld_col(c4 + q);
+        for (int u = 0; u < WT_U; ++u) {
+            const int q = q0 + u * 32 + lane;
+            cv[u] = q < n4 ? p.ld_col(c4 + q) : make_int4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < GT_U; ++u) {
-            int q = q0 + u * GT_NT + tid;
-            int base = q * 4 - lead;
-            int cc[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+        for (int u = 0; u < WT_U; ++u) {
+            const int q = q0 + u * 32 + lane;
+            const int base = q * 4 - lead;
+            const int cc[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
 #pragma unroll
             for (int j = 0; j < 4; ++j)
                 if (q < n4 && base + j >= 0 && base + j < nnz) part += p.load(cc[j]);
         }
     }
     part = warp_sum(part);
-    T* red = reinterpret_cast<T*>(sm.red);
-    if (lane == 0) red[warp] = part;
-    __syncthreads();
-    if (tid == 0) {
-        T s = T(0);
-#pragma unroll
-        for (int w = 0; w < GT_WARPS; ++w) s += red[w];
+    if (tk.hub < 0) {
+        if (lane == 0) {
+            const double dl = p.finalize(pre, part);
+            l1 += dl;
+            linf = fmax(linf, dl);
+        }
+        return;
+    }
+    if (lane == 0) {
+        const Hub h = a.hubs[tk.hub];
+        const int j = (int)((e0 - h.row_e0) / WT_HCH);
         T* hp = reinterpret_cast<T*>(a.hub_partial);
-        hp[h.slot + tk.a] = s;
+        hp[h.slot + j] = part;
         __threadfence();
-        uint32_t t = atomicAdd(&a.hub_ticket[tk.b], 1u);
-        sm.flag = (t == (uint32_t)h.nchunks - 1) ? 1 : 0;
+        const uint32_t t = atomicAdd(&a.hub_ticket[tk.hub], 1u);
+        if (t == (uint32_t)h.nchunks - 1) {
+            __threadfence();
+            const T* hq = reinterpret_cast<const T*>(a.hub_partial);
+            T s = T(0);
+            for (int c = 0; c < h.nchunks; ++c) s += __ldcg(hq + h.slot + c);
+            const typename P::Pre pr = p.prefetch(row);
+            a.hub_delta[tk.hub] = p.finalize(pr, s);
+            a.hub_ticket[tk.hub] = 0u;
+        }
     }
-    __syncthreads();
-    if (sm.flag && tid == 0) {
-        __threadfence();
-        const T* hp = reinterpret_cast<const T*>(a.hub_partial);
-        T s = T(0);
-        for (int j = 0; j < h.nchunks; ++j) s += __ldcg(hp + h.slot + j);
-        a.hub_delta[tk.b] = p.finalize(row, s);
-        a.hub_ticket[tk.b] = 0u;
-    }
-    __syncthreads();
 }
 
-// Runs every task assigned to this CTA (static round robin: task i -> CTA
-// i mod gridDim.x, so the per-CTA accumulation order is deterministic).
+// Runs every task assigned to this warp.  The per-thread (l1, linf)
+// accumulators therefore depend only on the static assignment.
 template <class P>
 __device__ __forceinline__ void engine_run(P& p, const EngineArgs& a, EngineSmem& sm, double& l1, double& linf) {
-    for (int64_t t = blockIdx.x; t < a.ntasks; t += gridDim.x) {
+    const int warp = threadIdx.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * GT_WARPS + warp;
+    const int64_t nw = (int64_t)gridDim.x * GT_WARPS;
+    WarpSmem& ws = sm.w[warp];
+    for (int64_t t = gw; t < a.ntasks; t += nw) {
         const Task tk = a.tasks[t];
-        if (tk.b < 0)
-            engine_rowblock(p, a, tk, sm, l1, linf);
+        if (tk.info >= 0)
+            engine_rowblock(p, a, tk, ws, l1, linf);
         else
-            engine_hubchunk(p, a, tk, sm);
+            engine_longchunk(p, a, tk, sm, l1, linf);
     }
 }
 

@@ -1,0 +1,29 @@
+"""Profiling driver: build config k on the GPU and run a fixed number of sweeps.
+Usage: python tools/prof_run.py <config> <mode: plain|reduced|async> <sweeps> [scale_override]"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import graphgen  # noqa: E402
+import paper_2109_09527_b200 as pr  # noqa: E402
+
+cfg = int(sys.argv[1])
+mode = sys.argv[2]
+sweeps = int(sys.argv[3])
+scale = int(sys.argv[4]) if len(sys.argv) > 4 else None
+gen = graphgen.make_config(cfg, scale_override=scale)
+s = torch.from_numpy(gen.src).cuda()
+t = torch.from_numpy(gen.dst).cuda()
+x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+g = pr.Graph(gen.n, s, t)
+m = {"plain": 0, "reduced": pr.PR_USE_REDUCTIONS, "async": pr.PR_MODE_ASYNC}[mode]
+if mode == "reduced":
+    g.preprocess()
+st, it, fd = g.run(x, gen.d, 0.0, sweeps, mode=m | pr.PR_TIMING)
+stt = g.stats()
+print(gen.name, mode, "iters", it, "gather ms/launch", stt["gather_ms"] / max(1, stt["timed_iterations"]),
+      "tasks", stt["n_tasks"], "rows", stt["gather_rows"], "edges", stt["gather_edges"], "ncontrib", stt["n_contrib"])
+g.close()
