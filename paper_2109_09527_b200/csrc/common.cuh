@@ -91,30 +91,57 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ int4 ld_stream_i4(const int4* ptr, uint64_t pol) {
-    int4 r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(ptr), "l"(pol));
-    return r;
-}
 // Read-only gathers of the contrib vector within one synchronous sweep.
 __device__ __forceinline__ double ld_gather_f64(const double* ptr, uint64_t pol) {
     double r;
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
     return r;
 }
-// Branch-free choice between a shared-memory copy (hot contribs) and the
-// global vector: one predicated load each, so the gathers of a round stay
-// independent (a C++ branch here serialises them).
-__device__ __forceinline__ double ld_hot_or_gather_f64(const double* gptr, uint32_t saddr, int hot, uint64_t pol) {
+
+// Two-tier gather: hot contribs (small index = high out-degree) stay in L1
+// (evict_last), cold ones bypass it (no_allocate) so they cannot evict the
+// hot lines.  One predicated load each, branch-free.
+__device__ __forceinline__ double ld_gather_tiered_f64(const double* ptr, int hot, uint64_t pol) {
     double r;
-    asm("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %4, 0;\n\t"
-        "@p ld.shared.f64 %0, [%1];\n\t"
-        "@!p ld.global.nc.L2::cache_hint.f64 %0, [%2], %3;\n\t}"
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.s32 p, %3, 0;\n\t"
+        "@p ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;\n\t"
+        "@!p ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n\t}"
         : "=d"(r)
-        : "r"(saddr), "l"(gptr), "l"(pol), "r"(hot));
+        : "l"(ptr), "l"(pol), "r"(hot));
     return r;
+}
+
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) + mbarrier --------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// Order earlier generic-proxy accesses of shared memory before later async-proxy writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// One elected lane: arm the barrier with `bytes` and start a global->shared
+// bulk copy (16-byte aligned addresses, size a multiple of 16).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
 }
 // Async (No-Sync) mode: the contrib vector is read and written in the same
 // launch, so loads/stores are relaxed gpu-scope atomics (never .nc).

@@ -17,9 +17,7 @@ namespace prgpu {
 // ----------------------------------------------------------------- policy --
 // ASYNC: No-Sync in-place sweep (relaxed loads/stores of one contrib buffer).
 // VID:   rows of the view are vid[r] (else row r is vertex r).
-// HOT:   contribs with index < nhot (the highest out-degrees, DESIGN.md "Data
-//        layout") are read from a shared-memory copy staged at kernel start.
-template <bool ASYNC, bool VID, bool HOT>
+template <bool ASYNC, bool VID>
 struct PRPolicy {
     using T = double;
     const double* y_in;
@@ -29,25 +27,18 @@ struct PRPolicy {
     const int32_t* cidx;
     const int32_t* vid;
     double c, d;
-    uint64_t pol_first, pol_last;
-    const double* hot;
-    int32_t nhot;
-    uint32_t hot_s;  // shared-state-space address of hot[0]
+    uint64_t pol_last;
 
-    __device__ __forceinline__ void begin() {
-        pol_first = policy_evict_first();
-        pol_last = policy_evict_last();
-    }
-    __device__ __forceinline__ int4 ld_col(const int4* p) const { return ld_stream_i4(p, pol_first); }
+    __device__ __forceinline__ void begin() { pol_last = policy_evict_last(); }
     __device__ __forceinline__ double load(int32_t u) const {
         if (ASYNC) return ld_relaxed_f64(y_in + u);
-        if (HOT) return ld_hot_or_gather_f64(y_in + u, hot_s + 8u * (uint32_t)u, u < nhot, pol_last);
-        return ld_gather_f64(y_in + u, pol_last);
+        return ld_gather_tiered_f64(y_in + u, u < GT_L1_TIER, pol_last);
     }
     struct Pre {
         double xo;
         int32_t v, od, ci, pad;
     };
+    Pre pre[2];
     // finalize operands, loaded before the row's gathers complete
     __device__ __forceinline__ Pre prefetch(int64_t r) const {
         Pre q;
@@ -58,6 +49,12 @@ struct PRPolicy {
         q.pad = 0;
         return q;
     }
+    // rows r0 + lane and r0 + lane + 32 of a task with nr rows
+    __device__ __forceinline__ void prefetch_rows(int64_t r0, int nr, int lane) {
+        if (lane < nr) pre[0] = prefetch(r0 + lane);
+        if (lane + 32 < nr) pre[1] = prefetch(r0 + lane + 32);
+    }
+    __device__ __forceinline__ const Pre& prefetched(int h) const { return pre[h]; }
     // x_t(v) = c + d*S, fused contrib y_t(v) = x_t(v)/outdeg(v), returns |x_t(v) - x_{t-1}(v)|.
     __device__ __forceinline__ double finalize(const Pre& q, double s) const {
         const double xn = __dadd_rn(c, __dmul_rn(d, s));
@@ -160,21 +157,12 @@ __device__ __forceinline__ void block_delta(double l1, double linf, double* red,
     }
 }
 
-template <bool ASYNC, bool VID, bool HOT>
+template <bool ASYNC, bool VID>
 __global__ void __launch_bounds__(GT_NT, GT_MIN_CTAS)
-    k_gather(PRPolicy<ASYNC, VID, HOT> p, EngineArgs a, IterArgs ia, int finalize) {
+    k_gather(PRPolicy<ASYNC, VID> p, EngineArgs a, IterArgs ia, int finalize) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
     if (ia.st->done) return;
-    if (HOT) {  // stage the hottest contribs (cidx < nhot) of y_{t-1} in shared memory
-        double* hot = reinterpret_cast<double*>(smem_raw + sizeof(EngineSmem));
-        const double2* src = reinterpret_cast<const double2*>(p.y_in);
-        double2* dst = reinterpret_cast<double2*>(hot);
-        for (int i = threadIdx.x; i < p.nhot / 2; i += GT_NT) dst[i] = __ldg(src + i);
-        p.hot = hot;
-        p.hot_s = (uint32_t)__cvta_generic_to_shared(hot);
-        __syncthreads();
-    }
     p.begin();
     double l1 = 0.0, linf = 0.0;
     engine_run(p, a, sm, l1, linf);
@@ -281,63 +269,40 @@ __global__ void k_init(double* __restrict__ x, double* __restrict__ y, const int
 // ------------------------------------------------------------------- host --
 
 struct GatherCfg {
-    bool async, vid, hot;
-    int nhot;
+    bool async, vid;
     size_t smem;
     int grid;
 };
 
-template <bool ASYNC, bool VID, bool HOT>
+template <bool ASYNC, bool VID>
 static int launch_gather_t(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
                            double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
-    PRPolicy<ASYNC, VID, HOT> p{y_in, y_out, x, g->outdeg, g->cidx, v.vid, c, d, 0, 0, nullptr, gc.nhot, 0u};
+    PRPolicy<ASYNC, VID> p{y_in, y_out, x, g->outdeg, g->cidx, v.vid, c, d, 0, {}};
     EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, v.col, v.hub_partial, v.hub_delta, v.hub_ticket};
-    PR_LAUNCH(ctx, (k_gather<ASYNC, VID, HOT>), gc.grid, GT_NT, gc.smem, p, a, ia, finalize);
+    PR_LAUNCH(ctx, (k_gather<ASYNC, VID>), gc.grid, GT_NT, gc.smem, p, a, ia, finalize);
     return PR_OK;
 }
 
 static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
                          double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
     if (gc.async)
-        return gc.vid ? launch_gather_t<true, true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
-                      : launch_gather_t<true, false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
-    if (gc.hot)
-        return gc.vid ? launch_gather_t<false, true, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
-                      : launch_gather_t<false, false, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
-    return gc.vid ? launch_gather_t<false, true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
-                  : launch_gather_t<false, false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
+        return gc.vid ? launch_gather_t<true, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
+                      : launch_gather_t<true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
+    return gc.vid ? launch_gather_t<false, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
+                  : launch_gather_t<false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
 }
 
 static const void* gather_fn(const GatherCfg& gc) {
-    if (gc.async) return gc.vid ? (const void*)k_gather<true, true, false> : (const void*)k_gather<true, false, false>;
-    if (gc.hot) return gc.vid ? (const void*)k_gather<false, true, true> : (const void*)k_gather<false, false, true>;
-    return gc.vid ? (const void*)k_gather<false, true, false> : (const void*)k_gather<false, false, false>;
+    if (gc.async) return gc.vid ? (const void*)k_gather<true, true> : (const void*)k_gather<true, false>;
+    return gc.vid ? (const void*)k_gather<false, true> : (const void*)k_gather<false, false>;
 }
 
-// Kernel variant, hot-cache size, dynamic shared memory and persistent grid.
-// The hot cache takes whatever shared memory the engine leaves (sync mode
-// only: in async mode the contribs change during the sweep).
+// Kernel variant, dynamic shared memory and persistent grid (all resident CTAs).
 static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, GatherCfg* gc) {
+    (void)g;
     gc->async = async;
     gc->vid = v.vid != nullptr;
-    gc->hot = false;
-    gc->nhot = 0;
     gc->smem = sizeof(EngineSmem);
-    const char* e = getenv("PRGPU_HOT");
-    int64_t hot_cap = e ? atoll(e) : (int64_t)GT_HOT_DEFAULT;
-    if (!async && hot_cap > 0 && g->n_contrib >= 1024) {
-        int dev = 0, optin = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        int64_t room = ((int64_t)optin - (int64_t)sizeof(EngineSmem) - 1024) / 8;
-        int64_t h = std::min<int64_t>(std::min<int64_t>(room, hot_cap), g->n_contrib);
-        h &= ~(int64_t)31;
-        if (h >= 1024) {
-            gc->hot = true;
-            gc->nhot = (int)h;
-            gc->smem = sizeof(EngineSmem) + (size_t)h * sizeof(double);
-        }
-    }
     const void* fn = gather_fn(*gc);
     PR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gc->smem));
     int per_sm = 0;

@@ -26,7 +26,6 @@ struct HashPolicy {
     const int32_t* vid;  // view rows -> vertex ids (nullptr: identity)
     uint64_t* out;
     __device__ __forceinline__ void begin() {}
-    __device__ __forceinline__ int4 ld_col(const int4* p) const { return __ldg(p); }
     __device__ __forceinline__ uint64_t load(int32_t u) const {
         return mix64((uint64_t)(uint32_t)u * 0x9E3779B97F4A7C15ULL + 0x2545F4914F6CDD1DULL);
     }
@@ -37,6 +36,12 @@ struct HashPolicy {
         const int64_t v = vid ? vid[r] : r;
         return Pre{v, rp[v + 1] - rp[v]};
     }
+    Pre pre[2];
+    __device__ __forceinline__ void prefetch_rows(int64_t r0, int nr, int lane) {
+        if (lane < nr) pre[0] = prefetch(r0 + lane);
+        if (lane + 32 < nr) pre[1] = prefetch(r0 + lane + 32);
+    }
+    __device__ __forceinline__ const Pre& prefetched(int h) const { return pre[h]; }
     __device__ __forceinline__ double finalize(const Pre& q, uint64_t s) const {
         out[q.v] = s + mix64((uint64_t)q.deg + kDegSalt);
         return 0.0;
@@ -269,7 +274,7 @@ static int find_identical(pr_graph* g, Ctx& ctx) {
     const View& v = g->plain;
     {
         if (v.vid) PR_LAUNCH(ctx, k_hash_empty, grid_of(ctx, n), 256, 0, h, n);
-        HashPolicy p{g->row_ptr, v.vid, h};
+        HashPolicy p{g->row_ptr, v.vid, h, {}};
         EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, g->col, v.hub_partial, v.hub_delta, v.hub_ticket};
         int per_sm = 0;
         cudaFuncSetAttribute(k_rowhash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EngineSmem));

@@ -4,19 +4,24 @@
 // For every row r of a View it computes  S(r) = sum_{e in row r} load(col[e])
 // and calls  finalize(r, S(r)).  The rows are cut into warp tasks (built by
 // build_view_tasks, ingest.cu); every warp of the grid walks its own static
-// list of tasks (task t -> global warp t mod #warps), with no CTA barrier:
-//   * row block  (info >= 0): consecutive rows with <= WT_MAXE edges, each of
-//     in-degree <= WT_LONG.  The warp issues the block's 128-bit col_idx loads
-//     and gathers at once (the edge range is in the descriptor), prefetches
-//     the finalize operands of its rows (x, outdeg, contrib slot) in the same
-//     wave, stages the gathered values in its private shared-memory slice,
-//     then sums rows: lengths <= WT_SHORT serially by the owning lane, longer
-//     ones cooperatively (lane-strided partials + xor tree).
-//   * long chunk (info < 0): up to WT_HCH edges of one row of in-degree >
-//     WT_LONG, reduced in registers (lane-strided, xor tree).  Single-chunk
-//     rows finalize directly; multi-chunk ("hub") rows write a partial slot
-//     and the warp taking the hub's last ticket sums the partials in chunk
-//     order and finalizes the row.
+// list of tasks (task t -> global warp t mod #warps), with no CTA barrier.
+// A task is consumed as a stream of "pieces" of <= WT_PIECE edges, run as a
+// two-stage software pipeline per warp:
+//   * the col_idx range of the NEXT piece is fetched into the warp's second
+//     shared-memory buffer by one TMA bulk copy (cp.async.bulk + mbarrier),
+//     so index loads never occupy the LSU/L1 pipe or registers, and their
+//     DRAM latency overlaps the current piece's gathers;
+//   * row block (info >= 0, one piece): rows of in-degree <= WT_LONG.  The
+//     finalize operands of its rows (x, outdeg, contrib slot) are prefetched,
+//     all lanes gather load(col) for the block's edges (indices first, then
+//     all gathers, then the stores, so they are in flight together) into the
+//     warp's vals buffer, and rows are summed: lengths <= WT_SHORT serially by
+//     the owning lane, longer ones cooperatively (lane-strided + xor tree);
+//   * chunk (info < 0): <= WT_HCH edges of one row of in-degree > WT_LONG,
+//     accumulated per lane over its pieces, then reduced (xor tree).
+//     Single-chunk rows finalize directly; multi-chunk ("hub") rows write a
+//     partial slot and the warp taking the hub's last ticket sums the
+//     partials in chunk order and finalizes the row.
 // Every sum is taken in an order that depends only on the row's data, so the
 // results are deterministic (not the oracle's order, Q-F).
 #pragma once
@@ -38,7 +43,9 @@ struct EngineArgs {
 };
 
 struct __align__(16) WarpSmem {
+    int32_t colbuf[2][WT_COLBUF];
     uint64_t vals[WT_VALS];
+    uint64_t bar[2];
     int32_t rp[WT_MAXROWS + 3];
 };
 
@@ -55,43 +62,50 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+__device__ __forceinline__ int task_nnz(const Task& tk) { return tk.info & 0xffff; }
+__device__ __forceinline__ int task_pieces(const Task& tk) { return (task_nnz(tk) + WT_PIECE - 1) / WT_PIECE; }
+
+// Lane 0: stage col[e - lead .. e + cnt) (16-byte aligned superset) into buf.
+__device__ __forceinline__ void stage_cols(const EngineArgs& a, int64_t e, int cnt, int32_t* buf, uint64_t* bar,
+                                           uint64_t pol) {
+    const int64_t a0 = e & ~(int64_t)3;
+    const uint32_t bytes = (uint32_t)(((e - a0) + cnt) * 4 + 15) & ~15u;
+    bulk_g2s(buf, a.col + a0, bytes, bar, pol);
+}
+
+// Gathers of one staged piece: gv[k] = load(col[e0 + k*32 + lane]) for the
+// first cnt edges (indices first, then every gather, so all are in flight).
 template <class P>
-__device__ __forceinline__ void engine_rowblock(P& p, const EngineArgs& a, const Task tk, WarpSmem& ws,
-                                                double& l1, double& linf) {
+__device__ __forceinline__ void gather_piece(const P& p, const int32_t* cb, int lead, int cnt,
+                                             typename P::T (&gv)[WT_PIECE / 32]) {
     using T = typename P::T;
+    const int lane = threadIdx.x & 31;
+    constexpr int K = WT_PIECE / 32;
+    int ci[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const int e = k * 32 + lane;
+        ci[k] = e < cnt ? cb[lead + e] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) gv[k] = ci[k] >= 0 ? p.load(ci[k]) : T(0);
+}
+
+template <class P>
+__device__ __forceinline__ void engine_rowblock(P& p, const Task& tk, WarpSmem& ws, const int32_t* cb, double& l1,
+                                                double& linf) {
+    using T = typename P::T;
+    constexpr int K = WT_PIECE / 32;
     T* vals = reinterpret_cast<T*>(ws.vals);
     const int lane = threadIdx.x & 31;
-    const int64_t r0 = tk.r0;
     const int nr = (tk.info >> 16) & 0x7fff;
-    const int nnz = tk.info & 0xffff;
-    const int64_t e0 = tk.e0;
-    // finalize operands of rows lane and lane+32 (independent of the gathers)
-    typename P::Pre pre0{}, pre1{};
-    if (lane < nr) pre0 = p.prefetch(r0 + lane);
-    if (lane + 32 < nr) pre1 = p.prefetch(r0 + lane + 32);
-    // row offsets relative to e0
-    for (int i = lane; i <= nr; i += 32) ws.rp[i] = (int32_t)(a.row_ptr[r0 + i] - e0);
-    // stream col_idx (aligned int4) and gather
-    const int64_t a0 = e0 & ~(int64_t)3;
-    const int lead = (int)(e0 - a0);
-    const int n4 = (lead + nnz + 3) >> 2;
-    const int4* c4 = reinterpret_cast<const int4*>(a.col + a0);
-    for (int q0 = 0; q0 < n4; q0 += 32 * WT_U) {
-        int4 cv[WT_U];
+    const int nnz = task_nnz(tk);
+    T gv[K];
+    gather_piece(p, cb, tk.e0 & 3, nnz, gv);
 #pragma unroll
-        for (int u = 0; u < WT_U; ++u) {
-            const int q = q0 + u * 32 + lane;
-            cv[u] = q < n4 ? p.ld_col(c4 + q) : make_int4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < WT_U; ++u) {
-            const int q = q0 + u * 32 + lane;
-            const int base = q * 4 - lead;
-            const int cc[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (q < n4 && base + j >= 0 && base + j < nnz) vals[base + j] = p.load(cc[j]);
-        }
+    for (int k = 0; k < K; ++k) {
+        const int e = k * 32 + lane;
+        if (e < nnz) vals[e] = gv[k];
     }
     __syncwarp();
 #pragma unroll
@@ -125,50 +139,24 @@ __device__ __forceinline__ void engine_rowblock(P& p, const EngineArgs& a, const
             if (lane == src) sum = part;
         }
         if (valid) {
-            const double dl = p.finalize(h ? pre1 : pre0, sum);
+            const double dl = p.finalize(p.prefetched(h), sum);
             l1 += dl;
             linf = fmax(linf, dl);
         }
     }
-    __syncwarp();
 }
 
+// End of a chunk task: reduce the lane partials and finalize (or hand the
+// partial to the hub protocol).
 template <class P>
-__device__ __forceinline__ void engine_longchunk(P& p, const EngineArgs& a, const Task tk, EngineSmem& sm,
+__device__ __forceinline__ void engine_chunk_end(P& p, const EngineArgs& a, const Task& tk, typename P::T part,
                                                  double& l1, double& linf) {
     using T = typename P::T;
     const int lane = threadIdx.x & 31;
-    const int64_t row = tk.r0;
-    const int nnz = tk.info & 0xffff;
-    const int64_t e0 = tk.e0;
-    typename P::Pre pre{};
-    if (lane == 0 && tk.hub < 0) pre = p.prefetch(row);
-    const int64_t a0 = e0 & ~(int64_t)3;
-    const int lead = (int)(e0 - a0);
-    const int n4 = (lead + nnz + 3) >> 2;
-    const int4* c4 = reinterpret_cast<const int4*>(a.col + a0);
-    T part = T(0);
-    for (int q0 = 0; q0 < n4; q0 += 32 * WT_U) {
-        int4 cv[WT_U];
-#pragma unroll
-        for (int u = 0; u < WT_U; ++u) {
-            const int q = q0 + u * 32 + lane;
-            cv[u] = q < n4 ? p.ld_col(c4 + q) : make_int4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < WT_U; ++u) {
-            const int q = q0 + u * 32 + lane;
-            const int base = q * 4 - lead;
-            const int cc[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (q < n4 && base + j >= 0 && base + j < nnz) part += p.load(cc[j]);
-        }
-    }
     part = warp_sum(part);
     if (tk.hub < 0) {
         if (lane == 0) {
-            const double dl = p.finalize(pre, part);
+            const double dl = p.finalize(p.prefetched(0), part);
             l1 += dl;
             linf = fmax(linf, dl);
         }
@@ -176,7 +164,7 @@ __device__ __forceinline__ void engine_longchunk(P& p, const EngineArgs& a, cons
     }
     if (lane == 0) {
         const Hub h = a.hubs[tk.hub];
-        const int j = (int)((e0 - h.row_e0) / WT_HCH);
+        const int j = (int)(((int64_t)tk.e0 - h.row_e0) / WT_HCH);
         T* hp = reinterpret_cast<T*>(a.hub_partial);
         hp[h.slot + j] = part;
         __threadfence();
@@ -186,8 +174,7 @@ __device__ __forceinline__ void engine_longchunk(P& p, const EngineArgs& a, cons
             const T* hq = reinterpret_cast<const T*>(a.hub_partial);
             T s = T(0);
             for (int c = 0; c < h.nchunks; ++c) s += __ldcg(hq + h.slot + c);
-            const typename P::Pre pr = p.prefetch(row);
-            a.hub_delta[tk.hub] = p.finalize(pr, s);
+            a.hub_delta[tk.hub] = p.finalize(p.prefetch((int64_t)tk.r0), s);
             a.hub_ticket[tk.hub] = 0u;
         }
     }
@@ -197,16 +184,68 @@ __device__ __forceinline__ void engine_longchunk(P& p, const EngineArgs& a, cons
 // accumulators therefore depend only on the static assignment.
 template <class P>
 __device__ __forceinline__ void engine_run(P& p, const EngineArgs& a, EngineSmem& sm, double& l1, double& linf) {
+    using T = typename P::T;
+    constexpr int K = WT_PIECE / 32;
+    const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int64_t gw = (int64_t)blockIdx.x * GT_WARPS + warp;
     const int64_t nw = (int64_t)gridDim.x * GT_WARPS;
+    int64_t t = (int64_t)blockIdx.x * GT_WARPS + warp;
     WarpSmem& ws = sm.w[warp];
-    for (int64_t t = gw; t < a.ntasks; t += nw) {
-        const Task tk = a.tasks[t];
-        if (tk.info >= 0)
-            engine_rowblock(p, a, tk, ws, l1, linf);
-        else
-            engine_longchunk(p, a, tk, sm, l1, linf);
+    if (t >= a.ntasks) return;
+    const uint64_t pol = policy_evict_first();
+    if (lane == 0) {
+        mbar_init(&ws.bar[0], 1);
+        mbar_init(&ws.bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    Task cur = a.tasks[t];
+    int j = 0;  // piece of cur
+    if (lane == 0) stage_cols(a, cur.e0, min(task_nnz(cur), WT_PIECE), ws.colbuf[0], &ws.bar[0], pol);
+    T part = T(0);
+    for (uint32_t k = 0;; ++k) {
+        const int b = k & 1;
+        // next piece: the rest of this chunk, else the first piece of the next task
+        Task nt = cur;
+        int nj = j + 1;
+        int64_t ntn = t;
+        if (nj >= task_pieces(cur)) {
+            ntn = t + nw;
+            nj = 0;
+            if (ntn < a.ntasks) nt = a.tasks[ntn];
+        }
+        const bool has_next = ntn < a.ntasks;
+        if (has_next && lane == 0) {
+            fence_proxy_async_smem();  // buffer b^1 was last read (generic proxy) by piece k-1
+            const int64_t e = (int64_t)nt.e0 + (int64_t)nj * WT_PIECE;
+            stage_cols(a, e, min(task_nnz(nt) - nj * WT_PIECE, WT_PIECE), ws.colbuf[b ^ 1], &ws.bar[b ^ 1], pol);
+        }
+        if (j == 0) {  // task start: finalize operands and row offsets, overlapping the copy
+            if (cur.info >= 0) {
+                const int nr = (cur.info >> 16) & 0x7fff;
+                for (int i = lane; i <= nr; i += 32) ws.rp[i] = (int32_t)(a.row_ptr[cur.r0 + i] - cur.e0);
+                p.prefetch_rows((int64_t)cur.r0, nr, lane);
+            } else if (cur.hub < 0 && lane == 0) {
+                p.prefetch_rows((int64_t)cur.r0, 1, 0);
+            }
+            part = T(0);
+        }
+        mbar_wait(&ws.bar[b], (k >> 1) & 1);
+        if (cur.info >= 0) {
+            engine_rowblock(p, cur, ws, ws.colbuf[b], l1, linf);
+        } else {
+            const int64_t e = (int64_t)cur.e0 + (int64_t)j * WT_PIECE;
+            T gv[K];
+            gather_piece(p, ws.colbuf[b], (int)(e & 3), min(task_nnz(cur) - j * WT_PIECE, WT_PIECE), gv);
+#pragma unroll
+            for (int q = 0; q < K; ++q) part += gv[q];
+            if (j + 1 == task_pieces(cur)) engine_chunk_end(p, a, cur, part, l1, linf);
+        }
+        __syncwarp();
+        if (!has_next) break;
+        cur = nt;
+        j = nj;
+        t = ntn;
     }
 }
 
