@@ -26,6 +26,19 @@ static int make_ctx(Ctx& ctx, void* stream) {
     int dev = 0;
     PR_CUDA(cudaGetDevice(&dev));
     PR_CUDA(cudaDeviceGetAttribute(&ctx.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    // Keep freed stream-ordered memory in the device pool instead of returning
+    // it to the OS at every synchronisation (re-mapping GBs per call otherwise
+    // costs tens of ms per pr_graph_create).
+    static bool pool_tuned[64] = {false};
+    if (dev >= 0 && dev < 64 && !pool_tuned[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+        pool_tuned[dev] = true;
+    }
     return PR_OK;
 }
 

@@ -14,25 +14,29 @@
 
 namespace prgpu {
 
-__global__ void k_pack(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m,
-                       int64_t n, int b, uint64_t* __restrict__ keys,
-                       unsigned long long* __restrict__ count, int* __restrict__ err) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t lt = lanemask_lt();
-    const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < m; base += wstride) {
-        int64_t i = base + lane;
-        bool valid = i < m;
-        int32_t s = valid ? src[i] : 0, t = valid ? dst[i] : 0;
-        bool bad = valid && (s < 0 || (int64_t)s >= n || t < 0 || (int64_t)t >= n);
-        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1);
-        bool keep = valid && !bad && s != t;
-        uint32_t mask = __ballot_sync(0xffffffffu, keep);
-        unsigned long long wbase = 0;
-        if (lane == 0 && mask) wbase = atomicAdd(count, (unsigned long long)__popc(mask));
-        wbase = __shfl_sync(0xffffffffu, wbase, 0);
-        if (keep) keys[wbase + __popc(mask & lt)] = ((uint64_t)(uint32_t)t << b) | (uint32_t)s;
+// key = dst << b | src; self-loops (and invalid ids, which abort the build)
+// become the sentinel 2^(2b) - 1, which sorts last and is dropped by the
+// unique pass (a real key equals it only for the self-loop (2^b-1, 2^b-1)).
+// No compaction here: the sort and the unique pass do not care about order.
+__global__ void k_pack(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m, int64_t n,
+                       int b, uint64_t sentinel, uint64_t* __restrict__ keys, int* __restrict__ err) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool any_bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+        const int32_t s = src[i], t = dst[i];
+        const bool bad = s < 0 || (int64_t)s >= n || t < 0 || (int64_t)t >= n;
+        any_bad |= bad;
+        keys[i] = (bad || s == t) ? sentinel : (((uint64_t)(uint32_t)t << b) | (uint32_t)s);
     }
+    if (__any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
+}
+
+__global__ void k_check_ids(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m, int64_t n,
+                            int* __restrict__ err) {
+    bool any_bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        any_bad |= src[i] < 0 || (int64_t)src[i] >= n || dst[i] < 0 || (int64_t)dst[i] >= n;
+    if (__any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
 }
 
 // In-degree histogram over the sorted unique dst array, one atomic per run of
@@ -65,7 +69,11 @@ __global__ void k_outdeg(const int32_t* __restrict__ col, int64_t E, int32_t* __
 
 struct UniqueGet {
     const uint64_t* k;
-    __device__ int64_t operator()(int64_t i) const { return (i == 0 || k[i] != k[i - 1]) ? 1 : 0; }
+    uint64_t sentinel;
+    __device__ int64_t operator()(int64_t i) const {
+        const uint64_t key = k[i];
+        return (key != sentinel && (i == 0 || key != k[i - 1])) ? 1 : 0;
+    }
 };
 struct UniqueEmit {
     const uint64_t* k;
@@ -112,44 +120,42 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
 
     uint64_t* keys = nullptr;
     uint64_t* keys_alt = nullptr;
-    int64_t* scratch = nullptr;  // [0] = kept count, [1] = error flag, [2] = E
-    PR_TRY(dalloc(&scratch, 4, s));
-    PR_CUDA(cudaMemsetAsync(scratch, 0, 4 * sizeof(int64_t), s));
-    int64_t kept = 0;
-    if (m > 0) {
-        PR_TRY(dalloc(&keys, (size_t)m, s));
-        PR_LAUNCH(ctx, k_pack, grid_for(ctx, m, 256), 256, 0, src, dst, m, n, b, keys,
-                  (unsigned long long*)scratch, (int*)(scratch + 1));
-        int64_t h[2];
-        PR_CUDA(cudaMemcpyAsync(h, scratch, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        PR_CUDA(cudaStreamSynchronize(s));
-        if (h[1] != 0) {
-            dfree(keys, s);
-            dfree(scratch, s);
-            set_error("pr_graph_create: vertex id outside [0, n)");
-            return PR_EINVAL;
-        }
-        kept = h[0];
-    }
+    int64_t* scratch = nullptr;  // [0] = E, [1] = error flag
+    PR_TRY(dalloc(&scratch, 2, s));
+    PR_CUDA(cudaMemsetAsync(scratch, 0, 2 * sizeof(int64_t), s));
+    // n == 1 (b == 0): every edge is a self-loop, nothing to sort
+    const int64_t mk = b > 0 ? m : 0;
+    const uint64_t sentinel = b > 0 ? ((2 * b >= 64) ? ~0ull : ((1ull << (2 * b)) - 1)) : 0ull;
 
-    // sort by (dst, src) and deduplicate
+    // pack, sort by (dst, src), deduplicate
     uint32_t* udst = nullptr;
-    PR_TRY(dalloc(&g->col, (size_t)(kept > 0 ? kept : 1), s));
-    if (kept > 0) {
-        PR_TRY(dalloc(&keys_alt, (size_t)kept, s));
+    PR_TRY(dalloc(&g->col, (size_t)(mk > 0 ? mk : 1), s));
+    if (mk > 0) {
+        PR_TRY(dalloc(&keys, (size_t)mk, s));
+        PR_LAUNCH(ctx, k_pack, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, sentinel, keys,
+                  (int*)(scratch + 1));
+        PR_TRY(dalloc(&keys_alt, (size_t)mk, s));
         bool alt = false;
-        PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, kept, 0, 2 * b, &alt)));
+        PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, 2 * b, &alt)));
         const uint64_t* sorted = alt ? keys_alt : keys;
-        PR_TRY(dalloc(&udst, (size_t)kept, s));
-        PR_TRY((device_scan<int64_t>(ctx, kept, UniqueGet{sorted},
-                                     UniqueEmit{sorted, g->col, udst, b, (b ? ((1ull << b) - 1) : 0ull)},
-                                     scratch + 2)));
-        PR_TRY(read_count(ctx, scratch + 2, &g->E));
+        PR_TRY(dalloc(&udst, (size_t)mk, s));
+        PR_TRY((device_scan<int64_t>(ctx, mk, UniqueGet{sorted, sentinel},
+                                     UniqueEmit{sorted, g->col, udst, b, (1ull << b) - 1}, scratch)));
         dfree(keys, s);
         dfree(keys_alt, s);
-    } else {
-        g->E = 0;
+    } else if (m > 0) {  // n == 1: still validate the ids
+        PR_LAUNCH(ctx, k_check_ids, grid_for(ctx, m, 256), 256, 0, src, dst, m, n, (int*)(scratch + 1));
     }
+    int64_t h[2];
+    PR_CUDA(cudaMemcpyAsync(h, scratch, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
+    if (h[1] != 0) {
+        dfree(udst, s);
+        dfree(scratch, s);
+        set_error("pr_graph_create: vertex id outside [0, n)");
+        return PR_EINVAL;
+    }
+    g->E = h[0];
 
     // row_ptr from the in-degree histogram; outdeg from the sources
     int32_t* indeg = nullptr;

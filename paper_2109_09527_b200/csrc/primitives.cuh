@@ -177,19 +177,29 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const K* __restrict__ keys, i
     }
 }
 
+// Stable scatter of one 8-bit digit.  Per tile of RS_TILE keys: warp-level
+// ranking (match_any), tile-local digit offsets, a local sort into shared
+// memory, then a coalesced write-out (consecutive threads write consecutive
+// addresses of one digit's run).
 template <class K, bool HAS_V>
 __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       int64_t n, int64_t per_cta, int shift,
                                                       const uint32_t* __restrict__ offs, int64_t G) {
-    __shared__ uint32_t base[RS_BINS];
+    static_assert(RS_NT == RS_BINS, "one thread per digit in the tile scan");
+    __shared__ uint32_t base[RS_BINS];      // global start of each digit for the current tile
+    __shared__ uint32_t toff[RS_BINS];      // tile-local start of each digit
     __shared__ uint32_t wc[RS_WARPS][RS_BINS + 1];
+    __shared__ uint32_t sw[33];
+    __shared__ K sk[RS_TILE];
+    __shared__ uint32_t sv[HAS_V ? RS_TILE : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = lanemask_lt();
-    for (int d = threadIdx.x; d < RS_BINS; d += RS_NT) base[d] = offs[(int64_t)d * G + blockIdx.x];
+    base[threadIdx.x] = offs[(int64_t)threadIdx.x * G + blockIdx.x];
     const int64_t b = (int64_t)blockIdx.x * per_cta;
     const int64_t e = min(n, b + per_cta);
     for (int64_t tb = b; tb < e; tb += RS_TILE) {
+        const int tn = (int)min((int64_t)RS_TILE, e - tb);
         for (int i = threadIdx.x; i < RS_WARPS * (RS_BINS + 1); i += RS_NT) (&wc[0][0])[i] = 0;
         __syncthreads();
         K k[RS_ROUNDS];
@@ -213,24 +223,44 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const K* __restrict__ kin,
             __syncwarp();
         }
         __syncthreads();
-        for (int d = threadIdx.x; d < RS_BINS; d += RS_NT) {
-            uint32_t run = base[d];
+        {   // digit d = threadIdx.x: tile count, tile-local offset, per-warp offsets
+            const int d = threadIdx.x;
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int w = 0; w < RS_WARPS; ++w) cnt += wc[w][d];
+            uint32_t tot;
+            const uint32_t off = block_exclusive_sum(cnt, &tot, sw);
+            toff[d] = off;
+            uint32_t run = off;
 #pragma unroll
             for (int w = 0; w < RS_WARPS; ++w) {
-                uint32_t c = wc[w][d];
+                const uint32_t c = wc[w][d];
                 wc[w][d] = run;
                 run += c;
             }
-            base[d] = run;
         }
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < RS_ROUNDS; ++r) {
             if (dg[r] < RS_BINS) {
-                uint32_t dst = wc[warp][dg[r]] + pos[r];
-                kout[dst] = k[r];
-                if (HAS_V) vout[dst] = v[r];
+                const uint32_t lp = wc[warp][dg[r]] + pos[r];
+                sk[lp] = k[r];
+                if (HAS_V) sv[lp] = v[r];
             }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < tn; i += RS_NT) {
+            const K key = sk[i];
+            const uint32_t d = (uint32_t)(key >> shift) & (RS_BINS - 1);
+            const uint32_t dst = base[d] + (uint32_t)i - toff[d];
+            kout[dst] = key;
+            if (HAS_V) vout[dst] = sv[i];
+        }
+        __syncthreads();
+        {   // advance the digit bases past this tile
+            const int d = threadIdx.x;
+            const uint32_t end = (d + 1 < RS_BINS) ? toff[d + 1] : (uint32_t)tn;
+            base[d] += end - toff[d];
         }
         __syncthreads();
     }
