@@ -9,6 +9,8 @@
 //   unique  adjacent-different flags -> scan -> col_idx / row dst  (dedup)
 //   rows    in-degree histogram (run-aggregated atomics) -> scan -> row_ptr
 //   outdeg  histogram of src over the deduplicated edges
+#include <stdlib.h>
+
 #include "internal.h"
 #include "primitives.cuh"
 
@@ -298,7 +300,7 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
         PR_TRY((device_scan<int64_t>(ctx, n, NonZeroInGet{g->row_ptr},
                                      NonZeroEmit{g->row_ptr, v.vid, v.row_ptr, n, v.nrows}, scratch)));
     }
-    PR_TRY(dalloc(&v.col, (size_t)(g->E > 0 ? g->E : 1), s));
+    PR_TRY(dalloc(&v.col, (size_t)stream_pad(g->E), s));
     if (g->E > 0)
         PR_LAUNCH(ctx, k_map_col, grid_for(ctx, g->E, 256), 256, 0, (const int32_t*)g->col, g->E,
                   (const int32_t*)g->cidx, v.col);
@@ -395,6 +397,19 @@ void free_view(View& v, cudaStream_t s) {
     dfree(v.hub_delta, s);
     dfree(v.hub_ticket, s);
     v.nrows = v.nedges = v.ntasks = v.nhubs = v.hub_slots = 0;
+    dfree(v.sflags, s);
+    dfree(v.step_row, s);
+    dfree(v.bin, s);
+    dfree(v.bout, s);
+    dfree(v.b_row, s);
+    dfree(v.b_s0, s);
+    dfree(v.b_s1, s);
+    dfree(v.part_in, s);
+    dfree(v.part_out, s);
+    dfree(v.bticket, s);
+    dfree(v.sums, s);
+    v.nsteps = v.nspans = v.nbound = 0;
+    v.span_steps = 1;
 }
 
 int build_view_tasks(View& v, Ctx& ctx) {
@@ -432,6 +447,104 @@ int build_view_tasks(View& v, Ctx& ctx) {
     dfree(P, s);
     dfree(starts, s);
     dfree(scratch, s);
+    return PR_OK;
+}
+
+// ------------------------------------------------------------ view stream --
+// Tables of the edge-stream engine (streamengine.cuh) for a view whose rows
+// all have in-degree >= 1: row-start bits, step_row, spans and boundary rows.
+__global__ void k_pad_col(int32_t* __restrict__ col, int64_t E, int64_t Epad, int32_t pad) {
+    for (int64_t e = E + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < Epad; e += (int64_t)gridDim.x * blockDim.x)
+        col[e] = pad;
+}
+__global__ void k_row_flags(const int64_t* __restrict__ rp, int64_t nrows, uint32_t* __restrict__ fl) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = rp[r];
+        atomicOr(fl + (e >> 5), 1u << (e & 31));
+    }
+}
+// step_row[s] = first row r with rp[r] >= s * SE_STEP (rp strictly increasing)
+__global__ void k_step_row(const int64_t* __restrict__ rp, int64_t nrows, int64_t nsteps, int32_t* __restrict__ sr) {
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s <= nsteps; s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t key = s * SE_STEP;
+        int64_t lo = 0, hi = nrows;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (rp[mid] < key)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        sr[s] = (int32_t)lo;
+    }
+}
+struct BoundGet {
+    const int64_t* rp;
+    int64_t span_e;
+    __device__ int64_t operator()(int64_t r) const { return rp[r] / span_e != (rp[r + 1] - 1) / span_e ? 1 : 0; }
+};
+struct BoundEmit {
+    const int64_t* rp;
+    int64_t span_e;
+    int32_t *b_row, *b_s0, *b_s1, *bin, *bout;
+    __device__ void operator()(int64_t r, int64_t b, int64_t f) const {
+        if (!f) return;
+        const int64_t s0 = rp[r] / span_e, s1 = (rp[r + 1] - 1) / span_e;
+        b_row[b] = (int32_t)r;
+        b_s0[b] = (int32_t)s0;
+        b_s1[b] = (int32_t)s1;
+        bout[s0] = (int32_t)b;
+        for (int64_t s = s0 + 1; s <= s1; ++s) bin[s] = (int32_t)b;
+    }
+};
+
+int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot) {
+    cudaStream_t s = ctx.stream;
+    v.nsteps = v.nspans = v.nbound = 0;
+    if (v.nrows == 0 || v.nedges == 0) return PR_OK;
+    const int64_t Epad = stream_pad(v.nedges);
+    v.nsteps = Epad / SE_STEP;
+    // one span per resident warp (1 CTA of SE_NT threads per SM): the gather's
+    // work per step is uniform, and every span costs two fences and a ticket
+    const int64_t warps = (int64_t)ctx.num_sms * (SE_NT / 32);
+    int64_t ss = (v.nsteps + warps - 1) / warps;
+    if (ss < 1) ss = 1;
+    if (const char* e = getenv("PRGPU_SPAN")) {  // tuning override
+        const int64_t o = atoll(e);
+        if (o >= 1) ss = o;
+    }
+    v.span_steps = ss;
+    v.nspans = (v.nsteps + ss - 1) / ss;
+    if (Epad > v.nedges)
+        PR_LAUNCH(ctx, k_pad_col, 1, 256, 0, v.col, v.nedges, Epad, pad_slot);
+    PR_TRY(dalloc(&v.sflags, (size_t)v.nsteps * 8, s));
+    PR_CUDA(cudaMemsetAsync(v.sflags, 0, sizeof(uint32_t) * (size_t)v.nsteps * 8, s));
+    PR_LAUNCH(ctx, k_row_flags, grid_for(ctx, v.nrows, 256), 256, 0, (const int64_t*)v.row_ptr, v.nrows, v.sflags);
+    PR_TRY(dalloc(&v.step_row, (size_t)v.nsteps + 1, s));
+    PR_LAUNCH(ctx, k_step_row, grid_for(ctx, v.nsteps + 1, 256), 256, 0, (const int64_t*)v.row_ptr, v.nrows,
+              v.nsteps, v.step_row);
+    PR_TRY(dalloc(&v.bin, (size_t)v.nspans, s));
+    PR_TRY(dalloc(&v.bout, (size_t)v.nspans, s));
+    PR_CUDA(cudaMemsetAsync(v.bin, 0xff, sizeof(int32_t) * (size_t)v.nspans, s));
+    PR_CUDA(cudaMemsetAsync(v.bout, 0xff, sizeof(int32_t) * (size_t)v.nspans, s));
+    // boundary rows <= nspans (each crosses at least one of the nspans - 1 span ends)
+    const int64_t cap = v.nspans;
+    PR_TRY(dalloc(&v.b_row, (size_t)cap, s));
+    PR_TRY(dalloc(&v.b_s0, (size_t)cap, s));
+    PR_TRY(dalloc(&v.b_s1, (size_t)cap, s));
+    int64_t* cnt = nullptr;
+    PR_TRY(dalloc(&cnt, 1, s));
+    const int64_t span_e = ss * SE_STEP;
+    PR_TRY((device_scan<int64_t>(ctx, v.nrows, BoundGet{v.row_ptr, span_e},
+                                 BoundEmit{v.row_ptr, span_e, v.b_row, v.b_s0, v.b_s1, v.bin, v.bout}, cnt)));
+    PR_TRY(read_count(ctx, cnt, &v.nbound));
+    dfree(cnt, s);
+    PR_TRY(dalloc(&v.part_in, (size_t)v.nspans, s));
+    PR_TRY(dalloc(&v.part_out, (size_t)v.nspans, s));
+    const int64_t nb = v.nbound > 0 ? v.nbound : 1;
+    PR_TRY(dalloc(&v.bticket, (size_t)nb, s));
+    PR_CUDA(cudaMemsetAsync(v.bticket, 0, sizeof(uint32_t) * (size_t)nb, s));
+    PR_TRY(dalloc(&v.sums, (size_t)v.nrows, s));
     return PR_OK;
 }
 

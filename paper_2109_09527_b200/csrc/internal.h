@@ -15,6 +15,19 @@ namespace prgpu {
 // with L1::evict_last, the rest with L1::no_allocate (measured: 1.57 -> 1.39
 // ms per R-MAT-24 sweep; insensitive to the tier size between 2K and 128K).
 constexpr int GT_L1_TIER = 8192;
+// Edge-stream engine (streamengine.cuh): SE_V edges per lane per step.
+constexpr int SE_V = 8;
+constexpr int SE_STEP = 32 * SE_V;
+#ifndef PRGPU_SE_NT
+#define PRGPU_SE_NT 1024
+#endif
+constexpr int SE_NT = PRGPU_SE_NT;          // threads per CTA of the stream gather (1 CTA per SM)
+// Contribs [0, hot_n) (the highest out-degrees) are copied into shared memory
+// by every CTA at the start of a synchronous sweep; [hot_n, SE_L1_TIER) are
+// gathered with L1::evict_last, the rest with L1::no_allocate.
+constexpr int SE_HOT_MAX = 16384;           // 128 KB of fp64
+constexpr int SE_L1_TIER = 32768;
+inline int64_t stream_pad(int64_t E) { return ((E > 0 ? E : 1) + SE_STEP - 1) / SE_STEP * SE_STEP; }
 constexpr int GT_NT = PRGPU_NT;              // threads per CTA (independent warps)
 constexpr int GT_MIN_CTAS = PRGPU_MIN_CTAS;  // __launch_bounds__ min CTAs/SM of the gather
 constexpr int WT_CAP = 256;                  // weight budget per row-block task (edges + ROW_W*rows)
@@ -65,6 +78,22 @@ struct View {
     double* hub_delta = nullptr;    // [nhubs] |delta| of each hub row (fixed-order reduce)
     uint32_t* hub_ticket = nullptr; // [nhubs]
     int64_t hub_slots = 0;
+    // edge-stream engine (build_view_stream; col is padded to nsteps * SE_STEP)
+    int64_t nsteps = 0;
+    int64_t span_steps = 1;
+    int64_t nspans = 0;
+    int64_t nbound = 0;
+    uint32_t* sflags = nullptr;     // [nsteps * 8] row-start bits
+    int32_t* step_row = nullptr;    // [nsteps + 1]
+    int32_t* bin = nullptr;         // [nspans]
+    int32_t* bout = nullptr;        // [nspans]
+    int32_t* b_row = nullptr;       // [nbound]
+    int32_t* b_s0 = nullptr;
+    int32_t* b_s1 = nullptr;
+    double* part_in = nullptr;      // [nspans]
+    double* part_out = nullptr;     // [nspans]
+    uint32_t* bticket = nullptr;    // [nbound]
+    double* sums = nullptr;         // [nrows] S(r) of the current sweep (K-GATHER -> K-FINALIZE)
 };
 
 // Device-resident iteration state (one per graph).
@@ -113,6 +142,7 @@ struct pr_graph {
     int32_t* mem_vid = nullptr;
     int32_t* mem_src = nullptr;
     int32_t* mem_k = nullptr;
+    int32_t* mem_srow = nullptr;    // reduced-view row of mem_src (K-FINALIZE reads its S)
     prgpu::View reduced;
     // iteration buffers (allocated lazily by pr_run)
     double* x = nullptr;            // fp64[n] (used when the caller's ranks are on the host)
@@ -132,6 +162,7 @@ namespace prgpu {
 int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx);
 int build_relabel(pr_graph* g, Ctx& ctx);
 int build_view_tasks(View& v, Ctx& ctx);
+int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot);
 void free_view(View& v, cudaStream_t s);
 int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx);
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,

@@ -7,10 +7,12 @@
 // contribute nothing (Alg.2; Q-D).  Delta_t is summed over all n
 // vertices (Q-R) and the loop runs "while err > threshold" (Q-S).
 #include <math.h>
+#include <stdlib.h>
 #include <vector>
 
 #include "internal.h"
 #include "rowengine.cuh"
+#include "streamengine.cuh"
 
 namespace prgpu {
 
@@ -70,6 +72,26 @@ struct PRPolicy {
     }
 };
 
+// Reduction scratch: red[0..RED_W) sums, red[RED_W..2*RED_W) maxima, one per warp.
+constexpr int RED_W = 32;
+
+// Policy of the edge-stream gather (streamengine.cuh), synchronous sweeps.
+// HOT: contribs [0, hot_n) are read from the CTA's shared-memory copy.
+template <bool HOT>
+struct StreamPolicy {
+    const double* y_in;
+    double* sums;
+    const double* hot;
+    int32_t hot_n;
+    uint64_t pol_last;
+
+    __device__ __forceinline__ double load(int32_t u) const {
+        if (HOT && u < hot_n) return hot[u];
+        return ld_gather_tiered_f64(y_in + u, u < SE_L1_TIER, pol_last);
+    }
+    __device__ __forceinline__ void emit(int64_t r, double s) const { sums[r] = s; }
+};
+
 struct IterArgs {
     DevState* st;
     double* cta_partial;        // (L1, Linf) per CTA: gather CTAs, scatter CTAs, zero-in CTAs
@@ -88,11 +110,11 @@ __device__ void global_finalize(const IterArgs& ia, double* red) {
     __threadfence();
     double s = 0.0, mx = 0.0;
     const int64_t nc = ia.gather_ctas + ia.scatter_ctas + ia.zero_ctas;
-    for (int64_t i = tid; i < nc; i += GT_NT) {
+    for (int64_t i = tid; i < nc; i += blockDim.x) {
         s += __ldcg(ia.cta_partial + 2 * i);
         mx = fmax(mx, __ldcg(ia.cta_partial + 2 * i + 1));
     }
-    for (int64_t i = tid; i < ia.nhubs; i += GT_NT) {
+    for (int64_t i = tid; i < ia.nhubs; i += blockDim.x) {
         double v = __ldcg(ia.hub_delta + i);
         s += v;
         mx = fmax(mx, v);
@@ -103,14 +125,14 @@ __device__ void global_finalize(const IterArgs& ia, double* red) {
     __syncthreads();
     if (lane == 0) {
         red[warp] = s;
-        red[GT_WARPS + warp] = mx;
+        red[RED_W + warp] = mx;
     }
     __syncthreads();
     if (tid == 0) {
         double l1 = 0.0, li = 0.0;
-        for (int w = 0; w < GT_WARPS; ++w) {
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
             l1 += red[w];
-            li = fmax(li, red[GT_WARPS + w]);
+            li = fmax(li, red[RED_W + w]);
         }
         DevState* st = ia.st;
         const int it = st->iters + 1;
@@ -143,14 +165,14 @@ __device__ __forceinline__ void block_delta(double l1, double linf, double* red,
     __syncthreads();
     if (lane == 0) {
         red[warp] = l1;
-        red[GT_WARPS + warp] = linf;
+        red[RED_W + warp] = linf;
     }
     __syncthreads();
     if (tid == 0) {
         double a = 0.0, b = 0.0;
-        for (int w = 0; w < GT_WARPS; ++w) {
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
             a += red[w];
-            b = fmax(b, red[GT_WARPS + w]);
+            b = fmax(b, red[RED_W + w]);
         }
         out[0] = a;
         out[1] = b;
@@ -177,6 +199,139 @@ __global__ void __launch_bounds__(GT_NT, GT_MIN_CTAS)
     if (sm.flag) global_finalize(ia, sm.red);
 }
 
+// K-GATHER, edge-stream form: S(r) of every row of the view into sums[r].
+// One CTA of SE_NT threads per SM; no Delta here (K-FINALIZE computes it).
+template <bool HOT>
+__global__ void __launch_bounds__(SE_NT, 1) k_stream(StreamPolicy<HOT> p, StreamArgs a, const DevState* st) {
+    extern __shared__ __align__(16) double hot_smem[];
+    if (st->done) return;
+    p.pol_last = policy_evict_last();
+    if (HOT) {
+        const double2* src = reinterpret_cast<const double2*>(p.y_in);
+        double2* dst = reinterpret_cast<double2*>(hot_smem);
+        for (int i = threadIdx.x; i < (p.hot_n >> 1); i += blockDim.x) dst[i] = __ldcg(src + i);
+        if ((p.hot_n & 1) && threadIdx.x == 0) hot_smem[p.hot_n - 1] = __ldcg(p.y_in + p.hot_n - 1);
+        p.hot = hot_smem;
+        __syncthreads();
+    }
+    stream_run(p, a);
+}
+
+// K-FINALIZE (sync sweeps): for every row r of the view
+//   x_t(v) = c + d*S(r)  (Eq.(1) in the "sum, then times d" form; Q-F),
+//   y_t(v) = x_t(v)/outdeg(v) into the next contrib buffer (fused contrib),
+// and, in reduced mode, every member m with source row q and distance k:
+//   x_t(m) = alpha_k + beta_k * (c + d*S(q))     ((0,1): exact copy; Q-C)
+// (c + d*S(q) is bit-identical to x_t of the source).  |x_t - x_{t-1}| of all
+// of them feeds the fixed-order Delta reduction and the stop test (a7).
+struct FinArgs {
+    const double* sums;
+    int64_t nrows;
+    const int32_t* vid;
+    const int32_t* mvid;
+    const int32_t* msrow;
+    const int32_t* mk;
+    int64_t nm;
+    const double* ab;
+    double* x;
+    double* y_out;
+    const int32_t* od;
+    const int32_t* cidx;
+    double c, d;
+};
+
+// Rows are visited grid-stride (all CTAs sweep the row space together, which
+// keeps the TLB working set small) in batches of FIN_U rows per thread whose
+// loads are all issued before any store.
+constexpr int FIN_U = 4;
+
+template <bool VID>
+__global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
+    __shared__ double red[2 * RED_W];
+    __shared__ int flag;
+    if (ia.st->done) return;
+    double l1 = 0.0, linf = 0.0;
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const double* __restrict__ sums = f.sums;
+    const int32_t* __restrict__ vid = f.vid;
+    const int32_t* __restrict__ od = f.od;
+    const int32_t* __restrict__ cidx = f.cidx;
+    double* __restrict__ x = f.x;
+    double* __restrict__ y = f.y_out;
+    for (int64_t r0 = t0; r0 < f.nrows; r0 += FIN_U * T) {
+        double S[FIN_U], xo[FIN_U];
+        int32_t v[FIN_U], o[FIN_U], ci[FIN_U];
+#pragma unroll
+        for (int u = 0; u < FIN_U; ++u) {
+            const int64_t r = r0 + u * T;
+            const bool ok = r < f.nrows;
+            S[u] = ok ? __ldcs(sums + r) : 0.0;
+            v[u] = ok ? (VID ? __ldcs(vid + r) : (int32_t)r) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < FIN_U; ++u) {
+            if (v[u] >= 0) {
+                xo[u] = x[v[u]];
+                o[u] = __ldg(od + v[u]);
+                ci[u] = __ldg(cidx + v[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < FIN_U; ++u) {
+            if (v[u] >= 0) {
+                const double xn = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
+                x[v[u]] = xn;
+                if (o[u] > 0) y[ci[u]] = xn / (double)o[u];
+                const double dl = fabs(xn - xo[u]);
+                l1 += dl;
+                linf = fmax(linf, dl);
+            }
+        }
+    }
+    for (int64_t i0 = t0; i0 < f.nm; i0 += FIN_U * T) {
+        double S[FIN_U], xo[FIN_U];
+        int32_t m[FIN_U], k[FIN_U], q[FIN_U], o[FIN_U], ci[FIN_U];
+#pragma unroll
+        for (int u = 0; u < FIN_U; ++u) {
+            const int64_t i = i0 + u * T;
+            const bool ok = i < f.nm;
+            m[u] = ok ? __ldcs(f.mvid + i) : -1;
+            k[u] = ok ? __ldcs(f.mk + i) : 0;
+            q[u] = ok ? __ldcs(f.msrow + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < FIN_U; ++u) {
+            if (m[u] >= 0) {
+                S[u] = sums[q[u]];
+                xo[u] = x[m[u]];
+                o[u] = __ldg(od + m[u]);
+                ci[u] = __ldg(cidx + m[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < FIN_U; ++u) {
+            if (m[u] >= 0) {
+                const double xs = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
+                const double xn = __dadd_rn(f.ab[2 * k[u]], __dmul_rn(f.ab[2 * k[u] + 1], xs));
+                x[m[u]] = xn;
+                if (o[u] > 0) y[ci[u]] = xn / (double)o[u];
+                const double dl = fabs(xn - xo[u]);
+                l1 += dl;
+                linf = fmax(linf, dl);
+            }
+        }
+    }
+    block_delta(l1, linf, red, ia.cta_partial + 2 * blockIdx.x);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        uint32_t t = atomicAdd(&ia.st->ticket_gather, 1u);
+        flag = (t == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (flag) global_finalize(ia, red);
+}
+
 // Members (reduced mode): x_t(m) = alpha_k + beta_k * x_t(src), with
 // (alpha_0, beta_0) = (0, 1) an exact copy for identical members and
 // alpha_{k+1} = c + d alpha_k, beta_{k+1} = d beta_k for chain members at
@@ -187,7 +342,7 @@ __global__ void __launch_bounds__(GT_NT) k_scatter(const int32_t* __restrict__ m
                                                    const double* __restrict__ ab, double* x, double* y_out,
                                                    const int32_t* __restrict__ od, const int32_t* __restrict__ cidx,
                                                    IterArgs ia) {
-    __shared__ double red[2 * GT_WARPS];
+    __shared__ double red[2 * RED_W];
     __shared__ int flag;
     if (ia.st->done) return;
     const int64_t b = (int64_t)blockIdx.x * per_cta;
@@ -228,7 +383,7 @@ __global__ void __launch_bounds__(GT_NT) k_scatter(const int32_t* __restrict__ m
 __global__ void __launch_bounds__(GT_NT) k_zero(const int32_t* __restrict__ zl, int64_t nz, int64_t per_cta, double c,
                                                 double* x, double* y_out, const int32_t* __restrict__ od,
                                                 const int32_t* __restrict__ cidx, double* partial) {
-    __shared__ double red[2 * GT_WARPS];
+    __shared__ double red[2 * RED_W];
     const int64_t b = (int64_t)blockIdx.x * per_cta;
     const int64_t e = min(nz, b + per_cta);
     double l1 = 0.0, linf = 0.0;
@@ -269,14 +424,17 @@ __global__ void k_init(double* __restrict__ x, double* __restrict__ y, const int
 // ------------------------------------------------------------------- host --
 
 struct GatherCfg {
+    bool stream;  // sync: edge-stream gather + K-FINALIZE; async (or PRGPU_ENGINE=tasks): row-task engine
     bool async, vid;
+    int hot_n;
     size_t smem;
     int grid;
+    int nt;
 };
 
 template <bool ASYNC, bool VID>
-static int launch_gather_t(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
-                           double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
+static int launch_tasks_t(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
+                          double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
     PRPolicy<ASYNC, VID> p{y_in, y_out, x, g->outdeg, g->cidx, v.vid, c, d, 0, {}};
     EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, v.col, v.hub_partial, v.hub_delta, v.hub_ticket};
     PR_LAUNCH(ctx, (k_gather<ASYNC, VID>), gc.grid, GT_NT, gc.smem, p, a, ia, finalize);
@@ -285,32 +443,65 @@ static int launch_gather_t(Ctx& ctx, const View& v, const double* y_in, double* 
 
 static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
                          double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
+    if (gc.stream) {
+        StreamArgs a{v.col,     (const uint8_t*)v.sflags, v.step_row, v.nsteps, v.span_steps, v.nspans, v.bin,
+                     v.bout,    v.b_row, v.b_s0, v.b_s1, v.part_in, v.part_out, v.bticket};
+        if (gc.hot_n > 0) {
+            StreamPolicy<true> p{y_in, v.sums, nullptr, gc.hot_n, 0};
+            PR_LAUNCH(ctx, k_stream<true>, gc.grid, gc.nt, gc.smem, p, a, (const DevState*)g->st);
+        } else {
+            StreamPolicy<false> p{y_in, v.sums, nullptr, 0, 0};
+            PR_LAUNCH(ctx, k_stream<false>, gc.grid, gc.nt, gc.smem, p, a, (const DevState*)g->st);
+        }
+        return PR_OK;
+    }
     if (gc.async)
-        return gc.vid ? launch_gather_t<true, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
-                      : launch_gather_t<true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
-    return gc.vid ? launch_gather_t<false, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
-                  : launch_gather_t<false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
+        return gc.vid ? launch_tasks_t<true, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
+                      : launch_tasks_t<true, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
+    return gc.vid ? launch_tasks_t<false, true>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize)
+                  : launch_tasks_t<false, false>(ctx, v, y_in, y_out, x, g, c, d, ia, gc, finalize);
 }
 
 static const void* gather_fn(const GatherCfg& gc) {
+    if (gc.stream) return gc.hot_n > 0 ? (const void*)k_stream<true> : (const void*)k_stream<false>;
     if (gc.async) return gc.vid ? (const void*)k_gather<true, true> : (const void*)k_gather<true, false>;
     return gc.vid ? (const void*)k_gather<false, true> : (const void*)k_gather<false, false>;
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+
 // Kernel variant, dynamic shared memory and persistent grid (all resident CTAs).
 static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, GatherCfg* gc) {
-    (void)g;
+    const char* eng = getenv("PRGPU_ENGINE");
+    gc->stream = !async && !(eng && eng[0] == 't');
     gc->async = async;
     gc->vid = v.vid != nullptr;
-    gc->smem = sizeof(EngineSmem);
+    gc->hot_n = 0;
+    if (gc->stream) {
+        int hot = env_int("PRGPU_HOT", SE_HOT_MAX);
+        if (hot > SE_HOT_MAX) hot = SE_HOT_MAX;
+        if (hot > g->n_contrib) hot = (int)g->n_contrib;
+        if (hot < 0) hot = 0;
+        gc->hot_n = hot;
+        gc->smem = (size_t)hot * sizeof(double);
+        gc->nt = SE_NT;
+    } else {
+        gc->smem = sizeof(EngineSmem);
+        gc->nt = GT_NT;
+    }
     const void* fn = gather_fn(*gc);
     PR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gc->smem));
     int per_sm = 0;
-    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GT_NT, gc->smem));
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, gc->nt, gc->smem));
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)ctx.num_sms * per_sm;
-    int64_t warps_needed = (v.ntasks + GT_WARPS - 1) / GT_WARPS;
-    if (grid > warps_needed) grid = warps_needed;
+    const int wpc = gc->nt / 32;
+    const int64_t units = gc->stream ? v.nspans : v.ntasks;
+    int64_t ctas_needed = (units + wpc - 1) / wpc;
+    if (grid > ctas_needed) grid = ctas_needed;
     if (grid < 1) grid = 1;
     gc->grid = (int)grid;
     return PR_OK;
@@ -337,20 +528,31 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         if (!g->x) PR_TRY(dalloc(&g->x, (size_t)n, s));
         x = g->x;
     }
-    const int64_t ny = g->n_contrib > 0 ? g->n_contrib : 1;
-    if (!g->y[0]) PR_TRY(dalloc(&g->y[0], (size_t)ny, s));
-    if (!g->y[1]) PR_TRY(dalloc(&g->y[1], (size_t)ny, s));
+    // contrib slots [0, n_contrib) + slot n_contrib = +0.0, the pad of the stream engine
+    const int64_t ny = g->n_contrib + 1;
+    for (int b = 0; b < 2; ++b)
+        if (!g->y[b]) {
+            PR_TRY(dalloc(&g->y[b], (size_t)ny, s));
+            PR_CUDA(cudaMemsetAsync(g->y[b] + g->n_contrib, 0, sizeof(double), s));
+        }
 
     GatherCfg gc;
     PR_TRY(gather_config(ctx, v, g, async, &gc));
-    const int ggrid = gc.grid;
-    const int64_t sgrid_cap = (int64_t)ctx.num_sms * 4;
-    int64_t sgrid = nm > 0 ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
-    if (sgrid > sgrid_cap) sgrid = sgrid_cap;
+    const int64_t cap4 = (int64_t)ctx.num_sms * 4;
+    // K-FINALIZE (stream path): fixed grid, so each CTA's rows and members (and
+    // hence its Delta partial) are a fixed set (deterministic)
+    int64_t fgrid = 0;
+    if (gc.stream) {
+        const int64_t work = v.nrows + nm;
+        fgrid = std::min<int64_t>(std::max<int64_t>((work + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
+    }
+    const int ggrid = gc.stream ? (int)fgrid : gc.grid;  // CTAs writing Delta partials first
+    int64_t sgrid = (!gc.stream && nm > 0) ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
+    if (sgrid > cap4) sgrid = cap4;
     const int64_t sper = sgrid > 0 ? (nm + sgrid - 1) / sgrid : 0;
     const int64_t nz = g->nz;
     int64_t zgrid = nz > 0 ? (nz + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
-    if (zgrid > sgrid_cap) zgrid = sgrid_cap;
+    if (zgrid > cap4) zgrid = cap4;
     const int64_t zper = zgrid > 0 ? (nz + zgrid - 1) / zgrid : 0;
     const int64_t need = 2 * ((int64_t)ggrid + sgrid + zgrid);
     if (g->partial_cap < need) {
@@ -387,12 +589,20 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     PR_LAUNCH(ctx, k_init, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, x,
               g->y[0], (const int32_t*)g->outdeg, (const int32_t*)g->cidx, n, 1.0 / (double)n);
 
-    const int64_t sctas = reduced ? sgrid : 0;
-    IterArgs ia_rest{g->st, g->cta_partial, (int64_t)ggrid, sctas, 0, v.hub_delta, v.nhubs, g->delta_log};
+    const int64_t sctas = (reduced && !gc.stream) ? sgrid : 0;
+    IterArgs ia_rest{g->st,
+                     g->cta_partial,
+                     (int64_t)ggrid,
+                     sctas,
+                     0,
+                     gc.stream ? nullptr : v.hub_delta,
+                     gc.stream ? 0 : v.nhubs,
+                     g->delta_log};
     IterArgs ia_first = ia_rest;
     ia_first.zero_ctas = zgrid;
     double* zero_partial = g->cta_partial + 2 * ((int64_t)ggrid + sctas);
-    const bool gather_finalizes = !(reduced && sgrid > 0);
+    const bool gather_finalizes = !gc.stream && !(reduced && sgrid > 0);
+    FinArgs fa{v.sums, v.nrows, v.vid, g->mem_vid, g->mem_srow, g->mem_k, nm, g->ab, x, nullptr, g->outdeg, g->cidx, c, d};
 
     std::vector<cudaEvent_t> ev;
     double gather_ms = 0.0, scatter_ms = 0.0;
@@ -417,13 +627,16 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                 PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y_out,
                           (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
-            {
-                int rc;
-                rc = launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, gather_finalizes);
-                if (rc != PR_OK) return rc;
-            }
+            PR_TRY(launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, gather_finalizes));
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
-            if (!gather_finalizes) {
+            if (gc.stream) {
+                FinArgs f = fa;
+                f.y_out = y_out;
+                if (gc.vid)
+                    PR_LAUNCH(ctx, k_finalize<true>, (unsigned)fgrid, GT_NT, 0, f, ia);
+                else
+                    PR_LAUNCH(ctx, k_finalize<false>, (unsigned)fgrid, GT_NT, 0, f, ia);
+            } else if (!gather_finalizes) {
                 if (async)
                     PR_LAUNCH(ctx, k_scatter<true>, (unsigned)sgrid, GT_NT, 0, (const int32_t*)g->mem_vid,
                               (const int32_t*)g->mem_src, (const int32_t*)g->mem_k, nm, sper, (const double*)g->ab, x,

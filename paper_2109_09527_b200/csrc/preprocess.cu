@@ -238,6 +238,16 @@ __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const i
     }
 }
 
+__global__ void k_rowof(const int32_t* __restrict__ vid, int64_t nrows, int32_t* __restrict__ rowof) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x)
+        rowof[vid[r]] = (int32_t)r;
+}
+__global__ void k_gather_i32(const int32_t* __restrict__ idx, int64_t cnt, const int32_t* __restrict__ tab,
+                             int32_t* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = tab[idx[i]];
+}
+
 static unsigned grid_of(const Ctx& ctx, int64_t work) {
     int64_t g = (work + 255) / 256;
     int64_t cap = (int64_t)ctx.num_sms * 16;
@@ -253,6 +263,7 @@ static void clear_reductions(pr_graph* g, cudaStream_t s) {
     dfree(g->mem_vid, s);
     dfree(g->mem_src, s);
     dfree(g->mem_k, s);
+    dfree(g->mem_srow, s);
     free_view(g->reduced, s);
     g->n_members = 0;
     g->max_chain = 0;
@@ -395,11 +406,23 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
     R.owns_row_ptr = true;
     PR_TRY((device_scan<int64_t>(ctx, R.nrows + 1, DegGet{g->row_ptr, R.vid, R.nrows}, PosEmit{R.row_ptr}, cnt)));
     PR_TRY(read_count(ctx, cnt, &R.nedges));
-    PR_TRY(dalloc(&R.col, (size_t)(R.nedges > 0 ? R.nedges : 1), s));
+    PR_TRY(dalloc(&R.col, (size_t)stream_pad(R.nedges), s));
     if (R.nrows > 0)
         PR_LAUNCH(ctx, k_copy_rows, grid_of(ctx, R.nrows * 32), 256, 0, (const int32_t*)R.vid, R.nrows,
                   (const int64_t*)g->row_ptr, (const int32_t*)g->plain.col, (const int64_t*)R.row_ptr, R.col);
     PR_TRY(build_view_tasks(R, ctx));
+    PR_TRY(build_view_stream(R, ctx, (int32_t)g->n_contrib));
+    // source row of every member in the reduced view (K-FINALIZE reads its S)
+    if (g->n_members > 0) {
+        int32_t* rowof = nullptr;
+        PR_TRY(dalloc(&rowof, (size_t)n, s));
+        if (R.nrows > 0)
+            PR_LAUNCH(ctx, k_rowof, grid_of(ctx, R.nrows), 256, 0, (const int32_t*)R.vid, R.nrows, rowof);
+        PR_TRY(dalloc(&g->mem_srow, (size_t)g->n_members, s));
+        PR_LAUNCH(ctx, k_gather_i32, grid_of(ctx, g->n_members), 256, 0, (const int32_t*)g->mem_src, g->n_members,
+                  (const int32_t*)rowof, g->mem_srow);
+        dfree(rowof, s);
+    }
     dfree(cnt, s);
     g->pre_done = true;
     g->pre_flags = flags;

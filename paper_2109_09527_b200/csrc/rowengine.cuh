@@ -51,7 +51,7 @@ struct __align__(16) WarpSmem {
 
 struct __align__(16) EngineSmem {
     WarpSmem w[GT_WARPS];
-    double red[2 * GT_WARPS];
+    double red[2 * 32];  // block reductions (one sum and one max per warp, up to 32 warps)
     int flag;
 };
 

@@ -1,0 +1,118 @@
+"""GPU tests of the edge-stream gather's decomposition (streamengine.cuh).
+
+The sync sweep is K-GATHER (flat edge stream: steps of 256 edges, spans of
+steps per warp, boundary rows assembled from per-span pieces by a ticket) +
+K-FINALIZE.  Its result must not depend on how the edge array is cut:
+  * span size (PRGPU_SPAN, read at graph build) changes only the summation
+    association -> oracle tolerance, iteration count +/-1 rule;
+  * the shared-memory hot tier (PRGPU_HOT) changes only WHERE a contrib is
+    read from -> bit-identical ranks and Delta logs;
+  * the legacy row-task engine (PRGPU_ENGINE=tasks) -> oracle tolerance.
+"""
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from tests import graphs as G
+from tests.test_gpu_parity import D, assert_close, assert_iters, dev, gpu_run
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_09527_b200 as m
+    return m
+
+
+def hub_graph(n=6000, seed=5):
+    """Random graph plus two long rows (a 5000-edge hub and a 700-edge row) and
+    a block of in-degree-1 rows, so rows start and end at every position of a
+    step and cross many span boundaries."""
+    rng = np.random.default_rng(seed)
+    edges = list(zip(rng.integers(0, n, 6 * n).tolist(), rng.integers(0, n, 6 * n).tolist()))
+    edges += [(int(u), 3) for u in rng.permutation(n)[:5000]]
+    edges += [(int(u), 4000) for u in rng.permutation(n)[:700]]
+    edges += [(int(v) - 1, int(v)) for v in range(100, 400)]
+    s, t = G.edges_to_arrays(edges)
+    return n, s, t
+
+
+@pytest.mark.parametrize("span", [1, 2, 3, 5, 17, 1000])
+def test_span_sizes_match_oracle(pr, monkeypatch, span):
+    monkeypatch.setenv("PRGPU_SPAN", str(span))
+    n, s, t = hub_graph()
+    ref_g = oracle.build_csr(n, s, t)
+    ref = oracle.pagerank(ref_g, D, 1e-12, 1000)
+    rep_o = oracle.identical(ref_g)
+    cs_o, ck_o, _ = oracle.chains(ref_g, rep_o)
+    ref_r = oracle.pagerank(ref_g, D, 1e-12, 1000, reduced=True, rep=rep_o, chain_k=ck_o)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        st, it, fd, x = gpu_run(pr, g, n, 1e-12)
+        assert_iters(it, ref, 1e-12)
+        assert_close(x, ref.x)
+        g.preprocess()
+        st, it, fd, xr = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS)
+        assert_iters(it, ref_r, 1e-12)
+        assert_close(xr, ref_r.x)
+
+
+@pytest.mark.parametrize("span", [1, 4])
+def test_single_long_row_spans(pr, monkeypatch, span):
+    """One row holding every edge (in-star): its pieces cross all spans."""
+    monkeypatch.setenv("PRGPU_SPAN", str(span))
+    n = 20000
+    s, t = G.edges_to_arrays(G.in_star(n))
+    ref_g = oracle.build_csr(n, s, t)
+    ref = oracle.pagerank(ref_g, D, 1e-13, 1000)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        st, it, fd, x = gpu_run(pr, g, n, 1e-13)
+        assert it == ref.iters
+        assert_close(x, ref.x)
+
+
+def test_hot_tier_is_bit_identical(pr, monkeypatch):
+    gen = graphgen.make_config(4, scale_override=14)
+    runs = []
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        g.preprocess()
+        for hot in ("0", "1", "7", "4096", "16384"):
+            monkeypatch.setenv("PRGPU_HOT", hot)
+            for mode in (0, pr.PR_USE_REDUCTIONS):
+                st, it, fd, x = gpu_run(pr, g, gen.n, 1e-10, mode=mode)
+                runs.append((hot, mode, it, x, g.delta_log()))
+    for mode in (0, pr.PR_USE_REDUCTIONS):
+        rs = [r for r in runs if r[1] == mode]
+        for r in rs[1:]:
+            assert r[2] == rs[0][2]
+            assert np.array_equal(r[3], rs[0][3]), (r[0], mode)
+            assert np.array_equal(r[4], rs[0][4])
+
+
+def test_task_engine_agrees(pr, monkeypatch):
+    gen = graphgen.make_config(4, scale_override=13)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    ref = oracle.pagerank(ref_g, D, 1e-10, 1000)
+    out = {}
+    for eng in ("stream", "tasks"):
+        monkeypatch.setenv("PRGPU_ENGINE", eng)
+        with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+            st, it, fd, x = gpu_run(pr, g, gen.n, 1e-10)
+            assert_iters(it, ref, 1e-10)
+            assert_close(x, ref.x)
+            out[eng] = x
+    assert np.abs(out["stream"] - out["tasks"]).max() <= 1e-15
+
+
+def test_stream_deterministic_across_graph_builds(pr):
+    gen = graphgen.make_config(2, scale_override=16)
+    xs = []
+    for _ in range(2):
+        with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+            g.preprocess()
+            xs.append(gpu_run(pr, g, gen.n, 1e-10, mode=pr.PR_USE_REDUCTIONS)[3])
+    assert np.array_equal(xs[0], xs[1])

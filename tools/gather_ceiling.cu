@@ -1,0 +1,220 @@
+// gather_ceiling.cu -- microbenchmark (tool, not product): the throughput
+// ceiling of the random fp64 contrib gather that dominates K-GATHER.
+//
+// A flat pass  acc += y[col[e]]  over a relabelled edge array, with no row
+// structure at all, so its time is a lower bound for any pull sweep over the
+// same col array on this GPU.  Variants:
+//   hot = 0 : every gather through L1TEX (ld.global.nc, L1::no_allocate)
+//   hot = H : contribs [0, H) are copied into shared memory once per CTA and
+//             served by LDS; the rest go through L1TEX as above.
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC
+//        -o tools/libceiling.so tools/gather_ceiling.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+__device__ __forceinline__ double ldg_na(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double ldg_el(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ int4 ldg_stream(const int4* p) {
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Each warp handles chunks of 32*4*U edges; per step a lane loads U int4 of
+// indices and then issues 4U independent gathers.
+template <int U, bool HOT>
+__global__ void __launch_bounds__(1024) k_flat(const int32_t* __restrict__ col, int64_t E, const double* __restrict__ y,
+                                              int hot_n, int tier, double* out) {
+    extern __shared__ double hot[];
+    if (HOT) {
+        for (int i = threadIdx.x; i < hot_n; i += blockDim.x) hot[i] = y[i];
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    constexpr int CH = 32 * 4 * U;
+    const int64_t nch = E / CH;  // tail ignored (bench tool)
+    double acc = 0.0;
+    for (int64_t c = warp; c < nch; c += nwarps) {
+        const int4* p = reinterpret_cast<const int4*>(col + c * CH) + lane;
+        int4 ix[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ix[u] = ldg_stream(p + 32 * u);
+        double v[4 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q[4] = {ix[u].x, ix[u].y, ix[u].z, ix[u].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (HOT) {
+                    v[4 * u + j] = q[j] < hot_n ? hot[q[j]] : (q[j] < tier ? ldg_el(y + q[j]) : ldg_na(y + q[j]));
+                } else {
+                    v[4 * u + j] = q[j] < tier ? ldg_el(y + q[j]) : ldg_na(y + q[j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4 * U; ++k) acc += v[k];
+    }
+    out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+extern "C" int ceiling_run(const int32_t* col, int64_t E, const double* y, int hot_n, int unroll, int ctas_per_sm,
+                           int reps, int threads, int tier, double* out, float* ms_out) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = sms * ctas_per_sm;
+    size_t smem = hot_n > 0 ? (size_t)hot_n * 8 : 0;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto launch = [&]() {
+#define L(U)                                                                                            \
+    if (unroll == U) {                                                                                  \
+        if (hot_n > 0) {                                                                                \
+            cudaFuncSetAttribute(k_flat<U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+            k_flat<U, true><<<grid, threads, smem>>>(col, E, y, hot_n, tier, out);                                \
+        } else {                                                                                        \
+            k_flat<U, false><<<grid, threads, 0>>>(col, E, y, 0, tier, out);                                      \
+        }                                                                                               \
+    }
+        L(1) L(2) L(4) L(8)
+#undef L
+    };
+    launch();
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return (int)cudaGetLastError();
+}
+
+// TMA gather4 variant: y viewed as a 2D tensor [ceil(nsrc/2)][2] of fp64 (16 B
+// rows); each lane issues one cp.async.bulk.tensor ... tile::gather4 for its
+// 4 indices (4 rows x 16 B -> 64 B of shared memory), S stages per warp.
+__device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <int S>
+__global__ void __launch_bounds__(1024) k_tma_g4(const __grid_constant__ CUtensorMap tm, const int32_t* __restrict__ col,
+                                                 int64_t E, double* out) {
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double* buf = reinterpret_cast<double*>(sm_raw) + (size_t)wib * S * 512;  // S x 32 lanes x 16 doubles (128 B slots)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw + (size_t)(blockDim.x >> 5) * S * 4096) + wib * S;
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t nch = E / 128;
+    if (lane == 0)
+        for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(bar + s)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    int4 ix[S];
+    auto issue = [&](int s, int64_t c) {
+        ix[s] = reinterpret_cast<const int4*>(col + c * 128)[lane];
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 2048;" ::"r"(sa(bar + s)) : "memory");
+        __syncwarp();
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(sa(buf + s * 512 + lane * 16)),
+            "l"(&tm), "r"(sa(bar + s)), "r"(0), "r"(ix[s].x >> 1), "r"(ix[s].y >> 1), "r"(ix[s].z >> 1),
+            "r"(ix[s].w >> 1)
+            : "memory");
+    };
+    double acc = 0.0;
+    int64_t c = warp;
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        if (c + s * nwarps < nch) issue(s, c + s * nwarps);
+    uint32_t ph = 0;
+    for (; c < nch; c += S * nwarps) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int64_t cc = c + s * nwarps;
+            if (cc >= nch) break;
+            asm volatile(
+                "{\n\t.reg .pred P;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra W_%=;\n\t}" ::"r"(
+                    sa(bar + s)),
+                "r"(ph)
+                : "memory");
+            const double* b = buf + s * 512 + lane * 16;
+            acc += b[ix[s].x & 1] + b[2 + (ix[s].y & 1)] + b[4 + (ix[s].z & 1)] + b[6 + (ix[s].w & 1)];
+            __syncwarp();
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const int64_t nx = cc + S * nwarps;
+            if (nx < nch) issue(s, nx);
+        }
+        ph ^= 1;
+    }
+    out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+extern "C" int ceiling_tma(const int32_t* col, int64_t E, const double* y, int64_t nsrc, int stages, int threads,
+                           int reps, double* out, float* ms_out) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess || !enc)
+        return -100;
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {2, (cuuint64_t)((nsrc + 1) / 2)};
+    cuuint64_t strides[1] = {16};
+    cuuint32_t box[2] = {2, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)y, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return -200 - (int)r;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int nw = threads / 32;
+    size_t smem = (size_t)nw * stages * 4096 + (size_t)nw * stages * 8;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto launch = [&]() {
+#define L(S)                                                                                                   \
+    if (stages == S) {                                                                                         \
+        cudaFuncSetAttribute(k_tma_g4<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+        k_tma_g4<S><<<sms, threads, smem>>>(tm, col, E, out);                                                  \
+    }
+        L(1) L(2) L(3) L(4) L(6)
+#undef L
+    };
+    launch();
+    {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            fprintf(stderr, "tma kernel: %s\n", cudaGetErrorString(e));
+            return -300;
+        }
+    }
+    cudaEventRecord(a);
+    for (int i = 0; i < reps; ++i) launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return (int)cudaGetLastError();
+}

@@ -1,0 +1,103 @@
+"""Gather-ceiling microbenchmark (tool): how fast can ANY kernel stream the
+relabelled col array of a config and gather y[col] on this B200?
+
+Usage: python tools/gather_ceiling.py [config=4]
+Prints one line per variant (ms per pass, G gathers/s, wavefront estimate).
+"""
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import graphgen  # noqa: E402
+import paper_2109_09527_b200 as pr  # noqa: E402
+
+so = os.path.join(ROOT, "tools", "libceiling.so")
+if not os.path.exists(so):
+    subprocess.check_call(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler",
+                           "-fPIC", "-o", so, os.path.join(ROOT, "tools", "gather_ceiling.cu")])
+lib = ctypes.CDLL(so)
+lib.ceiling_tma.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]
+lib.ceiling_run.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+gen = graphgen.make_config(cfg)
+dev = torch.device("cuda:0")
+s = torch.from_numpy(gen.src).to(dev)
+t = torch.from_numpy(gen.dst).to(dev)
+g = pr.Graph(gen.n, s, t)
+info = g.info()
+n, E = info["n"], info["E"]
+rp = torch.empty(n + 1, dtype=torch.int64, device=dev)
+ci = torch.empty(E, dtype=torch.int32, device=dev)
+od = torch.empty(n, dtype=torch.int32, device=dev)
+pr.pr_get_csr(g.handle, rp, ci, od)
+g.close()
+del s, t
+# relabel sources by (outdeg desc, id asc), as K-GATHER's contrib slots
+order = torch.sort(-od.to(torch.int64) * (1 << 32) + torch.arange(n, device=dev)).indices
+cidx = torch.empty(n, dtype=torch.int64, device=dev)
+cidx[order] = torch.arange(n, device=dev)
+col = cidx[ci.to(torch.int64)].to(torch.int32).contiguous()
+nsrc = int((od > 0).sum())
+y = torch.rand(nsrc, dtype=torch.float64, device=dev)
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+out = torch.empty(sms * 8 * 1024, dtype=torch.float64, device=dev)
+clk = 1.965e9
+
+
+REF = {}
+
+
+def check(colv, label):
+    # every variant sums y[col[e]] over the same whole chunks; compare the totals
+    tot = float(out.sum())
+    key = colv.data_ptr()
+    if key not in REF:
+        REF[key] = tot
+    rel = abs(tot - REF[key]) / abs(REF[key])
+    assert rel < 1e-9, (label, tot, REF[key])
+
+
+def run_tma(colv, stages, threads, label="skewed TMA gather4"):
+    ms = ctypes.c_float()
+    out.zero_()
+    rc = lib.ceiling_tma(colv.data_ptr(), colv.numel() // 128 * 128, y.data_ptr(), nsrc, stages, threads, 10,
+                         out.data_ptr(), ctypes.byref(ms))
+    assert rc == 0, rc
+    check(colv, label)
+    gps = colv.numel() / (ms.value * 1e-3) / 1e9
+    print(f"{label:38s} stages={stages} thr={threads}: {ms.value:.4f} ms  {gps:7.1f} G gathers/s  "
+          f"{gps * 1e9 / (sms * clk):.3f} gathers/SM/cycle@1965MHz", flush=True)
+
+
+def run(colv, hot, unroll, cps, label, threads=256, tier=0):
+    ms = ctypes.c_float()
+    out.zero_()
+    rc = lib.ceiling_run(colv.data_ptr(), colv.numel(), y.data_ptr(), hot, unroll, cps, 10, threads, tier, out.data_ptr(),
+                         ctypes.byref(ms))
+    assert rc == 0, rc
+    if unroll == 1:
+        check(colv, label)
+    gps = colv.numel() / (ms.value * 1e-3) / 1e9
+    print(f"{label:38s} hot={hot:6d} U={unroll} ctas/sm={cps} thr={threads} tier={tier}: {ms.value:.4f} ms  {gps:7.1f} G gathers/s  "
+          f"{gps * 1e9 / (sms * clk):.3f} gathers/SM/cycle@1965MHz", flush=True)
+
+
+print(f"{gen.name}: n={n} E={E} sources={nsrc}")
+for thr, cps in ((256, 2), (256, 3), (256, 4), (256, 6), (1024, 1), (1024, 2)):
+    for U in (1, 2, 4):
+        run(col, 0, U, cps, "skewed, L1 tier 32K", threads=thr, tier=32768)
+import sys as _s
+_s.exit(0)
+for tier in (0, 8192, 32768, 65536):
+    run(col, 0, 4, 2, "skewed, L1 tier", threads=1024, tier=tier)
+for hot in (12288, 16384, 20480):
+    for tier in (0, 32768, 65536):
+        run(col, hot, 4, 1, "skewed + hot smem + L1 tier", threads=1024, tier=tier)

@@ -24,6 +24,8 @@ if mode == "reduced":
     g.preprocess()
 st, it, fd = g.run(x, gen.d, 0.0, sweeps, mode=m | pr.PR_TIMING)
 stt = g.stats()
-print(gen.name, mode, "iters", it, "gather ms/launch", stt["gather_ms"] / max(1, stt["timed_iterations"]),
+ti = max(1, stt["timed_iterations"])
+print(gen.name, mode, "iters", it, "gather ms/launch", round(stt["gather_ms"] / ti, 4),
+      "finalize/scatter ms/launch", round(stt["scatter_ms"] / ti, 4),
       "tasks", stt["n_tasks"], "rows", stt["gather_rows"], "edges", stt["gather_edges"], "ncontrib", stt["n_contrib"])
 g.close()
