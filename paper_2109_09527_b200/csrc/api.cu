@@ -125,7 +125,7 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
         dfree(ddst, ctx.stream);
         if ((rc = build_relabel(g, ctx)) != PR_OK) break;
         if ((rc = build_view_tasks(g->plain, ctx)) != PR_OK) break;
-        if ((rc = build_view_stream(g->plain, ctx, (int32_t)g->n_contrib)) != PR_OK) break;
+        if ((rc = build_view_stream(g->plain, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx)) != PR_OK) break;
         if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) {
             set_error("pr_graph_create: %s", cudaGetErrorString(cudaGetLastError()));
             rc = PR_ECUDA;
@@ -213,6 +213,9 @@ void pr_destroy(pr_graph* g) {
     dfree(g->mem_src, s);
     dfree(g->mem_k, s);
     dfree(g->mem_srow, s);
+    dfree(g->mem_info, s);
+    dfree(g->xr, s);
+    dfree(g->xm, s);
     dfree(g->x, s);
     dfree(g->y[0], s);
     dfree(g->y[1], s);

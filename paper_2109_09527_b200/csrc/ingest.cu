@@ -408,6 +408,7 @@ void free_view(View& v, cudaStream_t s) {
     dfree(v.part_out, s);
     dfree(v.bticket, s);
     dfree(v.sums, s);
+    dfree(v.rinfo, s);
     v.nsteps = v.nspans = v.nbound = 0;
     v.span_steps = 1;
 }
@@ -498,7 +499,15 @@ struct BoundEmit {
     }
 };
 
-int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot) {
+__global__ void k_rinfo(const int32_t* __restrict__ vid, int64_t nrows, const int32_t* __restrict__ od,
+                        const int32_t* __restrict__ cidx, int2* __restrict__ info) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = vid ? vid[r] : (int32_t)r;
+        info[r] = make_int2(od[v], cidx[v]);
+    }
+}
+
+int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx) {
     cudaStream_t s = ctx.stream;
     v.nsteps = v.nspans = v.nbound = 0;
     if (v.nrows == 0 || v.nedges == 0) return PR_OK;
@@ -545,6 +554,8 @@ int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot) {
     PR_TRY(dalloc(&v.bticket, (size_t)nb, s));
     PR_CUDA(cudaMemsetAsync(v.bticket, 0, sizeof(uint32_t) * (size_t)nb, s));
     PR_TRY(dalloc(&v.sums, (size_t)v.nrows, s));
+    PR_TRY(dalloc(&v.rinfo, (size_t)v.nrows, s));
+    PR_LAUNCH(ctx, k_rinfo, grid_for(ctx, v.nrows, 256), 256, 0, (const int32_t*)v.vid, v.nrows, outdeg, cidx, v.rinfo);
     return PR_OK;
 }
 

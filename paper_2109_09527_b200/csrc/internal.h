@@ -94,6 +94,7 @@ struct View {
     double* part_out = nullptr;     // [nspans]
     uint32_t* bticket = nullptr;    // [nbound]
     double* sums = nullptr;         // [nrows] S(r) of the current sweep (K-GATHER -> K-FINALIZE)
+    int2* rinfo = nullptr;          // [nrows] (outdeg, contrib slot) of the row's vertex, row order
 };
 
 // Device-resident iteration state (one per graph).
@@ -143,9 +144,13 @@ struct pr_graph {
     int32_t* mem_src = nullptr;
     int32_t* mem_k = nullptr;
     int32_t* mem_srow = nullptr;    // reduced-view row of mem_src (K-FINALIZE reads its S)
+    int2* mem_info = nullptr;       // (outdeg, contrib slot) of each member
     prgpu::View reduced;
     // iteration buffers (allocated lazily by pr_run)
     double* x = nullptr;            // fp64[n] (used when the caller's ranks are on the host)
+    double* xr = nullptr;           // sync sweeps: x of the view's rows, row order (unpermuted at the end)
+    int64_t xr_cap = 0;
+    double* xm = nullptr;           // sync sweeps: x of the members, member order
     double* y[2] = {nullptr, nullptr};
     double* cta_partial = nullptr;  // [2 * (gather grid + scatter grid)] (L1, Linf)
     int64_t partial_cap = 0;
@@ -162,8 +167,10 @@ namespace prgpu {
 int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx);
 int build_relabel(pr_graph* g, Ctx& ctx);
 int build_view_tasks(View& v, Ctx& ctx);
-int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot);
+int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx);
 void free_view(View& v, cudaStream_t s);
+__global__ void k_rinfo(const int32_t* __restrict__ vid, int64_t nrows, const int32_t* __restrict__ od,
+                        const int32_t* __restrict__ cidx, int2* __restrict__ info);
 int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx);
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
         Ctx& ctx, int32_t* iters_out, double* delta_out);

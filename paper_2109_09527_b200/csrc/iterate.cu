@@ -227,25 +227,25 @@ __global__ void __launch_bounds__(SE_NT, 1) k_stream(StreamPolicy<HOT> p, Stream
 struct FinArgs {
     const double* sums;
     int64_t nrows;
-    const int32_t* vid;
-    const int32_t* mvid;
+    const int2* rinfo;     // (outdeg, contrib slot) per row
+    double* xr;            // x of the rows, row order
     const int32_t* msrow;
     const int32_t* mk;
+    const int2* minfo;     // (outdeg, contrib slot) per member
+    double* xm;            // x of the members, member order
     int64_t nm;
     const double* ab;
-    double* x;
     double* y_out;
-    const int32_t* od;
-    const int32_t* cidx;
     double c, d;
 };
 
 // Rows are visited grid-stride (all CTAs sweep the row space together, which
 // keeps the TLB working set small) in batches of FIN_U rows per thread whose
-// loads are all issued before any store.
+// loads are all issued before any store.  Every access is coalesced except the
+// contrib store y[slot]; x is kept in row / member order (xr, xm) during the
+// sweeps and written back to vertex order once, by k_unpermute.
 constexpr int FIN_U = 4;
 
-template <bool VID>
 __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     __shared__ double red[2 * RED_W];
     __shared__ int flag;
@@ -254,68 +254,56 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const double* __restrict__ sums = f.sums;
-    const int32_t* __restrict__ vid = f.vid;
-    const int32_t* __restrict__ od = f.od;
-    const int32_t* __restrict__ cidx = f.cidx;
-    double* __restrict__ x = f.x;
+    double* __restrict__ xr = f.xr;
     double* __restrict__ y = f.y_out;
     for (int64_t r0 = t0; r0 < f.nrows; r0 += FIN_U * T) {
         double S[FIN_U], xo[FIN_U];
-        int32_t v[FIN_U], o[FIN_U], ci[FIN_U];
+        int2 inf[FIN_U];
 #pragma unroll
         for (int u = 0; u < FIN_U; ++u) {
             const int64_t r = r0 + u * T;
-            const bool ok = r < f.nrows;
-            S[u] = ok ? __ldcs(sums + r) : 0.0;
-            v[u] = ok ? (VID ? __ldcs(vid + r) : (int32_t)r) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < FIN_U; ++u) {
-            if (v[u] >= 0) {
-                xo[u] = x[v[u]];
-                o[u] = __ldg(od + v[u]);
-                ci[u] = __ldg(cidx + v[u]);
+            if (r < f.nrows) {
+                S[u] = __ldcs(sums + r);
+                xo[u] = xr[r];
+                inf[u] = __ldg(f.rinfo + r);
             }
         }
 #pragma unroll
         for (int u = 0; u < FIN_U; ++u) {
-            if (v[u] >= 0) {
+            const int64_t r = r0 + u * T;
+            if (r < f.nrows) {
                 const double xn = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
-                x[v[u]] = xn;
-                if (o[u] > 0) y[ci[u]] = xn / (double)o[u];
+                xr[r] = xn;
+                if (inf[u].x > 0) y[inf[u].y] = xn / (double)inf[u].x;
                 const double dl = fabs(xn - xo[u]);
                 l1 += dl;
                 linf = fmax(linf, dl);
             }
         }
     }
+    double* __restrict__ xm = f.xm;
     for (int64_t i0 = t0; i0 < f.nm; i0 += FIN_U * T) {
         double S[FIN_U], xo[FIN_U];
-        int32_t m[FIN_U], k[FIN_U], q[FIN_U], o[FIN_U], ci[FIN_U];
+        int32_t k[FIN_U];
+        int2 inf[FIN_U];
 #pragma unroll
         for (int u = 0; u < FIN_U; ++u) {
             const int64_t i = i0 + u * T;
-            const bool ok = i < f.nm;
-            m[u] = ok ? __ldcs(f.mvid + i) : -1;
-            k[u] = ok ? __ldcs(f.mk + i) : 0;
-            q[u] = ok ? __ldcs(f.msrow + i) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < FIN_U; ++u) {
-            if (m[u] >= 0) {
-                S[u] = sums[q[u]];
-                xo[u] = x[m[u]];
-                o[u] = __ldg(od + m[u]);
-                ci[u] = __ldg(cidx + m[u]);
+            if (i < f.nm) {
+                k[u] = __ldg(f.mk + i);
+                S[u] = sums[__ldg(f.msrow + i)];
+                xo[u] = xm[i];
+                inf[u] = __ldg(f.minfo + i);
             }
         }
 #pragma unroll
         for (int u = 0; u < FIN_U; ++u) {
-            if (m[u] >= 0) {
+            const int64_t i = i0 + u * T;
+            if (i < f.nm) {
                 const double xs = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
                 const double xn = __dadd_rn(f.ab[2 * k[u]], __dmul_rn(f.ab[2 * k[u] + 1], xs));
-                x[m[u]] = xn;
-                if (o[u] > 0) y[ci[u]] = xn / (double)o[u];
+                xm[i] = xn;
+                if (inf[u].x > 0) y[inf[u].y] = xn / (double)inf[u].x;
                 const double dl = fabs(xn - xo[u]);
                 l1 += dl;
                 linf = fmax(linf, dl);
@@ -330,6 +318,20 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     }
     __syncthreads();
     if (flag) global_finalize(ia, red);
+}
+
+// Sync stream path: x in vertex order from the row / member ordered state.
+__global__ void k_unpermute(const double* __restrict__ xr, const int32_t* __restrict__ vid, int64_t nrows,
+                            const double* __restrict__ xm, const int32_t* __restrict__ mvid, int64_t nm,
+                            double* __restrict__ x) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += T) x[vid ? vid[r] : r] = xr[r];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += T) x[mvid[i]] = xm[i];
+}
+
+__global__ void k_fill_f64(double* __restrict__ a, int64_t cnt, double v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = v;
 }
 
 // Members (reduced mode): x_t(m) = alpha_k + beta_k * x_t(src), with
@@ -602,7 +604,19 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     ia_first.zero_ctas = zgrid;
     double* zero_partial = g->cta_partial + 2 * ((int64_t)ggrid + sctas);
     const bool gather_finalizes = !gc.stream && !(reduced && sgrid > 0);
-    FinArgs fa{v.sums, v.nrows, v.vid, g->mem_vid, g->mem_srow, g->mem_k, nm, g->ab, x, nullptr, g->outdeg, g->cidx, c, d};
+    if (gc.stream) {
+        const int64_t need_xr = std::max<int64_t>(std::max(g->plain.nrows, g->reduced.nrows), 1);
+        if (g->xr_cap < need_xr) {
+            dfree(g->xr, s);
+            PR_TRY(dalloc(&g->xr, (size_t)need_xr, s));
+            g->xr_cap = need_xr;
+        }
+        if (g->n_members > 0 && !g->xm) PR_TRY(dalloc(&g->xm, (size_t)g->n_members, s));
+        const unsigned fg = (unsigned)std::min<int64_t>((v.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+        PR_LAUNCH(ctx, k_fill_f64, fg, 256, 0, g->xr, v.nrows, 1.0 / (double)n);
+        if (nm > 0) PR_LAUNCH(ctx, k_fill_f64, fg, 256, 0, g->xm, nm, 1.0 / (double)n);
+    }
+    FinArgs fa{v.sums, v.nrows, v.rinfo, g->xr, g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, g->ab, nullptr, c, d};
 
     std::vector<cudaEvent_t> ev;
     double gather_ms = 0.0, scatter_ms = 0.0;
@@ -632,10 +646,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
             if (gc.stream) {
                 FinArgs f = fa;
                 f.y_out = y_out;
-                if (gc.vid)
-                    PR_LAUNCH(ctx, k_finalize<true>, (unsigned)fgrid, GT_NT, 0, f, ia);
-                else
-                    PR_LAUNCH(ctx, k_finalize<false>, (unsigned)fgrid, GT_NT, 0, f, ia);
+                PR_LAUNCH(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
             } else if (!gather_finalizes) {
                 if (async)
                     PR_LAUNCH(ctx, k_scatter<true>, (unsigned)sgrid, GT_NT, 0, (const int32_t*)g->mem_vid,
@@ -671,6 +682,11 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         if (batch < 64) batch *= 2;
     }
     for (auto e : ev) cudaEventDestroy(e);
+    if (gc.stream) {
+        const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+        PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
+                  (const double*)g->xm, (const int32_t*)g->mem_vid, nm, x);
+    }
     if (!ranks_dev) {
         PR_CUDA(cudaMemcpyAsync(ranks, x, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
         PR_CUDA(cudaStreamSynchronize(s));

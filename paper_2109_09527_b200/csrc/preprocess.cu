@@ -264,6 +264,8 @@ static void clear_reductions(pr_graph* g, cudaStream_t s) {
     dfree(g->mem_src, s);
     dfree(g->mem_k, s);
     dfree(g->mem_srow, s);
+    dfree(g->mem_info, s);
+    dfree(g->xm, s);
     free_view(g->reduced, s);
     g->n_members = 0;
     g->max_chain = 0;
@@ -411,7 +413,7 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
         PR_LAUNCH(ctx, k_copy_rows, grid_of(ctx, R.nrows * 32), 256, 0, (const int32_t*)R.vid, R.nrows,
                   (const int64_t*)g->row_ptr, (const int32_t*)g->plain.col, (const int64_t*)R.row_ptr, R.col);
     PR_TRY(build_view_tasks(R, ctx));
-    PR_TRY(build_view_stream(R, ctx, (int32_t)g->n_contrib));
+    PR_TRY(build_view_stream(R, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx));
     // source row of every member in the reduced view (K-FINALIZE reads its S)
     if (g->n_members > 0) {
         int32_t* rowof = nullptr;
@@ -422,6 +424,9 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
         PR_LAUNCH(ctx, k_gather_i32, grid_of(ctx, g->n_members), 256, 0, (const int32_t*)g->mem_src, g->n_members,
                   (const int32_t*)rowof, g->mem_srow);
         dfree(rowof, s);
+        PR_TRY(dalloc(&g->mem_info, (size_t)g->n_members, s));
+        PR_LAUNCH(ctx, k_rinfo, grid_of(ctx, g->n_members), 256, 0, (const int32_t*)g->mem_vid, g->n_members,
+                  (const int32_t*)g->outdeg, (const int32_t*)g->cidx, g->mem_info);
     }
     dfree(cnt, s);
     g->pre_done = true;

@@ -71,11 +71,14 @@ __device__ __forceinline__ void stream_piece(P& p, const StreamArgs& a, int32_t 
         a.part_out[span] = val;
     else
         a.part_in[span] = val;
-    __threadfence();
+    // release: the piece is visible before the ticket moves.  (A __threadfence
+    // here compiles to MEMBAR.SC + CCTL.IVALL, which would also invalidate this
+    // SM's L1 and with it the L1 tier of hot contribs.)
     const int32_t s0 = a.b_s0[b], s1 = a.b_s1[b];
-    const uint32_t t = atomicAdd(&a.bticket[b], 1u);
+    uint32_t t;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.bticket + b) : "memory");
     if (t == (uint32_t)(s1 - s0)) {
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");  // winner only: acquire the other pieces
         double sum = __ldcg(a.part_out + s0);
         for (int32_t s = s0 + 1; s <= s1; ++s) sum += __ldcg(a.part_in + s);
         p.emit((int64_t)a.b_row[b], sum);
@@ -120,11 +123,13 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
         // row starts: warp-exclusive rank of this lane's first start
         const int nf = __popc(f);
         int incl = nf;
+#ifndef PRGPU_ABL_NOISCAN
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += t;
         }
+#endif
         const int rank0 = incl - nf;
         const int nst = __shfl_sync(0xffffffffu, incl, 31);
         // in-lane segments: the i-th start (i >= 1) of this lane closes slot
@@ -149,6 +154,7 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
         if (lane == 0 && nf == 0) o = carry + o;
         double S = o;
         int F = nf > 0;
+#ifndef PRGPU_ABL_NODSCAN
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const double tS = __shfl_up_sync(0xffffffffu, S, d);
@@ -158,6 +164,7 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
                 F = tF;
             }
         }
+#endif
         double I = __shfl_up_sync(0xffffffffu, S, 1);
         if (lane == 0) I = carry;
         carry = __shfl_sync(0xffffffffu, S, 31);

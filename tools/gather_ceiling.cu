@@ -49,7 +49,12 @@ __global__ void __launch_bounds__(1024) k_flat(const int32_t* __restrict__ col, 
     constexpr int CH = 32 * 4 * U;
     const int64_t nch = E / CH;  // tail ignored (bench tool)
     double acc = 0.0;
-    for (int64_t c = warp; c < nch; c += nwarps) {
+    // tier < 0: contiguous chunk range per warp (like the stream engine's spans)
+    const bool contig = tier < 0;
+    if (contig) tier = -tier;
+    const int64_t per = (nch + nwarps - 1) / nwarps;
+    const int64_t cb = contig ? warp * per : warp, ce = contig ? min(nch, cb + per) : nch, cs = contig ? 1 : nwarps;
+    for (int64_t c = cb; c < ce; c += cs) {
         const int4* p = reinterpret_cast<const int4*>(col + c * CH) + lane;
         int4 ix[U];
 #pragma unroll

@@ -91,9 +91,9 @@ def run(colv, hot, unroll, cps, label, threads=256, tier=0):
 
 
 print(f"{gen.name}: n={n} E={E} sources={nsrc}")
-for thr, cps in ((256, 2), (256, 3), (256, 4), (256, 6), (1024, 1), (1024, 2)):
-    for U in (1, 2, 4):
-        run(col, 0, U, cps, "skewed, L1 tier 32K", threads=thr, tier=32768)
+for hot in (0, 16384):
+    for tier in (32768, -32768):
+        run(col, hot, 2, 1, "skewed hot+tier (neg tier = contiguous)", threads=1024, tier=tier)
 import sys as _s
 _s.exit(0)
 for tier in (0, 8192, 32768, 65536):
