@@ -1,3 +1,7 @@
+#include <stdlib.h>
+
+#include <chrono>
+#include <mutex>
 // api.cu -- the extern "C" boundary of libprgpu (include/prgpu.h).
 // Validation, host/device pointer handling, graph lifetime.  All compute is
 // in ingest.cu / preprocess.cu / iterate.cu.
@@ -19,6 +23,8 @@ void set_error(const char* fmt, ...) {
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
 }
+
+double g_alloc_ms = 0.0;
 
 static int make_ctx(Ctx& ctx, void* stream) {
     ctx.stream = (cudaStream_t)stream;
@@ -42,6 +48,71 @@ static int make_ctx(Ctx& ctx, void* stream) {
     return PR_OK;
 }
 
+// Grow the device pool once to `bytes` (allocate + free), so that later
+// stream-ordered allocations are carved from memory the pool already holds
+// instead of mapping new memory in the middle of a call (measured: up to
+// 60 ms per pr_graph_create under allocation churn otherwise).
+static void pool_reserve(cudaStream_t s, size_t bytes) {
+    const char* e = getenv("PRGPU_POOL_RESERVE");
+    if (e && e[0] == '0') return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t have = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have);
+    if (have >= bytes) return;
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    if (bytes > have + fr / 2) bytes = have + fr / 2;  // never take more than half of what is free
+    void* p = nullptr;
+    if (bytes > have && cudaMallocAsync(&p, bytes - have, s) == cudaSuccess) cudaFreeAsync(p, s);
+    cudaGetLastError();
+}
+
+// Pinned host copies of the per-graph DevState come from one process-wide
+// slab (cudaMallocHost / cudaFreeHost cost milliseconds and synchronise the
+// device, once per pr_graph_create / pr_destroy otherwise).
+constexpr int kSlabSlots = 256;
+static std::mutex g_slab_mu;
+static DevState* g_slab = nullptr;
+static bool g_slab_used[kSlabSlots] = {false};
+
+static DevState* pinned_state_alloc() {
+    {
+        std::lock_guard<std::mutex> lk(g_slab_mu);
+        if (!g_slab) {
+            void* p = nullptr;
+            if (cudaMallocHost(&p, sizeof(DevState) * kSlabSlots) == cudaSuccess) g_slab = (DevState*)p;
+            cudaGetLastError();
+        }
+        if (g_slab)
+            for (int i = 0; i < kSlabSlots; ++i)
+                if (!g_slab_used[i]) {
+                    g_slab_used[i] = true;
+                    return g_slab + i;
+                }
+    }
+    void* p = nullptr;  // slab exhausted: a private pinned allocation
+    if (cudaMallocHost(&p, sizeof(DevState)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return (DevState*)p;
+}
+
+static void pinned_state_free(DevState* p) {
+    if (!p) return;
+    {
+        std::lock_guard<std::mutex> lk(g_slab_mu);
+        if (g_slab && p >= g_slab && p < g_slab + kSlabSlots) {
+            g_slab_used[p - g_slab] = false;
+            return;
+        }
+    }
+    cudaFreeHost(p);
+}
+
 static bool is_device_ptr(const void* p) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -50,6 +121,60 @@ static bool is_device_ptr(const void* p) {
     }
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
+
+// PRGPU_PROFILE=1: host wall time of each phase (synchronising the stream at
+// every mark, so it perturbs the timing it reports); PRGPU_PROFILE=2: CUDA
+// events at every mark (no syncs), printed with the host time of each mark
+// when the timer is destroyed.  Diagnostics only.
+struct PhaseTimer {
+    cudaStream_t s;
+    const char* what;
+    int mode = 0;
+    std::chrono::steady_clock::time_point t0, t;
+    cudaEvent_t ev[16];
+    double host_ms[16];
+    const char* names[16];
+    int k = 0;
+    double alloc0 = g_alloc_ms;
+    PhaseTimer(cudaStream_t st, const char* w) : s(st), what(w) {
+        const char* e = getenv("PRGPU_PROFILE");
+        mode = e ? atoi(e) : 0;
+        if (mode == 1) cudaStreamSynchronize(s);
+        t0 = t = std::chrono::steady_clock::now();
+        if (mode == 2) {
+            cudaEventCreate(&ev[0]);
+            cudaEventRecord(ev[0], s);
+            k = 1;
+        }
+    }
+    void mark(const char* phase) {
+        if (mode == 1) {
+            cudaStreamSynchronize(s);
+            auto now = std::chrono::steady_clock::now();
+            fprintf(stderr, "[prgpu] %s.%s %.3f ms\n", what, phase,
+                    std::chrono::duration<double, std::milli>(now - t).count());
+            t = now;
+        } else if (mode == 2 && k < 16) {
+            cudaEventCreate(&ev[k]);
+            cudaEventRecord(ev[k], s);
+            host_ms[k] = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            names[k++] = phase;
+        }
+    }
+    ~PhaseTimer() {
+        if (mode == 2) fprintf(stderr, "[prgpu] %s host total %.3f ms, of which cudaMallocAsync %.3f ms\n", what,
+                               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+                               g_alloc_ms - alloc0);
+        if (mode != 2) return;
+        cudaEventSynchronize(ev[k - 1]);
+        for (int i = 1; i < k; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, "[prgpu] %s.%s gpu %.3f ms (host mark at %.3f ms)\n", what, names[i], ms, host_ms[i]);
+        }
+        for (int i = 0; i < k; ++i) cudaEventDestroy(ev[i]);
+    }
+};
 
 }  // namespace prgpu
 
@@ -81,6 +206,10 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
     }
     Ctx ctx;
     PR_TRY(make_ctx(ctx, stream));
+    PhaseTimer pt0(ctx.stream, "create");
+    // peak of create + preprocess + run: ~ 4 x 8 B per raw edge (sort ping-pong,
+    // views) + ~ 80 B per vertex
+    pool_reserve(ctx.stream, (size_t)m * 40 + (size_t)n * 96 + ((size_t)64 << 20));
     pr_graph* g = new (std::nothrow) pr_graph();
     if (!g) {
         set_error("pr_graph_create: host allocation failed");
@@ -94,8 +223,8 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
     int32_t* dsrc = nullptr;
     int32_t* ddst = nullptr;
     do {
-        if (cudaMallocHost(&g->st_host, sizeof(DevState)) != cudaSuccess) {
-            set_error("cudaMallocHost failed");
+        if (!(g->st_host = pinned_state_alloc())) {
+            set_error("pinned host allocation failed");
             rc = PR_ENOMEM;
             break;
         }
@@ -120,12 +249,18 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
             }
             t = ddst;
         }
+        pt0.mark("setup");
+        PhaseTimer pt(ctx.stream, "create");
         if ((rc = ingest(g, s, t, ctx)) != PR_OK) break;
+        pt.mark("ingest");
         dfree(dsrc, ctx.stream);
         dfree(ddst, ctx.stream);
         if ((rc = build_relabel(g, ctx)) != PR_OK) break;
+        pt.mark("relabel");
         if ((rc = build_view_tasks(g->plain, ctx)) != PR_OK) break;
+        pt.mark("tasks");
         if ((rc = build_view_stream(g->plain, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx)) != PR_OK) break;
+        pt.mark("stream");
         if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) {
             set_error("pr_graph_create: %s", cudaGetErrorString(cudaGetLastError()));
             rc = PR_ECUDA;
@@ -199,6 +334,7 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
 void pr_destroy(pr_graph* g) {
     if (!g) return;
     cudaStream_t s = 0;
+    PhaseTimer pt(s, "destroy");
     dfree(g->row_ptr, s);
     dfree(g->col, s);
     dfree(g->outdeg, s);
@@ -223,8 +359,9 @@ void pr_destroy(pr_graph* g) {
     dfree(g->ab, s);
     dfree(g->delta_log, s);
     dfree(g->st, s);
-    if (g->st_host) cudaFreeHost(g->st_host);
+    pinned_state_free(g->st_host);
     delete g;
+    pt.mark("all");
 }
 
 int pr_graph_info(const pr_graph* g, int64_t* n, int64_t* E, int64_t* n_members, int32_t* max_chain) {

@@ -4,11 +4,14 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <chrono>
+
 #include "../../include/prgpu.h"
 
 namespace prgpu {
 
 void set_error(const char* fmt, ...);
+extern double g_alloc_ms;  // host time spent in cudaMallocAsync (PRGPU_PROFILE diagnostics)
 
 // Return PR_ECUDA from the enclosing int function on a CUDA error.
 #define PR_CUDA(call)                                                              \
@@ -50,7 +53,9 @@ template <class T>
 int dalloc(T** p, size_t count, cudaStream_t s) {
     *p = nullptr;
     size_t bytes = count * sizeof(T) + 64;  // +64: vector tails may read past the end
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMallocAsync((void**)p, bytes, s);
+    g_alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (e != cudaSuccess) {
         set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));
         *p = nullptr;

@@ -148,12 +148,18 @@ int device_scan(Ctx& ctx, int64_t n, Get get, Emit emit, T* total_dev) {
 }
 
 // ------------------------------------------------------------ radix sort --
-constexpr int RS_NT = 256;
+// LSD radix sort, 8-bit digits, "reduce-then-scan" per pass with a fixed
+// number G of CTAs, each owning a contiguous chunk of the array (stable and
+// deterministic, no look-back).  Large tiles (RS_TILE = 8192 keys per CTA
+// step) keep the number of block barriers per key low and make each digit's
+// run in a tile ~32 keys long, so the write-out is coalesced.
+constexpr int RS_NT = 512;
 constexpr int RS_WARPS = RS_NT / 32;
-constexpr int RS_ROUNDS = 8;                       // items per thread per tile
-constexpr int RS_TILE = RS_NT * RS_ROUNDS;         // 2048
+constexpr int RS_ROUNDS = 16;                      // keys per thread per tile
+constexpr int RS_TILE = RS_NT * RS_ROUNDS;         // 8192
 constexpr int RS_BITS = 8;
 constexpr int RS_BINS = 1 << RS_BITS;
+static_assert(RS_NT >= RS_BINS, "one thread per digit in the tile scan");
 
 template <class K>
 __global__ void __launch_bounds__(RS_NT) k_rs_hist(const K* __restrict__ keys, int64_t n, int64_t per_cta,
@@ -177,6 +183,16 @@ __global__ void __launch_bounds__(RS_NT) k_rs_hist(const K* __restrict__ keys, i
     }
 }
 
+template <class K, bool HAS_V>
+struct RsSmem {
+    uint32_t base[RS_BINS];      // global start of each digit for the current tile
+    uint32_t toff[RS_BINS + 1];  // tile-local start of each digit
+    uint32_t wc[RS_WARPS][RS_BINS + 1];
+    uint32_t sw[33];
+    K sk[RS_TILE];
+    uint32_t sv[HAS_V ? RS_TILE : 1];
+};
+
 // Stable scatter of one 8-bit digit.  Per tile of RS_TILE keys: warp-level
 // ranking (match_any), tile-local digit offsets, a local sort into shared
 // memory, then a coalesced write-out (consecutive threads write consecutive
@@ -186,21 +202,16 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const K* __restrict__ kin,
                                                       K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       int64_t n, int64_t per_cta, int shift,
                                                       const uint32_t* __restrict__ offs, int64_t G) {
-    static_assert(RS_NT == RS_BINS, "one thread per digit in the tile scan");
-    __shared__ uint32_t base[RS_BINS];      // global start of each digit for the current tile
-    __shared__ uint32_t toff[RS_BINS];      // tile-local start of each digit
-    __shared__ uint32_t wc[RS_WARPS][RS_BINS + 1];
-    __shared__ uint32_t sw[33];
-    __shared__ K sk[RS_TILE];
-    __shared__ uint32_t sv[HAS_V ? RS_TILE : 1];
+    extern __shared__ __align__(16) unsigned char rs_raw[];
+    RsSmem<K, HAS_V>& sm = *reinterpret_cast<RsSmem<K, HAS_V>*>(rs_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = lanemask_lt();
-    base[threadIdx.x] = offs[(int64_t)threadIdx.x * G + blockIdx.x];
+    if (threadIdx.x < RS_BINS) sm.base[threadIdx.x] = offs[(int64_t)threadIdx.x * G + blockIdx.x];
     const int64_t b = (int64_t)blockIdx.x * per_cta;
     const int64_t e = min(n, b + per_cta);
     for (int64_t tb = b; tb < e; tb += RS_TILE) {
         const int tn = (int)min((int64_t)RS_TILE, e - tb);
-        for (int i = threadIdx.x; i < RS_WARPS * (RS_BINS + 1); i += RS_NT) (&wc[0][0])[i] = 0;
+        for (int i = threadIdx.x; i < RS_WARPS * (RS_BINS + 1); i += RS_NT) (&sm.wc[0][0])[i] = 0;
         __syncthreads();
         K k[RS_ROUNDS];
         uint32_t v[RS_ROUNDS];
@@ -209,58 +220,74 @@ __global__ void __launch_bounds__(RS_NT) k_rs_scatter(const K* __restrict__ kin,
         const int64_t s = tb + (int64_t)warp * (32 * RS_ROUNDS);
 #pragma unroll
         for (int r = 0; r < RS_ROUNDS; ++r) {
-            int64_t i = s + r * 32 + lane;
-            bool valid = i < e;
+            const int64_t i = s + r * 32 + lane;
+            const bool valid = i < e;
             k[r] = valid ? kin[i] : K(0);
             if (HAS_V) v[r] = valid ? vin[i] : 0u;
-            uint32_t d = valid ? ((uint32_t)(k[r] >> shift) & (RS_BINS - 1)) : RS_BINS;
+        }
+#pragma unroll
+        for (int r = 0; r < RS_ROUNDS; ++r) {
+            const bool valid = s + r * 32 + lane < e;
+            const uint32_t d = valid ? ((uint32_t)(k[r] >> shift) & (RS_BINS - 1)) : RS_BINS;
             dg[r] = d;
-            uint32_t peers = __match_any_sync(0xffffffffu, d);
-            uint32_t rank = __popc(peers & lt);
-            pos[r] = wc[warp][d] + rank;
+            // lanes with the same digit: 8 ballots (MATCH.ANY measured 1.6x slower here)
+            uint32_t peers = __ballot_sync(0xffffffffu, valid);
+            if (!valid) peers = ~peers;
+#pragma unroll
+            for (int bit = 0; bit < RS_BITS; ++bit) {
+                const bool on = (d >> bit) & 1u;
+                const uint32_t bb = __ballot_sync(0xffffffffu, on);
+                peers &= on ? bb : ~bb;
+            }
+            const uint32_t rank = __popc(peers & lt);
+            pos[r] = sm.wc[warp][d] + rank;
             __syncwarp();
-            if ((peers & lt) == 0) wc[warp][d] += __popc(peers);
+            if ((peers & lt) == 0) sm.wc[warp][d] += __popc(peers);
             __syncwarp();
         }
         __syncthreads();
         {   // digit d = threadIdx.x: tile count, tile-local offset, per-warp offsets
             const int d = threadIdx.x;
             uint32_t cnt = 0;
+            if (d < RS_BINS) {
 #pragma unroll
-            for (int w = 0; w < RS_WARPS; ++w) cnt += wc[w][d];
-            uint32_t tot;
-            const uint32_t off = block_exclusive_sum(cnt, &tot, sw);
-            toff[d] = off;
-            uint32_t run = off;
-#pragma unroll
-            for (int w = 0; w < RS_WARPS; ++w) {
-                const uint32_t c = wc[w][d];
-                wc[w][d] = run;
-                run += c;
+                for (int w = 0; w < RS_WARPS; ++w) cnt += sm.wc[w][d];
             }
+            uint32_t tot;
+            const uint32_t off = block_exclusive_sum(cnt, &tot, sm.sw);
+            if (d < RS_BINS) {
+                sm.toff[d] = off;
+                uint32_t run = off;
+#pragma unroll
+                for (int w = 0; w < RS_WARPS; ++w) {
+                    const uint32_t c = sm.wc[w][d];
+                    sm.wc[w][d] = run;
+                    run += c;
+                }
+            }
+            if (d == 0) sm.toff[RS_BINS] = (uint32_t)tn;
         }
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < RS_ROUNDS; ++r) {
             if (dg[r] < RS_BINS) {
-                const uint32_t lp = wc[warp][dg[r]] + pos[r];
-                sk[lp] = k[r];
-                if (HAS_V) sv[lp] = v[r];
+                const uint32_t lp = sm.wc[warp][dg[r]] + pos[r];
+                sm.sk[lp] = k[r];
+                if (HAS_V) sm.sv[lp] = v[r];
             }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < tn; i += RS_NT) {
-            const K key = sk[i];
+            const K key = sm.sk[i];
             const uint32_t d = (uint32_t)(key >> shift) & (RS_BINS - 1);
-            const uint32_t dst = base[d] + (uint32_t)i - toff[d];
+            const int64_t dst = (int64_t)sm.base[d] + (i - (int64_t)sm.toff[d]);
             kout[dst] = key;
-            if (HAS_V) vout[dst] = sv[i];
+            if (HAS_V) vout[dst] = sm.sv[i];
         }
         __syncthreads();
-        {   // advance the digit bases past this tile
+        if (threadIdx.x < RS_BINS) {  // advance the digit bases past this tile
             const int d = threadIdx.x;
-            const uint32_t end = (d + 1 < RS_BINS) ? toff[d + 1] : (uint32_t)tn;
-            base[d] += end - toff[d];
+            sm.base[d] += sm.toff[d + 1] - sm.toff[d];
         }
         __syncthreads();
     }
@@ -274,8 +301,17 @@ int radix_sort(Ctx& ctx, K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_al
                int begin_bit, int end_bit, bool* in_alt) {
     *in_alt = false;
     if (n <= 1 || end_bit <= begin_bit) return PR_OK;
+    if (n > (int64_t)UINT32_MAX) {
+        set_error("radix_sort: %lld keys exceed the 32-bit digit offsets", (long long)n);
+        return PR_EINVAL;
+    }
+    const size_t smem = sizeof(RsSmem<K, HAS_V>);
+    PR_CUDA(cudaFuncSetAttribute(k_rs_scatter<K, HAS_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rs_scatter<K, HAS_V>, RS_NT, smem));
+    if (per_sm < 1) per_sm = 1;
     int64_t G = (n + RS_TILE - 1) / RS_TILE;
-    int64_t cap = (int64_t)ctx.num_sms * 4;
+    const int64_t cap = (int64_t)ctx.num_sms * per_sm;
     if (G > cap) G = cap;
     int64_t per = (n + G - 1) / G;
     per = (per + RS_TILE - 1) / RS_TILE * RS_TILE;
@@ -291,7 +327,7 @@ int radix_sort(Ctx& ctx, K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_al
         PR_LAUNCH(ctx, (k_rs_hist<K>), (unsigned)G, RS_NT, 0, (const K*)kin, n, per, shift, hist, G);
         PR_LAUNCH(ctx, (k_scan_partials<uint32_t>), 1, 1024, 0, hist, (int64_t)RS_BINS * G,
                   (uint32_t*)nullptr);
-        PR_LAUNCH(ctx, (k_rs_scatter<K, HAS_V>), (unsigned)G, RS_NT, 0, (const K*)kin,
+        PR_LAUNCH(ctx, (k_rs_scatter<K, HAS_V>), (unsigned)G, RS_NT, smem, (const K*)kin,
                   (const uint32_t*)vin, kout, vout, n, per, shift, (const uint32_t*)hist, G);
         K* tk = kin; kin = kout; kout = tk;
         uint32_t* tv = vin; vin = vout; vout = tv;
