@@ -6,10 +6,12 @@
 // Pipeline (all hand-written kernels):
 //   pack    validate ids, drop self-loops, key = dst << b | src   (b = bits(n-1))
 //   sort    LSD radix sort of the keys on 2b bits (8-bit digits)  -> (dst, src) order
-//   unique  adjacent-different flags -> scan -> col_idx / row dst  (dedup)
-//   rows    in-degree histogram (run-aggregated atomics) -> scan -> row_ptr
+//   unique  adjacent-different flags -> scan -> col_idx and row_ptr in one
+//           pass (dedup; row starts from dst changes)
 //   outdeg  histogram of src over the deduplicated edges
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "internal.h"
 #include "primitives.cuh"
@@ -41,65 +43,102 @@ __global__ void k_check_ids(const int32_t* __restrict__ src, const int32_t* __re
     if (__any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
 }
 
-// In-degree histogram over the sorted unique dst array, one atomic per run of
-// equal dst within a thread's 16 consecutive positions (hub rows are long runs).
-__global__ void k_indeg(const uint32_t* __restrict__ udst, int64_t E, int32_t* __restrict__ indeg) {
-    constexpr int R = 16;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * R;
-    for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * R; b0 < E; b0 += stride) {
-        int64_t e1 = min(E, b0 + R);
-        uint32_t cur = udst[b0];
-        int run = 1;
-        for (int64_t p = b0 + 1; p < e1; ++p) {
-            uint32_t d = udst[p];
-            if (d == cur) {
-                ++run;
-            } else {
-                atomicAdd(&indeg[cur], run);
-                cur = d;
-                run = 1;
-            }
-        }
-        atomicAdd(&indeg[cur], run);
-    }
-}
-
 __global__ void k_outdeg(const int32_t* __restrict__ col, int64_t E, int32_t* __restrict__ outdeg) {
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(&outdeg[col[e]], 1);
 }
 
-struct UniqueGet {
-    const uint64_t* k;
-    uint64_t sentinel;
-    __device__ int64_t operator()(int64_t i) const {
-        const uint64_t key = k[i];
-        return (key != sentinel && (i == 0 || key != k[i - 1])) ? 1 : 0;
-    }
-};
-struct UniqueEmit {
-    const uint64_t* k;
-    int32_t* col;
-    uint32_t* udst;
-    int b;
-    uint64_t mask;
-    __device__ void operator()(int64_t i, int64_t pos, int64_t v) const {
-        if (v) {
-            uint64_t key = k[i];
-            col[pos] = (int32_t)(key & mask);
-            udst[pos] = (uint32_t)(key >> b);
+// ---- dedup + CSR in one pass over the sorted keys --------------------------
+// Key i is kept iff it is not the sentinel and differs from key i-1.
+// Kept key i lands at p = its rank among kept keys: col[p] = src; and when it
+// starts row d = dst (dst of key i-1 differs, or i == 0), row_ptr[d'+1 .. d]
+// = p for the previous dst d' (rows in between have in-degree 0).  Reduce-
+// then-scan with UQ_G fixed chunks (deterministic); tiles are staged through
+// shared memory so global loads and the col stores are coalesced.
+constexpr int UQ_NT = 256;
+constexpr int UQ_IPT = 12;
+constexpr int UQ_TILE = UQ_NT * UQ_IPT;
+
+__device__ __forceinline__ bool uq_kept(const uint64_t* k, int64_t i, uint64_t sentinel) {
+    const uint64_t key = k[i];
+    return key != sentinel && (i == 0 || key != k[i - 1]);
+}
+
+__global__ void __launch_bounds__(UQ_NT) k_uniq_count(const uint64_t* __restrict__ k, int64_t n, int64_t per_cta,
+                                                      uint64_t sentinel, int64_t* __restrict__ partial) {
+    __shared__ int64_t sw[33];
+    const int64_t b = (int64_t)blockIdx.x * per_cta;
+    const int64_t e = min(n, b + per_cta);
+    int64_t c = 0;
+    for (int64_t i = b + threadIdx.x; i < e; i += UQ_NT) c += uq_kept(k, i, sentinel) ? 1 : 0;
+    const int64_t tot = block_sum(c, sw);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict__ k, int64_t n, int64_t per_cta,
+                                                     uint64_t sentinel, int b, int64_t nv,
+                                                     const int64_t* __restrict__ partial,
+                                                     const int64_t* __restrict__ total, int32_t* __restrict__ col,
+                                                     int64_t* __restrict__ row_ptr) {
+    __shared__ uint64_t sk[UQ_TILE + 1];
+    __shared__ int32_t so[UQ_TILE];
+    __shared__ int64_t sw[33];
+    const uint64_t mask = (1ull << b) - 1;
+    const int64_t cb = (int64_t)blockIdx.x * per_cta;
+    const int64_t ce = min(n, cb + per_cta);
+    int64_t base = partial[blockIdx.x];
+    const int64_t E = *total;
+    for (int64_t tb = cb; tb < ce; tb += UQ_TILE) {
+        const int tn = (int)min((int64_t)UQ_TILE, ce - tb);
+        for (int i = threadIdx.x; i < tn; i += UQ_NT) sk[i + 1] = k[tb + i];
+        if (threadIdx.x == 0) sk[0] = tb > 0 ? k[tb - 1] : ~0ull;
+        __syncthreads();
+        // blocked: thread t owns tile items [t*IPT, t*IPT + IPT)
+        const int j0 = threadIdx.x * UQ_IPT;
+        uint32_t keep = 0;
+        int cnt = 0;
+#pragma unroll
+        for (int j = 0; j < UQ_IPT; ++j) {
+            const int i = j0 + j;
+            if (i < tn) {
+                const uint64_t key = sk[i + 1];
+                const bool kp = key != sentinel && (tb + i == 0 || key != sk[i]);
+                keep |= (uint32_t)kp << j;
+                cnt += kp;
+            }
         }
+        int64_t tile_tot;
+        const int64_t off = block_exclusive_sum((int64_t)cnt, &tile_tot, sw);
+        int64_t q = off;
+#pragma unroll
+        for (int j = 0; j < UQ_IPT; ++j) {
+            if (keep & (1u << j)) {
+                const int i = j0 + j;
+                const uint64_t key = sk[i + 1];
+                so[q] = (int32_t)(key & mask);
+                const int64_t d = (int64_t)(key >> b);
+                const int64_t dp = (tb + i == 0) ? -1 : (int64_t)(sk[i] >> b);
+                const int64_t p = base + q;
+                for (int64_t r = dp + 1; r <= d; ++r) row_ptr[r] = p;   // first edge of row d
+                ++q;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < UQ_IPT; ++j) {  // the last real key (kept or a duplicate) closes every later row
+            const int i = j0 + j;
+            if (i < tn) {
+                const uint64_t key = sk[i + 1];
+                if (key != sentinel &&
+                    (tb + i + 1 == n || (i + 1 < tn ? sk[i + 2] : k[tb + i + 1]) == sentinel))
+                    for (int64_t r = (int64_t)(key >> b) + 1; r <= nv; ++r) row_ptr[r] = E;
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < (int)tile_tot; i += UQ_NT) col[base + i] = so[i];
+        base += tile_tot;
+        __syncthreads();
     }
-};
-struct I32Get {
-    const int32_t* a;
-    int64_t n;
-    __device__ int64_t operator()(int64_t i) const { return i < n ? (int64_t)a[i] : 0; }
-};
-struct RowPtrEmit {
-    int64_t* row_ptr;
-    __device__ void operator()(int64_t i, int64_t pos, int64_t) const { row_ptr[i] = pos; }
-};
+}
 
 int read_count(Ctx& ctx, const int64_t* dev, int64_t* host) {
     PR_CUDA(cudaMemcpyAsync(host, dev, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
@@ -129,9 +168,10 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
     const int64_t mk = b > 0 ? m : 0;
     const uint64_t sentinel = b > 0 ? ((2 * b >= 64) ? ~0ull : ((1ull << (2 * b)) - 1)) : 0ull;
 
-    // pack, sort by (dst, src), deduplicate
-    uint32_t* udst = nullptr;
+    // pack, sort by (dst, src), deduplicate + CSR (row_ptr, col_idx) in one pass
     PR_TRY(dalloc(&g->col, (size_t)(mk > 0 ? mk : 1), s));
+    PR_TRY(dalloc(&g->row_ptr, (size_t)n + 1, s));
+    PR_CUDA(cudaMemsetAsync(g->row_ptr, 0, sizeof(int64_t) * (size_t)(n + 1), s));  // E == 0: all rows empty
     if (mk > 0) {
         PR_TRY(dalloc(&keys, (size_t)mk, s));
         PR_LAUNCH(ctx, k_pack, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, sentinel, keys,
@@ -140,9 +180,17 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
         bool alt = false;
         PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, 2 * b, &alt)));
         const uint64_t* sorted = alt ? keys_alt : keys;
-        PR_TRY(dalloc(&udst, (size_t)mk, s));
-        PR_TRY((device_scan<int64_t>(ctx, mk, UniqueGet{sorted, sentinel},
-                                     UniqueEmit{sorted, g->col, udst, b, (1ull << b) - 1}, scratch)));
+        int64_t G = std::min<int64_t>((mk + UQ_TILE - 1) / UQ_TILE, (int64_t)ctx.num_sms * 4);
+        int64_t per = (mk + G - 1) / G;
+        per = (per + UQ_TILE - 1) / UQ_TILE * UQ_TILE;
+        G = (mk + per - 1) / per;
+        int64_t* part = nullptr;
+        PR_TRY(dalloc(&part, (size_t)G, s));
+        PR_LAUNCH(ctx, k_uniq_count, (unsigned)G, UQ_NT, 0, sorted, mk, per, sentinel, part);
+        PR_LAUNCH(ctx, (k_scan_partials<int64_t>), 1, 1024, 0, part, G, scratch);
+        PR_LAUNCH(ctx, k_uniq_emit, (unsigned)G, UQ_NT, 0, sorted, mk, per, sentinel, b, n, (const int64_t*)part,
+                  (const int64_t*)scratch, g->col, g->row_ptr);
+        dfree(part, s);
         dfree(keys, s);
         dfree(keys_alt, s);
     } else if (m > 0) {  // n == 1: still validate the ids
@@ -152,27 +200,17 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
     PR_CUDA(cudaMemcpyAsync(h, scratch, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     PR_CUDA(cudaStreamSynchronize(s));
     if (h[1] != 0) {
-        dfree(udst, s);
         dfree(scratch, s);
         set_error("pr_graph_create: vertex id outside [0, n)");
         return PR_EINVAL;
     }
     g->E = h[0];
 
-    // row_ptr from the in-degree histogram; outdeg from the sources
-    int32_t* indeg = nullptr;
-    PR_TRY(dalloc(&indeg, (size_t)n, s));
-    PR_TRY(dalloc(&g->row_ptr, (size_t)n + 1, s));
+    // outdeg from the sources of the deduplicated edges
     PR_TRY(dalloc(&g->outdeg, (size_t)n, s));
-    PR_CUDA(cudaMemsetAsync(indeg, 0, sizeof(int32_t) * (size_t)n, s));
     PR_CUDA(cudaMemsetAsync(g->outdeg, 0, sizeof(int32_t) * (size_t)n, s));
-    if (g->E > 0) {
-        PR_LAUNCH(ctx, k_indeg, grid_for(ctx, (g->E + 15) / 16, 256), 256, 0, (const uint32_t*)udst, g->E, indeg);
+    if (g->E > 0)
         PR_LAUNCH(ctx, k_outdeg, grid_for(ctx, g->E, 256), 256, 0, (const int32_t*)g->col, g->E, g->outdeg);
-    }
-    PR_TRY((device_scan<int64_t>(ctx, n + 1, I32Get{indeg, n}, RowPtrEmit{g->row_ptr}, (int64_t*)nullptr)));
-    dfree(indeg, s);
-    dfree(udst, s);
     dfree(scratch, s);
     return PR_OK;
 }

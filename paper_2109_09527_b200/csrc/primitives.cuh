@@ -153,10 +153,19 @@ int device_scan(Ctx& ctx, int64_t n, Get get, Emit emit, T* total_dev) {
 // deterministic, no look-back).  Large tiles (RS_TILE = 8192 keys per CTA
 // step) keep the number of block barriers per key low and make each digit's
 // run in a tile ~32 keys long, so the write-out is coalesced.
-constexpr int RS_NT = 512;
+#ifndef PRGPU_RS_NT
+#define PRGPU_RS_NT 512
+#endif
+#ifndef PRGPU_RS_ROUNDS
+#define PRGPU_RS_ROUNDS 8
+#endif
+#ifndef PRGPU_RS_MINB
+#define PRGPU_RS_MINB 2
+#endif
+constexpr int RS_NT = PRGPU_RS_NT;
 constexpr int RS_WARPS = RS_NT / 32;
-constexpr int RS_ROUNDS = 16;                      // keys per thread per tile
-constexpr int RS_TILE = RS_NT * RS_ROUNDS;         // 8192
+constexpr int RS_ROUNDS = PRGPU_RS_ROUNDS;         // keys per thread per tile
+constexpr int RS_TILE = RS_NT * RS_ROUNDS;
 constexpr int RS_BITS = 8;
 constexpr int RS_BINS = 1 << RS_BITS;
 static_assert(RS_NT >= RS_BINS, "one thread per digit in the tile scan");
@@ -198,7 +207,7 @@ struct RsSmem {
 // memory, then a coalesced write-out (consecutive threads write consecutive
 // addresses of one digit's run).
 template <class K, bool HAS_V>
-__global__ void __launch_bounds__(RS_NT) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(RS_NT, PRGPU_RS_MINB) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       int64_t n, int64_t per_cta, int shift,
                                                       const uint32_t* __restrict__ offs, int64_t G) {
