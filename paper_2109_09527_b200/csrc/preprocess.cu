@@ -3,8 +3,10 @@
 //
 // Identical groups: v ~ w iff in(v) == in(w) as sets (after dedup); rep(v) =
 // min id of the class; the empty in-set is one class.
-//   1. row hash h(v) = mix(indeg) + sum_{u in in(v)} mix(u)  (row engine)
-//   2. stable radix sort of vertex ids by h  -> runs of equal hash, ids ascending
+//   1. row hash h(v) = mix(indeg) + sum_{u in in(v)} mix(u)  (row engine), for
+//      the rows of in-degree > 0 (the in-degree-0 vertices are one class)
+//   2. stable radix sort of those ids by the top 48 bits of h -> runs of equal
+//      bits, ids ascending
 //   3. exact verification of every member against the run's first vertex; on a
 //      hash collision the vertex scans its run for the first equal row.
 // Chains: chain(v) <=> indeg 1 and outdeg 1; pred(v) = the in-neighbour.
@@ -30,11 +32,11 @@ struct HashPolicy {
         return mix64((uint64_t)(uint32_t)u * 0x9E3779B97F4A7C15ULL + 0x2545F4914F6CDD1DULL);
     }
     struct Pre {
-        int64_t v, deg;
+        int64_t r, v, deg;
     };
     __device__ __forceinline__ Pre prefetch(int64_t r) const {
         const int64_t v = vid ? vid[r] : r;
-        return Pre{v, rp[v + 1] - rp[v]};
+        return Pre{r, v, rp[v + 1] - rp[v]};
     }
     Pre pre[2];
     __device__ __forceinline__ void prefetch_rows(int64_t r0, int nr, int lane) {
@@ -43,16 +45,21 @@ struct HashPolicy {
     }
     __device__ __forceinline__ const Pre& prefetched(int h) const { return pre[h]; }
     __device__ __forceinline__ double finalize(const Pre& q, uint64_t s) const {
-        out[q.v] = s + mix64((uint64_t)q.deg + kDegSalt);
+        out[q.r] = s + mix64((uint64_t)q.deg + kDegSalt);  // by view row
         return 0.0;
     }
 };
 
-// Hash of the empty in-set, for the rows the plain view leaves out.
-__global__ void k_hash_empty(uint64_t* __restrict__ h, int64_t n) {
-    const uint64_t e = mix64(kDegSalt);
+// The empty in-set is one class: its vertices (zlist, ascending) all
+// get the smallest of them as representative.
+__global__ void k_rep_empty(const int32_t* __restrict__ zl, int64_t nz, int32_t* __restrict__ rep) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += (int64_t)gridDim.x * blockDim.x)
+        rep[zl[i]] = zl[0];
+}
+
+__global__ void k_u32_from(const int32_t* __restrict__ a, int64_t n, uint32_t* __restrict__ out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        h[i] = e;
+        out[i] = a ? (uint32_t)a[i] : (uint32_t)i;
 }
 
 __global__ void __launch_bounds__(GT_NT) k_rowhash(HashPolicy p, EngineArgs a) {
@@ -62,10 +69,6 @@ __global__ void __launch_bounds__(GT_NT) k_rowhash(HashPolicy p, EngineArgs a) {
     engine_run(p, a, sm, l1, linf);
 }
 
-__global__ void k_iota(uint32_t* __restrict__ a, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        a[i] = (uint32_t)i;
-}
 
 __device__ __forceinline__ bool same_row(const int64_t* rp, const int32_t* col, int32_t u, int32_t v) {
     const int64_t du = rp[u + 1] - rp[u];
@@ -77,9 +80,9 @@ __device__ __forceinline__ bool same_row(const int64_t* rp, const int32_t* col, 
     return true;
 }
 
-struct RunGet {
+struct RunGet {  // runs of equal top-48 hash bits (the sorted bits)
     const uint64_t* h;
-    __device__ int64_t operator()(int64_t i) const { return (i == 0 || h[i] != h[i - 1]) ? 1 : 0; }
+    __device__ int64_t operator()(int64_t i) const { return (i == 0 || (h[i] >> 16) != (h[i - 1] >> 16)) ? 1 : 0; }
 };
 struct RunEmit {
     int32_t* rid;
@@ -275,18 +278,21 @@ static void clear_reductions(pr_graph* g, cudaStream_t s) {
 
 static int find_identical(pr_graph* g, Ctx& ctx) {
     cudaStream_t s = ctx.stream;
-    const int64_t n = g->n;
     uint64_t* h = nullptr;
     uint64_t* h2 = nullptr;
     uint32_t* sv = nullptr;
     uint32_t* sv2 = nullptr;
-    PR_TRY(dalloc(&h, (size_t)n, s));
-    PR_TRY(dalloc(&h2, (size_t)n, s));
-    PR_TRY(dalloc(&sv, (size_t)n, s));
-    PR_TRY(dalloc(&sv2, (size_t)n, s));
+    // only the rows of in-degree > 0 are hashed and sorted; the in-degree-0
+    // vertices form the empty class directly
     const View& v = g->plain;
+    const int64_t nr = v.nrows;
+    if (g->nz > 0) PR_LAUNCH(ctx, k_rep_empty, grid_of(ctx, g->nz), 256, 0, (const int32_t*)g->zlist, g->nz, g->rep);
+    if (nr == 0) return PR_OK;
+    PR_TRY(dalloc(&h, (size_t)nr, s));
+    PR_TRY(dalloc(&h2, (size_t)nr, s));
+    PR_TRY(dalloc(&sv, (size_t)nr, s));
+    PR_TRY(dalloc(&sv2, (size_t)nr, s));
     {
-        if (v.vid) PR_LAUNCH(ctx, k_hash_empty, grid_of(ctx, n), 256, 0, h, n);
         HashPolicy p{g->row_ptr, v.vid, h, {}};
         EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, g->col, v.hub_partial, v.hub_delta, v.hub_ticket};
         int per_sm = 0;
@@ -297,17 +303,19 @@ static int find_identical(pr_graph* g, Ctx& ctx) {
         if (grid < 1) grid = 1;
         PR_LAUNCH(ctx, k_rowhash, (unsigned)grid, GT_NT, sizeof(EngineSmem), p, a);
     }
-    PR_LAUNCH(ctx, k_iota, grid_of(ctx, n), 256, 0, sv, n);
+    PR_LAUNCH(ctx, k_u32_from, grid_of(ctx, nr), 256, 0, (const int32_t*)v.vid, nr, sv);
+    // stable sort of the rows (ids ascending) by the top 48 hash bits; equal
+    // top bits of different rows (p ~ nr^2/2^49) are split by k_verify
     bool alt = false;
-    PR_TRY((radix_sort<uint64_t, true>(ctx, h, h2, sv, sv2, n, 0, 64, &alt)));
+    PR_TRY((radix_sort<uint64_t, true>(ctx, h, h2, sv, sv2, nr, 16, 64, &alt)));
     const uint64_t* hs = alt ? h2 : h;
     const uint32_t* svs = alt ? sv2 : sv;
     int32_t* rid = nullptr;
     int64_t* rstart = nullptr;
-    PR_TRY(dalloc(&rid, (size_t)n, s));
-    PR_TRY(dalloc(&rstart, (size_t)n, s));
-    PR_TRY((device_scan<int64_t>(ctx, n, RunGet{hs}, RunEmit{rid, rstart}, (int64_t*)nullptr)));
-    PR_LAUNCH(ctx, k_verify, grid_of(ctx, n), 256, 0, svs, (const int32_t*)rid, (const int64_t*)rstart, n,
+    PR_TRY(dalloc(&rid, (size_t)nr, s));
+    PR_TRY(dalloc(&rstart, (size_t)nr, s));
+    PR_TRY((device_scan<int64_t>(ctx, nr, RunGet{hs}, RunEmit{rid, rstart}, (int64_t*)nullptr)));
+    PR_LAUNCH(ctx, k_verify, grid_of(ctx, nr), 256, 0, svs, (const int32_t*)rid, (const int64_t*)rstart, nr,
               (const int64_t*)g->row_ptr, (const int32_t*)g->col, g->rep);
     dfree(h, s);
     dfree(h2, s);
