@@ -229,15 +229,35 @@ struct PosEmit {
     __device__ void operator()(int64_t i, int64_t pos, int64_t) const { out[i] = pos; }
 };
 
+// Reduced view col: rows vid[i] of the plain view's col, packed at rpR[i].
+// Edge-parallel: every warp copies a fixed 1024-edge range of the OUTPUT
+// (binary search for its first row, then row segment by row segment), so a
+// mega-hub row is spread over many warps instead of serialising one.
+constexpr int CR_CHUNK = 1024;
 __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const int64_t* __restrict__ rp,
                             const int32_t* __restrict__ col, const int64_t* __restrict__ rpR, int32_t* __restrict__ colR) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = w0; i < nr; i += nw) {
-        const int32_t v = vid[i];
-        const int64_t s = rp[v], len = rp[v + 1] - s, o = rpR[i];
-        for (int64_t k = lane; k < len; k += 32) colR[o + k] = col[s + k];
+    const int64_t ER = rpR[nr];
+    for (int64_t o0 = w0 * CR_CHUNK; o0 < ER; o0 += nw * CR_CHUNK) {
+        const int64_t o1 = min(ER, o0 + CR_CHUNK);
+        int64_t lo = 0, hi = nr;  // last row i with rpR[i] <= o0
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (rpR[mid] <= o0)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        int64_t i = lo, o = o0;
+        while (o < o1) {
+            const int64_t re = min(o1, rpR[i + 1]);
+            const int64_t src = rp[vid[i]] + (o - rpR[i]);
+            for (int64_t k = lane; k < re - o; k += 32) colR[o + k] = col[src + k];
+            o = re;
+            ++i;
+        }
     }
 }
 
