@@ -449,6 +449,12 @@ void free_view(View& v, cudaStream_t s) {
     dfree(v.rinfo, s);
     v.nsteps = v.nspans = v.nbound = 0;
     v.span_steps = 1;
+    if (v.seg) {
+        for (int i = 0; i < v.nseg; ++i) free_view(v.seg[i], s);
+        delete[] v.seg;
+        v.seg = nullptr;
+    }
+    v.nseg = 0;
 }
 
 int build_view_tasks(View& v, Ctx& ctx) {
@@ -591,9 +597,12 @@ int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg
     const int64_t nb = v.nbound > 0 ? v.nbound : 1;
     PR_TRY(dalloc(&v.bticket, (size_t)nb, s));
     PR_CUDA(cudaMemsetAsync(v.bticket, 0, sizeof(uint32_t) * (size_t)nb, s));
-    PR_TRY(dalloc(&v.sums, (size_t)v.nrows, s));
-    PR_TRY(dalloc(&v.rinfo, (size_t)v.nrows, s));
-    PR_LAUNCH(ctx, k_rinfo, grid_for(ctx, v.nrows, 256), 256, 0, (const int32_t*)v.vid, v.nrows, outdeg, cidx, v.rinfo);
+    if (outdeg) {  // a top-level view (sub-views of a blocked view accumulate into their parent's sums)
+        PR_TRY(dalloc(&v.sums, (size_t)v.nrows, s));
+        PR_TRY(dalloc(&v.rinfo, (size_t)v.nrows, s));
+        PR_LAUNCH(ctx, k_rinfo, grid_for(ctx, v.nrows, 256), 256, 0, (const int32_t*)v.vid, v.nrows, outdeg, cidx,
+                  v.rinfo);
+    }
     return PR_OK;
 }
 

@@ -94,6 +94,12 @@ struct View {
     double* part_out = nullptr;     // [nspans]
     uint32_t* bticket = nullptr;    // [nbound]
     double* sums = nullptr;         // [nrows] S(r) of the current sweep (K-GATHER -> K-FINALIZE)
+    // source-blocked form (blocked.cu), for contrib vectors larger than L2:
+    // seg[i] holds the edges whose contrib slot lies in [i << seg_bits, (i+1) << seg_bits),
+    // rows in view order; its vid maps a sub-view row to the row of THIS view
+    int nseg = 0;
+    int seg_bits = 0;
+    View* seg = nullptr;
     int2* rinfo = nullptr;          // [nrows] (outdeg, contrib slot) of the row's vertex, row order
 };
 
@@ -168,6 +174,7 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx);
 int build_relabel(pr_graph* g, Ctx& ctx);
 int build_view_tasks(View& v, Ctx& ctx);
 int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx);
+int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib);
 void free_view(View& v, cudaStream_t s);
 __global__ void k_rinfo(const int32_t* __restrict__ vid, int64_t nrows, const int32_t* __restrict__ od,
                         const int32_t* __restrict__ cidx, int2* __restrict__ info);

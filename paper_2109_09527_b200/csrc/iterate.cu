@@ -79,6 +79,7 @@ constexpr int RED_W = 32;
 // HOT: contribs [0, hot_n) are read from the CTA's shared-memory copy.
 template <bool HOT>
 struct StreamPolicy {
+    static constexpr bool kHot = HOT;
     const double* y_in;
     double* sums;
     const double* hot;
@@ -90,6 +91,53 @@ struct StreamPolicy {
         return ld_gather_tiered_f64(y_in + u, u < SE_L1_TIER, pol_last);
     }
     __device__ __forceinline__ void emit(int64_t r, double s) const { sums[r] = s; }
+    __device__ __forceinline__ void prep(int64_t, uint32_t) {}
+    __device__ __forceinline__ void emit_at(int, int64_t r, double s) const { sums[r] = s; }
+    __device__ __forceinline__ void emit_first(int64_t r, double s) const { sums[r] = s; }
+};
+
+// One segment pass of a source-blocked view (blocked.cu): gathers come from
+// one L2-resident slice of y; S_seg(r) is added to the parent row's sum.
+struct AccumPolicy {
+    static constexpr bool kHot = false;
+    const double* y_in;
+    double* sums;
+    const int32_t* map;  // sub-view row -> parent view row
+    const double* hot;
+    int32_t hot_n;
+    uint64_t pol_last;
+
+    // the slice is re-read ~20x per pass: keep it in L2 against the streams
+    // of col, flags, parent ids and the sums updates (evict_first / default)
+    __device__ __forceinline__ double load(int32_t u) const {
+        double r;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(y_in + u), "l"(pol_last));
+        return r;
+    }
+    // S(parent) += S_seg as a fire-and-forget red.add: each parent row gets
+    // at most one per pass and passes are serial launches, so the additions
+    // happen in segment order (deterministic).  The parent ids of a step's
+    // closures are prefetched by prep() before the gathers are consumed.
+    int32_t m_first;
+    int32_t m[SE_V];
+    __device__ __forceinline__ static void red_add(double* p, double v) {
+#ifdef PRGPU_RED_EVICT_FIRST
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+        asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+#endif
+    }
+    __device__ __forceinline__ void prep(int64_t base, uint32_t f) {
+        if (f) m_first = __ldg(map + base);
+#pragma unroll
+        for (int j = 0; j < SE_V; ++j)
+            if (f & (1u << j)) m[j] = __ldg(map + base + __popc(f & ((1u << j) - 1)));
+    }
+    __device__ __forceinline__ void emit(int64_t r, double s) const { red_add(sums + map[r], s); }
+    __device__ __forceinline__ void emit_at(int j, int64_t, double s) const { red_add(sums + m[j], s); }
+    __device__ __forceinline__ void emit_first(int64_t, double s) const { red_add(sums + m_first, s); }
 };
 
 struct IterArgs {
@@ -201,12 +249,12 @@ __global__ void __launch_bounds__(GT_NT, GT_MIN_CTAS)
 
 // K-GATHER, edge-stream form: S(r) of every row of the view into sums[r].
 // One CTA of SE_NT threads per SM; no Delta here (K-FINALIZE computes it).
-template <bool HOT>
-__global__ void __launch_bounds__(SE_NT, 1) k_stream(StreamPolicy<HOT> p, StreamArgs a, const DevState* st) {
+template <class P>
+__global__ void __launch_bounds__(SE_NT, 1) k_stream(P p, StreamArgs a, const DevState* st) {
     extern __shared__ __align__(16) double hot_smem[];
     if (st->done) return;
     p.pol_last = policy_evict_last();
-    if (HOT) {
+    if (P::kHot) {
         const double2* src = reinterpret_cast<const double2*>(p.y_in);
         double2* dst = reinterpret_cast<double2*>(hot_smem);
         for (int i = threadIdx.x; i < (p.hot_n >> 1); i += blockDim.x) dst[i] = __ldcg(src + i);
@@ -446,14 +494,24 @@ static int launch_tasks_t(Ctx& ctx, const View& v, const double* y_in, double* y
 static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
                          double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
     if (gc.stream) {
-        StreamArgs a{v.col,     (const uint8_t*)v.sflags, v.step_row, v.nsteps, v.span_steps, v.nspans, v.bin,
-                     v.bout,    v.b_row, v.b_s0, v.b_s1, v.part_in, v.part_out, v.bticket};
-        if (gc.hot_n > 0) {
+        auto args = [](const View& w) {
+            return StreamArgs{w.col,  (const uint8_t*)w.sflags, w.step_row, w.nsteps, w.span_steps, w.nspans, w.bin,
+                              w.bout, w.b_row, w.b_s0, w.b_s1, w.part_in, w.part_out, w.bticket};
+        };
+        if (v.nseg > 0) {  // source-blocked: S = 0, then one accumulating pass per slot segment
+            PR_CUDA(cudaMemsetAsync(v.sums, 0, sizeof(double) * (size_t)v.nrows, ctx.stream));
+            for (int q = 0; q < v.nseg; ++q) {
+                const View& sv = v.seg[q];
+                if (sv.nspans == 0) continue;
+                AccumPolicy p{y_in, v.sums, sv.vid, nullptr, 0, 0, 0, {}};
+                PR_LAUNCH(ctx, k_stream<AccumPolicy>, gc.grid, gc.nt, 0, p, args(sv), (const DevState*)g->st);
+            }
+        } else if (gc.hot_n > 0) {
             StreamPolicy<true> p{y_in, v.sums, nullptr, gc.hot_n, 0};
-            PR_LAUNCH(ctx, k_stream<true>, gc.grid, gc.nt, gc.smem, p, a, (const DevState*)g->st);
+            PR_LAUNCH(ctx, k_stream<StreamPolicy<true>>, gc.grid, gc.nt, gc.smem, p, args(v), (const DevState*)g->st);
         } else {
             StreamPolicy<false> p{y_in, v.sums, nullptr, 0, 0};
-            PR_LAUNCH(ctx, k_stream<false>, gc.grid, gc.nt, gc.smem, p, a, (const DevState*)g->st);
+            PR_LAUNCH(ctx, k_stream<StreamPolicy<false>>, gc.grid, gc.nt, gc.smem, p, args(v), (const DevState*)g->st);
         }
         return PR_OK;
     }
@@ -465,7 +523,8 @@ static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_
 }
 
 static const void* gather_fn(const GatherCfg& gc) {
-    if (gc.stream) return gc.hot_n > 0 ? (const void*)k_stream<true> : (const void*)k_stream<false>;
+    if (gc.stream)
+        return gc.hot_n > 0 ? (const void*)k_stream<StreamPolicy<true>> : (const void*)k_stream<StreamPolicy<false>>;
     if (gc.async) return gc.vid ? (const void*)k_gather<true, true> : (const void*)k_gather<true, false>;
     return gc.vid ? (const void*)k_gather<false, true> : (const void*)k_gather<false, false>;
 }
@@ -483,7 +542,7 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, Gathe
     gc->vid = v.vid != nullptr;
     gc->hot_n = 0;
     if (gc->stream) {
-        int hot = env_int("PRGPU_HOT", SE_HOT_MAX);
+        int hot = v.nseg > 0 ? 0 : env_int("PRGPU_HOT", SE_HOT_MAX);
         if (hot > SE_HOT_MAX) hot = SE_HOT_MAX;
         if (hot > g->n_contrib) hot = (int)g->n_contrib;
         if (hot < 0) hot = 0;
@@ -501,7 +560,11 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, Gathe
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)ctx.num_sms * per_sm;
     const int wpc = gc->nt / 32;
-    const int64_t units = gc->stream ? v.nspans : v.ntasks;
+    int64_t units = gc->stream ? v.nspans : v.ntasks;
+    if (gc->stream && v.nseg > 0) {
+        units = 0;
+        for (int q = 0; q < v.nseg; ++q) units = std::max<int64_t>(units, v.seg[q].nspans);
+    }
     int64_t ctas_needed = (units + wpc - 1) / wpc;
     if (grid > ctas_needed) grid = ctas_needed;
     if (grid < 1) grid = 1;

@@ -442,6 +442,7 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
                   (const int64_t*)g->row_ptr, (const int32_t*)g->plain.col, (const int64_t*)R.row_ptr, R.col);
     PR_TRY(build_view_tasks(R, ctx));
     PR_TRY(build_view_stream(R, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx));
+    PR_TRY(build_view_blocked(R, ctx, g->n_contrib));
     // source row of every member in the reduced view (K-FINALIZE reads its S)
     if (g->n_members > 0) {
         int32_t* rowof = nullptr;

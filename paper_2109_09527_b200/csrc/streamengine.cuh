@@ -1,6 +1,8 @@
 // streamengine.cuh -- the edge-stream engine behind K-GATHER (sync / reduced /
 // async sweeps).  It computes, for every row r of a View,
-//     S(r) = sum_{e in row r} y[col[e]]       and calls  emit(r, S(r)),
+//     S(r) = sum_{e in row r} y[col[e]]       and calls  emit(r, S(r))
+// (emit_at(j, ...) / emit_first(...) for the closures of a step, after
+// prep(first row, start bits) let the policy prefetch per-row data),
 // i.e. the sum of Eq.(1) over in-neighbours, as ONE flat pass over
 // the view's col array with no per-row work units.  It only emits S(r) (one
 // store per row, no loads): the rank update, fused contrib and Delta run in the
@@ -132,6 +134,7 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
 #endif
         const int rank0 = incl - nf;
         const int nst = __shfl_sync(0xffffffffu, incl, 31);
+        p.prep((int64_t)R0 - 1 + rank0, f);  // policy may prefetch per-row data of this lane's closures
         // in-lane segments: the i-th start (i >= 1) of this lane closes slot
         // rank0 + i, i.e. row R0 - 1 + rank0 + i, with the lane-local segment
         double run = 0.0, head = 0.0;
@@ -142,7 +145,7 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
                 if (i == 0) {
                     head = run;
                 } else {
-                    p.emit((int64_t)R0 - 1 + rank0 + i, run);
+                    p.emit_at(j, (int64_t)R0 - 1 + rank0 + i, run);
                 }
                 ++i;
                 run = 0.0;
@@ -174,7 +177,7 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
                 if (bin >= 0) stream_piece(p, a, bin, span, val, false);
                 // else: the span begins with a row start; slot 0 is the previous span's row
             } else {
-                p.emit((int64_t)R0 - 1 + rank0, val);
+                p.emit_first((int64_t)R0 - 1 + rank0, val);
             }
         }
         if (nst > 0) first_closure = false;

@@ -116,3 +116,37 @@ def test_stream_deterministic_across_graph_builds(pr):
             g.preprocess()
             xs.append(gpu_run(pr, g, gen.n, 1e-10, mode=pr.PR_USE_REDUCTIONS)[3])
     assert np.array_equal(xs[0], xs[1])
+
+
+@pytest.mark.parametrize("bits", [3, 6, 10])
+def test_blocked_segments_match_oracle(pr, monkeypatch, bits):
+    """Source-blocked sweeps (PRGPU_SEG_BITS forces 2^bits contrib slots per
+    segment): the per-segment partial sums add up to the oracle's result."""
+    monkeypatch.setenv("PRGPU_SEG_BITS", str(bits))
+    n, s, t = hub_graph()
+    ref_g = oracle.build_csr(n, s, t)
+    ref = oracle.pagerank(ref_g, D, 1e-12, 1000)
+    rep_o = oracle.identical(ref_g)
+    cs_o, ck_o, _ = oracle.chains(ref_g, rep_o)
+    ref_r = oracle.pagerank(ref_g, D, 1e-12, 1000, reduced=True, rep=rep_o, chain_k=ck_o)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        st, it, fd, x = gpu_run(pr, g, n, 1e-12)
+        assert_iters(it, ref, 1e-12)
+        assert_close(x, ref.x)
+        a = gpu_run(pr, g, n, 1e-12)[3]
+        assert np.array_equal(a, x)                      # deterministic
+        g.preprocess()
+        st, it, fd, xr = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS)
+        assert_iters(it, ref_r, 1e-12)
+        assert_close(xr, ref_r.x)
+
+
+def test_blocked_rmat(pr, monkeypatch):
+    monkeypatch.setenv("PRGPU_SEG_BITS", "8")
+    gen = graphgen.make_config(4, scale_override=14)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    ref = oracle.pagerank(ref_g, D, 1e-10, 1000)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        st, it, fd, x = gpu_run(pr, g, gen.n, 1e-10)
+        assert_iters(it, ref, 1e-10)
+        assert_close(x, ref.x)

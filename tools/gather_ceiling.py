@@ -91,9 +91,11 @@ def run(colv, hot, unroll, cps, label, threads=256, tier=0):
 
 
 print(f"{gen.name}: n={n} E={E} sources={nsrc}")
-for hot in (0, 16384):
-    for tier in (32768, -32768):
-        run(col, hot, 2, 1, "skewed hot+tier (neg tier = contiguous)", threads=1024, tier=tier)
+for mb in (4, 8, 16, 24, 32, 48, 64, 96):
+    slots = mb * (1 << 20) // 8
+    u = torch.randint(0, min(slots, nsrc), (E,), dtype=torch.int32, device=dev)
+    run(u, 0, 4, 2, f"uniform over {mb} MB", threads=1024)
+    del u
 import sys as _s
 _s.exit(0)
 for tier in (0, 8192, 32768, 65536):
