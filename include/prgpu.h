@@ -58,6 +58,15 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
 #define PR_USE_REDUCTIONS 4u  /* compute one vertex per identical group, resolve chain
                                  members from their head; needs pr_preprocess */
 #define PR_TIMING         8u  /* record CUDA events around every gather launch (bench) */
+#define PR_MODE_NOSYNC   16u  /* persistent barrier-free No-Sync kernel with thread-level
+                                 (here: CTA-level) convergence (Alg.3 P:535-565, P:416-418;
+                                 SURVEY f1): one launch, every CTA sweeps its own static work
+                                 in place until the sum (L1) / max (L-inf) of the deltas the
+                                 CTAs last published is <= threshold; then the residual
+                                 ||F(x) - x|| of the ORIGINAL system is certified by one
+                                 synchronous gather and the kernel is relaunched if it is
+                                 above threshold.  iterations = the largest number of local
+                                 sweeps of any CTA. */
 
 /*
  * pr_graph_create -- build the in-edge CSR and out-degrees on the device
@@ -95,7 +104,8 @@ int pr_preprocess(pr_graph *g, uint32_t flags, void *stream);
  *   d          damping, 0 < d < 1 ("initialized to 0.85")
  *   threshold  >= 0 (P:438 uses 1e-16 with L-inf; configs use 1e-10 / 1e-12 L1)
  *   max_iter   >= 1; reaching it returns PR_NOT_CONVERGED with valid ranks
- *   mode       PR_MODE_* | PR_NORM_* | PR_USE_REDUCTIONS | PR_TIMING
+ *   mode       PR_MODE_SYNC | PR_MODE_ASYNC | PR_MODE_NOSYNC, | PR_NORM_* |
+ *              PR_USE_REDUCTIONS | PR_TIMING
  *   ranks      fp64[n] output in vertex-id order (host or device, caller-owned)
  *   iters_out  (host, nullable) number of update sweeps including the final
  *              one that met the stop test (Q-I)
@@ -156,6 +166,9 @@ typedef struct {
     int64_t scatter_members;    /* members one scatter launch processes (0 plain) */
     int64_t n_contrib;          /* vertices with outdeg > 0 (size of the contrib vector) */
     int64_t n_tasks;            /* row-block + hub-chunk tasks of the gather launch */
+    int32_t nosync_min_iters;   /* PR_MODE_NOSYNC: fewest local sweeps of any CTA */
+    int32_t nosync_launches;    /* PR_MODE_NOSYNC: persistent launches (1 + relaunches) */
+    double  residual;           /* PR_MODE_NOSYNC: certified ||F(x) - x|| (run norm) at exit */
 } pr_run_stats;
 
 int pr_get_run_stats(const pr_graph *g, pr_run_stats *out);

@@ -35,6 +35,7 @@ PR_NORM_L1 = 0
 PR_NORM_LINF = 2
 PR_USE_REDUCTIONS = 4
 PR_TIMING = 8
+PR_MODE_NOSYNC = 16
 
 # every symbol include/prgpu.h declares (tests check the .so exports them)
 ABI_SYMBOLS = (
@@ -66,6 +67,9 @@ class pr_run_stats(ctypes.Structure):
         ("scatter_members", ctypes.c_int64),
         ("n_contrib", ctypes.c_int64),
         ("n_tasks", ctypes.c_int64),
+        ("nosync_min_iters", ctypes.c_int32),
+        ("nosync_launches", ctypes.c_int32),
+        ("residual", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -316,8 +316,12 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
         set_error("pr_run: max_iter=%d < 1", max_iter);
         return PR_EINVAL;
     }
-    if (mode & ~(PR_MODE_ASYNC | PR_NORM_LINF | PR_USE_REDUCTIONS | PR_TIMING)) {
+    if (mode & ~(PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_NORM_LINF | PR_USE_REDUCTIONS | PR_TIMING)) {
         set_error("pr_run: unknown mode bits 0x%x", mode);
+        return PR_EINVAL;
+    }
+    if ((mode & PR_MODE_ASYNC) && (mode & PR_MODE_NOSYNC)) {
+        set_error("pr_run: PR_MODE_ASYNC and PR_MODE_NOSYNC are exclusive");
         return PR_EINVAL;
     }
     if ((mode & PR_USE_REDUCTIONS) && !g->pre_done) {
@@ -414,8 +418,7 @@ int pr_get_delta_log(const pr_graph* g, double* log, int32_t cap) {
         set_error("pr_get_delta_log: bad arguments");
         return PR_EINVAL;
     }
-    int32_t k = g->last.iterations;
-    if (k > g->log_cap) k = g->log_cap;
+    int32_t k = g->log_len;
     if (k > cap) k = cap;
     if (k > 0) PR_CUDA(cudaMemcpy(log, g->delta_log, sizeof(double) * 2 * (size_t)k, cudaMemcpyDeviceToHost));
     return k;

@@ -163,6 +163,7 @@ struct pr_graph {
     double* ab = nullptr;           // chain alpha/beta [2 * (max_chain+1)]
     double* delta_log = nullptr;    // [2 * log_cap]
     int32_t log_cap = 0;
+    int32_t log_len = 0;            // entries of delta_log written by the last pr_run
     prgpu::DevState* st = nullptr;
     prgpu::DevState* st_host = nullptr;  // pinned
     int64_t launches = 0;

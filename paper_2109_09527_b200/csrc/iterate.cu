@@ -8,6 +8,7 @@
 // vertices (Q-R) and the loop runs "while err > threshold" (Q-S).
 #include <math.h>
 #include <stdlib.h>
+#include <algorithm>
 #include <vector>
 
 #include "internal.h"
@@ -471,6 +472,99 @@ __global__ void k_init(double* __restrict__ x, double* __restrict__ y, const int
     }
 }
 
+// ------------------------------------------------------ No-Sync --
+// Persistent barrier-free kernel (Alg.3 "No-Sync"): every CTA sweeps
+// its own static share of the row tasks (and of the members) in place --
+// gathers read whatever contribs are visible (relaxed loads), every row's x and
+// y are written at once (relaxed stores) -- and after each local sweep publishes
+// its (L1, L-inf) delta; it stops when the sum (L1) / max (L-inf) over the
+// deltas all CTAs last published is <= tau ("thread-level convergence",
+// P:416-418, with the per-iteration reset of Q-E).  No grid barrier: a CTA
+// never waits for another one.  Grid = resident CTAs only (a CTA must not wait
+// for an unscheduled CTA's first delta, which starts at +big).
+struct NoSyncArgs {
+    double* err;        // [2 * grid] (L1, Linf) of each CTA's last local sweep
+    int32_t* iters;     // [grid] local sweeps of each CTA, over all launches
+    int norm_linf;
+    double tau;
+    int32_t max_local;  // local sweeps allowed in this launch
+    const int32_t* mvid;
+    const int32_t* msrc;
+    const int32_t* mk;
+    int64_t nm;
+    int64_t mper;
+    const double* ab;
+    double* x;
+    double* y;
+    const int32_t* od;
+    const int32_t* cidx;
+};
+
+template <bool VID>
+__global__ void __launch_bounds__(GT_NT, GT_MIN_CTAS) k_nosync(PRPolicy<true, VID> p, EngineArgs a, NoSyncArgs na) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
+    __shared__ double res[2];
+    p.begin();
+    const int64_t mb = (int64_t)blockIdx.x * na.mper;
+    const int64_t me = min(na.nm, mb + na.mper);
+    uint32_t kbase = 0;  // per-warp mbarrier phase count across local sweeps (lane 0 uses it)
+    for (int it = 1;; ++it) {
+        double l1 = 0.0, linf = 0.0;
+        engine_run(p, a, sm, l1, linf, &kbase);
+        for (int64_t i = mb + threadIdx.x; i < me; i += blockDim.x) {  // members (Q-C)
+            const int32_t v = na.mvid[i], sv = na.msrc[i], k = na.mk[i];
+            const double xs = ld_relaxed_f64(na.x + sv);
+            const double xn = __dadd_rn(na.ab[2 * k], __dmul_rn(na.ab[2 * k + 1], xs));
+            const double xo = na.x[v];
+            st_relaxed_f64(na.x + v, xn);
+            const int32_t o = na.od[v];
+            if (o > 0) st_relaxed_f64(na.y + na.cidx[v], xn / (double)o);
+            const double dl = fabs(xn - xo);
+            l1 += dl;
+            linf = fmax(linf, dl);
+        }
+        block_delta(l1, linf, sm.red, res);
+        if (threadIdx.x == 0) {
+            st_relaxed_f64(na.err + 2 * blockIdx.x, res[0]);
+            st_relaxed_f64(na.err + 2 * blockIdx.x + 1, res[1]);
+            na.iters[blockIdx.x] += 1;
+            double tot = 0.0, mx = 0.0;
+            for (unsigned c = 0; c < gridDim.x; ++c) {
+                tot += ld_relaxed_f64(na.err + 2 * c);
+                mx = fmax(mx, ld_relaxed_f64(na.err + 2 * c + 1));
+            }
+            const double nv = na.norm_linf ? mx : tot;
+            sm.flag = (nv <= na.tau || it >= na.max_local) ? 1 : 0;
+        }
+        __syncthreads();
+        if (sm.flag) break;
+    }
+}
+
+// Certificate of a No-Sync result: ||F(x) - x|| of the ORIGINAL system, with
+// S(r) from one synchronous edge-stream gather of the plain view over the
+// current contribs (F(x) = c + d*M*x, Eq.(1)); ||x - x*||_1 <= ||F(x)-x||_1/(1-d).
+// (Sum by atomics: not bit-reproducible in its last digits; it is a check.)
+template <bool VID>
+__global__ void k_residual(const double* __restrict__ sums, int64_t nrows, const int32_t* __restrict__ vid,
+                           const double* __restrict__ x, double c, double d, double* out) {
+    __shared__ double red[2 * RED_W];
+    __shared__ double res[2];
+    double l1 = 0.0, linf = 0.0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = VID ? vid[r] : (int32_t)r;
+        const double dl = fabs(__dadd_rn(c, __dmul_rn(d, sums[r])) - x[v]);
+        l1 += dl;
+        linf = fmax(linf, dl);
+    }
+    block_delta(l1, linf, red, res);
+    if (threadIdx.x == 0) {
+        atomicAdd(out, res[0]);
+        atomicMax(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)__double_as_longlong(res[1]));
+    }
+}
+
 // ------------------------------------------------------------------- host --
 
 struct GatherCfg {
@@ -535,9 +629,9 @@ static int env_int(const char* name, int dflt) {
 }
 
 // Kernel variant, dynamic shared memory and persistent grid (all resident CTAs).
-static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, GatherCfg* gc) {
+static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, GatherCfg* gc, bool force_stream = false) {
     const char* eng = getenv("PRGPU_ENGINE");
-    gc->stream = !async && !(eng && eng[0] == 't');
+    gc->stream = !async && (force_stream || !(eng && eng[0] == 't'));
     gc->async = async;
     gc->vid = v.vid != nullptr;
     gc->hot_n = 0;
@@ -572,8 +666,12 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, Gathe
     return PR_OK;
 }
 
+static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
+                      int32_t* iters_out, double* delta_out);
+
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
         int32_t* iters_out, double* delta_out) {
+    if (mode & PR_MODE_NOSYNC) return run_nosync(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     cudaStream_t s = ctx.stream;
     const bool async = (mode & PR_MODE_ASYNC) != 0;
     const bool reduced = (mode & PR_USE_REDUCTIONS) != 0;
@@ -756,6 +854,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         ++host_syncs;
     }
     pr_run_stats& rs = g->last;
+    g->log_len = std::min<int32_t>(hs->iters, g->log_cap);
     rs.iterations = hs->iters;
     rs.status = hs->status;
     rs.delta_l1 = hs->l1;
@@ -773,6 +872,172 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     if (iters_out) *iters_out = hs->iters;
     if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
     return hs->status;
+}
+
+// ---------------------------------------------------------------- No-Sync --
+static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
+                      int32_t* iters_out, double* delta_out) {
+    cudaStream_t s = ctx.stream;
+    const bool reduced = (mode & PR_USE_REDUCTIONS) != 0;
+    const int64_t n = g->n;
+    const View& v = reduced ? g->reduced : g->plain;
+    const int64_t nm = reduced ? g->n_members : 0;
+    const int64_t launches0 = ctx.launches;
+    cudaPointerAttributes at{};
+    const bool ranks_dev = cudaPointerGetAttributes(&at, ranks) == cudaSuccess &&
+                           (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    double* x = ranks;
+    if (!ranks_dev) {
+        if (!g->x) PR_TRY(dalloc(&g->x, (size_t)n, s));
+        x = g->x;
+    }
+    const int64_t ny = g->n_contrib + 1;
+    for (int b = 0; b < 2; ++b)
+        if (!g->y[b]) {
+            PR_TRY(dalloc(&g->y[b], (size_t)ny, s));
+            PR_CUDA(cudaMemsetAsync(g->y[b] + g->n_contrib, 0, sizeof(double), s));
+        }
+    double* y = g->y[0];
+    GatherCfg gc;  // row-task engine, persistent grid (all resident CTAs)
+    PR_TRY(gather_config(ctx, v, g, true, &gc));
+    GatherCfg gp;  // certificate: synchronous edge-stream gather of the plain view
+    PR_TRY(gather_config(ctx, g->plain, g, false, &gp, true));
+    const int grid = gc.grid;
+    const double c = (1.0 - d) / (double)n;
+    if (reduced && nm > 0) {
+        std::vector<double> ab(2 * ((size_t)g->max_chain + 1));
+        ab[0] = 0.0;
+        ab[1] = 1.0;
+        for (int k = 1; k <= g->max_chain; ++k) {
+            ab[2 * k] = c + d * ab[2 * (k - 1)];
+            ab[2 * k + 1] = d * ab[2 * (k - 1) + 1];
+        }
+        dfree(g->ab, s);
+        PR_TRY(dalloc(&g->ab, ab.size(), s));
+        PR_CUDA(cudaMemcpyAsync(g->ab, ab.data(), ab.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    const int log_cap = max_iter < 4096 ? max_iter : 4096;
+    if (g->log_cap < log_cap) {
+        dfree(g->delta_log, s);
+        PR_TRY(dalloc(&g->delta_log, (size_t)(2 * log_cap), s));
+        g->log_cap = log_cap;
+    }
+    const int64_t cap4 = (int64_t)ctx.num_sms * 4;
+    const int64_t nz = g->nz;
+    int64_t zgrid = nz > 0 ? std::min<int64_t>((nz + GT_NT * 4 - 1) / (GT_NT * 4), cap4) : 0;
+    const int64_t zper = zgrid > 0 ? (nz + zgrid - 1) / zgrid : 0;
+    // scratch: err[2*grid] | residual[2] | zero-row partials[2*zgrid]; iters[grid]
+    double* scratch = nullptr;
+    int32_t* iters = nullptr;
+    PR_TRY(dalloc(&scratch, (size_t)(2 * grid + 2 + 2 * zgrid), s));
+    PR_TRY(dalloc(&iters, (size_t)grid, s));
+    PR_CUDA(cudaMemsetAsync(iters, 0, sizeof(int32_t) * (size_t)grid, s));
+    double* err = scratch;
+    double* resid = scratch + 2 * grid;
+    DevState* hs = g->st_host;
+    *hs = DevState{};
+    hs->max_iter = max_iter;
+    hs->tau = tau;
+    PR_CUDA(cudaMemcpyAsync(g->st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
+    PR_LAUNCH(ctx, k_init, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, x, y,
+              (const int32_t*)g->outdeg, (const int32_t*)g->cidx, n, 1.0 / (double)n);
+    // in-degree-0 vertices take their fixed value c (Q-Z) before the first sweep
+    if (zgrid > 0)
+        PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y,
+                  (const int32_t*)g->outdeg, (const int32_t*)g->cidx, resid + 2);
+    const int64_t mper = nm > 0 ? (nm + grid - 1) / grid : 0;
+    NoSyncArgs na{err, iters, (mode & PR_NORM_LINF) ? 1 : 0, tau, 0, g->mem_vid, g->mem_src, g->mem_k, nm, mper,
+                  g->ab, x, y, g->outdeg, g->cidx};
+    PRPolicy<true, true> pv{y, y, x, g->outdeg, g->cidx, v.vid, c, d, 0, {}};
+    PRPolicy<true, false> pn{y, y, x, g->outdeg, g->cidx, v.vid, c, d, 0, {}};
+    EngineArgs ea{v.tasks, v.ntasks, v.hubs, v.row_ptr, v.col, v.hub_partial, v.hub_delta, v.hub_ticket, 1};
+    const void* fn = gc.vid ? (const void*)k_nosync<true> : (const void*)k_nosync<false>;
+    PR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gc.smem));
+    int per_sm = 0;
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GT_NT, gc.smem));
+    if ((int64_t)grid > (int64_t)ctx.num_sms * std::max(per_sm, 1)) {
+        set_error("pr_run(NOSYNC): grid %d exceeds the resident CTAs", grid);
+        return PR_ECUDA;
+    }
+    std::vector<int32_t> hit(grid);
+    std::vector<double> hlog;
+    int32_t max_it = 0, min_it = 0, launches = 0, status = PR_NOT_CONVERGED;
+    double r_l1 = 0.0, r_linf = 0.0;
+    const View& pv_view = g->plain;
+    while (true) {
+        PR_LAUNCH(ctx, k_fill_f64, 1, 256, 0, err, (int64_t)(2 * grid), 1e300);
+        na.max_local = max_iter - max_it;
+        if (gc.vid)
+            PR_LAUNCH(ctx, k_nosync<true>, (unsigned)grid, GT_NT, gc.smem, pv, ea, na);
+        else
+            PR_LAUNCH(ctx, k_nosync<false>, (unsigned)grid, GT_NT, gc.smem, pn, ea, na);
+        ++launches;
+        // certificate: S over the current contribs, then ||F(x) - x||
+        PR_CUDA(cudaMemsetAsync(resid, 0, 2 * sizeof(double), s));
+        IterArgs dummy{g->st, nullptr, 0, 0, 0, nullptr, 0, nullptr};
+        PR_TRY(launch_gather(ctx, pv_view, y, nullptr, x, g, c, d, dummy, gp, 0));
+        const unsigned rg = (unsigned)std::min<int64_t>((pv_view.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 8);
+        if (pv_view.nrows > 0) {
+            if (pv_view.vid)
+                PR_LAUNCH(ctx, k_residual<true>, rg, 256, 0, (const double*)pv_view.sums, pv_view.nrows,
+                          (const int32_t*)pv_view.vid, (const double*)x, c, d, resid);
+            else
+                PR_LAUNCH(ctx, k_residual<false>, rg, 256, 0, (const double*)pv_view.sums, pv_view.nrows,
+                          (const int32_t*)nullptr, (const double*)x, c, d, resid);
+        }
+        double hr[2];
+        PR_CUDA(cudaMemcpyAsync(hr, resid, sizeof(hr), cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaMemcpyAsync(hit.data(), iters, sizeof(int32_t) * (size_t)grid, cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        r_l1 = hr[0];
+        r_linf = hr[1];
+        max_it = *std::max_element(hit.begin(), hit.end());
+        min_it = *std::min_element(hit.begin(), hit.end());
+        hlog.push_back(r_l1);
+        hlog.push_back(r_linf);
+        const double rn = (mode & PR_NORM_LINF) ? r_linf : r_l1;
+        if (rn <= tau) {
+            status = PR_OK;
+            break;
+        }
+        if (max_it >= max_iter) break;
+    }
+    // delta log: the certified residual after each persistent launch
+    const int nlog = std::min<int>((int)hlog.size() / 2, log_cap);
+    if (nlog > 0)
+        PR_CUDA(cudaMemcpyAsync(g->delta_log, hlog.data(), sizeof(double) * 2 * nlog, cudaMemcpyHostToDevice, s));
+    g->log_len = nlog;
+    hs->iters = max_it;
+    hs->log_cap = log_cap;
+    hs->status = status;
+    hs->l1 = r_l1;
+    hs->linf = r_linf;
+    hs->done = 1;
+    PR_CUDA(cudaMemcpyAsync(g->st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
+    if (!ranks_dev) PR_CUDA(cudaMemcpyAsync(ranks, x, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
+    dfree(scratch, s);
+    dfree(iters, s);
+    PR_CUDA(cudaStreamSynchronize(s));
+    pr_run_stats& rs = g->last;
+    rs = pr_run_stats{};
+    rs.iterations = max_it;
+    rs.status = status;
+    rs.delta_l1 = r_l1;
+    rs.delta_linf = r_linf;
+    rs.run_launches = ctx.launches - launches0;
+    rs.host_syncs = launches + 1;
+    rs.gather_rows = v.nrows;
+    rs.gather_edges = v.nedges;
+    rs.scatter_members = nm;
+    rs.n_contrib = g->n_contrib;
+    rs.n_tasks = v.ntasks;
+    rs.nosync_min_iters = min_it;
+    rs.nosync_launches = launches;
+    rs.residual = (mode & PR_NORM_LINF) ? r_linf : r_l1;
+    if (iters_out) *iters_out = max_it;
+    if (delta_out) *delta_out = rs.residual;
+    return status;
 }
 
 }  // namespace prgpu

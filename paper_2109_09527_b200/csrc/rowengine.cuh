@@ -40,6 +40,7 @@ struct EngineArgs {
     void* hub_partial;
     double* hub_delta;
     uint32_t* hub_ticket;
+    int hub_local = 0;  // also add a hub row's |delta| to the finalizing warp's (l1, linf) (No-Sync kernel)
 };
 
 struct __align__(16) WarpSmem {
@@ -168,22 +169,34 @@ __device__ __forceinline__ void engine_chunk_end(P& p, const EngineArgs& a, cons
         T* hp = reinterpret_cast<T*>(a.hub_partial);
         hp[h.slot + j] = part;
         __threadfence();
-        const uint32_t t = atomicAdd(&a.hub_ticket[tk.hub], 1u);
+        // wrapping ticket (atomicInc: nchunks-1 -> 0): no separate reset, so it
+        // also works when chunks of different sweeps interleave (persistent
+        // No-Sync kernel: the finalize then reads each chunk's latest partial)
+        const uint32_t t = atomicInc(&a.hub_ticket[tk.hub], (uint32_t)h.nchunks - 1);
         if (t == (uint32_t)h.nchunks - 1) {
             __threadfence();
             const T* hq = reinterpret_cast<const T*>(a.hub_partial);
             T s = T(0);
             for (int c = 0; c < h.nchunks; ++c) s += __ldcg(hq + h.slot + c);
-            a.hub_delta[tk.hub] = p.finalize(p.prefetch((int64_t)tk.r0), s);
-            a.hub_ticket[tk.hub] = 0u;
+            const double dh = p.finalize(p.prefetch((int64_t)tk.r0), s);
+            a.hub_delta[tk.hub] = dh;
+            if (a.hub_local) {
+                l1 += dh;
+                linf = fmax(linf, dh);
+            }
         }
     }
 }
 
 // Runs every task assigned to this warp.  The per-thread (l1, linf)
 // accumulators therefore depend only on the static assignment.
+// kbase (optional, per warp, persistent kernels): pieces this warp's
+// barriers have completed in earlier calls -- the barriers are initialised
+// once (kbase == 0) and later calls continue their phase sequence (an
+// mbarrier must not be re-initialised while it is in use).
 template <class P>
-__device__ __forceinline__ void engine_run(P& p, const EngineArgs& a, EngineSmem& sm, double& l1, double& linf) {
+__device__ __forceinline__ void engine_run(P& p, const EngineArgs& a, EngineSmem& sm, double& l1, double& linf,
+                                           uint32_t* kbase = nullptr) {
     using T = typename P::T;
     constexpr int K = WT_PIECE / 32;
     const int lane = threadIdx.x & 31;
@@ -193,7 +206,8 @@ __device__ __forceinline__ void engine_run(P& p, const EngineArgs& a, EngineSmem
     WarpSmem& ws = sm.w[warp];
     if (t >= a.ntasks) return;
     const uint64_t pol = policy_evict_first();
-    if (lane == 0) {
+    const uint32_t k0 = kbase ? *kbase : 0u;
+    if (lane == 0 && k0 == 0) {
         mbar_init(&ws.bar[0], 1);
         mbar_init(&ws.bar[1], 1);
         fence_mbar_init();
@@ -201,9 +215,12 @@ __device__ __forceinline__ void engine_run(P& p, const EngineArgs& a, EngineSmem
     __syncwarp();
     Task cur = a.tasks[t];
     int j = 0;  // piece of cur
-    if (lane == 0) stage_cols(a, cur.e0, min(task_nnz(cur), WT_PIECE), ws.colbuf[0], &ws.bar[0], pol);
+    if (lane == 0) {
+        if (k0) fence_proxy_async_smem();  // the buffer was last read by the generic proxy
+        stage_cols(a, cur.e0, min(task_nnz(cur), WT_PIECE), ws.colbuf[k0 & 1], &ws.bar[k0 & 1], pol);
+    }
     T part = T(0);
-    for (uint32_t k = 0;; ++k) {
+    for (uint32_t k = k0;; ++k) {
         const int b = k & 1;
         // next piece: the rest of this chunk, else the first piece of the next task
         Task nt = cur;
@@ -242,7 +259,10 @@ __device__ __forceinline__ void engine_run(P& p, const EngineArgs& a, EngineSmem
             if (j + 1 == task_pieces(cur)) engine_chunk_end(p, a, cur, part, l1, linf);
         }
         __syncwarp();
-        if (!has_next) break;
+        if (!has_next) {
+            if (kbase) *kbase = k + 1;
+            break;
+        }
         cur = nt;
         j = nj;
         t = ntn;

@@ -1,0 +1,46 @@
+"""Time-to-converge and iteration counts of the sync, async and No-Sync modes
+on config k at its own threshold (the analogue of the paper's Fig.7).
+Usage: python tools/converge_compare.py [config=4] [reps=3]"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import graphgen  # noqa: E402
+import paper_2109_09527_b200 as pr  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+gen = graphgen.make_config(cfg)
+s = torch.from_numpy(gen.src).cuda()
+t = torch.from_numpy(gen.dst).cuda()
+x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+st = torch.cuda.current_stream()
+g = pr.Graph(gen.n, s, t)
+g.preprocess()
+out = {"workload": gen.name, "tau": gen.tau}
+for name, mode in (("sync", 0), ("sync_reduced", pr.PR_USE_REDUCTIONS), ("async", pr.PR_MODE_ASYNC),
+                   ("nosync", pr.PR_MODE_NOSYNC), ("nosync_reduced", pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS)):
+    best = None
+    for _ in range(reps + 1):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        rc, it, fd = g.run(x, gen.d, gen.tau, gen.max_iter, mode=mode)
+        b.record(st)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if best is None or ms < best[0]:
+            best = (ms, it, fd, g.stats())
+    ms, it, fd, stt = best
+    rec = {"ms": round(ms, 3), "iterations": it, "final_delta": fd, "status": rc}
+    if "nosync" in name:
+        rec.update(min_local_sweeps=stt["nosync_min_iters"], launches=stt["nosync_launches"],
+                   certified_residual=stt["residual"])
+    out[name] = rec
+    print(name, rec, flush=True)
+print(json.dumps(out))
+g.close()

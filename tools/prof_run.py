@@ -19,8 +19,9 @@ s = torch.from_numpy(gen.src).cuda()
 t = torch.from_numpy(gen.dst).cuda()
 x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
 g = pr.Graph(gen.n, s, t)
-m = {"plain": 0, "reduced": pr.PR_USE_REDUCTIONS, "async": pr.PR_MODE_ASYNC}[mode]
-if mode == "reduced":
+m = {"plain": 0, "reduced": pr.PR_USE_REDUCTIONS, "async": pr.PR_MODE_ASYNC, "nosync": pr.PR_MODE_NOSYNC,
+     "nosync_reduced": pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS}[mode]
+if "reduced" in mode:
     g.preprocess()
 st, it, fd = g.run(x, gen.d, 0.0, sweeps, mode=m | pr.PR_TIMING)
 stt = g.stats()
