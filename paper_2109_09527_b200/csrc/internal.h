@@ -22,6 +22,8 @@ constexpr int SE_STEP = 32 * SE_V;
 #define PRGPU_SE_NT 1024
 #endif
 constexpr int SE_NT = PRGPU_SE_NT;          // threads per CTA of the stream gather (1 CTA per SM)
+constexpr int SE_NT_IP = 512;               // in-place (async / No-Sync) stream kernels: 128 registers
+                                            // for the prefetched finalize operands of a step
 // Contribs [0, hot_n) (the highest out-degrees) are copied into shared memory
 // by every CTA at the start of a synchronous sweep; [hot_n, SE_L1_TIER) are
 // gathered with L1::evict_last, the rest with L1::no_allocate.

@@ -565,10 +565,157 @@ __global__ void k_residual(const double* __restrict__ sums, int64_t nrows, const
     }
 }
 
+// ------------------------------------------- in-place edge-stream sweeps --
+// Async (PR_MODE_ASYNC, one launch per sweep) and No-Sync (PR_MODE_NOSYNC,
+// persistent) on the edge-stream engine: the finalize is fused into the
+// gather, so a row's new contrib is visible to the gathers that follow in the
+// same sweep (Alg.3's in-place pr(u) <- tmp; Q-Y).  Contribs are
+// read with relaxed loads, except the hottest slots [0, hot_n), which every
+// CTA copies into shared memory at the start of each (local) sweep -- a
+// snapshot of values that were visible then, which No-Sync allows.  x is kept
+// in row / member order (xr, xm; unpermuted at the end); the finalize operands
+// of a step's row closures ((outdeg, slot), x_old) are prefetched right after
+// the row-start scan, before the gathers are consumed.
+struct InPlacePolicy {
+    static constexpr bool kHot = true;
+    const double* y_in;   // == y: relaxed loads
+    double* y;            // relaxed stores
+    const double* hot;
+    int32_t hot_n;
+    uint64_t pol_last;
+    double* xr;
+    const int2* rinfo;
+    double c, d;
+    double l1, linf;
+    int2 inf_f;
+    double xo_f;
+    int2 inf[SE_V];
+    double xo[SE_V];
+
+    __device__ __forceinline__ double load(int32_t u) const {
+        if (u < hot_n) return hot[u];
+        return ld_relaxed_f64(y_in + u);
+    }
+    __device__ __forceinline__ void prep(int64_t base, uint32_t f) {
+        if (f) {
+            inf_f = __ldg(rinfo + base);
+            xo_f = ld_relaxed_f64(xr + base);
+        }
+#pragma unroll
+        for (int j = 0; j < SE_V; ++j)
+            if (f & (1u << j)) {
+                const int64_t r = base + __popc(f & ((1u << j) - 1));
+                inf[j] = __ldg(rinfo + r);
+                xo[j] = ld_relaxed_f64(xr + r);
+            }
+    }
+    __device__ __forceinline__ void fin(int64_t r, double s, int2 q, double xold) {
+        const double xn = __dadd_rn(c, __dmul_rn(d, s));
+        st_relaxed_f64(xr + r, xn);
+        if (q.x > 0) st_relaxed_f64(y + q.y, xn / (double)q.x);
+        const double dl = fabs(xn - xold);
+        l1 += dl;
+        linf = fmax(linf, dl);
+    }
+    __device__ __forceinline__ void emit(int64_t r, double s) { fin(r, s, __ldg(rinfo + r), ld_relaxed_f64(xr + r)); }
+    __device__ __forceinline__ void emit_at(int j, int64_t r, double s) { fin(r, s, inf[j], xo[j]); }
+    __device__ __forceinline__ void emit_first(int64_t r, double s) { fin(r, s, inf_f, xo_f); }
+};
+
+// Members of a reduced view, in place: x(m) = alpha_k + beta_k * x(src) with
+// x(src) as currently visible (its row in xr), fused contrib, Delta.
+struct MemArgs {
+    const int32_t* msrow;
+    const int32_t* mk;
+    const int2* minfo;
+    double* xm;
+    int64_t nm;
+    int64_t mper;
+    const double* ab;
+};
+
+__device__ __forceinline__ void members_inplace(InPlacePolicy& p, const MemArgs& ma) {
+    const int64_t mb = (int64_t)blockIdx.x * ma.mper;
+    const int64_t me = min(ma.nm, mb + ma.mper);
+    for (int64_t i = mb + threadIdx.x; i < me; i += blockDim.x) {
+        const int32_t k = ma.mk[i];
+        const double xs = ld_relaxed_f64(p.xr + ma.msrow[i]);
+        const double xn = __dadd_rn(ma.ab[2 * k], __dmul_rn(ma.ab[2 * k + 1], xs));
+        const double xo = ma.xm[i];
+        ma.xm[i] = xn;
+        const int2 q = ma.minfo[i];
+        if (q.x > 0) st_relaxed_f64(p.y + q.y, xn / (double)q.x);
+        const double dl = fabs(xn - xo);
+        p.l1 += dl;
+        p.linf = fmax(p.linf, dl);
+    }
+}
+
+__device__ __forceinline__ void refresh_hot(InPlacePolicy& p, double* hot_smem) {
+    for (int i = threadIdx.x; i < p.hot_n; i += blockDim.x) hot_smem[i] = ld_relaxed_f64(p.y_in + i);
+    p.hot = hot_smem;
+    __syncthreads();
+}
+
+// One async sweep (launch level).
+__global__ void __launch_bounds__(SE_NT_IP, 1)
+    k_stream_async(InPlacePolicy p, StreamArgs a, MemArgs ma, IterArgs ia) {
+    extern __shared__ __align__(16) double hot_smem[];
+    __shared__ double red[2 * RED_W];
+    __shared__ int flag;
+    if (ia.st->done) return;
+    p.pol_last = 0;
+    refresh_hot(p, hot_smem);
+    p.l1 = 0.0;
+    p.linf = 0.0;
+    stream_run(p, a);
+    members_inplace(p, ma);
+    block_delta(p.l1, p.linf, red, ia.cta_partial + 2 * blockIdx.x);
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t t = atomicAdd(&ia.st->ticket_gather, 1u);
+        flag = (t == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (flag) global_finalize(ia, red);
+}
+
+// Persistent No-Sync on the edge-stream engine (see k_nosync for the protocol).
+__global__ void __launch_bounds__(SE_NT_IP, 1) k_nosync_stream(InPlacePolicy p, StreamArgs a, MemArgs ma, NoSyncArgs na) {
+    extern __shared__ __align__(16) double hot_smem[];
+    __shared__ double red[2 * RED_W];
+    __shared__ double res[2];
+    __shared__ int flag;
+    p.pol_last = 0;
+    for (int it = 1;; ++it) {
+        refresh_hot(p, hot_smem);
+        p.l1 = 0.0;
+        p.linf = 0.0;
+        stream_run(p, a);
+        members_inplace(p, ma);
+        block_delta(p.l1, p.linf, red, res);
+        if (threadIdx.x == 0) {
+            st_relaxed_f64(na.err + 2 * blockIdx.x, res[0]);
+            st_relaxed_f64(na.err + 2 * blockIdx.x + 1, res[1]);
+            na.iters[blockIdx.x] += 1;
+            double tot = 0.0, mx = 0.0;
+            for (unsigned cc = 0; cc < gridDim.x; ++cc) {
+                tot += ld_relaxed_f64(na.err + 2 * cc);
+                mx = fmax(mx, ld_relaxed_f64(na.err + 2 * cc + 1));
+            }
+            const double nv = na.norm_linf ? mx : tot;
+            flag = (nv <= na.tau || it >= na.max_local) ? 1 : 0;
+        }
+        __syncthreads();
+        if (flag) break;
+    }
+}
+
 // ------------------------------------------------------------------- host --
 
 struct GatherCfg {
     bool stream;  // sync: edge-stream gather + K-FINALIZE; async (or PRGPU_ENGINE=tasks): row-task engine
+    bool inplace; // async on the edge-stream engine (k_stream_async; PRGPU_ENGINE=tasks: row-task engine)
     bool async, vid;
     int hot_n;
     size_t smem;
@@ -631,11 +778,19 @@ static int env_int(const char* name, int dflt) {
 // Kernel variant, dynamic shared memory and persistent grid (all resident CTAs).
 static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, GatherCfg* gc, bool force_stream = false) {
     const char* eng = getenv("PRGPU_ENGINE");
-    gc->stream = !async && (force_stream || !(eng && eng[0] == 't'));
+    const bool tasks = eng && eng[0] == 't';
+    gc->stream = !async && (force_stream || !tasks);
+    gc->inplace = async && !tasks;
     gc->async = async;
     gc->vid = v.vid != nullptr;
     gc->hot_n = 0;
-    if (gc->stream) {
+    if (gc->inplace) {
+        int hot = env_int("PRGPU_HOT", SE_HOT_MAX);
+        hot = std::max(0, std::min<int>(std::min(hot, SE_HOT_MAX), (int)g->n_contrib));
+        gc->hot_n = hot;
+        gc->smem = (size_t)hot * sizeof(double);
+        gc->nt = SE_NT_IP;
+    } else if (gc->stream) {
         int hot = v.nseg > 0 ? 0 : env_int("PRGPU_HOT", SE_HOT_MAX);
         if (hot > SE_HOT_MAX) hot = SE_HOT_MAX;
         if (hot > g->n_contrib) hot = (int)g->n_contrib;
@@ -647,14 +802,14 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, Gathe
         gc->smem = sizeof(EngineSmem);
         gc->nt = GT_NT;
     }
-    const void* fn = gather_fn(*gc);
+    const void* fn = gc->inplace ? (const void*)k_stream_async : gather_fn(*gc);
     PR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gc->smem));
     int per_sm = 0;
     PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, gc->nt, gc->smem));
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)ctx.num_sms * per_sm;
     const int wpc = gc->nt / 32;
-    int64_t units = gc->stream ? v.nspans : v.ntasks;
+    int64_t units = (gc->stream || gc->inplace) ? v.nspans : v.ntasks;
     if (gc->stream && v.nseg > 0) {
         units = 0;
         for (int q = 0; q < v.nseg; ++q) units = std::max<int64_t>(units, v.seg[q].nspans);
@@ -710,7 +865,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         fgrid = std::min<int64_t>(std::max<int64_t>((work + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
     }
     const int ggrid = gc.stream ? (int)fgrid : gc.grid;  // CTAs writing Delta partials first
-    int64_t sgrid = (!gc.stream && nm > 0) ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
+    int64_t sgrid = (!gc.stream && !gc.inplace && nm > 0) ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
     if (sgrid > cap4) sgrid = cap4;
     const int64_t sper = sgrid > 0 ? (nm + sgrid - 1) / sgrid : 0;
     const int64_t nz = g->nz;
@@ -752,20 +907,23 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     PR_LAUNCH(ctx, k_init, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, x,
               g->y[0], (const int32_t*)g->outdeg, (const int32_t*)g->cidx, n, 1.0 / (double)n);
 
-    const int64_t sctas = (reduced && !gc.stream) ? sgrid : 0;
+    const int64_t sctas = (reduced && !gc.stream && !gc.inplace) ? sgrid : 0;
     IterArgs ia_rest{g->st,
                      g->cta_partial,
                      (int64_t)ggrid,
                      sctas,
                      0,
-                     gc.stream ? nullptr : v.hub_delta,
-                     gc.stream ? 0 : v.nhubs,
+                     (gc.stream || gc.inplace) ? nullptr : v.hub_delta,
+                     (gc.stream || gc.inplace) ? 0 : v.nhubs,
                      g->delta_log};
     IterArgs ia_first = ia_rest;
     ia_first.zero_ctas = zgrid;
     double* zero_partial = g->cta_partial + 2 * ((int64_t)ggrid + sctas);
     const bool gather_finalizes = !gc.stream && !(reduced && sgrid > 0);
-    if (gc.stream) {
+    const StreamArgs sa{v.col,  (const uint8_t*)v.sflags, v.step_row, v.nsteps, v.span_steps, v.nspans, v.bin,
+                        v.bout, v.b_row, v.b_s0, v.b_s1, v.part_in, v.part_out, v.bticket};
+    const MemArgs ma{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, nm > 0 ? (nm + gc.grid - 1) / gc.grid : 0, g->ab};
+    if (gc.stream || gc.inplace) {
         const int64_t need_xr = std::max<int64_t>(std::max(g->plain.nrows, g->reduced.nrows), 1);
         if (g->xr_cap < need_xr) {
             dfree(g->xr, s);
@@ -802,13 +960,25 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                 PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y_out,
                           (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
-            PR_TRY(launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, gather_finalizes));
+            if (gc.inplace) {
+                InPlacePolicy ip{};
+                ip.y_in = g->y[0];
+                ip.y = g->y[0];
+                ip.hot_n = gc.hot_n;
+                ip.xr = g->xr;
+                ip.rinfo = v.rinfo;
+                ip.c = c;
+                ip.d = d;
+                PR_LAUNCH(ctx, k_stream_async, gc.grid, gc.nt, gc.smem, ip, sa, ma, ia);
+            } else {
+                PR_TRY(launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, gather_finalizes));
+            }
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
             if (gc.stream) {
                 FinArgs f = fa;
                 f.y_out = y_out;
                 PR_LAUNCH(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
-            } else if (!gather_finalizes) {
+            } else if (!gather_finalizes && !gc.inplace) {
                 if (async)
                     PR_LAUNCH(ctx, k_scatter<true>, (unsigned)sgrid, GT_NT, 0, (const int32_t*)g->mem_vid,
                               (const int32_t*)g->mem_src, (const int32_t*)g->mem_k, nm, sper, (const double*)g->ab, x,
@@ -843,7 +1013,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         if (batch < 64) batch *= 2;
     }
     for (auto e : ev) cudaEventDestroy(e);
-    if (gc.stream) {
+    if (gc.stream || gc.inplace) {
         const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
         PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
                   (const double*)g->xm, (const int32_t*)g->mem_vid, nm, x);
@@ -946,16 +1116,29 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
     if (zgrid > 0)
         PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y,
                   (const int32_t*)g->outdeg, (const int32_t*)g->cidx, resid + 2);
+    if (gc.inplace) {  // edge-stream No-Sync: x in row / member order, unpermuted after each launch
+        const int64_t need_xr = std::max<int64_t>(std::max(g->plain.nrows, g->reduced.nrows), 1);
+        if (g->xr_cap < need_xr) {
+            dfree(g->xr, s);
+            PR_TRY(dalloc(&g->xr, (size_t)need_xr, s));
+            g->xr_cap = need_xr;
+        }
+        if (g->n_members > 0 && !g->xm) PR_TRY(dalloc(&g->xm, (size_t)g->n_members, s));
+        const unsigned fg = (unsigned)std::min<int64_t>((v.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+        PR_LAUNCH(ctx, k_fill_f64, fg, 256, 0, g->xr, v.nrows, 1.0 / (double)n);
+        if (nm > 0) PR_LAUNCH(ctx, k_fill_f64, fg, 256, 0, g->xm, nm, 1.0 / (double)n);
+    }
     const int64_t mper = nm > 0 ? (nm + grid - 1) / grid : 0;
     NoSyncArgs na{err, iters, (mode & PR_NORM_LINF) ? 1 : 0, tau, 0, g->mem_vid, g->mem_src, g->mem_k, nm, mper,
                   g->ab, x, y, g->outdeg, g->cidx};
     PRPolicy<true, true> pv{y, y, x, g->outdeg, g->cidx, v.vid, c, d, 0, {}};
     PRPolicy<true, false> pn{y, y, x, g->outdeg, g->cidx, v.vid, c, d, 0, {}};
     EngineArgs ea{v.tasks, v.ntasks, v.hubs, v.row_ptr, v.col, v.hub_partial, v.hub_delta, v.hub_ticket, 1};
-    const void* fn = gc.vid ? (const void*)k_nosync<true> : (const void*)k_nosync<false>;
+    const void* fn = gc.inplace ? (const void*)k_nosync_stream
+                                : (gc.vid ? (const void*)k_nosync<true> : (const void*)k_nosync<false>);
     PR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gc.smem));
     int per_sm = 0;
-    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, GT_NT, gc.smem));
+    PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, gc.nt, gc.smem));
     if ((int64_t)grid > (int64_t)ctx.num_sms * std::max(per_sm, 1)) {
         set_error("pr_run(NOSYNC): grid %d exceeds the resident CTAs", grid);
         return PR_ECUDA;
@@ -968,10 +1151,27 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
     while (true) {
         PR_LAUNCH(ctx, k_fill_f64, 1, 256, 0, err, (int64_t)(2 * grid), 1e300);
         na.max_local = max_iter - max_it;
-        if (gc.vid)
+        if (gc.inplace) {
+            InPlacePolicy ip{};
+            ip.y_in = y;
+            ip.y = y;
+            ip.hot_n = gc.hot_n;
+            ip.xr = g->xr;
+            ip.rinfo = v.rinfo;
+            ip.c = c;
+            ip.d = d;
+            const StreamArgs sa{v.col,  (const uint8_t*)v.sflags, v.step_row, v.nsteps, v.span_steps, v.nspans, v.bin,
+                                v.bout, v.b_row, v.b_s0, v.b_s1, v.part_in, v.part_out, v.bticket};
+            const MemArgs ma{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, mper, g->ab};
+            PR_LAUNCH(ctx, k_nosync_stream, (unsigned)grid, gc.nt, gc.smem, ip, sa, ma, na);
+            const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+            PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
+                      (const double*)g->xm, (const int32_t*)g->mem_vid, nm, x);
+        } else if (gc.vid) {
             PR_LAUNCH(ctx, k_nosync<true>, (unsigned)grid, GT_NT, gc.smem, pv, ea, na);
-        else
+        } else {
             PR_LAUNCH(ctx, k_nosync<false>, (unsigned)grid, GT_NT, gc.smem, pn, ea, na);
+        }
         ++launches;
         // certificate: S over the current contribs, then ||F(x) - x||
         PR_CUDA(cudaMemsetAsync(resid, 0, 2 * sizeof(double), s));

@@ -76,15 +76,20 @@ __device__ __forceinline__ void stream_piece(P& p, const StreamArgs& a, int32_t 
     // release: the piece is visible before the ticket moves.  (A __threadfence
     // here compiles to MEMBAR.SC + CCTL.IVALL, which would also invalidate this
     // SM's L1 and with it the L1 tier of hot contribs.)
+    // wrapping ticket (atom.inc: count-1 -> 0), so no reset store is needed and
+    // pieces of different sweeps may interleave (in-place persistent kernel:
+    // the winner then sums each span's latest piece)
     const int32_t s0 = a.b_s0[b], s1 = a.b_s1[b];
     uint32_t t;
-    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.bticket + b) : "memory");
+    asm volatile("atom.inc.release.gpu.u32 %0, [%1], %2;"
+                 : "=r"(t)
+                 : "l"(a.bticket + b), "r"((uint32_t)(s1 - s0))
+                 : "memory");
     if (t == (uint32_t)(s1 - s0)) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");  // winner only: acquire the other pieces
         double sum = __ldcg(a.part_out + s0);
         for (int32_t s = s0 + 1; s <= s1; ++s) sum += __ldcg(a.part_in + s);
         p.emit((int64_t)a.b_row[b], sum);
-        a.bticket[b] = 0u;
     }
 }
 
