@@ -335,6 +335,34 @@ def main():
                                 "iterations": sp["iterations"]}
         g.close()
 
+    # time-to-converge of the three iteration modes on the same graph (the
+    # paper's Barriers vs No-Sync comparison, Fig.7): sync (Alg.1),
+    # launch-level in-place async, persistent barrier-free No-Sync (Alg.3)
+    modes = {}
+    g = pr.Graph(n, src_d, dst_d)
+    if flags:
+        g.preprocess(flags)
+    red = pr.PR_USE_REDUCTIONS if flags else 0
+    for name, md in (("sync", red), ("async", red | pr.PR_MODE_ASYNC), ("nosync", red | pr.PR_MODE_NOSYNC)):
+        best = None
+        for _ in range(3):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rc_, it_, fd_ = g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=md)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms_ = a.elapsed_time(b)
+            if best is None or ms_ < best[0]:
+                best = (ms_, it_, fd_, g.stats())
+        rec = {"time_to_converge_ms": round(best[0], 3), "iterations": best[1], "final_delta": best[2]}
+        if name == "nosync":
+            rec["min_local_sweeps"] = best[3]["nosync_min_iters"]
+            rec["certified_residual"] = best[3]["residual"]
+        modes[name] = rec
+    g.close()
+    extra["modes"] = modes
+
     # e2e: the same step through the same ABI calls with HOST (pinned) buffers
     e2e = None
     if not args.no_e2e:

@@ -785,7 +785,7 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, Gathe
     gc->vid = v.vid != nullptr;
     gc->hot_n = 0;
     if (gc->inplace) {
-        int hot = env_int("PRGPU_HOT", SE_HOT_MAX);
+        int hot = env_int("PRGPU_HOT", SE_HOT_IP);
         hot = std::max(0, std::min<int>(std::min(hot, SE_HOT_MAX), (int)g->n_contrib));
         gc->hot_n = hot;
         gc->smem = (size_t)hot * sizeof(double);
