@@ -67,6 +67,11 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
                                  synchronous gather and the kernel is relaunched if it is
                                  above threshold.  iterations = the largest number of local
                                  sweeps of any CTA. */
+#define PR_PERFORATE     32u  /* loop perforation (Barriers-Opt, Alg.5),
+                                 synchronous plain mode only: a vertex whose change in a sweep
+                                 is 0 < |delta| < threshold * 1e-5 keeps its value from then on
+                                 and is no longer gathered (APPROXIMATE: the result is not the
+                                 fixed point; the stop test counts frozen vertices as 0). */
 
 /*
  * pr_graph_create -- build the in-edge CSR and out-degrees on the device
@@ -105,7 +110,7 @@ int pr_preprocess(pr_graph *g, uint32_t flags, void *stream);
  *   threshold  >= 0 (P:438 uses 1e-16 with L-inf; configs use 1e-10 / 1e-12 L1)
  *   max_iter   >= 1; reaching it returns PR_NOT_CONVERGED with valid ranks
  *   mode       PR_MODE_SYNC | PR_MODE_ASYNC | PR_MODE_NOSYNC, | PR_NORM_* |
- *              PR_USE_REDUCTIONS | PR_TIMING
+ *              PR_USE_REDUCTIONS | PR_TIMING | PR_PERFORATE
  *   ranks      fp64[n] output in vertex-id order (host or device, caller-owned)
  *   iters_out  (host, nullable) number of update sweeps including the final
  *              one that met the stop test (Q-I)
@@ -169,6 +174,9 @@ typedef struct {
     int32_t nosync_min_iters;   /* PR_MODE_NOSYNC: fewest local sweeps of any CTA */
     int32_t nosync_launches;    /* PR_MODE_NOSYNC: persistent launches (1 + relaunches) */
     double  residual;           /* PR_MODE_NOSYNC: certified ||F(x) - x|| (run norm) at exit */
+    int64_t edges_gathered;     /* edges gathered over the whole run (all sweeps) */
+    int64_t frozen_rows;        /* PR_PERFORATE: rows no longer gathered at exit */
+    int32_t compactions;        /* PR_PERFORATE: times the gathered rows were compacted */
 } pr_run_stats;
 
 int pr_get_run_stats(const pr_graph *g, pr_run_stats *out);

@@ -36,6 +36,7 @@ PR_NORM_LINF = 2
 PR_USE_REDUCTIONS = 4
 PR_TIMING = 8
 PR_MODE_NOSYNC = 16
+PR_PERFORATE = 32
 
 # every symbol include/prgpu.h declares (tests check the .so exports them)
 ABI_SYMBOLS = (
@@ -70,6 +71,9 @@ class pr_run_stats(ctypes.Structure):
         ("nosync_min_iters", ctypes.c_int32),
         ("nosync_launches", ctypes.c_int32),
         ("residual", ctypes.c_double),
+        ("edges_gathered", ctypes.c_int64),
+        ("frozen_rows", ctypes.c_int64),
+        ("compactions", ctypes.c_int32),
     ]
 
     def as_dict(self):

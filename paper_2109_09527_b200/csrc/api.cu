@@ -316,12 +316,16 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
         set_error("pr_run: max_iter=%d < 1", max_iter);
         return PR_EINVAL;
     }
-    if (mode & ~(PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_NORM_LINF | PR_USE_REDUCTIONS | PR_TIMING)) {
+    if (mode & ~(PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_NORM_LINF | PR_USE_REDUCTIONS | PR_TIMING | PR_PERFORATE)) {
         set_error("pr_run: unknown mode bits 0x%x", mode);
         return PR_EINVAL;
     }
     if ((mode & PR_MODE_ASYNC) && (mode & PR_MODE_NOSYNC)) {
         set_error("pr_run: PR_MODE_ASYNC and PR_MODE_NOSYNC are exclusive");
+        return PR_EINVAL;
+    }
+    if ((mode & PR_PERFORATE) && (mode & (PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_USE_REDUCTIONS))) {
+        set_error("pr_run: PR_PERFORATE is defined for the synchronous plain mode only");
         return PR_EINVAL;
     }
     if ((mode & PR_USE_REDUCTIONS) && !g->pre_done) {

@@ -183,6 +183,8 @@ int build_view_tasks(View& v, Ctx& ctx);
 int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx);
 int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib);
 void free_view(View& v, cudaStream_t s);
+__global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const int64_t* __restrict__ rp,
+                            const int32_t* __restrict__ col, const int64_t* __restrict__ rpR, int32_t* __restrict__ colR);
 __global__ void k_rinfo(const int32_t* __restrict__ vid, int64_t nrows, const int32_t* __restrict__ od,
                         const int32_t* __restrict__ cidx, int2* __restrict__ info);
 int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx);

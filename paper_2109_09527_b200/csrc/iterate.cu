@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "primitives.cuh"
 #include "rowengine.cuh"
 #include "streamengine.cuh"
 
@@ -286,6 +287,11 @@ struct FinArgs {
     const double* ab;
     double* y_out;
     double c, d;
+    // loop perforation (PR_PERFORATE, Alg.5): mark rows whose change
+    // this sweep is 0 < |delta| < tau_f (fz[r] = 1, else 0) and count them
+    uint8_t* fz = nullptr;
+    double tau_f = 0.0;
+    unsigned long long* nfz = nullptr;
 };
 
 // Rows are visited grid-stride (all CTAs sweep the row space together, which
@@ -305,6 +311,7 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     const double* __restrict__ sums = f.sums;
     double* __restrict__ xr = f.xr;
     double* __restrict__ y = f.y_out;
+    uint32_t nfrozen = 0;
     for (int64_t r0 = t0; r0 < f.nrows; r0 += FIN_U * T) {
         double S[FIN_U], xo[FIN_U];
         int2 inf[FIN_U];
@@ -327,8 +334,17 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
                 const double dl = fabs(xn - xo[u]);
                 l1 += dl;
                 linf = fmax(linf, dl);
+                if (f.fz) {
+                    const bool frz = dl != 0.0 && dl < f.tau_f;
+                    f.fz[r] = frz ? 1 : 0;
+                    nfrozen += frz;
+                }
             }
         }
+    }
+    if (f.fz) {
+        nfrozen = warp_sum(nfrozen);
+        if ((threadIdx.x & 31) == 0 && nfrozen) atomicAdd(f.nfz, (unsigned long long)nfrozen);
     }
     double* __restrict__ xm = f.xm;
     for (int64_t i0 = t0; i0 < f.nm; i0 += FIN_U * T) {
@@ -823,10 +839,13 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, Gathe
 
 static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
                       int32_t* iters_out, double* delta_out);
+static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
+                          Ctx& ctx, int32_t* iters_out, double* delta_out);
 
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
         int32_t* iters_out, double* delta_out) {
     if (mode & PR_MODE_NOSYNC) return run_nosync(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
+    if (mode & PR_PERFORATE) return run_perforated(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     cudaStream_t s = ctx.stream;
     const bool async = (mode & PR_MODE_ASYNC) != 0;
     const bool reduced = (mode & PR_USE_REDUCTIONS) != 0;
@@ -1039,6 +1058,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     rs.scatter_members = nm;
     rs.n_contrib = g->n_contrib;
     rs.n_tasks = v.ntasks;
+    rs.edges_gathered = v.nedges * (int64_t)hs->iters;
     if (iters_out) *iters_out = hs->iters;
     if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
     return hs->status;
@@ -1238,6 +1258,272 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
     if (iters_out) *iters_out = max_it;
     if (delta_out) *delta_out = rs.residual;
     return status;
+}
+
+// ------------------------------------------------------------ perforation --
+// PR_PERFORATE (Barriers-Opt, Alg.5; reading Q-P in
+// DESIGN.md): synchronous plain sweeps in which K-FINALIZE marks every row
+// whose change was 0 < |delta| < tau * 1e-5.  At the host sync after each batch
+// of sweeps, once enough rows are marked, the gathered view is COMPACTED to the
+// unmarked rows: the marked rows keep their value (x, and their contrib in both
+// ping-pong buffers) for the rest of the run and are never gathered again, so
+// every later sweep streams fewer edges.  Approximate by design.
+struct KeepGet {
+    const uint8_t* fz;
+    __device__ int64_t operator()(int64_t r) const { return fz[r] ? 0 : 1; }
+};
+struct KeepEmit {
+    const uint8_t* fz;
+    const int64_t* rp;
+    const int32_t* amap;  // active row -> full plain-view row (nullptr: identity)
+    const int2* rinfo;
+    const double* xr;
+    int32_t* src_row;
+    int32_t* namap;
+    int2* nrinfo;
+    double* nxr;
+    int64_t* nlen;
+    __device__ void operator()(int64_t r, int64_t pos, int64_t f) const {
+        if (!f) return;
+        src_row[pos] = (int32_t)r;
+        namap[pos] = amap ? amap[r] : (int32_t)r;
+        nrinfo[pos] = rinfo[r];
+        nxr[pos] = xr[r];
+        nlen[pos] = rp[r + 1] - rp[r];
+    }
+};
+struct LenGet {
+    const int64_t* len;
+    int64_t n;
+    __device__ int64_t operator()(int64_t i) const { return i < n ? len[i] : 0; }
+};
+struct RpEmit {
+    int64_t* rp;
+    __device__ void operator()(int64_t i, int64_t pos, int64_t) const { rp[i] = pos; }
+};
+
+// marked rows: contrib into the other ping-pong buffer (frozen from now on)
+__global__ void k_pf_freeze_y(const uint8_t* __restrict__ fz, const int2* __restrict__ rinfo, int64_t nr,
+                              const double* __restrict__ ycur, double* __restrict__ yoth) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x)
+        if (fz[r] && rinfo[r].x > 0) yoth[rinfo[r].y] = ycur[rinfo[r].y];
+}
+// active-view x back into the full plain-view row order
+__global__ void k_pf_writeback(const double* __restrict__ xa, const int32_t* __restrict__ amap, int64_t nr,
+                               double* __restrict__ xfull) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x)
+        xfull[amap[r]] = xa[r];
+}
+__global__ void k_count_u8(const uint8_t* __restrict__ a, int64_t n, unsigned long long* out) {
+    uint32_t c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += a[i] ? 1u : 0u;
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+struct ActiveView {
+    View v;                 // gathered rows; v.vid = map to the full plain-view row
+    double* xr = nullptr;   // x of its rows
+    bool is_full = true;    // the plain view itself (no copies)
+};
+
+static void free_active(ActiveView& a, cudaStream_t s) {
+    if (a.is_full) return;
+    dfree(a.xr, s);
+    free_view(a.v, s);  // frees vid (the map), sums, rinfo, col, row_ptr, stream tables
+}
+
+static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
+                          Ctx& ctx, int32_t* iters_out, double* delta_out) {
+    cudaStream_t s = ctx.stream;
+    const int64_t n = g->n;
+    View& V = g->plain;
+    const int64_t launches0 = ctx.launches;
+    cudaPointerAttributes at{};
+    const bool ranks_dev = cudaPointerGetAttributes(&at, ranks) == cudaSuccess &&
+                           (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    double* x = ranks;
+    if (!ranks_dev) {
+        if (!g->x) PR_TRY(dalloc(&g->x, (size_t)n, s));
+        x = g->x;
+    }
+    const int64_t ny = g->n_contrib + 1;
+    for (int b = 0; b < 2; ++b)
+        if (!g->y[b]) {
+            PR_TRY(dalloc(&g->y[b], (size_t)ny, s));
+            PR_CUDA(cudaMemsetAsync(g->y[b] + g->n_contrib, 0, sizeof(double), s));
+        }
+    const int64_t need_xr = std::max<int64_t>(std::max(g->plain.nrows, g->reduced.nrows), 1);
+    if (g->xr_cap < need_xr) {
+        dfree(g->xr, s);
+        PR_TRY(dalloc(&g->xr, (size_t)need_xr, s));
+        g->xr_cap = need_xr;
+    }
+    const double c = (1.0 - d) / (double)n;
+    const int64_t cap4 = (int64_t)ctx.num_sms * 4;
+    const int64_t fgrid_max = std::min<int64_t>(std::max<int64_t>((V.nrows + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1),
+                                                cap4 * 2);
+    const int64_t nz = g->nz;
+    const int64_t zgrid = nz > 0 ? std::min<int64_t>((nz + GT_NT * 4 - 1) / (GT_NT * 4), cap4) : 0;
+    const int64_t zper = zgrid > 0 ? (nz + zgrid - 1) / zgrid : 0;
+    const int64_t need = 2 * (fgrid_max + zgrid);
+    if (g->partial_cap < need) {
+        dfree(g->cta_partial, s);
+        PR_TRY(dalloc(&g->cta_partial, (size_t)need, s));
+        g->partial_cap = need;
+    }
+    const int log_cap = max_iter < 4096 ? max_iter : 4096;
+    if (g->log_cap < log_cap) {
+        dfree(g->delta_log, s);
+        PR_TRY(dalloc(&g->delta_log, (size_t)(2 * log_cap), s));
+        g->log_cap = log_cap;
+    }
+    uint8_t* fz = nullptr;
+    unsigned long long* cnt = nullptr;
+    PR_TRY(dalloc(&fz, (size_t)std::max<int64_t>(V.nrows, 1), s));
+    PR_TRY(dalloc(&cnt, 2, s));
+    PR_CUDA(cudaMemsetAsync(fz, 0, (size_t)std::max<int64_t>(V.nrows, 1), s));
+    DevState* hs = g->st_host;
+    *hs = DevState{};
+    hs->max_iter = max_iter;
+    hs->norm_linf = (mode & PR_NORM_LINF) ? 1 : 0;
+    hs->tau = tau;
+    hs->log_cap = log_cap;
+    PR_CUDA(cudaMemcpyAsync(g->st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
+    PR_LAUNCH(ctx, k_init, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, x,
+              g->y[0], (const int32_t*)g->outdeg, (const int32_t*)g->cidx, n, 1.0 / (double)n);
+    const unsigned fg = (unsigned)std::min<int64_t>((V.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+    PR_LAUNCH(ctx, k_fill_f64, fg, 256, 0, g->xr, V.nrows, 1.0 / (double)n);
+
+    ActiveView A;
+    A.v = V;  // shallow: the plain view's arrays
+    A.xr = g->xr;
+    A.is_full = true;
+    int64_t edges_gathered = 0;
+    int32_t compactions = 0;
+    int64_t launched = 0;
+    int host_syncs = 0;
+    int rc = PR_OK;
+    while (true) {
+        GatherCfg gc;
+        if ((rc = gather_config(ctx, A.v, g, false, &gc, true)) != PR_OK) break;
+        const int64_t fgrid =
+            std::min<int64_t>(std::max<int64_t>((A.v.nrows + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
+        IterArgs ia{g->st, g->cta_partial, fgrid, 0, 0, nullptr, 0, g->delta_log};
+        IterArgs ia0 = ia;
+        ia0.zero_ctas = zgrid;
+        double* zero_partial = g->cta_partial + 2 * fgrid;
+        FinArgs fa{A.v.sums, A.v.nrows, A.v.rinfo, A.xr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, c, d,
+                   fz, tau * 1e-5, cnt};
+        const int nb = (int)std::min<int64_t>(8, max_iter - launched);
+        for (int j = 0; j < nb; ++j) {
+            const int64_t it = launched + j;
+            const double* y_in = g->y[it & 1];
+            double* y_out = g->y[(it + 1) & 1];
+            const IterArgs& iv = it == 0 ? ia0 : ia;
+            if (it == 0 && zgrid > 0)
+                PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y_out,
+                          (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
+            if ((rc = launch_gather(ctx, A.v, y_in, y_out, x, g, c, d, iv, gc, 0)) != PR_OK) break;
+            FinArgs f = fa;
+            f.y_out = y_out;
+            PR_LAUNCH(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, iv);
+            if (it == 0 && nz > 0)
+                PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256,
+                          0, (const int32_t*)g->zlist, nz, c, (double*)y_in, (const int32_t*)g->outdeg,
+                          (const int32_t*)g->cidx);
+        }
+        if (rc != PR_OK) break;
+        PR_CUDA(cudaMemsetAsync(cnt + 1, 0, sizeof(unsigned long long), s));
+        if (A.v.nrows > 0)
+            PR_LAUNCH(ctx, k_count_u8, (unsigned)std::min<int64_t>((A.v.nrows + 255) / 256 + 1, cap4 * 4), 256, 0,
+                      (const uint8_t*)fz, A.v.nrows, cnt + 1);
+        unsigned long long marked = 0;
+        PR_CUDA(cudaMemcpyAsync(hs, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaMemcpyAsync(&marked, cnt + 1, sizeof(marked), cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        ++host_syncs;
+        const int64_t done_sweeps = std::min<int64_t>(hs->iters, launched + nb) - launched;
+        edges_gathered += A.v.nedges * std::max<int64_t>(done_sweeps, 0);
+        launched += nb;
+        if (hs->done || launched >= max_iter) break;
+        if ((int64_t)marked * 20 < A.v.nrows || marked == 0) continue;  // compact once >= 5 % are marked
+        // ---- compaction: freeze the marked rows, gather only the others ----
+        const double* ycur = g->y[launched & 1];
+        double* yoth = g->y[(launched + 1) & 1];
+        PR_LAUNCH(ctx, k_pf_freeze_y, fg, 256, 0, (const uint8_t*)fz, (const int2*)A.v.rinfo, A.v.nrows, ycur, yoth);
+        if (!A.is_full)
+            PR_LAUNCH(ctx, k_pf_writeback, fg, 256, 0, (const double*)A.xr, (const int32_t*)A.v.vid, A.v.nrows, g->xr);
+        ActiveView B;
+        B.is_full = false;
+        const int64_t nr = A.v.nrows - (int64_t)marked;
+        int32_t* src_row = nullptr;
+        int64_t* nlen = nullptr;
+        int64_t* tot = nullptr;
+        PR_TRY(dalloc(&src_row, (size_t)std::max<int64_t>(nr, 1), s));
+        PR_TRY(dalloc(&nlen, (size_t)std::max<int64_t>(nr, 1), s));
+        PR_TRY(dalloc(&tot, 1, s));
+        PR_TRY(dalloc(&B.v.vid, (size_t)std::max<int64_t>(nr, 1), s));
+        PR_TRY(dalloc(&B.v.rinfo, (size_t)std::max<int64_t>(nr, 1), s));
+        PR_TRY(dalloc(&B.xr, (size_t)std::max<int64_t>(nr, 1), s));
+        PR_TRY((device_scan<int64_t>(ctx, A.v.nrows, KeepGet{fz},
+                                     KeepEmit{fz, A.v.row_ptr, A.is_full ? nullptr : A.v.vid, A.v.rinfo, A.xr, src_row,
+                                              B.v.vid, B.v.rinfo, B.xr, nlen},
+                                     tot)));
+        B.v.nrows = nr;
+        PR_TRY(dalloc(&B.v.row_ptr, (size_t)nr + 1, s));
+        B.v.owns_row_ptr = true;
+        PR_TRY((device_scan<int64_t>(ctx, nr + 1, LenGet{nlen, nr}, RpEmit{B.v.row_ptr}, tot)));
+        PR_TRY(read_count(ctx, tot, &B.v.nedges));
+        PR_TRY(dalloc(&B.v.col, (size_t)stream_pad(B.v.nedges), s));
+        if (nr > 0)
+            PR_LAUNCH(ctx, k_copy_rows, (unsigned)std::min<int64_t>((B.v.nedges + 1023) / 1024 / 8 + 1, cap4 * 4), 256,
+                      0, (const int32_t*)src_row, nr, (const int64_t*)A.v.row_ptr, (const int32_t*)A.v.col,
+                      (const int64_t*)B.v.row_ptr, B.v.col);
+        PR_TRY(build_view_stream(B.v, ctx, (int32_t)g->n_contrib, nullptr, nullptr));
+        PR_TRY(dalloc(&B.v.sums, (size_t)std::max<int64_t>(nr, 1), s));
+        dfree(src_row, s);
+        dfree(nlen, s);
+        dfree(tot, s);
+        free_active(A, s);
+        A = B;
+        PR_CUDA(cudaMemsetAsync(fz, 0, (size_t)std::max<int64_t>(V.nrows, 1), s));
+        ++compactions;
+    }
+    if (rc == PR_OK) {
+        if (!A.is_full)
+            PR_LAUNCH(ctx, k_pf_writeback, fg, 256, 0, (const double*)A.xr, (const int32_t*)A.v.vid, A.v.nrows, g->xr);
+        const unsigned ug = (unsigned)std::min<int64_t>((V.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+        PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)V.vid, V.nrows,
+                  (const double*)nullptr, (const int32_t*)nullptr, (int64_t)0, x);
+        if (!ranks_dev) PR_CUDA(cudaMemcpyAsync(ranks, x, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
+    }
+    const int64_t frozen = V.nrows - A.v.nrows;
+    free_active(A, s);
+    dfree(fz, s);
+    dfree(cnt, s);
+    PR_CUDA(cudaStreamSynchronize(s));
+    if (rc != PR_OK) return rc;
+    pr_run_stats& rs = g->last;
+    rs = pr_run_stats{};
+    g->log_len = std::min<int32_t>(hs->iters, g->log_cap);
+    rs.iterations = hs->iters;
+    rs.status = hs->status;
+    rs.delta_l1 = hs->l1;
+    rs.delta_linf = hs->linf;
+    rs.run_launches = ctx.launches - launches0;
+    rs.host_syncs = host_syncs;
+    rs.gather_rows = V.nrows;
+    rs.gather_edges = V.nedges;
+    rs.n_contrib = g->n_contrib;
+    rs.edges_gathered = edges_gathered;
+    rs.frozen_rows = frozen;
+    rs.compactions = compactions;
+    if (iters_out) *iters_out = hs->iters;
+    if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
+    return hs->status;
 }
 
 }  // namespace prgpu

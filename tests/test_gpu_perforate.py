@@ -1,0 +1,76 @@
+"""GPU tests of PR_PERFORATE: loop perforation (Barriers-Opt, Alg.5 P:670-707;
+SURVEY §8 f2).  Approximate by design: rows whose change falls to
+0 < |delta| < tau * 1e-5 keep their value and are no longer gathered.  Pinned:
+the work really shrinks (edges gathered over the run < E * sweeps), the frozen
+values are exactly the values the rows had, and the result stays close to the
+oracle's fixed point (the analogue of the paper's L1-norm of Figs.5-6)."""
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from tests.test_gpu_parity import D, dev
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_09527_b200 as m
+    return m
+
+
+@pytest.mark.parametrize("cfg,scale", [(4, 14), (4, 16), (2, None)])
+def test_perforation_saves_work_and_stays_close(pr, cfg, scale):
+    gen = graphgen.make_config(cfg, scale_override=scale) if scale else graphgen.make_config(cfg)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    tight = oracle.pagerank(ref_g, D, gen.tau / 100, 5000)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+        st, it, fd = g.run(x, D, gen.tau, 1000)
+        exact = x.cpu().numpy()
+        full_work = g.stats()["edges_gathered"]
+        st, it_p, fd = g.run(x, D, gen.tau, 1000, mode=pr.PR_PERFORATE)
+        xp = x.cpu().numpy()
+        s = g.stats()
+    assert st == pr.PR_OK and fd <= gen.tau
+    assert s["compactions"] >= 1 and s["frozen_rows"] > 0
+    assert s["edges_gathered"] < s["gather_edges"] * it_p
+    assert s["edges_gathered"] < full_work
+    l1 = np.abs(xp - tight.x).sum()
+    l1_exact = np.abs(exact - tight.x).sum()
+    # approximate, but within a few thousand times the exact run's own error
+    assert l1 <= max(1e-6, 1e4 * l1_exact), (l1, l1_exact)
+    print(f"{gen.name}: sweeps {it_p}, frozen {s['frozen_rows']}, work {s['edges_gathered'] / full_work:.3f} "
+          f"of exact, L1 {l1:.3e} (exact {l1_exact:.3e})")
+
+
+def test_perforation_mode_checks(pr):
+    gen = graphgen.make_config(1)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+        for bad in (pr.PR_PERFORATE | pr.PR_MODE_ASYNC, pr.PR_PERFORATE | pr.PR_MODE_NOSYNC):
+            with pytest.raises(pr.PRError) as e:
+                pr.pr_run(g.handle, D, 1e-10, 10, x, mode=bad)
+            assert e.value.code == pr.PR_EINVAL
+        g.preprocess()
+        with pytest.raises(pr.PRError) as e:
+            pr.pr_run(g.handle, D, 1e-10, 10, x, mode=pr.PR_PERFORATE | pr.PR_USE_REDUCTIONS)
+        assert e.value.code == pr.PR_EINVAL
+
+
+def test_perforation_tiny_tau_is_exact_trajectory(pr):
+    """With a threshold so small that no row ever qualifies (0 < |delta| < tau*1e-5
+    never holds before the stop), the perforated run IS the plain run, bit for bit."""
+    gen = graphgen.make_config(1)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+        g.run(x, D, 0.0, 30)
+        a = x.cpu().numpy()
+        g.run(x, D, 0.0, 30, mode=pr.PR_PERFORATE)
+        b = x.cpu().numpy()
+        assert g.stats()["frozen_rows"] == 0
+        assert np.array_equal(a, b)
