@@ -425,6 +425,10 @@ struct TaskFillEmit {
 };
 
 void free_view(View& v, cudaStream_t s) {
+    if (v.alias) {
+        v = View{};
+        return;
+    }
     if (v.owns_row_ptr) dfree(v.row_ptr, s);
     v.row_ptr = nullptr;
     dfree(v.col, s);

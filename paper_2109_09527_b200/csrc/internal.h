@@ -70,6 +70,7 @@ struct Hub {
 // A set of rows over which the gather runs: all vertices (plain) or the
 // computed representatives R (reduced).  Rows are in increasing vertex id.
 struct View {
+    bool alias = false;             // a shallow copy of another view (owns nothing)
     int64_t nrows = 0;
     int64_t nedges = 0;
     int64_t* row_ptr = nullptr;     // int64[nrows+1] (plain: aliases the canonical row_ptr)

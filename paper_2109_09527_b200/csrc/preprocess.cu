@@ -432,6 +432,17 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
     g->n_members = h[0];
     R.nrows = h[1];
     g->max_chain = (int32_t)(h[2] & 0xffffffff);
+    if (g->n_members == 0) {
+        // nothing to resolve (config 5): the computed set is every row of
+        // in-degree > 0, i.e. the plain view itself -- alias it, no copies
+        dfree(R.vid, s);
+        dfree(cnt, s);
+        R = g->plain;
+        R.alias = true;
+        g->pre_done = true;
+        g->pre_flags = flags;
+        return PR_OK;
+    }
     PR_TRY(dalloc(&R.row_ptr, (size_t)R.nrows + 1, s));
     R.owns_row_ptr = true;
     PR_TRY((device_scan<int64_t>(ctx, R.nrows + 1, DegGet{g->row_ptr, R.vid, R.nrows}, PosEmit{R.row_ptr}, cnt)));

@@ -198,8 +198,12 @@ struct RsSmem {
     uint32_t toff[RS_BINS + 1];  // tile-local start of each digit
     uint32_t wc[RS_WARPS][RS_BINS + 1];
     uint32_t sw[33];
-    K sk[RS_TILE];
-    uint32_t sv[HAS_V ? RS_TILE : 1];
+    alignas(16) K sk[RS_TILE];
+    alignas(16) uint32_t sv[HAS_V ? RS_TILE : 4];
+    // the NEXT tile, staged by one TMA bulk copy while this one is ranked
+    alignas(16) K stk[RS_TILE];
+    alignas(16) uint32_t stv[HAS_V ? RS_TILE : 4];
+    alignas(8) uint64_t bar;
 };
 
 // Stable scatter of one 8-bit digit.  Per tile of RS_TILE keys: warp-level
@@ -218,21 +222,53 @@ __global__ void __launch_bounds__(RS_NT, PRGPU_RS_MINB) k_rs_scatter(const K* __
     if (threadIdx.x < RS_BINS) sm.base[threadIdx.x] = offs[(int64_t)threadIdx.x * G + blockIdx.x];
     const int64_t b = (int64_t)blockIdx.x * per_cta;
     const int64_t e = min(n, b + per_cta);
+    // stage tile [tb, tb + tn) (16-byte rounded; allocations carry >= 64 B of slack)
+    auto stage = [&](int64_t tb) {
+        const int tn = (int)min((int64_t)RS_TILE, e - tb);
+        const uint32_t kb = ((uint32_t)(tn * sizeof(K)) + 15u) & ~15u;
+        const uint32_t vb = HAS_V ? (((uint32_t)(tn * 4) + 15u) & ~15u) : 0u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&sm.bar)), "r"(kb + vb)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(sm.stk)),
+            "l"(kin + tb), "r"(kb), "r"(smem_addr(&sm.bar))
+            : "memory");
+        if (HAS_V)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(sm.stv)),
+                "l"(vin + tb), "r"(vb), "r"(smem_addr(&sm.bar))
+                : "memory");
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&sm.bar, 1);
+        fence_mbar_init();
+        if (b < e) stage(b);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
     for (int64_t tb = b; tb < e; tb += RS_TILE) {
         const int tn = (int)min((int64_t)RS_TILE, e - tb);
         for (int i = threadIdx.x; i < RS_WARPS * (RS_BINS + 1); i += RS_NT) (&sm.wc[0][0])[i] = 0;
-        __syncthreads();
         K k[RS_ROUNDS];
         uint32_t v[RS_ROUNDS];
         uint32_t dg[RS_ROUNDS];
         uint32_t pos[RS_ROUNDS];
         const int64_t s = tb + (int64_t)warp * (32 * RS_ROUNDS);
+        mbar_wait(&sm.bar, phase);
+        phase ^= 1u;
 #pragma unroll
         for (int r = 0; r < RS_ROUNDS; ++r) {
-            const int64_t i = s + r * 32 + lane;
-            const bool valid = i < e;
-            k[r] = valid ? kin[i] : K(0);
-            if (HAS_V) v[r] = valid ? vin[i] : 0u;
+            const int li = warp * (32 * RS_ROUNDS) + r * 32 + lane;
+            const bool valid = li < tn;
+            k[r] = valid ? sm.stk[li] : K(0);
+            if (HAS_V) v[r] = valid ? sm.stv[li] : 0u;
+        }
+        __syncthreads();  // staging buffer consumed (and wc cleared): prefetch the next tile
+        if (threadIdx.x == 0 && tb + RS_TILE < e) {
+            fence_proxy_async_smem();
+            stage(tb + RS_TILE);
         }
 #pragma unroll
         for (int r = 0; r < RS_ROUNDS; ++r) {
