@@ -1,5 +1,6 @@
 """GPU parity at BASELINE.json's full sizes (configs 4 and 5), in the launch
-configuration bench.py times (persistent gather grid, reduced and plain modes).
+configuration bench.py times (persistent gather grid, reduced and plain modes),
+plus the in-place async and the persistent No-Sync modes on both.
 
 A converged oracle run at these sizes takes ~10 min single-threaded (config 4:
 644 s measured, tests/golden/config_iters.json), so the checks are:
@@ -121,12 +122,22 @@ def _fullsize(pr, k, async_too):
             res_a = oracle.residual_l1(ref_g, d, xa)
             assert res_a / (1 - d) <= 1e-8
             assert np.abs(xa - x).max() <= 1e-10
+            # persistent barrier-free No-Sync (f1): certified residual of the original system
+            st, it_n, fd, xn = run(pr, g, n, d, gen.tau, gen.max_iter, mode=pr.PR_MODE_NOSYNC)
+            assert st == pr.PR_OK and fd <= gen.tau
+            res_n = oracle.residual_l1(ref_g, d, xn)
+            assert res_n <= gen.tau * (1 + 1e-6) + 1e-15
+            assert np.abs(xn - x).max() <= 1e-10
+            st, it_n, fd, xn = run(pr, g, n, d, gen.tau, gen.max_iter,
+                                   mode=pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS)
+            assert st == pr.PR_OK and fd <= gen.tau
+            assert oracle.residual_l1(ref_g, d, xn) / (1 - d) <= 1e-9
     finally:
         g.close()
 
 
 def test_config4_rmat24_fullsize(pr):
-    _fullsize(pr, 4, async_too=False)
+    _fullsize(pr, 4, async_too=True)
 
 
 def test_config5_poisson_fullsize(pr):
