@@ -592,10 +592,15 @@ __global__ void k_residual(const double* __restrict__ sums, int64_t nrows, const
 // in row / member order (xr, xm; unpermuted at the end); the finalize operands
 // of a step's row closures ((outdeg, slot), x_old) are prefetched right after
 // the row-start scan, before the gathers are consumed.
-struct InPlacePolicy {
+// SYNC = true: the same fused finalize for a SYNCHRONOUS sweep (K-GATHER +
+// K-FINALIZE in one launch): contribs are read from y_in (not written in this
+// sweep: shared-memory hot tier, L1 tier, .nc loads) and the new contribs go to
+// the other ping-pong buffer y.
+template <bool SYNC>
+struct InPlacePolicyT {
     static constexpr bool kHot = true;
-    const double* y_in;   // == y: relaxed loads
-    double* y;            // relaxed stores
+    const double* y_in;   // async: == y, relaxed loads; sync: the previous sweep's contribs
+    double* y;            // async: relaxed stores; sync: plain stores into the next buffer
     const double* hot;
     int32_t hot_n;
     uint64_t pol_last;
@@ -610,6 +615,7 @@ struct InPlacePolicy {
 
     __device__ __forceinline__ double load(int32_t u) const {
         if (u < hot_n) return hot[u];
+        if (SYNC) return ld_gather_tiered_f64(y_in + u, u < SE_L1_TIER, pol_last);
         return ld_relaxed_f64(y_in + u);
     }
     __device__ __forceinline__ void prep(int64_t base, uint32_t f) {
@@ -628,7 +634,12 @@ struct InPlacePolicy {
     __device__ __forceinline__ void fin(int64_t r, double s, int2 q, double xold) {
         const double xn = __dadd_rn(c, __dmul_rn(d, s));
         st_relaxed_f64(xr + r, xn);
-        if (q.x > 0) st_relaxed_f64(y + q.y, xn / (double)q.x);
+        if (q.x > 0) {
+            if (SYNC)
+                y[q.y] = xn / (double)q.x;
+            else
+                st_relaxed_f64(y + q.y, xn / (double)q.x);
+        }
         const double dl = fabs(xn - xold);
         l1 += dl;
         linf = fmax(linf, dl);
@@ -637,6 +648,8 @@ struct InPlacePolicy {
     __device__ __forceinline__ void emit_at(int j, int64_t r, double s) { fin(r, s, inf[j], xo[j]); }
     __device__ __forceinline__ void emit_first(int64_t r, double s) { fin(r, s, inf_f, xo_f); }
 };
+
+using InPlacePolicy = InPlacePolicyT<false>;
 
 // Members of a reduced view, in place: x(m) = alpha_k + beta_k * x(src) with
 // x(src) as currently visible (its row in xr), fused contrib, Delta.
@@ -696,6 +709,70 @@ __global__ void __launch_bounds__(SE_NT_IP, 1)
     if (flag) global_finalize(ia, red);
 }
 
+// One synchronous sweep with the finalize fused into the gather (rows only;
+// in reduced mode k_members_sync follows and runs the global reduction).
+__global__ void __launch_bounds__(SE_NT_IP, 1)
+    k_stream_fused(InPlacePolicyT<true> p, StreamArgs a, IterArgs ia, int finalize) {
+    extern __shared__ __align__(16) double hot_smem[];
+    __shared__ double red[2 * RED_W];
+    __shared__ int flag;
+    if (ia.st->done) return;
+    p.pol_last = policy_evict_last();
+    {
+        const double2* src = reinterpret_cast<const double2*>(p.y_in);
+        double2* dst = reinterpret_cast<double2*>(hot_smem);
+        for (int i = threadIdx.x; i < (p.hot_n >> 1); i += blockDim.x) dst[i] = __ldcg(src + i);
+        if ((p.hot_n & 1) && threadIdx.x == 0) hot_smem[p.hot_n - 1] = __ldcg(p.y_in + p.hot_n - 1);
+        p.hot = hot_smem;
+        __syncthreads();
+    }
+    p.l1 = 0.0;
+    p.linf = 0.0;
+    stream_run(p, a);
+    block_delta(p.l1, p.linf, red, ia.cta_partial + 2 * blockIdx.x);
+    if (!finalize) return;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t t = atomicAdd(&ia.st->ticket_gather, 1u);
+        flag = (t == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (flag) global_finalize(ia, red);
+}
+
+// Members after a fused synchronous sweep: x(m) = alpha_k + beta_k * x_t(src)
+// (the source's new value, row order), next contrib, Delta; the last CTA runs
+// the global reduction over the gather and member partials.
+__global__ void __launch_bounds__(GT_NT) k_members_sync(MemArgs ma, const double* __restrict__ xr, double* y_out,
+                                                        IterArgs ia) {
+    __shared__ double red[2 * RED_W];
+    __shared__ int flag;
+    if (ia.st->done) return;
+    double l1 = 0.0, linf = 0.0;
+    const int64_t mb = (int64_t)blockIdx.x * ma.mper;
+    const int64_t me = min(ma.nm, mb + ma.mper);
+    for (int64_t i = mb + threadIdx.x; i < me; i += blockDim.x) {
+        const int32_t k = ma.mk[i];
+        const double xs = __ldcg(xr + ma.msrow[i]);
+        const double xn = __dadd_rn(ma.ab[2 * k], __dmul_rn(ma.ab[2 * k + 1], xs));
+        const double xo = ma.xm[i];
+        ma.xm[i] = xn;
+        const int2 q = ma.minfo[i];
+        if (q.x > 0) y_out[q.y] = xn / (double)q.x;
+        const double dl = fabs(xn - xo);
+        l1 += dl;
+        linf = fmax(linf, dl);
+    }
+    block_delta(l1, linf, red, ia.cta_partial + 2 * (ia.gather_ctas + blockIdx.x));
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t t = atomicAdd(&ia.st->ticket_scatter, 1u);
+        flag = (t == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (flag) global_finalize(ia, red);
+}
+
 // Persistent No-Sync on the edge-stream engine (see k_nosync for the protocol).
 __global__ void __launch_bounds__(SE_NT_IP, 1) k_nosync_stream(InPlacePolicy p, StreamArgs a, MemArgs ma, NoSyncArgs na) {
     extern __shared__ __align__(16) double hot_smem[];
@@ -732,6 +809,7 @@ __global__ void __launch_bounds__(SE_NT_IP, 1) k_nosync_stream(InPlacePolicy p, 
 struct GatherCfg {
     bool stream;  // sync: edge-stream gather + K-FINALIZE; async (or PRGPU_ENGINE=tasks): row-task engine
     bool inplace; // async on the edge-stream engine (k_stream_async; PRGPU_ENGINE=tasks: row-task engine)
+    bool fused;   // sync stream sweep with the finalize fused into the gather (k_stream_fused)
     bool async, vid;
     int hot_n;
     size_t smem;
@@ -797,10 +875,17 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, Gathe
     const bool tasks = eng && eng[0] == 't';
     gc->stream = !async && (force_stream || !tasks);
     gc->inplace = async && !tasks;
+    gc->fused = gc->stream && !force_stream && v.nseg == 0 && env_int("PRGPU_FUSED", 0) != 0;
     gc->async = async;
     gc->vid = v.vid != nullptr;
     gc->hot_n = 0;
-    if (gc->inplace) {
+    if (gc->fused) {
+        int hot = env_int("PRGPU_HOT", SE_HOT_MAX);
+        hot = std::max(0, std::min<int>(std::min(hot, SE_HOT_MAX), (int)g->n_contrib));
+        gc->hot_n = hot;
+        gc->smem = (size_t)hot * sizeof(double);
+        gc->nt = SE_NT_IP;
+    } else if (gc->inplace) {
         int hot = env_int("PRGPU_HOT", SE_HOT_IP);
         hot = std::max(0, std::min<int>(std::min(hot, SE_HOT_MAX), (int)g->n_contrib));
         gc->hot_n = hot;
@@ -818,7 +903,8 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, bool async, Gathe
         gc->smem = sizeof(EngineSmem);
         gc->nt = GT_NT;
     }
-    const void* fn = gc->inplace ? (const void*)k_stream_async : gather_fn(*gc);
+    const void* fn = gc->fused ? (const void*)k_stream_fused
+                               : (gc->inplace ? (const void*)k_stream_async : gather_fn(*gc));
     PR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gc->smem));
     int per_sm = 0;
     PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, gc->nt, gc->smem));
@@ -883,8 +969,8 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         const int64_t work = v.nrows + nm;
         fgrid = std::min<int64_t>(std::max<int64_t>((work + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
     }
-    const int ggrid = gc.stream ? (int)fgrid : gc.grid;  // CTAs writing Delta partials first
-    int64_t sgrid = (!gc.stream && !gc.inplace && nm > 0) ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
+    const int ggrid = (gc.stream && !gc.fused) ? (int)fgrid : gc.grid;  // CTAs writing Delta partials first
+    int64_t sgrid = ((gc.fused || (!gc.stream && !gc.inplace)) && nm > 0) ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
     if (sgrid > cap4) sgrid = cap4;
     const int64_t sper = sgrid > 0 ? (nm + sgrid - 1) / sgrid : 0;
     const int64_t nz = g->nz;
@@ -926,7 +1012,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     PR_LAUNCH(ctx, k_init, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, x,
               g->y[0], (const int32_t*)g->outdeg, (const int32_t*)g->cidx, n, 1.0 / (double)n);
 
-    const int64_t sctas = (reduced && !gc.stream && !gc.inplace) ? sgrid : 0;
+    const int64_t sctas = (reduced && (gc.fused || (!gc.stream && !gc.inplace))) ? sgrid : 0;
     IterArgs ia_rest{g->st,
                      g->cta_partial,
                      (int64_t)ggrid,
@@ -938,7 +1024,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     IterArgs ia_first = ia_rest;
     ia_first.zero_ctas = zgrid;
     double* zero_partial = g->cta_partial + 2 * ((int64_t)ggrid + sctas);
-    const bool gather_finalizes = !gc.stream && !(reduced && sgrid > 0);
+    const bool gather_finalizes = (gc.fused || !gc.stream) && !(reduced && sgrid > 0);
     const StreamArgs sa{v.col,  (const uint8_t*)v.sflags, v.step_row, v.nsteps, v.span_steps, v.nspans, v.bin,
                         v.bout, v.b_row, v.b_s0, v.b_s1, v.part_in, v.part_out, v.bticket};
     const MemArgs ma{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, nm > 0 ? (nm + gc.grid - 1) / gc.grid : 0, g->ab};
@@ -979,7 +1065,17 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                 PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y_out,
                           (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
-            if (gc.inplace) {
+            if (gc.fused) {
+                InPlacePolicyT<true> fp{};
+                fp.y_in = y_in;
+                fp.y = y_out;
+                fp.hot_n = gc.hot_n;
+                fp.xr = g->xr;
+                fp.rinfo = v.rinfo;
+                fp.c = c;
+                fp.d = d;
+                PR_LAUNCH(ctx, k_stream_fused, gc.grid, gc.nt, gc.smem, fp, sa, ia, gather_finalizes ? 1 : 0);
+            } else             if (gc.inplace) {
                 InPlacePolicy ip{};
                 ip.y_in = g->y[0];
                 ip.y = g->y[0];
@@ -993,7 +1089,12 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                 PR_TRY(launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, gather_finalizes));
             }
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
-            if (gc.stream) {
+            if (gc.fused) {
+                if (!gather_finalizes) {
+                    MemArgs mf{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, (nm + sgrid - 1) / sgrid, g->ab};
+                    PR_LAUNCH(ctx, k_members_sync, (unsigned)sgrid, GT_NT, 0, mf, (const double*)g->xr, y_out, ia);
+                }
+            } else if (gc.stream) {
                 FinArgs f = fa;
                 f.y_out = y_out;
                 PR_LAUNCH(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);

@@ -150,3 +150,22 @@ def test_blocked_rmat(pr, monkeypatch):
         st, it, fd, x = gpu_run(pr, g, gen.n, 1e-10)
         assert_iters(it, ref, 1e-10)
         assert_close(x, ref.x)
+
+
+def test_fused_sweep_matches_split(pr, monkeypatch):
+    """K-GATHER with the finalize fused in (PRGPU_FUSED=1, measured slower) vs
+    the default split K-GATHER + K-FINALIZE: same S per row, same update
+    formula, so the ranks are bit-identical (the Delta sums may differ in their
+    last bits)."""
+    gen = graphgen.make_config(4, scale_override=15)
+    out = {}
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        g.preprocess()
+        for fused in ("1", "0"):
+            monkeypatch.setenv("PRGPU_FUSED", fused)
+            for mode in (0, pr.PR_USE_REDUCTIONS):
+                out[(fused, mode)] = gpu_run(pr, g, gen.n, 0.0, max_iter=40, mode=mode)
+    for mode in (0, pr.PR_USE_REDUCTIONS):
+        a, b = out[("1", mode)], out[("0", mode)]
+        assert a[1] == b[1] == 40
+        assert np.array_equal(a[3], b[3])
