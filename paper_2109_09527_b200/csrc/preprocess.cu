@@ -250,13 +250,25 @@ __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const i
             else
                 hi = mid;
         }
-        int64_t i = lo, o = o0;
+        // rows of the chunk, 32 at a time: every lane fetches one row's
+        // (output start, source start) so the row walk has no dependent loads
+        int64_t i0 = lo, o = o0;
         while (o < o1) {
-            const int64_t re = min(o1, rpR[i + 1]);
-            const int64_t src = rp[vid[i]] + (o - rpR[i]);
-            for (int64_t k = lane; k < re - o; k += 32) colR[o + k] = col[src + k];
-            o = re;
-            ++i;
+            const int64_t ri = i0 + lane;
+            int64_t ostart = 0, sstart = 0;
+            if (ri < nr) {
+                ostart = rpR[ri];
+                sstart = rp[vid[ri]];
+            }
+            for (int q = 0; q < 32 && o < o1; ++q) {
+                const int64_t os = __shfl_sync(0xffffffffu, ostart, q);
+                const int64_t ss = __shfl_sync(0xffffffffu, sstart, q);
+                const int64_t oe = min(o1, (i0 + q + 1 < nr) ? __shfl_sync(0xffffffffu, ostart, (q + 1) & 31) : ER);
+                const int64_t re = (q == 31) ? min(o1, (i0 + 32 < nr) ? rpR[i0 + 32] : ER) : oe;
+                for (int64_t k = o + lane; k < re; k += 32) colR[k] = col[ss + (k - os)];
+                o = re;
+            }
+            i0 += 32;
         }
     }
 }

@@ -68,7 +68,7 @@ template <class T>
 __global__ void __launch_bounds__(1024) k_scan_partials(T* partial, int64_t G, T* total) {
     __shared__ T sw[33];
     T carry = T(0);
-    constexpr int IPT = 8;
+    constexpr int IPT = sizeof(T) == 4 ? 32 : 16;  // few block scans: this kernel is latency-bound
     for (int64_t base = 0; base < G; base += 1024 * IPT) {
         T v[IPT];
         T ts = T(0);
