@@ -450,19 +450,33 @@ __global__ void __launch_bounds__(GT_NT) k_scatter(const int32_t* __restrict__ m
 __global__ void __launch_bounds__(GT_NT) k_zero(const int32_t* __restrict__ zl, int64_t nz, int64_t per_cta, double c,
                                                 double* x, double* y_out, const int32_t* __restrict__ od,
                                                 const int32_t* __restrict__ cidx, double* partial) {
+    // grid-stride, 4 vertices per thread with all loads issued first (the
+    // old x is read too: it is 1/n from k_init, but Delta_1 must be measured)
+    (void)per_cta;
     __shared__ double red[2 * RED_W];
-    const int64_t b = (int64_t)blockIdx.x * per_cta;
-    const int64_t e = min(nz, b + per_cta);
     double l1 = 0.0, linf = 0.0;
-    for (int64_t i = b + threadIdx.x; i < e; i += GT_NT) {
-        const int32_t v = zl[i];
-        const double xo = x[v];
-        x[v] = c;
-        const int32_t o = od[v];
-        if (o > 0) y_out[cidx[v]] = c / (double)o;
-        const double dl = fabs(c - xo);
-        l1 += dl;
-        linf = fmax(linf, dl);
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < nz; i0 += 4 * T) {
+        int32_t v[4], o[4], ci[4];
+        double xo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = i0 + u * T < nz ? __ldg(zl + i0 + u * T) : -1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (v[u] >= 0) {
+                xo[u] = x[v[u]];
+                o[u] = __ldg(od + v[u]);
+                ci[u] = __ldg(cidx + v[u]);
+            }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (v[u] >= 0) {
+                x[v[u]] = c;
+                if (o[u] > 0) y_out[ci[u]] = c / (double)o[u];
+                const double dl = fabs(c - xo[u]);
+                l1 += dl;
+                linf = fmax(linf, dl);
+            }
     }
     block_delta(l1, linf, red, partial + 2 * blockIdx.x);
 }
