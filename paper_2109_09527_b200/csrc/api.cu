@@ -257,8 +257,7 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
         dfree(ddst, ctx.stream);
         if ((rc = build_relabel(g, ctx)) != PR_OK) break;
         pt.mark("relabel");
-        if ((rc = build_view_tasks(g->plain, ctx)) != PR_OK) break;
-        pt.mark("tasks");
+
         if ((rc = build_view_stream(g->plain, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx)) != PR_OK) break;
         if ((rc = build_view_blocked(g->plain, ctx, g->n_contrib)) != PR_OK) break;
         pt.mark("stream");

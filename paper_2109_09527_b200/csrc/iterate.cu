@@ -81,6 +81,7 @@ constexpr int RED_W = 32;
 // HOT: contribs [0, hot_n) are read from the CTA's shared-memory copy.
 template <bool HOT>
 struct StreamPolicy {
+    using T = double;
     static constexpr bool kHot = HOT;
     const double* y_in;
     double* sums;
@@ -101,6 +102,7 @@ struct StreamPolicy {
 // One segment pass of a source-blocked view (blocked.cu): gathers come from
 // one L2-resident slice of y; S_seg(r) is added to the parent row's sum.
 struct AccumPolicy {
+    using T = double;
     static constexpr bool kHot = false;
     const double* y_in;
     double* sums;
@@ -612,6 +614,7 @@ __global__ void k_residual(const double* __restrict__ sums, int64_t nrows, const
 // the other ping-pong buffer y.
 template <bool SYNC>
 struct InPlacePolicyT {
+    using T = double;
     static constexpr bool kHot = true;
     const double* y_in;   // async: == y, relaxed loads; sync: the previous sweep's contribs
     double* y;            // async: relaxed stores; sync: plain stores into the next buffer
@@ -942,8 +945,27 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
 static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
                           Ctx& ctx, int32_t* iters_out, double* delta_out);
 
+// The row-task engine's tables are built on first use (async / No-Sync with
+// PRGPU_ENGINE=tasks); an aliased reduced view shares the plain view's.
+static bool tasks_engine_requested() {
+    const char* e = getenv("PRGPU_ENGINE");
+    return e && e[0] == 't';
+}
+static int ensure_tasks(pr_graph* g, bool reduced, Ctx& ctx) {
+    View& v = reduced ? g->reduced : g->plain;
+    if (v.alias) {
+        PR_TRY(ensure_tasks(g, false, ctx));
+        g->reduced = g->plain;
+        g->reduced.alias = true;
+        return PR_OK;
+    }
+    if (!v.tasks && v.nrows > 0) PR_TRY(build_view_tasks(v, ctx));
+    return PR_OK;
+}
+
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
         int32_t* iters_out, double* delta_out) {
+    if (tasks_engine_requested()) PR_TRY(ensure_tasks(g, (mode & PR_USE_REDUCTIONS) != 0, ctx));
     if (mode & PR_MODE_NOSYNC) return run_nosync(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     if (mode & PR_PERFORATE) return run_perforated(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     cudaStream_t s = ctx.stream;

@@ -3,8 +3,9 @@
 //
 // Identical groups: v ~ w iff in(v) == in(w) as sets (after dedup); rep(v) =
 // min id of the class; the empty in-set is one class.
-//   1. row hash h(v) = mix(indeg) + sum_{u in in(v)} mix(u)  (row engine), for
-//      the rows of in-degree > 0 (the in-degree-0 vertices are one class)
+//   1. row hash h(v) = mix(indeg) + sum over the row's contrib slots of mix(slot)
+//      (edge-stream engine, uint64 sums), for the rows of in-degree > 0 (the
+//      in-degree-0 vertices are one class)
 //   2. stable radix sort of those ids by the top 48 bits of h -> runs of equal
 //      bits, ids ascending
 //   3. exact verification of every member against the run's first vertex; on a
@@ -13,42 +14,17 @@
 //   Pointer jumping over chain vertices (next = pred while pred is a chain
 //   vertex) gives every vertex its head and distance k; vertices that never
 //   reach a head lie on pure cycles and are not members.
+#include <algorithm>
+
 #include "internal.h"
 #include "primitives.cuh"
 #include "rowengine.cuh"
+#include "streamengine.cuh"
 
 namespace prgpu {
 
 // ---------------------------------------------------------------- hashing --
 constexpr uint64_t kDegSalt = 0xD6E8FEB86659FD93ULL;
-
-struct HashPolicy {
-    using T = uint64_t;
-    const int64_t* rp;   // canonical row_ptr (by vertex id)
-    const int32_t* vid;  // view rows -> vertex ids (nullptr: identity)
-    uint64_t* out;
-    __device__ __forceinline__ void begin() {}
-    __device__ __forceinline__ uint64_t load(int32_t u) const {
-        return mix64((uint64_t)(uint32_t)u * 0x9E3779B97F4A7C15ULL + 0x2545F4914F6CDD1DULL);
-    }
-    struct Pre {
-        int64_t r, v, deg;
-    };
-    __device__ __forceinline__ Pre prefetch(int64_t r) const {
-        const int64_t v = vid ? vid[r] : r;
-        return Pre{r, v, rp[v + 1] - rp[v]};
-    }
-    Pre pre[2];
-    __device__ __forceinline__ void prefetch_rows(int64_t r0, int nr, int lane) {
-        if (lane < nr) pre[0] = prefetch(r0 + lane);
-        if (lane + 32 < nr) pre[1] = prefetch(r0 + lane + 32);
-    }
-    __device__ __forceinline__ const Pre& prefetched(int h) const { return pre[h]; }
-    __device__ __forceinline__ double finalize(const Pre& q, uint64_t s) const {
-        out[q.r] = s + mix64((uint64_t)q.deg + kDegSalt);  // by view row
-        return 0.0;
-    }
-};
 
 // The empty in-set is one class: its vertices (zlist, ascending) all
 // get the smallest of them as representative.
@@ -62,12 +38,37 @@ __global__ void k_u32_from(const int32_t* __restrict__ a, int64_t n, uint32_t* _
         out[i] = a ? (uint32_t)a[i] : (uint32_t)i;
 }
 
-__global__ void __launch_bounds__(GT_NT) k_rowhash(HashPolicy p, EngineArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    EngineSmem& sm = *reinterpret_cast<EngineSmem*>(smem_raw);
-    double l1 = 0.0, linf = 0.0;
-    engine_run(p, a, sm, l1, linf);
+// The same row hash on the edge-stream engine (sum type uint64, wrapping):
+// S(r) = sum over the row's contrib slots of mix(slot) -- slots are a bijection
+// on sources, so equal in-sets <=> equal slot sets; the pad slot adds 0.
+struct HashStreamPolicy {
+    using T = uint64_t;
+    static constexpr bool kHot = false;
+    uint64_t* out;     // by view row
+    int32_t pad;       // the padding slot (contributes nothing)
+    const double* hot;
+    int32_t hot_n;
+    uint64_t pol_last;
+    __device__ __forceinline__ uint64_t load(int32_t u) const {
+        return u == pad ? 0ull : mix64((uint64_t)(uint32_t)u * 0x9E3779B97F4A7C15ULL + 0x2545F4914F6CDD1DULL);
+    }
+    __device__ __forceinline__ void emit(int64_t r, uint64_t s) const { out[r] = s; }
+    __device__ __forceinline__ void prep(int64_t, uint32_t) {}
+    __device__ __forceinline__ void emit_at(int, int64_t r, uint64_t s) const { out[r] = s; }
+    __device__ __forceinline__ void emit_first(int64_t r, uint64_t s) const { out[r] = s; }
+};
+
+__global__ void __launch_bounds__(SE_NT, 1) k_rowhash_stream(HashStreamPolicy p, StreamArgs a) { stream_run(p, a); }
+
+// + mix(indeg + salt): rows of different in-degree never share a hash by construction
+__global__ void k_hash_deg(uint64_t* __restrict__ h, int64_t nr, const int32_t* __restrict__ vid,
+                           const int64_t* __restrict__ rp) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = vid ? vid[r] : r;
+        h[r] += mix64((uint64_t)(rp[v + 1] - rp[v]) + kDegSalt);
+    }
 }
+
 
 
 __device__ __forceinline__ bool same_row(const int64_t* rp, const int32_t* col, int32_t u, int32_t v) {
@@ -325,15 +326,12 @@ static int find_identical(pr_graph* g, Ctx& ctx) {
     PR_TRY(dalloc(&sv, (size_t)nr, s));
     PR_TRY(dalloc(&sv2, (size_t)nr, s));
     {
-        HashPolicy p{g->row_ptr, v.vid, h, {}};
-        EngineArgs a{v.tasks, v.ntasks, v.hubs, v.row_ptr, g->col, v.hub_partial, v.hub_delta, v.hub_ticket};
-        int per_sm = 0;
-        cudaFuncSetAttribute(k_rowhash, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EngineSmem));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rowhash, GT_NT, sizeof(EngineSmem));
-        int64_t grid = (int64_t)ctx.num_sms * (per_sm > 0 ? per_sm : 1);
-        if (grid > v.ntasks) grid = v.ntasks;
-        if (grid < 1) grid = 1;
-        PR_LAUNCH(ctx, k_rowhash, (unsigned)grid, GT_NT, sizeof(EngineSmem), p, a);
+        const StreamArgs sa{v.col,  (const uint8_t*)v.sflags, v.step_row, v.nsteps, v.span_steps, v.nspans, v.bin,
+                            v.bout, v.b_row, v.b_s0, v.b_s1, v.part_in, v.part_out, v.bticket};
+        HashStreamPolicy hp{h, (int32_t)g->n_contrib, nullptr, 0, 0};
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ctx.num_sms, (v.nspans + SE_NT / 32 - 1) / (SE_NT / 32)));
+        if (v.nspans > 0) PR_LAUNCH(ctx, k_rowhash_stream, (unsigned)grid, SE_NT, 0, hp, sa);
+        PR_LAUNCH(ctx, k_hash_deg, grid_of(ctx, nr), 256, 0, h, nr, (const int32_t*)v.vid, (const int64_t*)g->row_ptr);
     }
     PR_LAUNCH(ctx, k_u32_from, grid_of(ctx, nr), 256, 0, (const int32_t*)v.vid, nr, sv);
     // stable sort of the rows (ids ascending) by the top 48 hash bits; equal
@@ -463,7 +461,6 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
     if (R.nrows > 0)
         PR_LAUNCH(ctx, k_copy_rows, grid_of(ctx, R.nrows * 32), 256, 0, (const int32_t*)R.vid, R.nrows,
                   (const int64_t*)g->row_ptr, (const int32_t*)g->plain.col, (const int64_t*)R.row_ptr, R.col);
-    PR_TRY(build_view_tasks(R, ctx));
     PR_TRY(build_view_stream(R, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx));
     PR_TRY(build_view_blocked(R, ctx, g->n_contrib));
     // source row of every member in the reduced view (K-FINALIZE reads its S)

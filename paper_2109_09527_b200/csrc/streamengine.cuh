@@ -45,7 +45,7 @@ struct StreamArgs {
     const int32_t* b_row;      // [nbound] row id
     const int32_t* b_s0;       // [nbound] first span of the row
     const int32_t* b_s1;       // [nbound] last span of the row
-    double* part_in;           // [nspans]
+    double* part_in;           // [nspans] (8-byte pieces; reinterpreted for non-fp64 sums)
     double* part_out;          // [nspans]
     uint32_t* bticket;         // [nbound]
 };
@@ -67,12 +67,16 @@ __device__ __forceinline__ uint32_t ld_stream_u8(const uint8_t* p) {
 // `span`) to the ticket protocol; the last of the b_s1 - b_s0 + 1 pieces sums
 // them in span order and finalizes the row.
 template <class P>
-__device__ __forceinline__ void stream_piece(P& p, const StreamArgs& a, int32_t b, int64_t span, double val,
-                                             bool out_piece) {
+__device__ __forceinline__ void stream_piece(P& p, const StreamArgs& a, int32_t b, int64_t span,
+                                             typename P::T val, bool out_piece) {
+    using T = typename P::T;
+    static_assert(sizeof(T) == sizeof(double), "8-byte pieces");
+    T* pin = reinterpret_cast<T*>(a.part_in);
+    T* pout = reinterpret_cast<T*>(a.part_out);
     if (out_piece)
-        a.part_out[span] = val;
+        pout[span] = val;
     else
-        a.part_in[span] = val;
+        pin[span] = val;
     // release: the piece is visible before the ticket moves.  (A __threadfence
     // here compiles to MEMBAR.SC + CCTL.IVALL, which would also invalidate this
     // SM's L1 and with it the L1 tier of hot contribs.)
@@ -87,8 +91,8 @@ __device__ __forceinline__ void stream_piece(P& p, const StreamArgs& a, int32_t 
                  : "memory");
     if (t == (uint32_t)(s1 - s0)) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");  // winner only: acquire the other pieces
-        double sum = __ldcg(a.part_out + s0);
-        for (int32_t s = s0 + 1; s <= s1; ++s) sum += __ldcg(a.part_in + s);
+        T sum = __ldcg(pout + s0);
+        for (int32_t s = s0 + 1; s <= s1; ++s) sum += __ldcg(pin + s);
         p.emit((int64_t)a.b_row[b], sum);
     }
 }
@@ -101,7 +105,8 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
     const int64_t se = min(a.nsteps, sb + a.span_steps);
     const int32_t bin = a.bin[span];
     bool first_closure = true;  // no row has started in this span yet
-    double carry = 0.0;         // sum of the row open at the current step's start
+    using T = typename P::T;
+    T carry = T(0);             // sum of the row open at the current step's start
     // software pipeline: the indices, flags and step_row of step s+1 are loaded
     // while the gathers of step s are in flight
     int4 c0 = ld_stream_v4(a.col + sb * SE_STEP + (int64_t)lane * SE_V, pol_stream);
@@ -109,7 +114,7 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
     uint32_t fn = ld_stream_u8(a.flags8 + sb * 32 + lane);
     int32_t Rn = a.step_row[sb];
     for (int64_t s = sb; s < se; ++s) {
-        double v[SE_V];
+        T v[SE_V];
         v[0] = p.load(c0.x);
         v[1] = p.load(c0.y);
         v[2] = p.load(c0.z);
@@ -142,7 +147,7 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
         p.prep((int64_t)R0 - 1 + rank0, f);  // policy may prefetch per-row data of this lane's closures
         // in-lane segments: the i-th start (i >= 1) of this lane closes slot
         // rank0 + i, i.e. row R0 - 1 + rank0 + i, with the lane-local segment
-        double run = 0.0, head = 0.0;
+        T run = T(0), head = T(0);
         int i = 0;
 #pragma unroll
         for (int j = 0; j < SE_V; ++j) {
@@ -153,19 +158,19 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
                     p.emit_at(j, (int64_t)R0 - 1 + rank0 + i, run);
                 }
                 ++i;
-                run = 0.0;
+                run = T(0);
             }
             run += v[j];
         }
         // open segment of each lane flows right until the next lane with a start
-        double o = run;
+        T o = run;
         if (lane == 0 && nf == 0) o = carry + o;
-        double S = o;
+        T S = o;
         int F = nf > 0;
 #ifndef PRGPU_ABL_NODSCAN
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const double tS = __shfl_up_sync(0xffffffffu, S, d);
+            const T tS = __shfl_up_sync(0xffffffffu, S, d);
             const int tF = __shfl_up_sync(0xffffffffu, F, d);
             if (lane >= d && !F) {
                 S = tS + S;
@@ -173,11 +178,11 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
             }
         }
 #endif
-        double I = __shfl_up_sync(0xffffffffu, S, 1);
+        T I = __shfl_up_sync(0xffffffffu, S, 1);
         if (lane == 0) I = carry;
         carry = __shfl_sync(0xffffffffu, S, 31);
         if (nf > 0) {  // the first start of this lane closes slot rank0
-            const double val = I + head;
+            const T val = I + head;
             if (rank0 == 0 && first_closure) {
                 if (bin >= 0) stream_piece(p, a, bin, span, val, false);
                 // else: the span begins with a row start; slot 0 is the previous span's row
