@@ -44,6 +44,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-modes", action="store_true", help="skip the async / No-Sync / perforation comparison")
+    p.add_argument("--no-plain", action="store_true", help="skip the extra plain-sweep roofline run")
     return p.parse_args()
 
 
@@ -205,6 +207,52 @@ def run_reference(args, ws, rank):
     return 0
 
 
+def compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags):
+    """Time to converge of the iteration modes on the same graph, outside the
+    timed region: sync (Barriers, Alg.1), launch-level in-place async,
+    persistent barrier-free No-Sync (Alg.3) -- the paper's Fig.7 comparison,
+    P:994 -- and loop perforation (Barriers-Opt, Alg.5; plain sync only,
+    approximate) with its work fraction and L1 distance to the exact plain
+    result (the Figs.5-6 analogue)."""
+    def timed(g, mode):
+        best = None
+        for _ in range(3):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            rc_, it_, fd_ = g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=mode)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms_ = a.elapsed_time(b)
+            if best is None or ms_ < best[0]:
+                best = (ms_, it_, fd_, g.stats())
+        return best
+
+    modes = {}
+    g = pr.Graph(n, src_d, dst_d)
+    if flags:
+        g.preprocess(flags)
+    red = pr.PR_USE_REDUCTIONS if flags else 0
+    for name, md in (("sync", red), ("async", red | pr.PR_MODE_ASYNC), ("nosync", red | pr.PR_MODE_NOSYNC)):
+        ms_, it_, fd_, st_ = timed(g, md)
+        rec = {"time_to_converge_ms": round(ms_, 3), "iterations": it_, "final_delta": fd_}
+        if name == "nosync":
+            rec["min_local_sweeps"] = st_["nosync_min_iters"]
+            rec["certified_residual"] = st_["residual"]
+        modes[name] = rec
+    rc_, it_e, fd_ = g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=0)
+    x_exact = x_d.clone()
+    work_exact = g.stats()["edges_gathered"]
+    ms_, it_, fd_, st_ = timed(g, pr.PR_PERFORATE)
+    modes["perforated_plain"] = {
+        "time_to_converge_ms": round(ms_, 3), "iterations": it_,
+        "work_fraction": round(st_["edges_gathered"] / max(1, work_exact), 4),
+        "frozen_rows": st_["frozen_rows"], "compactions": st_["compactions"],
+        "l1_vs_exact_plain": float((x_d - x_exact).abs().sum()), "exact_plain_iterations": it_e}
+    g.close()
+    return modes
+
+
 # --------------------------------------------------------------------- ours --
 def main():
     args = parse()
@@ -317,7 +365,7 @@ def main():
 
     # plain-mode sweep (the north_star 60 % target), one extra untimed run
     extra = {}
-    if args.mode != "plain":
+    if args.mode != "plain" and not args.no_plain:
         g = pr.Graph(n, src_d, dst_d)
         g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=pr.PR_TIMING)
         sp = g.stats()
@@ -335,54 +383,8 @@ def main():
                                 "iterations": sp["iterations"]}
         g.close()
 
-    # time-to-converge of the three iteration modes on the same graph (the
-    # paper's Barriers vs No-Sync comparison, Fig.7): sync (Alg.1),
-    # launch-level in-place async, persistent barrier-free No-Sync (Alg.3)
-    modes = {}
-    g = pr.Graph(n, src_d, dst_d)
-    if flags:
-        g.preprocess(flags)
-    red = pr.PR_USE_REDUCTIONS if flags else 0
-    for name, md in (("sync", red), ("async", red | pr.PR_MODE_ASYNC), ("nosync", red | pr.PR_MODE_NOSYNC)):
-        best = None
-        for _ in range(3):
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            rc_, it_, fd_ = g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=md)
-            b.record(stream)
-            torch.cuda.synchronize()
-            ms_ = a.elapsed_time(b)
-            if best is None or ms_ < best[0]:
-                best = (ms_, it_, fd_, g.stats())
-        rec = {"time_to_converge_ms": round(best[0], 3), "iterations": best[1], "final_delta": best[2]}
-        if name == "nosync":
-            rec["min_local_sweeps"] = best[3]["nosync_min_iters"]
-            rec["certified_residual"] = best[3]["residual"]
-        modes[name] = rec
-    # loop perforation (Barriers-Opt, Alg.5; plain sync only, approximate):
-    # time, work and L1 distance to the exact plain sync result (Figs.5-6 analogue)
-    rc_, it_e, fd_ = g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=0)
-    x_exact = x_d.clone()
-    work_exact = g.stats()["edges_gathered"]
-    best = None
-    for _ in range(3):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        rc_, it_, fd_ = g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=pr.PR_PERFORATE)
-        b.record(stream)
-        torch.cuda.synchronize()
-        ms_ = a.elapsed_time(b)
-        if best is None or ms_ < best[0]:
-            best = (ms_, it_, g.stats())
-    modes["perforated_plain"] = {
-        "time_to_converge_ms": round(best[0], 3), "iterations": best[1],
-        "work_fraction": round(best[2]["edges_gathered"] / max(1, work_exact), 4),
-        "frozen_rows": best[2]["frozen_rows"], "compactions": best[2]["compactions"],
-        "l1_vs_exact_plain": float((x_d - x_exact).abs().sum()), "exact_plain_iterations": it_e}
-    g.close()
-    extra["modes"] = modes
+    if not args.no_modes:
+        extra["modes"] = compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags)
 
     # e2e: the same step through the same ABI calls with HOST (pinned) buffers
     e2e = None
