@@ -101,6 +101,13 @@ int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib) {
 
     uint32_t *keys = nullptr, *keys_alt = nullptr, *rows = nullptr, *rows_alt = nullptr;
     int64_t* start = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(keys);
+    tg_.track(keys_alt);
+    tg_.track(rows);
+    tg_.track(rows_alt);
+    tg_.track(start);
+
     PR_TRY(dalloc(&keys, (size_t)E, s));
     PR_TRY(dalloc(&keys_alt, (size_t)E, s));
     PR_TRY(dalloc(&rows, (size_t)E, s));
@@ -129,6 +136,7 @@ int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib) {
     v.nseg = nseg;
     v.seg_bits = bits;
     int64_t* cnt = nullptr;
+    tg_.track(cnt);
     PR_TRY(dalloc(&cnt, 1, s));
     for (int q = 0; q < nseg; ++q) {
         View& sv = v.seg[q];

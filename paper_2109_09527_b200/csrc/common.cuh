@@ -69,6 +69,30 @@ void dfree(T*& p, cudaStream_t s) {
     p = nullptr;
 }
 
+// Frees the device temporaries registered with track() when the scope ends,
+// early error returns included; a pointer already released with dfree (and so
+// set to nullptr) is skipped.  Graph-owned buffers are never tracked: on error
+// pr_destroy releases those.
+struct TmpGuard {
+    cudaStream_t s;
+    void** slot[48];
+    int k = 0;
+    explicit TmpGuard(cudaStream_t st) : s(st) {}
+    TmpGuard(const TmpGuard&) = delete;
+    TmpGuard& operator=(const TmpGuard&) = delete;
+    template <class T>
+    void track(T*& p) {
+        if (k < 48) slot[k++] = reinterpret_cast<void**>(&p);
+    }
+    ~TmpGuard() {
+        for (int i = k - 1; i >= 0; --i)
+            if (*slot[i]) {
+                cudaFreeAsync(*slot[i], s);
+                *slot[i] = nullptr;
+            }
+    }
+};
+
 constexpr int WARP = 32;
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }

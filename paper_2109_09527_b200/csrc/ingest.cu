@@ -162,6 +162,11 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
     uint64_t* keys = nullptr;
     uint64_t* keys_alt = nullptr;
     int64_t* scratch = nullptr;  // [0] = E, [1] = error flag
+    TmpGuard tg_(ctx.stream);
+    tg_.track(keys);
+    tg_.track(keys_alt);
+    tg_.track(scratch);
+
     PR_TRY(dalloc(&scratch, 2, s));
     PR_CUDA(cudaMemsetAsync(scratch, 0, 2 * sizeof(int64_t), s));
     // n == 1 (b == 0): every edge is a self-loop, nothing to sort
@@ -288,6 +293,9 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
     cudaStream_t s = ctx.stream;
     const int64_t n = g->n;
     int64_t* scratch = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(scratch);
+
     PR_TRY(dalloc(&scratch, 2, s));
     PR_CUDA(cudaMemsetAsync(scratch, 0, 2 * sizeof(int64_t), s));
     PR_LAUNCH(ctx, k_max_i32, grid_for(ctx, n, 256), 256, 0, (const int32_t*)g->outdeg, n, (int*)(scratch + 1));
@@ -301,6 +309,8 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
 
     uint64_t* keys = nullptr;
     uint64_t* keys_alt = nullptr;
+    tg_.track(keys);
+    tg_.track(keys_alt);
     PR_TRY(dalloc(&keys, (size_t)n, s));
     PR_TRY((device_scan<int64_t>(ctx, n, NdGet{g->outdeg},
                                  NdEmit{g->outdeg, keys, b, by_degree ? maxod : 0}, scratch)));

@@ -1257,6 +1257,9 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
     // scratch: err[2*grid] | residual[2] | zero-row partials[2*zgrid]; iters[grid]
     double* scratch = nullptr;
     int32_t* iters = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(scratch);
+    tg_.track(iters);
     PR_TRY(dalloc(&scratch, (size_t)(2 * grid + 2 + 2 * zgrid), s));
     PR_TRY(dalloc(&iters, (size_t)grid, s));
     PR_CUDA(cudaMemsetAsync(iters, 0, sizeof(int32_t) * (size_t)grid, s));
@@ -1519,6 +1522,9 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
     }
     uint8_t* fz = nullptr;
     unsigned long long* cnt = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(fz);
+    tg_.track(cnt);
     PR_TRY(dalloc(&fz, (size_t)std::max<int64_t>(V.nrows, 1), s));
     PR_TRY(dalloc(&cnt, 2, s));
     PR_CUDA(cudaMemsetAsync(fz, 0, (size_t)std::max<int64_t>(V.nrows, 1), s));

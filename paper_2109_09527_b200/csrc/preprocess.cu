@@ -315,6 +315,17 @@ static int find_identical(pr_graph* g, Ctx& ctx) {
     uint64_t* h2 = nullptr;
     uint32_t* sv = nullptr;
     uint32_t* sv2 = nullptr;
+    uint64_t* hv = nullptr;
+    int32_t* rid = nullptr;
+    int64_t* rstart = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(h);
+    tg_.track(h2);
+    tg_.track(sv);
+    tg_.track(sv2);
+    tg_.track(hv);
+    tg_.track(rid);
+    tg_.track(rstart);
     // only the rows of in-degree > 0 are hashed and sorted; the in-degree-0
     // vertices form the empty class directly
     const View& v = g->plain;
@@ -340,8 +351,6 @@ static int find_identical(pr_graph* g, Ctx& ctx) {
     PR_TRY((radix_sort<uint64_t, true>(ctx, h, h2, sv, sv2, nr, 16, 64, &alt)));
     const uint64_t* hs = alt ? h2 : h;
     const uint32_t* svs = alt ? sv2 : sv;
-    int32_t* rid = nullptr;
-    int64_t* rstart = nullptr;
     PR_TRY(dalloc(&rid, (size_t)nr, s));
     PR_TRY(dalloc(&rstart, (size_t)nr, s));
     PR_TRY((device_scan<int64_t>(ctx, nr, RunGet{hs}, RunEmit{rid, rstart}, (int64_t*)nullptr)));
@@ -374,6 +383,9 @@ static int find_chains(pr_graph* g, Ctx& ctx) {
     const int64_t n = g->n;
     int64_t* cnt = nullptr;
     int32_t* cl = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(cnt);
+    tg_.track(cl);
     PR_TRY(dalloc(&cnt, 1, s));
     PR_TRY(dalloc(&cl, (size_t)n, s));
     PR_TRY((device_scan<int64_t>(ctx, n, ChainGet{g->row_ptr, g->outdeg}, ListEmit{cl}, cnt)));
@@ -425,6 +437,8 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
 
     // members (scatter list) and the computed set R (reduced gather view)
     int64_t* cnt = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(cnt);
     PR_TRY(dalloc(&cnt, 3, s));
     PR_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(int64_t), s));
     PR_LAUNCH(ctx, k_max_chain, grid_of(ctx, n), 256, 0, (const int32_t*)g->chain_k, n, (int*)(cnt + 2));
