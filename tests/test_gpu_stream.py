@@ -169,3 +169,38 @@ def test_fused_sweep_matches_split(pr, monkeypatch):
         a, b = out[("1", mode)], out[("0", mode)]
         assert a[1] == b[1] == 40
         assert np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_blocked_views_with_every_mode(pr, monkeypatch, bits):
+    """Source-blocked views only change the synchronous gather; the in-place
+    modes (which use the unblocked tables), the No-Sync certificate (a blocked
+    sync gather) and perforation (blocked first, unblocked after compaction)
+    must all still reach the oracle's fixed point."""
+    monkeypatch.setenv("PRGPU_SEG_BITS", str(bits))
+    n, s, t = hub_graph(seed=11)
+    ref_g = oracle.build_csr(n, s, t)
+    tight = oracle.pagerank(ref_g, D, 1e-14, 5000)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        g.preprocess()
+        for mode in (pr.PR_MODE_ASYNC, pr.PR_MODE_NOSYNC, pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS,
+                     pr.PR_MODE_ASYNC | pr.PR_USE_REDUCTIONS):
+            st, it, fd, x = gpu_run(pr, g, n, 1e-12, max_iter=5000, mode=mode)
+            assert st == pr.PR_OK
+            assert np.abs(x - tight.x).max() <= 1e-10, mode
+        st, it, fd, x = gpu_run(pr, g, n, 1e-12, mode=pr.PR_PERFORATE)
+        assert st == pr.PR_OK
+        assert np.abs(x - tight.x).sum() <= 1e-6
+
+
+def test_perforation_can_freeze_everything(pr):
+    """A graph that converges row by row (a long path) lets perforation freeze
+    rows until the active view is empty; the run still ends correctly."""
+    n = 3000
+    s, t = G.edges_to_arrays(G.path(n))
+    ref_g = oracle.build_csr(n, s, t)
+    ref = oracle.pagerank(ref_g, D, 1e-13, 5000)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        st, it, fd, x = gpu_run(pr, g, n, 1e-13, max_iter=5000, mode=pr.PR_PERFORATE)
+        assert st == pr.PR_OK
+        assert np.abs(x - ref.x).max() <= 1e-12
