@@ -238,6 +238,7 @@ def compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags):
         rec = {"time_to_converge_ms": round(ms_, 3), "iterations": it_, "final_delta": fd_}
         if name == "nosync":
             rec["min_local_sweeps"] = st_["nosync_min_iters"]
+            rec["median_local_sweeps"] = st_["nosync_median_iters"]
             rec["certified_residual"] = st_["residual"]
         modes[name] = rec
     rc_, it_e, fd_ = g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=0)

@@ -173,6 +173,9 @@ typedef struct {
     int64_t n_tasks;            /* row-block + hub-chunk tasks of the gather launch */
     int32_t nosync_min_iters;   /* PR_MODE_NOSYNC: fewest local sweeps of any CTA */
     int32_t nosync_launches;    /* PR_MODE_NOSYNC: persistent launches (1 + relaunches) */
+    int32_t nosync_median_iters;/* PR_MODE_NOSYNC: median local sweeps over the CTAs (the max
+                                   usually belongs to the least-loaded CTA, which sweeps its
+                                   short share more often) */
     double  residual;           /* PR_MODE_NOSYNC: certified ||F(x) - x|| (run norm) at exit */
     int64_t edges_gathered;     /* edges gathered over the whole run (all sweeps) */
     int64_t frozen_rows;        /* PR_PERFORATE: rows no longer gathered at exit */

@@ -70,6 +70,7 @@ class pr_run_stats(ctypes.Structure):
         ("n_tasks", ctypes.c_int64),
         ("nosync_min_iters", ctypes.c_int32),
         ("nosync_launches", ctypes.c_int32),
+        ("nosync_median_iters", ctypes.c_int32),
         ("residual", ctypes.c_double),
         ("edges_gathered", ctypes.c_int64),
         ("frozen_rows", ctypes.c_int64),

@@ -1305,7 +1305,7 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
     }
     std::vector<int32_t> hit(grid);
     std::vector<double> hlog;
-    int32_t max_it = 0, min_it = 0, launches = 0, status = PR_NOT_CONVERGED;
+    int32_t max_it = 0, min_it = 0, med_it = 0, launches = 0, status = PR_NOT_CONVERGED;
     double r_l1 = 0.0, r_linf = 0.0;
     const View& pv_view = g->plain;
     while (true) {
@@ -1354,6 +1354,15 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
         r_linf = hr[1];
         max_it = *std::max_element(hit.begin(), hit.end());
         min_it = *std::min_element(hit.begin(), hit.end());
+        {
+            std::vector<int32_t> tmp(hit);
+            std::nth_element(tmp.begin(), tmp.begin() + tmp.size() / 2, tmp.end());
+            med_it = tmp[tmp.size() / 2];
+        }
+        if (getenv("PRGPU_NOSYNC_DUMP")) {  // diagnostics: local sweeps of every CTA
+            for (int b = 0; b < grid; ++b) fprintf(stderr, "%d%c", hit[b], (b + 1) % 37 ? ' ' : '\n');
+            fprintf(stderr, "\n");
+        }
         hlog.push_back(r_l1);
         hlog.push_back(r_linf);
         const double rn = (mode & PR_NORM_LINF) ? r_linf : r_l1;
@@ -1394,6 +1403,7 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
     rs.n_tasks = v.ntasks;
     rs.nosync_min_iters = min_it;
     rs.nosync_launches = launches;
+    rs.nosync_median_iters = med_it;
     rs.residual = (mode & PR_NORM_LINF) ? r_linf : r_l1;
     if (iters_out) *iters_out = max_it;
     if (delta_out) *delta_out = rs.residual;

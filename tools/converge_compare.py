@@ -38,7 +38,8 @@ for name, mode in (("sync", 0), ("sync_reduced", pr.PR_USE_REDUCTIONS), ("async"
     ms, it, fd, stt = best
     rec = {"ms": round(ms, 3), "iterations": it, "final_delta": fd, "status": rc}
     if "nosync" in name:
-        rec.update(min_local_sweeps=stt["nosync_min_iters"], launches=stt["nosync_launches"],
+        rec.update(min_local_sweeps=stt["nosync_min_iters"], median_local_sweeps=stt["nosync_median_iters"],
+                   launches=stt["nosync_launches"],
                    certified_residual=stt["residual"])
     out[name] = rec
     print(name, rec, flush=True)
