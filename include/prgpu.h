@@ -109,17 +109,21 @@ int pr_preprocess(pr_graph *g, uint32_t flags, void *stream);
  *   d          damping, 0 < d < 1 ("initialized to 0.85")
  *   threshold  >= 0 (P:438 uses 1e-16 with L-inf; configs use 1e-10 / 1e-12 L1)
  *   max_iter   >= 1; reaching it returns PR_NOT_CONVERGED with valid ranks
- *   mode       PR_MODE_SYNC | PR_MODE_ASYNC | PR_MODE_NOSYNC, | PR_NORM_* |
- *              PR_USE_REDUCTIONS | PR_TIMING | PR_PERFORATE
+ *   mode       one of PR_MODE_SYNC (0) / PR_MODE_ASYNC / PR_MODE_NOSYNC, or'ed
+ *              with PR_NORM_LINF, PR_USE_REDUCTIONS, PR_TIMING; PR_PERFORATE only
+ *              with the plain synchronous mode
  *   ranks      fp64[n] output in vertex-id order (host or device, caller-owned)
  *   iters_out  (host, nullable) number of update sweeps including the final
- *              one that met the stop test (Q-I)
- *   final_delta_out (host, nullable) the stop-test norm of the last sweep
+ *              one that met the stop test (Q-I); PR_MODE_NOSYNC: the
+ *              largest number of local sweeps of any CTA
+ *   final_delta_out (host, nullable) the stop-test norm of the last sweep;
+ *              PR_MODE_NOSYNC: the certified ||F(x) - x||
  * Sync mode is deterministic (fixed-order reductions): identical inputs give
- * bit-identical ranks and iteration counts.  Async mode is not deterministic;
- * it reaches the same fixed point (Lemma 2).
- * Errors: PR_EINVAL (bad d / threshold / max_iter / NULL ranks),
- * PR_ESTATE (PR_USE_REDUCTIONS before pr_preprocess).
+ * bit-identical ranks and iteration counts.  The async and No-Sync modes are
+ * not deterministic; they reach the same fixed point (Lemma 2).
+ * PR_PERFORATE is approximate (Alg.5): frozen vertices keep their value.
+ * Errors: PR_EINVAL (bad d / threshold / max_iter / NULL ranks / unknown or
+ * incompatible mode bits), PR_ESTATE (PR_USE_REDUCTIONS before pr_preprocess).
  */
 int pr_run(pr_graph *g, double d, double threshold, int32_t max_iter, void *stream,
            uint32_t mode, double *ranks, int32_t *iters_out, double *final_delta_out);
@@ -163,14 +167,17 @@ typedef struct {
     int64_t run_launches;       /* kernels launched by the last pr_run (incl. early-exit ones) */
     int64_t total_launches;     /* kernels launched for this graph since pr_graph_create */
     int32_t host_syncs;         /* stream synchronisations inside the last pr_run */
-    int32_t timed_iterations;   /* PR_TIMING: gather launches timed */
-    double  gather_ms;          /* PR_TIMING: summed CUDA-event time of those gather launches */
-    double  scatter_ms;         /* PR_TIMING: summed time of the member-scatter launches */
-    int64_t gather_rows;        /* rows one gather launch processes (n, or |R| reduced) */
+    int32_t timed_iterations;   /* PR_TIMING: sweeps timed */
+    double  gather_ms;          /* PR_TIMING: summed CUDA-event time of the gather launches
+                                   (K-GATHER; in-place modes: the whole fused sweep) */
+    double  scatter_ms;         /* PR_TIMING: summed time of the launches after the gather:
+                                   K-FINALIZE in sync mode (rows + members), the member
+                                   scatter of the row-task engine, 0 in place */
+    int64_t gather_rows;        /* rows one gather launch processes (in-degree > 0: all, or |R| reduced) */
     int64_t gather_edges;       /* edges one gather launch processes */
     int64_t scatter_members;    /* members one scatter launch processes (0 plain) */
     int64_t n_contrib;          /* vertices with outdeg > 0 (size of the contrib vector) */
-    int64_t n_tasks;            /* row-block + hub-chunk tasks of the gather launch */
+    int64_t n_tasks;            /* row-task engine tasks (0 until that engine is first used) */
     int32_t nosync_min_iters;   /* PR_MODE_NOSYNC: fewest local sweeps of any CTA */
     int32_t nosync_launches;    /* PR_MODE_NOSYNC: persistent launches (1 + relaunches) */
     int32_t nosync_median_iters;/* PR_MODE_NOSYNC: median local sweeps over the CTAs (the max
