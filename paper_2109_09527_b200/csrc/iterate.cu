@@ -963,9 +963,21 @@ static int ensure_tasks(pr_graph* g, bool reduced, Ctx& ctx) {
     return PR_OK;
 }
 
+// Boundary-row / hub tickets count the pieces of the current sweep.  A
+// persistent No-Sync launch stops with CTAs at different sweeps, so tickets can
+// be left mid-count; every run starts from zero.
+static int reset_tickets(const View& v, cudaStream_t s) {
+    if (v.bticket && v.nbound > 0) PR_CUDA(cudaMemsetAsync(v.bticket, 0, sizeof(uint32_t) * (size_t)v.nbound, s));
+    if (v.hub_ticket && v.nhubs > 0) PR_CUDA(cudaMemsetAsync(v.hub_ticket, 0, sizeof(uint32_t) * (size_t)v.nhubs, s));
+    for (int q = 0; q < v.nseg; ++q) PR_TRY(reset_tickets(v.seg[q], s));
+    return PR_OK;
+}
+
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
         int32_t* iters_out, double* delta_out) {
     if (tasks_engine_requested()) PR_TRY(ensure_tasks(g, (mode & PR_USE_REDUCTIONS) != 0, ctx));
+    PR_TRY(reset_tickets(g->plain, ctx.stream));
+    if (g->pre_done) PR_TRY(reset_tickets(g->reduced, ctx.stream));
     if (mode & PR_MODE_NOSYNC) return run_nosync(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     if (mode & PR_PERFORATE) return run_perforated(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     cudaStream_t s = ctx.stream;

@@ -112,3 +112,27 @@ def test_nosync_max_iter_and_modes(pr):
         with pytest.raises(pr.PRError) as e:
             pr.pr_run(g.handle, D, 1e-10, 10, x0, mode=pr.PR_MODE_NOSYNC | pr.PR_MODE_ASYNC)
         assert e.value.code == pr.PR_EINVAL
+
+
+def test_sync_after_nosync_is_unaffected(pr, monkeypatch):
+    """A persistent No-Sync launch stops with its CTAs at different sweeps, so
+    the boundary-row tickets it shares with the synchronous engine can be left
+    mid-count; the following synchronous runs must still be bit-identical to a
+    fresh graph's (one-step spans: every row crossing a step is a boundary row)."""
+    monkeypatch.setenv("PRGPU_SPAN", "1")
+    gen = graphgen.make_config(4, scale_override=14)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g0:
+        x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+        g0.run(x, D, 1e-10, 1000)
+        fresh = x.cpu().numpy()
+        g0.run(x, D, 1e-10, 1000, mode=pr.PR_PERFORATE)
+        fresh_pf = x.cpu().numpy()
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+        for _ in range(3):
+            g.run(x, D, 1e-10, 1000, mode=pr.PR_MODE_NOSYNC)
+            g.run(x, D, 1e-10, 1000)
+            assert np.array_equal(x.cpu().numpy(), fresh)
+            g.run(x, D, 1e-10, 1000, mode=pr.PR_MODE_NOSYNC)
+            g.run(x, D, 1e-10, 1000, mode=pr.PR_PERFORATE)
+            assert np.array_equal(x.cpu().numpy(), fresh_pf)
