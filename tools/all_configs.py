@@ -1,0 +1,99 @@
+"""The north_star report on all five BASELINE.json configs (one GPU): GTEPS per
+iteration, time to converge, sweeps, the gather's roofline fraction, and the
+fp64 oracle's time on this host (one core, bounded sample, as bench.py's
+cpu_baseline).  Usage: python tools/all_configs.py [configs...] > out.json"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import graphgen  # noqa: E402
+import oracle  # noqa: E402   (test infrastructure: timed as the CPU baseline only)
+import paper_2109_09527_b200 as pr  # noqa: E402
+
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+
+
+def timed_run(g, x, gen, mode, reps=3):
+    st = torch.cuda.current_stream()
+    best = None
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        rc, it, fd = g.run(x, gen.d, gen.tau, gen.max_iter, mode=mode)
+        b.record(st)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        if best is None or ms < best[0]:
+            best = (ms, it, rc)
+    g.run(x, gen.d, gen.tau, gen.max_iter, mode=mode | pr.PR_TIMING)
+    s = g.stats()
+    ti = max(1, s["timed_iterations"])
+    return best, s, s["gather_ms"] / ti, s["scatter_ms"] / ti
+
+
+def cpu_sample(gen, frac):
+    ms = gen.m // frac
+    t0 = time.perf_counter()
+    c = oracle.build_csr(gen.n, gen.src[:ms], gen.dst[:ms])
+    t_build = time.perf_counter() - t0
+    r = oracle.pagerank(c, gen.d, 0.0, 2)
+    t_sweep = r.seconds / 2
+    return c.E * frac, t_build * frac, t_sweep * frac
+
+
+cfgs = [int(a) for a in sys.argv[1:]] or [1, 2, 3, 4, 5]
+out = []
+for k in cfgs:
+    gen = graphgen.make_config(k)
+    s = torch.from_numpy(gen.src).cuda()
+    t = torch.from_numpy(gen.dst).cuda()
+    x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream()
+    w = pr.Graph(gen.n, s, t)  # warm-up build (the first one in a process also grows the memory pool)
+    w.preprocess()
+    w.close()
+    a, b, c_ = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    a.record(st)
+    g = pr.Graph(gen.n, s, t)
+    b.record(st)
+    g.preprocess()
+    c_.record(st)
+    torch.cuda.synchronize()
+    info = g.info()
+    E, n = info["E"], gen.n
+    rec = {"config": k, "workload": gen.name, "n": n, "E": E, "tau": gen.tau,
+           "create_ms": round(a.elapsed_time(b), 3), "preprocess_ms": round(b.elapsed_time(c_), 3)}
+    for name, mode in (("plain", 0), ("reduced", pr.PR_USE_REDUCTIONS), ("async", pr.PR_MODE_ASYNC),
+                       ("nosync", pr.PR_MODE_NOSYNC)):
+        (ms, it, rc), stt, gms, fms = timed_run(g, x, gen, mode)
+        r = {"time_to_converge_ms": round(ms, 3), "iterations": it, "status": rc}
+        if name in ("plain", "reduced"):
+            sweep = gms + fms
+            alg = 12 * stt["gather_edges"] + 8 * stt["gather_rows"]
+            r.update(sweep_ms=round(sweep, 4), gteps_per_iteration=round(E / (sweep * 1e-3) / 1e9, 2),
+                     gather_ms=round(gms, 4), gather_frac_of_peak=round(alg / (gms * 1e-3) / 1e9 / PEAK, 4),
+                     sweep_model_frac=round((12 * E + 24 * n + 8) / (sweep * 1e-3) / 1e9 / PEAK, 4))
+        if name == "nosync":
+            r.update(median_local_sweeps=stt["nosync_median_iters"], certified_residual=stt["residual"])
+        rec[name] = r
+    g.close()
+    del s, t, x
+    torch.cuda.empty_cache()
+    frac = 1 if gen.m <= 20_000_000 else (4 if gen.m <= 300_000_000 else 16)
+    E_full, tb, tsw = cpu_sample(gen, frac)
+    it = rec["plain"]["iterations"]
+    rec["oracle_1core"] = {"sample": f"first 1/{frac} of the raw edges, CSR build + 2 sweeps, scaled x{frac}",
+                           "csr_build_s": float(f"{tb:.4g}"), "sweep_s": float(f"{tsw:.4g}"),
+                           "time_to_converge_s": float(f"{tb + it * tsw:.4g}"),
+                           "gteps_per_iteration": round(E_full / tsw / 1e9, 4), "cores": 1,
+                           "host_cores": os.cpu_count()}
+    out.append(rec)
+    print(json.dumps(rec), file=sys.stderr, flush=True)
+print(json.dumps(out, indent=1))
