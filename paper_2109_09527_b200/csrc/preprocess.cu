@@ -6,7 +6,7 @@
 //   1. row hash h(v) = mix(indeg) + sum over the row's contrib slots of mix(slot)
 //      (edge-stream engine, uint64 sums), for the rows of in-degree > 0 (the
 //      in-degree-0 vertices are one class)
-//   2. stable radix sort of those ids by the top 48 bits of h -> runs of equal
+//   2. stable radix sort of those ids by the top 32 bits of h -> runs of equal
 //      bits, ids ascending
 //   3. exact verification of every member against the run's first vertex; on a
 //      hash collision the vertex scans its run for the first equal row.
@@ -81,9 +81,9 @@ __device__ __forceinline__ bool same_row(const int64_t* rp, const int32_t* col, 
     return true;
 }
 
-struct RunGet {  // runs of equal top-48 hash bits (the sorted bits)
+struct RunGet {  // runs of equal top-32 hash bits (the sorted bits)
     const uint64_t* h;
-    __device__ int64_t operator()(int64_t i) const { return (i == 0 || (h[i] >> 16) != (h[i - 1] >> 16)) ? 1 : 0; }
+    __device__ int64_t operator()(int64_t i) const { return (i == 0 || (h[i] >> 32) != (h[i - 1] >> 32)) ? 1 : 0; }
 };
 struct RunEmit {
     int32_t* rid;
@@ -345,10 +345,11 @@ static int find_identical(pr_graph* g, Ctx& ctx) {
         PR_LAUNCH(ctx, k_hash_deg, grid_of(ctx, nr), 256, 0, h, nr, (const int32_t*)v.vid, (const int64_t*)g->row_ptr);
     }
     PR_LAUNCH(ctx, k_u32_from, grid_of(ctx, nr), 256, 0, (const int32_t*)v.vid, nr, sv);
-    // stable sort of the rows (ids ascending) by the top 48 hash bits; equal
-    // top bits of different rows (p ~ nr^2/2^49) are split by k_verify
+    // stable sort of the rows (ids ascending) by the top 32 hash bits (4 radix
+    // passes); equal top bits of different rows (~nr^2/2^33 pairs: a few
+    // thousand on R-MAT-24, runs of two) are split exactly by k_verify
     bool alt = false;
-    PR_TRY((radix_sort<uint64_t, true>(ctx, h, h2, sv, sv2, nr, 16, 64, &alt)));
+    PR_TRY((radix_sort<uint64_t, true>(ctx, h, h2, sv, sv2, nr, 32, 64, &alt)));
     const uint64_t* hs = alt ? h2 : h;
     const uint32_t* svs = alt ? sv2 : sv;
     PR_TRY(dalloc(&rid, (size_t)nr, s));
