@@ -209,7 +209,8 @@ def run_reference(args, ws, rank):
 
 def compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags):
     """Time to converge of the iteration modes on the same graph, outside the
-    timed region: sync (Barriers, Alg.1), launch-level in-place async,
+    timed region: sync (Barriers, Alg.1), phased in-place sweeps (block
+    Gauss-Seidel, deterministic; DESIGN.md Q-B), launch-level in-place async,
     persistent barrier-free No-Sync (Alg.3) -- the paper's Fig.7 comparison,
     P:994 -- and loop perforation (Barriers-Opt, Alg.5; plain sync only,
     approximate) with its work fraction and L1 distance to the exact plain
@@ -233,9 +234,12 @@ def compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags):
     if flags:
         g.preprocess(flags)
     red = pr.PR_USE_REDUCTIONS if flags else 0
-    for name, md in (("sync", red), ("async", red | pr.PR_MODE_ASYNC), ("nosync", red | pr.PR_MODE_NOSYNC)):
+    for name, md in (("sync", red), ("phased", red | pr.PR_MODE_PHASED), ("async", red | pr.PR_MODE_ASYNC),
+                     ("nosync", red | pr.PR_MODE_NOSYNC)):
         ms_, it_, fd_, st_ = timed(g, md)
         rec = {"time_to_converge_ms": round(ms_, 3), "iterations": it_, "final_delta": fd_}
+        if name == "phased":
+            rec["phases"] = st_["phases"]
         if name == "nosync":
             rec["min_local_sweeps"] = st_["nosync_min_iters"]
             rec["median_local_sweeps"] = st_["nosync_median_iters"]

@@ -72,6 +72,15 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
                                  is 0 < |delta| < threshold * 1e-5 keeps its value from then on
                                  and is no longer gathered (APPROXIMATE: the result is not the
                                  fixed point; the stop test counts frozen vertices as 0). */
+#define PR_MODE_PHASED   64u  /* in-place sweeps in K ordered phases (block Gauss-Seidel; Q-B):
+                                 one contrib buffer; phase k gathers a contiguous 1/K of the
+                                 edge stream and finalizes the rows ending in it, so it reads
+                                 the values phases 0..k-1 of the same sweep wrote (the
+                                 in-place reads of Alg.3 P:545-565 in a fixed order).
+                                 Deterministic.  K = PRGPU_PHASES (default: 8 when each phase
+                                 still has >= 24 edge steps of 256 per resident warp, fewer on
+                                 small graphs; one phase on a source-blocked view).  Exclusive
+                                 with ASYNC / NOSYNC / PERFORATE. */
 
 /*
  * pr_graph_create -- build the in-edge CSR and out-degrees on the device
@@ -109,7 +118,8 @@ int pr_preprocess(pr_graph *g, uint32_t flags, void *stream);
  *   d          damping, 0 < d < 1 ("initialized to 0.85")
  *   threshold  >= 0 (P:438 uses 1e-16 with L-inf; configs use 1e-10 / 1e-12 L1)
  *   max_iter   >= 1; reaching it returns PR_NOT_CONVERGED with valid ranks
- *   mode       one of PR_MODE_SYNC (0) / PR_MODE_ASYNC / PR_MODE_NOSYNC, or'ed
+ *   mode       one of PR_MODE_SYNC (0) / PR_MODE_ASYNC / PR_MODE_NOSYNC /
+ *              PR_MODE_PHASED, or'ed
  *              with PR_NORM_LINF, PR_USE_REDUCTIONS, PR_TIMING; PR_PERFORATE only
  *              with the plain synchronous mode
  *   ranks      fp64[n] output in vertex-id order (host or device, caller-owned)
@@ -118,8 +128,8 @@ int pr_preprocess(pr_graph *g, uint32_t flags, void *stream);
  *              largest number of local sweeps of any CTA
  *   final_delta_out (host, nullable) the stop-test norm of the last sweep;
  *              PR_MODE_NOSYNC: the certified ||F(x) - x||
- * Sync mode is deterministic (fixed-order reductions): identical inputs give
- * bit-identical ranks and iteration counts.  The async and No-Sync modes are
+ * Sync and phased modes are deterministic (fixed-order reductions): identical
+ * inputs give bit-identical ranks and iteration counts.  The async and No-Sync modes are
  * not deterministic; they reach the same fixed point (Lemma 2).
  * PR_PERFORATE is approximate (Alg.5): frozen vertices keep their value.
  * Errors: PR_EINVAL (bad d / threshold / max_iter / NULL ranks / unknown or
@@ -187,6 +197,7 @@ typedef struct {
     int64_t edges_gathered;     /* edges gathered over the whole run (all sweeps) */
     int64_t frozen_rows;        /* PR_PERFORATE: rows no longer gathered at exit */
     int32_t compactions;        /* PR_PERFORATE: times the gathered rows were compacted */
+    int32_t phases;             /* phases per sweep (PR_MODE_PHASED: K; else 1) */
 } pr_run_stats;
 
 int pr_get_run_stats(const pr_graph *g, pr_run_stats *out);

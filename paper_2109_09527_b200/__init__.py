@@ -37,6 +37,7 @@ PR_USE_REDUCTIONS = 4
 PR_TIMING = 8
 PR_MODE_NOSYNC = 16
 PR_PERFORATE = 32
+PR_MODE_PHASED = 64
 
 # every symbol include/prgpu.h declares (tests check the .so exports them)
 ABI_SYMBOLS = (
@@ -75,6 +76,7 @@ class pr_run_stats(ctypes.Structure):
         ("edges_gathered", ctypes.c_int64),
         ("frozen_rows", ctypes.c_int64),
         ("compactions", ctypes.c_int32),
+        ("phases", ctypes.c_int32),
     ]
 
     def as_dict(self):

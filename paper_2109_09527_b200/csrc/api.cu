@@ -26,6 +26,14 @@ void set_error(const char* fmt, ...) {
 
 double g_alloc_ms = 0.0;
 
+bool pdl_enabled() {  // PRGPU_PDL=0 turns programmatic dependent launch off (measurement)
+    static const bool on = [] {
+        const char* e = getenv("PRGPU_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 static int make_ctx(Ctx& ctx, void* stream) {
     ctx.stream = (cudaStream_t)stream;
     ctx.launches = 0;
@@ -315,12 +323,17 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
         set_error("pr_run: max_iter=%d < 1", max_iter);
         return PR_EINVAL;
     }
-    if (mode & ~(PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_NORM_LINF | PR_USE_REDUCTIONS | PR_TIMING | PR_PERFORATE)) {
+    if (mode & ~(PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_NORM_LINF | PR_USE_REDUCTIONS | PR_TIMING | PR_PERFORATE |
+                 PR_MODE_PHASED)) {
         set_error("pr_run: unknown mode bits 0x%x", mode);
         return PR_EINVAL;
     }
     if ((mode & PR_MODE_ASYNC) && (mode & PR_MODE_NOSYNC)) {
         set_error("pr_run: PR_MODE_ASYNC and PR_MODE_NOSYNC are exclusive");
+        return PR_EINVAL;
+    }
+    if ((mode & PR_MODE_PHASED) && (mode & (PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_PERFORATE))) {
+        set_error("pr_run: PR_MODE_PHASED is exclusive with PR_MODE_ASYNC / PR_MODE_NOSYNC / PR_PERFORATE");
         return PR_EINVAL;
     }
     if ((mode & PR_PERFORATE) && (mode & (PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_USE_REDUCTIONS))) {

@@ -42,6 +42,35 @@ extern double g_alloc_ms;  // host time spent in cudaMallocAsync (PRGPU_PROFILE 
         }                                                                               \
     } while (0)
 
+// Programmatic dependent launch for the kernels of the sweep loop: the next
+// kernel's CTAs are dispatched while the previous kernel drains, and wait in
+// pdl_wait() (griddepcontrol.wait: full completion and visibility of the
+// previous grid) before touching anything it wrote.  A kernel launched this
+// way MUST call pdl_wait() before its first dependent access.
+bool pdl_enabled();
+#define PR_LAUNCH_PDL(ctx, kernel, grid, block, smem, ...)                                   \
+    do {                                                                                     \
+        cudaLaunchConfig_t _cfg = {};                                                        \
+        _cfg.gridDim = dim3((unsigned)(grid));                                               \
+        _cfg.blockDim = dim3((unsigned)(block));                                             \
+        _cfg.dynamicSmemBytes = (size_t)(smem);                                              \
+        _cfg.stream = (ctx).stream;                                                          \
+        cudaLaunchAttribute _at[1];                                                          \
+        _at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                      \
+        _at[0].val.programmaticStreamSerializationAllowed = 1;                               \
+        _cfg.attrs = _at;                                                                    \
+        _cfg.numAttrs = ::prgpu::pdl_enabled() ? 1 : 0;                                      \
+        cudaError_t _le = cudaLaunchKernelEx(&_cfg, kernel, __VA_ARGS__);                    \
+        (ctx).launches += 1;                                                                 \
+        if (_le != cudaSuccess) {                                                            \
+            ::prgpu::set_error("launch %s: %s", #kernel, cudaGetErrorString(_le));           \
+            return PR_ECUDA;                                                                 \
+        }                                                                                    \
+    } while (0)
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct Ctx {
     cudaStream_t stream;
     int num_sms;

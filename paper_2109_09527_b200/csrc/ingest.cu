@@ -439,6 +439,7 @@ void free_view(View& v, cudaStream_t s) {
         v = View{};
         return;
     }
+    free_phase_view(v, s);
     if (v.owns_row_ptr) dfree(v.row_ptr, s);
     v.row_ptr = nullptr;
     dfree(v.col, s);
@@ -451,14 +452,7 @@ void free_view(View& v, cudaStream_t s) {
     v.nrows = v.nedges = v.ntasks = v.nhubs = v.hub_slots = 0;
     dfree(v.sflags, s);
     dfree(v.step_row, s);
-    dfree(v.bin, s);
-    dfree(v.bout, s);
-    dfree(v.b_row, s);
-    dfree(v.b_s0, s);
-    dfree(v.b_s1, s);
-    dfree(v.part_in, s);
-    dfree(v.part_out, s);
-    dfree(v.bticket, s);
+    free_spans(v, s);
     dfree(v.sums, s);
     dfree(v.rinfo, s);
     v.nsteps = v.nspans = v.nbound = 0;
@@ -580,8 +574,6 @@ int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg
         const int64_t o = atoll(e);
         if (o >= 1) ss = o;
     }
-    v.span_steps = ss;
-    v.nspans = (v.nsteps + ss - 1) / ss;
     if (Epad > v.nedges)
         PR_LAUNCH(ctx, k_pad_col, 1, 256, 0, v.col, v.nedges, Epad, pad_slot);
     PR_TRY(dalloc(&v.sflags, (size_t)v.nsteps * 8, s));
@@ -590,6 +582,21 @@ int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg
     PR_TRY(dalloc(&v.step_row, (size_t)v.nsteps + 1, s));
     PR_LAUNCH(ctx, k_step_row, grid_for(ctx, v.nsteps + 1, 256), 256, 0, (const int64_t*)v.row_ptr, v.nrows,
               v.nsteps, v.step_row);
+    PR_TRY(build_spans(v, ctx, ss));
+    if (outdeg) {  // a top-level view (sub-views of a blocked view accumulate into their parent's sums)
+        PR_TRY(dalloc(&v.sums, (size_t)v.nrows, s));
+        PR_TRY(dalloc(&v.rinfo, (size_t)v.nrows, s));
+        PR_LAUNCH(ctx, k_rinfo, grid_for(ctx, v.nrows, 256), 256, 0, (const int32_t*)v.vid, v.nrows, outdeg, cidx,
+                  v.rinfo);
+    }
+    return PR_OK;
+}
+
+// The span tables of a view for spans of ss steps (needs row_ptr, nsteps).
+int build_spans(View& v, Ctx& ctx, int64_t ss) {
+    cudaStream_t s = ctx.stream;
+    v.span_steps = ss;
+    v.nspans = (v.nsteps + ss - 1) / ss;
     PR_TRY(dalloc(&v.bin, (size_t)v.nspans, s));
     PR_TRY(dalloc(&v.bout, (size_t)v.nspans, s));
     PR_CUDA(cudaMemsetAsync(v.bin, 0xff, sizeof(int32_t) * (size_t)v.nspans, s));
@@ -611,13 +618,59 @@ int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg
     const int64_t nb = v.nbound > 0 ? v.nbound : 1;
     PR_TRY(dalloc(&v.bticket, (size_t)nb, s));
     PR_CUDA(cudaMemsetAsync(v.bticket, 0, sizeof(uint32_t) * (size_t)nb, s));
-    if (outdeg) {  // a top-level view (sub-views of a blocked view accumulate into their parent's sums)
-        PR_TRY(dalloc(&v.sums, (size_t)v.nrows, s));
-        PR_TRY(dalloc(&v.rinfo, (size_t)v.nrows, s));
-        PR_LAUNCH(ctx, k_rinfo, grid_for(ctx, v.nrows, 256), 256, 0, (const int32_t*)v.vid, v.nrows, outdeg, cidx,
-                  v.rinfo);
-    }
     return PR_OK;
+}
+
+void free_spans(View& v, cudaStream_t s) {
+    dfree(v.bin, s);
+    dfree(v.bout, s);
+    dfree(v.b_row, s);
+    dfree(v.b_s0, s);
+    dfree(v.b_s1, s);
+    dfree(v.part_in, s);
+    dfree(v.part_out, s);
+    dfree(v.bticket, s);
+    v.nspans = v.nbound = 0;
+}
+
+// PR_MODE_PHASED: a shallow copy of v (sharing its edge stream, rows and sums)
+// with spans K times finer, so each phase's 1/K of the spans still gives every
+// resident warp one span.
+int build_phase_view(View& v, Ctx& ctx, int K) {
+    if (v.phv && v.phv_k == K) return PR_OK;
+    free_phase_view(v, ctx.stream);
+    View* p = new (std::nothrow) View(v);
+    if (!p) {
+        set_error("build_phase_view: host allocation failed");
+        return PR_ENOMEM;
+    }
+    p->alias = true;  // owns only its span tables (free_phase_view)
+    p->phv = nullptr;
+    p->seg = nullptr;
+    p->nseg = 0;
+    p->bin = p->bout = p->b_row = p->b_s0 = p->b_s1 = nullptr;
+    p->part_in = p->part_out = nullptr;
+    p->bticket = nullptr;
+    p->phase_k = 0;
+    const int64_t warps = (int64_t)ctx.num_sms * (SE_NT / 32);
+    int64_t ss = (v.nsteps + warps * K - 1) / (warps * K);
+    if (ss < 1) ss = 1;
+    if (v.span_steps < ss) ss = v.span_steps;  // PRGPU_SPAN overrides stay as fine
+    if (const char* e = getenv("PRGPU_PHASE_SPAN")) {  // tuning override
+        const int64_t o = atoll(e);
+        if (o >= 1) ss = o;
+    }
+    v.phv = p;
+    v.phv_k = K;
+    return build_spans(*p, ctx, ss);
+}
+
+void free_phase_view(View& v, cudaStream_t s) {
+    if (!v.phv) return;
+    free_spans(*v.phv, s);
+    delete v.phv;
+    v.phv = nullptr;
+    v.phv_k = 0;
 }
 
 }  // namespace prgpu

@@ -32,6 +32,7 @@ constexpr int SE_HOT_MAX = 16384;           // 128 KB of fp64
 // (local) sweep, so a larger tier makes sweeps faster but fresher values rarer:
 // R-MAT-24 async, hot 0 / 2K / 8K / 16K: 61 / 68 / 73 / 78 sweeps, 109 / 78 / 80 / 82 ms.
 constexpr int SE_HOT_IP = 2048;
+constexpr int SE_MAX_PHASES = 64;   // PR_MODE_PHASED: most phases per sweep
 constexpr int SE_L1_TIER = 32768;
 inline int64_t stream_pad(int64_t E) { return ((E > 0 ? E : 1) + SE_STEP - 1) / SE_STEP * SE_STEP; }
 constexpr int GT_NT = PRGPU_NT;              // threads per CTA (independent warps)
@@ -108,6 +109,12 @@ struct View {
     int seg_bits = 0;
     View* seg = nullptr;
     int2* rinfo = nullptr;          // [nrows] (outdeg, contrib slot) of the row's vertex, row order
+    // PR_MODE_PHASED (cached per phase count): phase k runs spans
+    // [k*nspans/K, (k+1)*nspans/K) and finalizes rows [phase_rb[k], phase_rb[k+1])
+    int phase_k = 0;
+    int64_t phase_rb[SE_MAX_PHASES + 1];
+    View* phv = nullptr;            // the view with K-times finer spans (build_phase_view)
+    int phv_k = 0;
 };
 
 // Device-resident iteration state (one per graph).
@@ -182,6 +189,10 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx);
 int build_relabel(pr_graph* g, Ctx& ctx);
 int build_view_tasks(View& v, Ctx& ctx);
 int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx);
+int build_spans(View& v, Ctx& ctx, int64_t span_steps);
+void free_spans(View& v, cudaStream_t s);
+int build_phase_view(View& v, Ctx& ctx, int K);
+void free_phase_view(View& v, cudaStream_t s);
 int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib);
 void free_view(View& v, cudaStream_t s);
 __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const int64_t* __restrict__ rp,

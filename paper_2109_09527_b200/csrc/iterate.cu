@@ -256,6 +256,8 @@ __global__ void __launch_bounds__(GT_NT, GT_MIN_CTAS)
 template <class P>
 __global__ void __launch_bounds__(SE_NT, 1) k_stream(P p, StreamArgs a, const DevState* st) {
     extern __shared__ __align__(16) double hot_smem[];
+    pdl_wait();
+    pdl_trigger();
     if (st->done) return;
     p.pol_last = policy_evict_last();
     if (P::kHot) {
@@ -294,6 +296,11 @@ struct FinArgs {
     uint8_t* fz = nullptr;
     double tau_f = 0.0;
     unsigned long long* nfz = nullptr;
+    // PR_MODE_PHASED: rows [row0, nrows) only, Delta partials at CTA index
+    // part_off + blockIdx.x, and the stop test only in the sweep's last phase
+    int64_t row0 = 0;
+    int64_t part_off = 0;
+    int last = 1;
 };
 
 // Rows are visited grid-stride (all CTAs sweep the row space together, which
@@ -306,6 +313,8 @@ constexpr int FIN_U = 4;
 __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     __shared__ double red[2 * RED_W];
     __shared__ int flag;
+    pdl_wait();
+    pdl_trigger();
     if (ia.st->done) return;
     double l1 = 0.0, linf = 0.0;
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
@@ -314,7 +323,7 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     double* __restrict__ xr = f.xr;
     double* __restrict__ y = f.y_out;
     uint32_t nfrozen = 0;
-    for (int64_t r0 = t0; r0 < f.nrows; r0 += FIN_U * T) {
+    for (int64_t r0 = f.row0 + t0; r0 < f.nrows; r0 += FIN_U * T) {
         double S[FIN_U], xo[FIN_U];
         int2 inf[FIN_U];
 #pragma unroll
@@ -377,7 +386,8 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
             }
         }
     }
-    block_delta(l1, linf, red, ia.cta_partial + 2 * blockIdx.x);
+    block_delta(l1, linf, red, ia.cta_partial + 2 * (f.part_off + blockIdx.x));
+    if (!f.last) return;
     if (threadIdx.x == 0) {
         __threadfence();
         uint32_t t = atomicAdd(&ia.st->ticket_gather, 1u);
@@ -844,11 +854,17 @@ static int launch_tasks_t(Ctx& ctx, const View& v, const double* y_in, double* y
 }
 
 static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
-                         double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize) {
+                         double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize,
+                         int64_t span_lo = 0, int64_t span_hi = -1) {
     if (gc.stream) {
-        auto args = [](const View& w) {
-            return StreamArgs{w.col,  (const uint8_t*)w.sflags, w.step_row, w.nsteps, w.span_steps, w.nspans, w.bin,
-                              w.bout, w.b_row, w.b_s0, w.b_s1, w.part_in, w.part_out, w.bticket};
+        auto args = [&](const View& w) {
+            StreamArgs a{w.col,  (const uint8_t*)w.sflags, w.step_row, w.nsteps, w.span_steps, w.nspans, w.bin,
+                         w.bout, w.b_row, w.b_s0, w.b_s1, w.part_in, w.part_out, w.bticket};
+            if (&w == &v) {
+                a.span_lo = span_lo;
+                a.span_hi = span_hi;
+            }
+            return a;
         };
         if (v.nseg > 0) {  // source-blocked: S = 0, then one accumulating pass per slot segment
             PR_CUDA(cudaMemsetAsync(v.sums, 0, sizeof(double) * (size_t)v.nrows, ctx.stream));
@@ -856,14 +872,16 @@ static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_
                 const View& sv = v.seg[q];
                 if (sv.nspans == 0) continue;
                 AccumPolicy p{y_in, v.sums, sv.vid, nullptr, 0, 0, 0, {}};
-                PR_LAUNCH(ctx, k_stream<AccumPolicy>, gc.grid, gc.nt, 0, p, args(sv), (const DevState*)g->st);
+                PR_LAUNCH_PDL(ctx, k_stream<AccumPolicy>, gc.grid, gc.nt, 0, p, args(sv), (const DevState*)g->st);
             }
         } else if (gc.hot_n > 0) {
             StreamPolicy<true> p{y_in, v.sums, nullptr, gc.hot_n, 0};
-            PR_LAUNCH(ctx, k_stream<StreamPolicy<true>>, gc.grid, gc.nt, gc.smem, p, args(v), (const DevState*)g->st);
+            PR_LAUNCH_PDL(ctx, k_stream<StreamPolicy<true>>, gc.grid, gc.nt, gc.smem, p, args(v),
+                          (const DevState*)g->st);
         } else {
             StreamPolicy<false> p{y_in, v.sums, nullptr, 0, 0};
-            PR_LAUNCH(ctx, k_stream<StreamPolicy<false>>, gc.grid, gc.nt, gc.smem, p, args(v), (const DevState*)g->st);
+            PR_LAUNCH_PDL(ctx, k_stream<StreamPolicy<false>>, gc.grid, gc.nt, gc.smem, p, args(v),
+                          (const DevState*)g->st);
         }
         return PR_OK;
     }
@@ -963,6 +981,62 @@ static int ensure_tasks(pr_graph* g, bool reduced, Ctx& ctx) {
     return PR_OK;
 }
 
+// PR_MODE_PHASED: the phase plan of a view (K contiguous span ranges; the
+// rows each phase finalizes are those whose last edge lies in its spans, so a
+// row crossing a phase boundary is summed by the later phase's ticket winner).
+__global__ void k_phase_rows(const int32_t* __restrict__ step_row, const uint8_t* __restrict__ flags8,
+                             int64_t span_steps, int64_t nspans, int K, int64_t nrows, int64_t* __restrict__ rb) {
+    const int k = threadIdx.x;
+    if (k > K) return;
+    if (k == 0) {
+        rb[0] = 0;
+    } else if (k == K) {
+        rb[K] = nrows;
+    } else {  // the row containing the phase's first edge (it ends in this phase or later)
+        const int64_t st = (int64_t)k * nspans / K * span_steps;
+        rb[k] = (int64_t)step_row[st] - ((flags8[st * 32] & 1) ? 0 : 1);
+    }
+}
+
+static int phase_plan(pr_graph* g, bool reduced, Ctx& ctx, int* K_out) {
+    View& v = reduced ? g->reduced : g->plain;
+    if (v.alias) {  // an aliased reduced view shares the plain view's plan
+        PR_TRY(phase_plan(g, false, ctx, K_out));
+        g->reduced = g->plain;
+        g->reduced.alias = true;
+        return PR_OK;
+    }
+    // default: 8 phases when every phase still gives each resident warp a span
+    // of >= 24 steps (R-MAT-24: 8); fewer on small graphs, where the ~15-20 us
+    // a phase costs (two launches, ramp and tail) outweighs the saved sweeps
+    const int64_t warps = (int64_t)ctx.num_sms * (SE_NT / 32);
+    int K = env_int("PRGPU_PHASES", (int)std::min<int64_t>(8, v.nsteps / (warps * 24)));
+    if (K < 1) K = 1;
+    if (K > SE_MAX_PHASES) K = SE_MAX_PHASES;
+    if (v.nseg > 0 || v.nspans == 0) K = 1;  // source-blocked views run one phase (an in-place Jacobi sweep)
+    *K_out = K;
+    if (K == 1) {
+        if (v.phase_k != 1) {
+            v.phase_rb[0] = 0;
+            v.phase_rb[1] = v.nrows;
+            v.phase_k = 1;
+        }
+        return PR_OK;
+    }
+    PR_TRY(build_phase_view(v, ctx, K));
+    const View& pv = *v.phv;
+    if (v.phase_k == K) return PR_OK;
+    int64_t* rb = nullptr;
+    PR_TRY(dalloc(&rb, (size_t)K + 1, ctx.stream));
+    PR_LAUNCH(ctx, k_phase_rows, 1, 128, 0, (const int32_t*)pv.step_row, (const uint8_t*)pv.sflags, pv.span_steps,
+              pv.nspans, K, v.nrows, rb);
+    PR_CUDA(cudaMemcpyAsync(v.phase_rb, rb, sizeof(int64_t) * (size_t)(K + 1), cudaMemcpyDeviceToHost, ctx.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    dfree(rb, ctx.stream);
+    v.phase_k = K;
+    return PR_OK;
+}
+
 // Boundary-row / hub tickets count the pieces of the current sweep.  A
 // persistent No-Sync launch stops with CTAs at different sweeps, so tickets can
 // be left mid-count; every run starts from zero.
@@ -970,6 +1044,7 @@ static int reset_tickets(const View& v, cudaStream_t s) {
     if (v.bticket && v.nbound > 0) PR_CUDA(cudaMemsetAsync(v.bticket, 0, sizeof(uint32_t) * (size_t)v.nbound, s));
     if (v.hub_ticket && v.nhubs > 0) PR_CUDA(cudaMemsetAsync(v.hub_ticket, 0, sizeof(uint32_t) * (size_t)v.nhubs, s));
     for (int q = 0; q < v.nseg; ++q) PR_TRY(reset_tickets(v.seg[q], s));
+    if (v.phv) PR_TRY(reset_tickets(*v.phv, s));
     return PR_OK;
 }
 
@@ -982,6 +1057,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     if (mode & PR_PERFORATE) return run_perforated(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     cudaStream_t s = ctx.stream;
     const bool async = (mode & PR_MODE_ASYNC) != 0;
+    const bool phased = (mode & PR_MODE_PHASED) != 0;
     const bool reduced = (mode & PR_USE_REDUCTIONS) != 0;
     const bool timing = (mode & PR_TIMING) != 0;
     const int64_t n = g->n;
@@ -1007,15 +1083,27 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
             PR_CUDA(cudaMemsetAsync(g->y[b] + g->n_contrib, 0, sizeof(double), s));
         }
 
+    // phases of a sweep (PR_MODE_PHASED: K >= 1; else one); K > 1 gathers
+    // through the view's finer-span copy
+    int K = 1;
+    if (phased) PR_TRY(phase_plan(g, reduced, ctx, &K));
+    const View& gv = K > 1 ? *v.phv : v;
     GatherCfg gc;
-    PR_TRY(gather_config(ctx, v, g, async, &gc));
+    PR_TRY(gather_config(ctx, gv, g, async, &gc, phased));
     const int64_t cap4 = (int64_t)ctx.num_sms * 4;
-    // K-FINALIZE (stream path): fixed grid, so each CTA's rows and members (and
-    // hence its Delta partial) are a fixed set (deterministic)
+    // K-FINALIZE (stream path): fixed grid per phase, so each CTA's rows and
+    // members (and hence its Delta partial) are a fixed set (deterministic)
+    int64_t fgrid_k[SE_MAX_PHASES], foff_k[SE_MAX_PHASES];
     int64_t fgrid = 0;
     if (gc.stream) {
-        const int64_t work = v.nrows + nm;
-        fgrid = std::min<int64_t>(std::max<int64_t>((work + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
+        for (int k = 0; k < K; ++k) {
+            const int64_t rows = phased ? v.phase_rb[k + 1] - v.phase_rb[k] : v.nrows;
+            const int64_t work = rows + (k == K - 1 ? nm : 0);
+            fgrid_k[k] =
+                std::min<int64_t>(std::max<int64_t>((work + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
+            foff_k[k] = fgrid;
+            fgrid += fgrid_k[k];
+        }
     }
     const int ggrid = (gc.stream && !gc.fused) ? (int)fgrid : gc.grid;  // CTAs writing Delta partials first
     int64_t sgrid = ((gc.fused || (!gc.stream && !gc.inplace)) && nm > 0) ? (nm + GT_NT * 4 - 1) / (GT_NT * 4) : 0;
@@ -1106,14 +1194,34 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         }
         for (int j = 0; j < nb; ++j) {
             const int64_t it = launched + j;
-            const double* y_in = async ? g->y[0] : g->y[it & 1];
-            double* y_out = async ? g->y[0] : g->y[(it + 1) & 1];
+            const double* y_in = (async || phased) ? g->y[0] : g->y[it & 1];
+            double* y_out = (async || phased) ? g->y[0] : g->y[(it + 1) & 1];
             const IterArgs& ia = it == 0 ? ia_first : ia_rest;
-            if (it == 0 && zgrid > 0)
+            if (it == 0 && zgrid > 0 && !phased)
                 PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y_out,
                           (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
-            if (gc.fused) {
+            if (phased) {
+                // in place, phase by phase: the gather of phase k reads the
+                // contribs phases 0..k-1 of this sweep wrote (block Gauss-Seidel)
+                for (int k = 0; k < K; ++k) {
+                    PR_TRY(launch_gather(ctx, gv, y_in, y_out, x, g, c, d, ia, gc, 0, (int64_t)k * gv.nspans / K,
+                                         (int64_t)(k + 1) * gv.nspans / K));
+                    FinArgs f = fa;
+                    f.y_out = y_out;
+                    f.row0 = v.phase_rb[k];
+                    f.nrows = v.phase_rb[k + 1];
+                    f.nm = k == K - 1 ? nm : 0;
+                    f.part_off = foff_k[k];
+                    f.last = k == K - 1;
+                    // in-degree-0 vertices (sweep 1) once every gather of the
+                    // sweep has read their initial contribs, as in sync mode
+                    if (it == 0 && zgrid > 0 && k == K - 1)
+                        PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x,
+                                  y_out, (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
+                    PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid_k[k], GT_NT, 0, f, ia);
+                }
+            } else if (gc.fused) {
                 InPlacePolicyT<true> fp{};
                 fp.y_in = y_in;
                 fp.y = y_out;
@@ -1137,7 +1245,9 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                 PR_TRY(launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, gather_finalizes));
             }
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
-            if (gc.fused) {
+            if (phased) {
+                // the whole sweep is timed as gather_ms
+            } else if (gc.fused) {
                 if (!gather_finalizes) {
                     MemArgs mf{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, (nm + sgrid - 1) / sgrid, g->ab};
                     PR_LAUNCH(ctx, k_members_sync, (unsigned)sgrid, GT_NT, 0, mf, (const double*)g->xr, y_out, ia);
@@ -1145,7 +1255,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
             } else if (gc.stream) {
                 FinArgs f = fa;
                 f.y_out = y_out;
-                PR_LAUNCH(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
+                PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
             } else if (!gather_finalizes && !gc.inplace) {
                 if (async)
                     PR_LAUNCH(ctx, k_scatter<true>, (unsigned)sgrid, GT_NT, 0, (const int32_t*)g->mem_vid,
@@ -1157,7 +1267,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                               y_out, (const int32_t*)g->outdeg, (const int32_t*)g->cidx, ia);
             }
             if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
-            if (it == 0 && nz > 0 && !async)
+            if (it == 0 && nz > 0 && !async && !phased)
                 PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256,
                           0, (const int32_t*)g->zlist, nz, c, (double*)y_in, (const int32_t*)g->outdeg,
                           (const int32_t*)g->cidx);
@@ -1208,6 +1318,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     rs.n_contrib = g->n_contrib;
     rs.n_tasks = v.ntasks;
     rs.edges_gathered = v.nedges * (int64_t)hs->iters;
+    rs.phases = K;
     if (iters_out) *iters_out = hs->iters;
     if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
     return hs->status;
@@ -1402,6 +1513,7 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
     PR_CUDA(cudaStreamSynchronize(s));
     pr_run_stats& rs = g->last;
     rs = pr_run_stats{};
+    rs.phases = 1;
     rs.iterations = max_it;
     rs.status = status;
     rs.delta_l1 = r_l1;
@@ -1673,6 +1785,7 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
     if (rc != PR_OK) return rc;
     pr_run_stats& rs = g->last;
     rs = pr_run_stats{};
+    rs.phases = 1;
     g->log_len = std::min<int32_t>(hs->iters, g->log_cap);
     rs.iterations = hs->iters;
     rs.status = hs->status;

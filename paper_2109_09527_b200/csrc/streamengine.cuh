@@ -48,6 +48,8 @@ struct StreamArgs {
     double* part_in;           // [nspans] (8-byte pieces; reinterpreted for non-fp64 sums)
     double* part_out;          // [nspans]
     uint32_t* bticket;         // [nbound]
+    int64_t span_lo = 0;       // this launch runs spans [span_lo, span_hi) (span_hi < 0: nspans);
+    int64_t span_hi = -1;      // PR_MODE_PHASED runs a sweep as several span ranges
 };
 
 __device__ __forceinline__ int4 ld_stream_v4(const int32_t* p, uint64_t pol) {
@@ -211,7 +213,8 @@ __device__ __forceinline__ void stream_run(P& p, const StreamArgs& a) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint64_t pol = policy_evict_first();
-    for (int64_t span = w; span < a.nspans; span += nw) stream_span(p, a, span, pol);
+    const int64_t hi = a.span_hi < 0 ? a.nspans : a.span_hi;
+    for (int64_t span = a.span_lo + w; span < hi; span += nw) stream_span(p, a, span, pol);
 }
 
 }  // namespace prgpu

@@ -117,6 +117,15 @@ def _fullsize(pr, k, async_too):
         assert np.abs(xr - x).max() <= 1e-10 and np.abs(xr - x).sum() <= 2e-9
 
         if async_too:
+            # phased in-place sweeps (default phase count: 8 on R-MAT-24, 1 on the blocked config 5)
+            for extra in (0, pr.PR_USE_REDUCTIONS):
+                st, it_p, fd, xp = run(pr, g, n, d, gen.tau, gen.max_iter, mode=pr.PR_MODE_PHASED | extra)
+                assert st == pr.PR_OK and fd <= gen.tau
+                assert g.stats()["phases"] == (8 if k == 4 else 1)
+                assert oracle.residual_l1(ref_g, d, xp) / (1 - d) <= 1e-8
+                assert np.abs(xp - x).max() <= 1e-10
+                if k == 4:
+                    assert it_p < it   # block Gauss-Seidel: fewer sweeps on R-MAT
             st, it_a, fd, xa = run(pr, g, n, d, gen.tau, gen.max_iter, mode=pr.PR_MODE_ASYNC)
             assert st == pr.PR_OK and fd <= gen.tau
             res_a = oracle.residual_l1(ref_g, d, xa)

@@ -1,0 +1,151 @@
+"""GPU tests of PR_MODE_PHASED: in-place sweeps in K ordered phases (block
+Gauss-Seidel, DESIGN.md Q-B; the in-place reads of Alg.3 P:545-565 in a fixed
+order).
+
+Pins, none of which uses the CUDA path as its own reference:
+  * one phase is an in-place Jacobi sweep: bit-identical to PR_MODE_SYNC
+    (ranks and sweep count), whose parity with the oracle is pinned elsewhere;
+  * K phases reach the oracle's fixed point (residual certificate of the
+    original system, and an oracle run at tau/100);
+  * the mode is deterministic (fixed phases, fixed-order sums);
+  * on R-MAT (many dangling vertices) it needs fewer sweeps than Jacobi.  (Not
+    on every graph: on a graph without dangling vertices Jacobi conserves
+    sum(x) exactly and its L1 delta falls faster than the in-place one's,
+    DESIGN.md Q-Y.)
+"""
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from tests import graphs as G
+from tests.test_gpu_parity import D, TOL_V, dev
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_09527_b200 as m
+    return m
+
+
+def run(pr, g, n, tau, mode, max_iter=2000):
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    st, it, fd = g.run(x, D, tau, max_iter, mode=mode)
+    return st, it, fd, x.cpu().numpy()
+
+
+def check_fixed_point(pr, g, ref_g, n, tau, extra=0):
+    st, it, fd, x = run(pr, g, n, tau, pr.PR_MODE_PHASED | extra)
+    assert st == pr.PR_OK and fd <= tau
+    res = oracle.residual_l1(ref_g, D, x)
+    tight = oracle.pagerank(ref_g, D, tau / 100, 5000)
+    err = np.abs(x - tight.x).sum()
+    assert err <= res / (1 - D) + 5.67 * tau / 100 + 1e-15
+    assert np.abs(x - tight.x).max() <= max(TOL_V, 10 * tau)
+    return it, x
+
+
+GRAPHS = {
+    "planted0": lambda: G.planted_graph(0, n_base=150, chains=(2, 9, 16, 1)),
+    "planted3": lambda: G.planted_graph(3, n_base=150, chains=(2, 9, 16, 1)),
+    "random": lambda: (400, G.random_edges(400, 1600, 17)),
+    "in_star": lambda: (300, G.in_star(300)),
+    "path": lambda: (64, G.path(64)),
+    "single": lambda: (1, []),
+    "no_edges": lambda: (9, []),
+}
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+@pytest.mark.parametrize("span", ["1", ""])
+def test_one_phase_is_sync(pr, monkeypatch, name, span):
+    monkeypatch.setenv("PRGPU_PHASES", "1")
+    if span:
+        monkeypatch.setenv("PRGPU_SPAN", span)
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        g.preprocess()
+        for extra in (0, pr.PR_USE_REDUCTIONS, pr.PR_NORM_LINF):
+            a = run(pr, g, n, 1e-12, extra)
+            b = run(pr, g, n, 1e-12, pr.PR_MODE_PHASED | extra)
+            assert a[:3] == b[:3] and np.array_equal(a[3], b[3]), (extra, a[:3], b[:3])
+            assert g.stats()["phases"] == 1
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+@pytest.mark.parametrize("phases", ["2", "8", "64"])
+def test_phased_fixed_point(pr, monkeypatch, name, phases):
+    monkeypatch.setenv("PRGPU_PHASES", phases)
+    monkeypatch.setenv("PRGPU_SPAN", "1")  # many spans, so the phases really split the rows
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    ref_g = oracle.build_csr(n, s, t)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        check_fixed_point(pr, g, ref_g, n, 1e-12)
+        g.preprocess()
+        check_fixed_point(pr, g, ref_g, n, 1e-12, pr.PR_USE_REDUCTIONS)
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_phased_configs(pr, monkeypatch, cfg):
+    monkeypatch.setenv("PRGPU_PHASES", "8")
+    gen = graphgen.make_config(cfg)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        it, x = check_fixed_point(pr, g, ref_g, gen.n, gen.tau)
+        assert g.stats()["phases"] > 1
+        again = run(pr, g, gen.n, gen.tau, pr.PR_MODE_PHASED)
+        assert again[1] == it and np.array_equal(again[3], x)  # deterministic
+        g.preprocess()
+        it_r, _ = check_fixed_point(pr, g, ref_g, gen.n, gen.tau, pr.PR_USE_REDUCTIONS)
+
+
+def test_phased_default_phase_count(pr):
+    """Small graphs default to one phase (the launches would cost more than
+    the sweeps saved); PRGPU_PHASES overrides."""
+    gen = graphgen.make_config(2)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        run(pr, g, gen.n, gen.tau, pr.PR_MODE_PHASED)
+        assert g.stats()["phases"] == 1
+
+
+def test_phased_rmat_fewer_sweeps(pr, monkeypatch):
+    """R-MAT (config 4's generator at scale 16): the phased sweep count drops
+    well below Jacobi's, and stays deterministic across runs."""
+    monkeypatch.setenv("PRGPU_PHASES", "8")
+    gen = graphgen.make_config(4, scale_override=16)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        it_sync = run(pr, g, gen.n, gen.tau, 0)[1]
+        it, x = check_fixed_point(pr, g, ref_g, gen.n, gen.tau)
+        assert it < it_sync, (it, it_sync)
+        again = run(pr, g, gen.n, gen.tau, pr.PR_MODE_PHASED)
+        assert again[1] == it and np.array_equal(again[3], x)
+
+
+def test_phased_blocked_view_runs_one_phase(pr, monkeypatch):
+    monkeypatch.setenv("PRGPU_SEG_BITS", "6")
+    n, edges = G.planted_graph(1, n_base=150, chains=(2, 9, 16, 1))
+    s, t = G.edges_to_arrays(edges)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        a = run(pr, g, n, 1e-12, 0)
+        b = run(pr, g, n, 1e-12, pr.PR_MODE_PHASED)
+        assert g.stats()["phases"] == 1
+        assert a[:3] == b[:3] and np.array_equal(a[3], b[3])
+
+
+def test_phased_mode_validation(pr):
+    n = 50
+    s, t = G.edges_to_arrays(G.random_edges(n, 200, 3))
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        for bad in (pr.PR_MODE_ASYNC, pr.PR_MODE_NOSYNC, pr.PR_PERFORATE):
+            with pytest.raises(pr.PRError) as e:
+                pr.pr_run(g.handle, D, 1e-10, 10, x, mode=pr.PR_MODE_PHASED | bad)
+            assert e.value.code == pr.PR_EINVAL

@@ -70,8 +70,8 @@ for k in cfgs:
     E, n = info["E"], gen.n
     rec = {"config": k, "workload": gen.name, "n": n, "E": E, "tau": gen.tau,
            "create_ms": round(a.elapsed_time(b), 3), "preprocess_ms": round(b.elapsed_time(c_), 3)}
-    for name, mode in (("plain", 0), ("reduced", pr.PR_USE_REDUCTIONS), ("async", pr.PR_MODE_ASYNC),
-                       ("nosync", pr.PR_MODE_NOSYNC)):
+    for name, mode in (("plain", 0), ("reduced", pr.PR_USE_REDUCTIONS), ("phased", pr.PR_MODE_PHASED),
+                       ("async", pr.PR_MODE_ASYNC), ("nosync", pr.PR_MODE_NOSYNC)):
         (ms, it, rc), stt, gms, fms = timed_run(g, x, gen, mode)
         r = {"time_to_converge_ms": round(ms, 3), "iterations": it, "status": rc}
         if name in ("plain", "reduced"):
@@ -80,6 +80,8 @@ for k in cfgs:
             r.update(sweep_ms=round(sweep, 4), gteps_per_iteration=round(E / (sweep * 1e-3) / 1e9, 2),
                      gather_ms=round(gms, 4), gather_frac_of_peak=round(alg / (gms * 1e-3) / 1e9 / PEAK, 4),
                      sweep_model_frac=round((12 * E + 24 * n + 8) / (sweep * 1e-3) / 1e9 / PEAK, 4))
+        if name == "phased":
+            r.update(phases=stt["phases"])
         if name == "nosync":
             r.update(median_local_sweeps=stt["nosync_median_iters"], certified_residual=stt["residual"])
         rec[name] = r

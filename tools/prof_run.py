@@ -1,5 +1,5 @@
 """Profiling driver: build config k on the GPU and run a fixed number of sweeps.
-Usage: python tools/prof_run.py <config> <mode: plain|reduced|async> <sweeps> [scale_override]"""
+Usage: python tools/prof_run.py <config> <mode: plain|reduced|async|nosync|phased|..._reduced> <sweeps> [scale_override]"""
 import os
 import sys
 
@@ -20,7 +20,8 @@ t = torch.from_numpy(gen.dst).cuda()
 x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
 g = pr.Graph(gen.n, s, t)
 m = {"plain": 0, "reduced": pr.PR_USE_REDUCTIONS, "async": pr.PR_MODE_ASYNC, "nosync": pr.PR_MODE_NOSYNC,
-     "nosync_reduced": pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS}[mode]
+     "nosync_reduced": pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS, "phased": pr.PR_MODE_PHASED,
+     "phased_reduced": pr.PR_MODE_PHASED | pr.PR_USE_REDUCTIONS}[mode]
 if "reduced" in mode:
     g.preprocess()
 st, it, fd = g.run(x, gen.d, 0.0, sweeps, mode=m | pr.PR_TIMING)
