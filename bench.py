@@ -46,6 +46,12 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-modes", action="store_true", help="skip the async / No-Sync / perforation comparison")
     p.add_argument("--no-plain", action="store_true", help="skip the extra plain-sweep roofline run")
+    p.add_argument("--parallel", choices=["replicas", "shard"], default="replicas",
+                   help="N>1: independent replicas (weak scaling, default) or ONE graph row-sharded over the "
+                        "ranks with a per-sweep all-gather (pr_run_sharded, strong scaling; plain sync mode)")
+    p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                   help="process-group backend of our arm (gloo + PRGPU_BENCH_ONE_GPU=1: test the sharded "
+                        "multi-process plumbing with every rank on cuda:0)")
     return p.parse_args()
 
 
@@ -119,7 +125,9 @@ def dist_init(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        dist.init_process_group(args.backend if args.impl == "ours" else "gloo")
+    if os.environ.get("PRGPU_BENCH_ONE_GPU") == "1":
+        local = 0
     return ws, rank, local
 
 
@@ -258,6 +266,101 @@ def compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags):
     return modes
 
 
+# ------------------------------------------------------------ ours, sharded --
+def run_shard_bench(args, ws, rank, local, dev, pr, torch, gen, W, K):
+    """--parallel shard: one R-MAT-24 graph row-sharded over the ranks
+    (SURVEY f3).  Step = pr_graph_create (every rank ingests the same edge
+    list) + pr_graph_shard + pr_run_sharded (plain sync, one in-place
+    all-gather of the contrib chunks per sweep) + pr_destroy.  value = E *
+    iterations / max-over-ranks time (ONE graph: strong scaling)."""
+    n = gen.n
+    stream = torch.cuda.current_stream(dev)
+    exchange = pr.torch_dist_exchange() if ws > 1 else (lambda *a: None)
+    src_h = torch.from_numpy(gen.src).pin_memory()
+    dst_h = torch.from_numpy(gen.dst).pin_memory()
+    src_d, dst_d = src_h.to(dev), dst_h.to(dev)
+    x_d = torch.empty(n, dtype=torch.float64, device=dev)
+    x_h = torch.empty(n, dtype=torch.float64).pin_memory()
+
+    def step(src, dst, to_host=False, timing=False):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record(stream)
+        g = pr.Graph(n, src, dst)
+        g.shard(rank, ws)
+        e[1].record(stream)
+        st, it, fd = g.run_sharded(x_d, exchange, gen.d, gen.tau, gen.max_iter,
+                                   mode=pr.PR_TIMING if timing else 0)
+        e[2].record(stream)
+        if to_host:
+            x_h.copy_(x_d, non_blocking=True)
+        rec = {"iters": it, "E": g.info()["E"], "info": g.shard_info(), "stats": g.stats(), "ev": e}
+        g.close()
+        return rec
+
+    for _ in range(W):
+        step(src_d, dst_d)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = Clocks(local)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.start()
+    a.record(stream)
+    recs = [step(src_d, dst_d) for _ in range(K)]
+    b.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    barrier(ws)
+    t = max_over_ranks(a.elapsed_time(b), ws, dev)
+    run_ms = max_over_ranks(statistics.median(r["ev"][1].elapsed_time(r["ev"][2]) for r in recs), ws, dev)
+    setup_ms = max_over_ranks(statistics.median(r["ev"][0].elapsed_time(r["ev"][1]) for r in recs), ws, dev)
+    E = recs[0]["E"]
+    iters = recs[0]["iters"]
+    value = E * sum(r["iters"] for r in recs) / (t * 1e-3) / 1e9
+    launches = int(sum_over_ranks(float(sum(r["stats"]["run_launches"] for r in recs)), ws, dev))
+    tr = step(src_d, dst_d, timing=True)
+    sp = tr["stats"]
+    ti = max(1, sp["timed_iterations"])
+    pg = sp["gather_ms"] / ti
+    hbm_peak, peak_src = load_peaks()
+    alg = 12 * sp["gather_edges"] + 8 * sp["gather_rows"]
+    roofline = {"kernel": "k_stream (K-GATHER, this rank's rows)", "bound": "hbm",
+                "achieved": round(alg / (pg * 1e-3) / 1e9, 1) if pg > 0 else None, "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(alg / (pg * 1e-3) / 1e9 / hbm_peak, 4) if pg > 0 else None,
+                "traffic": None, "peak_source": peak_src, "rank": rank}
+    torch.cuda.synchronize()
+    barrier(ws)
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    er = step(src_h, dst_h, to_host=True)
+    eb.record(stream)
+    torch.cuda.synchronize()
+    te = max_over_ranks(ea.elapsed_time(eb), ws, dev)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": round(t / K, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": gen.name, "n": n, "m_raw": gen.m, "E": E, "d": gen.d, "tau": gen.tau,
+                       "norm": "L1", "mode": "plain", "iterations": iters, "parallelism": f"shard{ws}",
+                       "backend": args.backend if ws > 1 else None,
+                       "l2": "inputs larger than L2 (edge list 8m bytes)",
+                       "time_to_converge_ms": round(run_ms, 3), "create_and_shard_ms": round(setup_ms, 3),
+                       "rank0_shard": recs[0]["info"]},
+            "roofline": roofline,
+            "cpu_baseline": None,
+            "e2e": {"value": round(E * er["iters"] / (te * 1e-3) / 1e9, 4), "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * gen.m, "d2h_bytes_per_step": 8 * n, "ms_per_step": round(te, 3)},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    barrier(ws)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 # --------------------------------------------------------------------- ours --
 def main():
     args = parse()
@@ -279,6 +382,8 @@ def main():
     K = max(1, args.steps)
 
     gen = graphgen.make_config(args.config)
+    if args.parallel == "shard":
+        return run_shard_bench(args, ws, rank, local, dev, pr, torch, gen, W, K)
     n, m = gen.n, gen.m
     src_h = torch.from_numpy(gen.src).pin_memory()
     dst_h = torch.from_numpy(gen.dst).pin_memory()

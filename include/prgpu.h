@@ -202,6 +202,61 @@ typedef struct {
 
 int pr_get_run_stats(const pr_graph *g, pr_run_stats *out);
 
+/*
+ * ---- Row sharding over P ranks ----
+ * The sync pull iteration split by destination rows: every rank holds the
+ * in-edges of the vertices it owns and a full replica of the contrib vector;
+ * after each sweep ONE in-place all-gather of fixed-size per-rank chunks
+ * (owned contribs + that rank's (L1, L-inf) delta) gives every rank the next
+ * contrib vector and all deltas, summed in rank order for an identical stop
+ * decision.  The paper has no multi-device form; the sweep is Eq.(1)
+ * over the owned rows, exactly as in pr_run.
+ *
+ * pr_exchange_fn -- caller-supplied exchange: on `stream`, all-gather IN PLACE
+ * the `world` chunks of `chunk` doubles of the device buffer `buf`
+ * (world * chunk doubles; this rank's chunk, at rank * chunk, is filled when
+ * the call is made, ordered on `stream`).  Called once per sweep from the
+ * host thread running pr_run_sharded, before the rank-order delta reduction
+ * is enqueued.  Returns 0, or nonzero to abort the run with PR_ECUDA.
+ */
+typedef int (*pr_exchange_fn)(void *ctx, double *buf, int64_t chunk, int32_t world, void *stream);
+
+/*
+ * pr_graph_shard -- make g (created from the SAME edge list on every rank) the
+ * rank's share of a world-rank row partition: contrib-carrying vertices are cut
+ * into world ranges of the internal contrib order balanced by
+ * sum(in-degree + 1), dangling vertices by id range.  Deterministic: every
+ * rank derives the same partition.  1 <= world <= 4096, 0 <= rank < world
+ * (else PR_EINVAL).  pr_run / pr_preprocess keep working on the whole graph.
+ */
+int pr_graph_shard(pr_graph *g, int32_t rank, int32_t world, void *stream);
+
+/*
+ * pr_run_sharded -- the synchronous plain iteration (PR_MODE_SYNC, optionally
+ * PR_NORM_LINF / PR_TIMING; other bits PR_EINVAL) over this rank's rows.
+ *   ranks  fp64[n] DEVICE buffer: owned vertices get their rank, every other
+ *          entry 0.0 (so a sum all-reduce over the ranks assembles the vector
+ *          exactly); a host pointer is PR_EINVAL
+ *   exchange, exchange_ctx  the all-gather above (non-NULL)
+ *   iters_out / final_delta_out as pr_run (identical on every rank)
+ * PR_ESTATE without a prior pr_graph_shard.  world = 1 is bit-identical to
+ * pr_run(PR_MODE_SYNC).
+ */
+int pr_run_sharded(pr_graph *g, double d, double threshold, int32_t max_iter, void *stream, uint32_t mode,
+                   double *ranks, pr_exchange_fn exchange, void *exchange_ctx, int32_t *iters_out,
+                   double *final_delta_out);
+
+typedef struct {
+    int32_t rank;
+    int32_t world;
+    int64_t owned_vertices;  /* vertices this rank computes */
+    int64_t rows;            /* owned vertices of in-degree > 0 (gathered) */
+    int64_t edges;           /* in-edges of those rows */
+    int64_t chunk;           /* doubles per rank in the exchanged buffer */
+} pr_shard_info;
+
+int pr_get_shard_info(const pr_graph *g, pr_shard_info *out);
+
 #ifdef __cplusplus
 }
 #endif

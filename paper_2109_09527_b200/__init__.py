@@ -43,6 +43,7 @@ PR_MODE_PHASED = 64
 ABI_SYMBOLS = (
     "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_last_error",
     "pr_graph_info", "pr_get_csr", "pr_get_reductions", "pr_get_delta_log", "pr_get_run_stats",
+    "pr_graph_shard", "pr_run_sharded", "pr_get_shard_info",
 )
 
 
@@ -83,6 +84,25 @@ class pr_run_stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class pr_shard_info(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("owned_vertices", ctypes.c_int64),
+        ("rows", ctypes.c_int64),
+        ("edges", ctypes.c_int64),
+        ("chunk", ctypes.c_int64),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+# int (*pr_exchange_fn)(void *ctx, double *buf, int64_t chunk, int32_t world, void *stream)
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                               ctypes.c_void_p)
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libprgpu.so not built at {LIB_PATH}; run `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -110,6 +130,13 @@ def _load():
     lib.pr_get_delta_log.restype = ctypes.c_int
     lib.pr_get_run_stats.argtypes = [p, ctypes.POINTER(pr_run_stats)]
     lib.pr_get_run_stats.restype = ctypes.c_int
+    lib.pr_graph_shard.argtypes = [p, i32, i32, p]
+    lib.pr_graph_shard.restype = ctypes.c_int
+    lib.pr_run_sharded.argtypes = [p, dbl, dbl, i32, p, u32, p, EXCHANGE_FN, p, ctypes.POINTER(i32),
+                                   ctypes.POINTER(dbl)]
+    lib.pr_run_sharded.restype = ctypes.c_int
+    lib.pr_get_shard_info.argtypes = [p, ctypes.POINTER(pr_shard_info)]
+    lib.pr_get_shard_info.restype = ctypes.c_int
     return lib
 
 
@@ -217,6 +244,76 @@ def pr_get_run_stats(g) -> dict:
     return st.as_dict()
 
 
+def pr_graph_shard(g, rank: int, world: int, stream=None) -> None:
+    """Make g this rank's share of a world-rank row partition."""
+    _check(lib.pr_graph_shard(g, rank, world, _stream(stream)))
+
+
+def pr_get_shard_info(g) -> dict:
+    info = pr_shard_info()
+    _check(lib.pr_get_shard_info(g, ctypes.byref(info)))
+    return info.as_dict()
+
+
+def device_f64(ptr: int, count: int):
+    """A torch view (no copy) of `count` doubles of device memory at `ptr`."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                    "version": 2, "strides": None}
+    return torch.as_tensor(_CAI(), device="cuda")
+
+
+def torch_dist_exchange(group=None):
+    """The per-sweep exchange of pr_run_sharded through torch.distributed
+    (NCCL over NVLink on a GPU node): an in-place all_gather_into_tensor of the
+    world chunks, ordered on the library's stream."""
+    import torch
+    import torch.distributed as dist
+
+    nccl = dist.get_backend(group) == "nccl"
+
+    def exchange(buf: int, chunk: int, world: int, stream: int):
+        full = device_f64(buf, chunk * world)
+        rank = dist.get_rank(group)
+        # stream 0 (ctypes passes it as None) is the legacy default stream
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+        with torch.cuda.stream(s):
+            if nccl:
+                dist.all_gather_into_tensor(full, full[rank * chunk:(rank + 1) * chunk], group=group)
+            else:  # gloo (multi-process tests on one GPU): list all-gather, host-synchronous
+                s.synchronize()
+                parts = list(full.view(world, chunk).unbind(0))
+                dist.all_gather(parts, parts[rank].clone(), group=group)
+                torch.cuda.synchronize()
+    return exchange
+
+
+def pr_run_sharded(g, d: float, threshold: float, max_iter: int, ranks, exchange, stream=None, mode: int = 0):
+    """The sharded sync iteration; `exchange(buf_ptr, chunk, world, stream_ptr)`
+    all-gathers the chunks in place.  Returns (status, iterations, final_delta);
+    ranks (device fp64[n]) holds the owned vertices' ranks, 0.0 elsewhere."""
+    err = []
+
+    def _cb(ctx, buf, chunk, world, strm):
+        try:
+            exchange(buf, chunk, world, strm)
+            return 0
+        except BaseException as e:  # reported after the call returns
+            err.append(e)
+            return 1
+    cb = EXCHANGE_FN(_cb)
+    it = ctypes.c_int32(0)
+    fd = ctypes.c_double(0.0)
+    rc = lib.pr_run_sharded(g, d, threshold, max_iter, _stream(stream), mode, _ptr(ranks), cb, None,
+                            ctypes.byref(it), ctypes.byref(fd))
+    if err:
+        raise err[0]
+    _check(rc, ok=(PR_OK, PR_NOT_CONVERGED))
+    return rc, it.value, fd.value
+
+
 class Graph:
     """RAII convenience wrapper around one pr_graph (still only marshalling)."""
 
@@ -230,6 +327,16 @@ class Graph:
 
     def run(self, ranks, d=0.85, threshold=1e-10, max_iter=1000, mode=0, stream=None):
         return pr_run(self.handle, d, threshold, max_iter, ranks, stream, mode)
+
+    def shard(self, rank: int, world: int, stream=None):
+        pr_graph_shard(self.handle, rank, world, stream)
+        return self
+
+    def shard_info(self):
+        return pr_get_shard_info(self.handle)
+
+    def run_sharded(self, ranks, exchange, d=0.85, threshold=1e-10, max_iter=1000, mode=0, stream=None):
+        return pr_run_sharded(self.handle, d, threshold, max_iter, ranks, exchange, stream, mode)
 
     def info(self):
         return pr_graph_info(self.handle)

@@ -352,10 +352,96 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
     return rc;
 }
 
+int pr_graph_shard(pr_graph* g, int32_t rank, int32_t world, void* stream) {
+    g_err[0] = 0;
+    if (!g) {
+        set_error("pr_graph_shard: NULL graph");
+        return PR_EINVAL;
+    }
+    if (world < 1 || world > 4096 || rank < 0 || rank >= world) {
+        set_error("pr_graph_shard: rank=%d world=%d (need 0 <= rank < world <= 4096)", rank, world);
+        return PR_EINVAL;
+    }
+    Ctx ctx;
+    PR_TRY(make_ctx(ctx, stream));
+    int rc = build_shard(g, rank, world, ctx);
+    g->launches += ctx.launches;
+    if (rc != PR_OK) {
+        clear_shard(g, ctx.stream);
+        return rc;
+    }
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
+    return PR_OK;
+}
+
+int pr_run_sharded(pr_graph* g, double d, double threshold, int32_t max_iter, void* stream, uint32_t mode,
+                   double* ranks, pr_exchange_fn exchange, void* exchange_ctx, int32_t* iters_out,
+                   double* final_delta_out) {
+    g_err[0] = 0;
+    if (!g || !ranks || !exchange) {
+        set_error("pr_run_sharded: NULL graph, ranks or exchange");
+        return PR_EINVAL;
+    }
+    if (!(d > 0.0 && d < 1.0)) {
+        set_error("pr_run_sharded: d=%g outside (0,1)", d);
+        return PR_EINVAL;
+    }
+    if (!(threshold >= 0.0)) {
+        set_error("pr_run_sharded: threshold must be >= 0 and not NaN");
+        return PR_EINVAL;
+    }
+    if (max_iter < 1) {
+        set_error("pr_run_sharded: max_iter=%d < 1", max_iter);
+        return PR_EINVAL;
+    }
+    if (mode & ~(PR_NORM_LINF | PR_TIMING)) {
+        set_error("pr_run_sharded: mode 0x%x (only PR_MODE_SYNC, PR_NORM_LINF, PR_TIMING)", mode);
+        return PR_EINVAL;
+    }
+    cudaPointerAttributes at{};
+    const bool dev = cudaPointerGetAttributes(&at, ranks) == cudaSuccess &&
+                     (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    if (!dev) {
+        set_error("pr_run_sharded: ranks must be device memory");
+        return PR_EINVAL;
+    }
+    if (g->shard_world < 1) {
+        set_error("pr_run_sharded: pr_graph_shard has not run");
+        return PR_ESTATE;
+    }
+    Ctx ctx;
+    PR_TRY(make_ctx(ctx, stream));
+    int rc = run_sharded(g, d, threshold, max_iter, mode, ranks, ctx, exchange, exchange_ctx, iters_out,
+                         final_delta_out);
+    g->launches += ctx.launches;
+    g->last.total_launches = g->launches;
+    return rc;
+}
+
+int pr_get_shard_info(const pr_graph* g, pr_shard_info* out) {
+    if (!g || !out) {
+        set_error("pr_get_shard_info: bad arguments");
+        return PR_EINVAL;
+    }
+    if (g->shard_world < 1) {
+        set_error("pr_get_shard_info: pr_graph_shard has not run");
+        return PR_ESTATE;
+    }
+    out->rank = g->shard_rank;
+    out->world = g->shard_world;
+    out->owned_vertices = g->shard_owned;
+    out->rows = g->shard.nrows;
+    out->edges = g->shard.nedges;
+    out->chunk = g->shard_chunk;
+    return PR_OK;
+}
+
 void pr_destroy(pr_graph* g) {
     if (!g) return;
     cudaStream_t s = 0;
     PhaseTimer pt(s, "destroy");
+    clear_shard(g, s);
     dfree(g->row_ptr, s);
     dfree(g->col, s);
     dfree(g->outdeg, s);

@@ -166,6 +166,19 @@ struct pr_graph {
     int32_t* mem_srow = nullptr;    // reduced-view row of mem_src (K-FINALIZE reads its S)
     int2* mem_info = nullptr;       // (outdeg, contrib slot) of each member
     prgpu::View reduced;
+    // row sharding over P ranks (pr_graph_shard, shard.cu)
+    int32_t shard_rank = -1;
+    int32_t shard_world = 0;
+    int64_t shard_chunk = 0;        // doubles per rank in the exchanged buffer (owned contribs + (L1, Linf))
+    int64_t shard_owned = 0;        // vertices this rank computes
+    int32_t* sowner = nullptr;      // [n] rank owning each vertex
+    int32_t* scidx = nullptr;       // [n] sharded contrib slot (or -1)
+    int32_t* szlist = nullptr;      // owned vertices of in-degree 0
+    int64_t shard_hot = 0;          // H: contribs [0, H) are copies of the H hottest (gather tiers)
+    int32_t* shot_src = nullptr;    // [H] chunk slot of each hot copy
+    int64_t snz = 0;
+    prgpu::View shard;              // owned rows of in-degree > 0, columns in sharded slots
+    double* sy[2] = {nullptr, nullptr};  // [H + world * chunk + 1] ping-pong, last slot = +0.0
     // iteration buffers (allocated lazily by pr_run)
     double* x = nullptr;            // fp64[n] (used when the caller's ranks are on the host)
     double* xr = nullptr;           // sync sweeps: x of the view's rows, row order (unpermuted at the end)
@@ -203,4 +216,8 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx);
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
         Ctx& ctx, int32_t* iters_out, double* delta_out);
 int read_count(Ctx& ctx, const int64_t* dev, int64_t* host);
+int build_shard(pr_graph* g, int rank, int world, Ctx& ctx);
+void clear_shard(pr_graph* g, cudaStream_t s);
+int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
+                pr_exchange_fn exchange, void* exchange_ctx, int32_t* iters_out, double* delta_out);
 }  // namespace prgpu

@@ -153,7 +153,32 @@ struct IterArgs {
     const double* hub_delta;    // of the gather view
     int64_t nhubs;
     double* delta_log;
+    // sharded run: the last CTA writes this rank's (L1, Linf) here (the tail
+    // of its exchanged chunk) instead of taking the stop decision
+    double* shard_out = nullptr;
 };
+
+// The stop test on a sweep's (L1, Linf): iteration count, delta log, done /
+// status ("while err > threshold", P:454 / BASELINE L1; max_iter S:176).
+__device__ void stop_test(const IterArgs& ia, double l1, double li) {
+    DevState* st = ia.st;
+    const int it = st->iters + 1;
+    st->iters = it;
+    st->l1 = l1;
+    st->linf = li;
+    if (it <= st->log_cap) {
+        ia.delta_log[2 * (it - 1)] = l1;
+        ia.delta_log[2 * (it - 1) + 1] = li;
+    }
+    const double dn = st->norm_linf ? li : l1;
+    if (dn <= st->tau) {
+        st->done = 1;
+        st->status = PR_OK;
+    } else if (it >= st->max_iter) {
+        st->done = 1;
+        st->status = PR_NOT_CONVERGED;
+    }
+}
 
 // Deterministic fixed-order reduction over all CTA partials and hub deltas,
 // then the stop test; executed by the last CTA of the iteration.
@@ -187,21 +212,11 @@ __device__ void global_finalize(const IterArgs& ia, double* red) {
             li = fmax(li, red[RED_W + w]);
         }
         DevState* st = ia.st;
-        const int it = st->iters + 1;
-        st->iters = it;
-        st->l1 = l1;
-        st->linf = li;
-        if (it <= st->log_cap) {
-            ia.delta_log[2 * (it - 1)] = l1;
-            ia.delta_log[2 * (it - 1) + 1] = li;
-        }
-        const double dn = st->norm_linf ? li : l1;
-        if (dn <= st->tau) {
-            st->done = 1;
-            st->status = PR_OK;
-        } else if (it >= st->max_iter) {
-            st->done = 1;
-            st->status = PR_NOT_CONVERGED;
+        if (ia.shard_out) {
+            ia.shard_out[0] = l1;
+            ia.shard_out[1] = li;
+        } else {
+            stop_test(ia, l1, li);
         }
         st->ticket_gather = 0u;
         st->ticket_scatter = 0u;
@@ -1319,6 +1334,184 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     rs.n_tasks = v.ntasks;
     rs.edges_gathered = v.nedges * (int64_t)hs->iters;
     rs.phases = K;
+    if (iters_out) *iters_out = hs->iters;
+    if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
+    return hs->status;
+}
+
+// -------------------------------------------------------- sharded (f3) --
+// After the exchange: refresh the hot copy y[0, H) from the chunks, and sum
+// every rank's (L1, Linf) (the tail of its chunk) in rank order -- identical on
+// every rank -- for the stop test.
+__global__ void k_shard_combine(IterArgs ia, double* __restrict__ y, const int32_t* __restrict__ hot_src, int64_t H,
+                                int world, int64_t chunk, int stop) {
+    if (ia.st->done) return;  // (block 0 may set it below; a late hot copy is then unused)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < H; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = y[hot_src[i]];
+    if (blockIdx.x != 0 || threadIdx.x != 0 || !stop) return;
+    const double* ch = y + H;
+    double l1 = 0.0, li = 0.0;
+    for (int r = 0; r < world; ++r) {
+        l1 += ch[(int64_t)r * chunk + chunk - 2];
+        li = fmax(li, ch[(int64_t)r * chunk + chunk - 1]);
+    }
+    stop_test(ia, l1, li);
+}
+
+// ranks[v] = x[v] for the vertices this rank owns, 0.0 elsewhere
+__global__ void k_shard_ranks(const double* __restrict__ x, const int32_t* __restrict__ owner, int rank, int64_t n,
+                              double* __restrict__ ranks) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        ranks[v] = owner[v] == rank ? x[v] : 0.0;
+}
+
+int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
+                pr_exchange_fn exchange, void* exchange_ctx, int32_t* iters_out, double* delta_out) {
+    cudaStream_t s = ctx.stream;
+    const bool timing = (mode & PR_TIMING) != 0;
+    const int64_t n = g->n;
+    const View& v = g->shard;
+    const int world = g->shard_world, rank = g->shard_rank;
+    const int64_t chunk = g->shard_chunk, H = g->shard_hot;
+    const int64_t launches0 = ctx.launches;
+    PR_TRY(reset_tickets(v, s));
+    if (!g->x) PR_TRY(dalloc(&g->x, (size_t)n, s));
+    double* x = g->x;
+
+    GatherCfg gc;
+    PR_TRY(gather_config(ctx, v, g, false, &gc, true));
+    if (gc.hot_n > H) {  // the shared-memory tier reads the hot copy only
+        gc.hot_n = (int)H;
+        gc.smem = (size_t)gc.hot_n * sizeof(double);
+    }
+    const int64_t cap4 = (int64_t)ctx.num_sms * 4;
+    const int64_t fgrid =
+        std::min<int64_t>(std::max<int64_t>((v.nrows + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
+    const int64_t nz = g->snz;
+    int64_t zgrid = nz > 0 ? std::min<int64_t>((nz + GT_NT * 4 - 1) / (GT_NT * 4), cap4) : 0;
+    const int64_t zper = zgrid > 0 ? (nz + zgrid - 1) / zgrid : 0;
+    const int64_t need = 2 * (fgrid + zgrid);
+    if (g->partial_cap < need) {
+        dfree(g->cta_partial, s);
+        PR_TRY(dalloc(&g->cta_partial, (size_t)need, s));
+        g->partial_cap = need;
+    }
+    const int log_cap = max_iter < 4096 ? max_iter : 4096;
+    if (g->log_cap < log_cap) {
+        dfree(g->delta_log, s);
+        PR_TRY(dalloc(&g->delta_log, (size_t)(2 * log_cap), s));
+        g->log_cap = log_cap;
+    }
+    const int64_t need_xr = std::max<int64_t>(std::max(g->plain.nrows, v.nrows), 1);
+    if (g->xr_cap < need_xr) {
+        dfree(g->xr, s);
+        PR_TRY(dalloc(&g->xr, (size_t)need_xr, s));
+        g->xr_cap = need_xr;
+    }
+    const double c = (1.0 - d) / (double)n;
+    DevState* hs = g->st_host;
+    *hs = DevState{};
+    hs->max_iter = max_iter;
+    hs->norm_linf = (mode & PR_NORM_LINF) ? 1 : 0;
+    hs->tau = tau;
+    hs->log_cap = log_cap;
+    PR_CUDA(cudaMemcpyAsync(g->st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
+    // x0 = 1/n and y0 of EVERY contrib slot (the replica starts complete)
+    PR_LAUNCH(ctx, k_init, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, x,
+              g->sy[0], (const int32_t*)g->outdeg, (const int32_t*)g->scidx, n, 1.0 / (double)n);
+    IterArgs ia0{g->st, g->cta_partial, 0, 0, 0, nullptr, 0, g->delta_log};
+    const unsigned cgrid = (unsigned)std::max<int64_t>(1, (H + 255) / 256);
+    PR_LAUNCH(ctx, k_shard_combine, cgrid, 256, 0, ia0, g->sy[0], (const int32_t*)g->shot_src, H, world, chunk, 0);
+    const unsigned fg = (unsigned)std::min<int64_t>((v.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+    PR_LAUNCH(ctx, k_fill_f64, fg, 256, 0, g->xr, v.nrows, 1.0 / (double)n);
+    IterArgs ia_rest{g->st, g->cta_partial, fgrid, 0, 0, nullptr, 0, g->delta_log};
+    IterArgs ia_first = ia_rest;
+    ia_first.zero_ctas = zgrid;
+    double* zero_partial = g->cta_partial + 2 * fgrid;
+    FinArgs fa{v.sums, v.nrows, v.rinfo, g->xr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, c, d};
+
+    std::vector<cudaEvent_t> ev;
+    double gather_ms = 0.0, scatter_ms = 0.0;
+    int timed = 0, host_syncs = 0;
+    int64_t launched = 0;
+    int batch = 8;
+    while (true) {
+        int nb = batch;
+        if (launched + nb > max_iter) nb = (int)(max_iter - launched);
+        if (timing && (int)ev.size() < 4 * nb) {
+            size_t old = ev.size();
+            ev.resize(4 * nb);
+            for (size_t i = old; i < ev.size(); ++i) PR_CUDA(cudaEventCreate(&ev[i]));
+        }
+        for (int j = 0; j < nb; ++j) {
+            const int64_t it = launched + j;
+            double* y_in = g->sy[it & 1];
+            double* y_out = g->sy[(it + 1) & 1];
+            IterArgs ia = it == 0 ? ia_first : ia_rest;
+            ia.shard_out = y_out + H + (int64_t)rank * chunk + chunk - 2;
+            if (it == 0 && zgrid > 0)
+                PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->szlist, nz, zper, c, x, y_out,
+                          (const int32_t*)g->outdeg, (const int32_t*)g->scidx, zero_partial);
+            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
+            if (v.nrows > 0) PR_TRY(launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, 0));
+            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
+            FinArgs f = fa;
+            f.y_out = y_out;
+            PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
+            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
+            if (it == 0 && nz > 0)
+                PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256,
+                          0, (const int32_t*)g->szlist, nz, c, y_in, (const int32_t*)g->outdeg,
+                          (const int32_t*)g->scidx);
+            if (exchange(exchange_ctx, y_out + H, chunk, world, (void*)s) != 0) {
+                set_error("pr_run_sharded: the exchange callback failed at sweep %lld", (long long)it + 1);
+                for (auto e : ev) cudaEventDestroy(e);
+                return PR_ECUDA;
+            }
+            PR_LAUNCH(ctx, k_shard_combine, cgrid, 256, 0, ia, y_out, (const int32_t*)g->shot_src, H, world, chunk, 1);
+        }
+        PR_CUDA(cudaMemcpyAsync(hs, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        ++host_syncs;
+        if (timing) {
+            for (int j = 0; j < nb; ++j) {
+                if (launched + j >= hs->iters) break;
+                float a = 0.f, b2 = 0.f;
+                PR_CUDA(cudaEventElapsedTime(&a, ev[4 * j], ev[4 * j + 1]));
+                PR_CUDA(cudaEventElapsedTime(&b2, ev[4 * j + 1], ev[4 * j + 2]));
+                gather_ms += a;
+                scatter_ms += b2;
+                ++timed;
+            }
+        }
+        launched += nb;
+        if (hs->done || launched >= max_iter) break;
+        if (batch < 64) batch *= 2;
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+    const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+    PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
+              (const double*)nullptr, (const int32_t*)nullptr, (int64_t)0, x);
+    PR_LAUNCH(ctx, k_shard_ranks, (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0,
+              (const double*)x, (const int32_t*)g->sowner, rank, n, ranks);
+    PR_CUDA(cudaStreamSynchronize(s));
+    pr_run_stats& rs = g->last;
+    rs = pr_run_stats{};
+    rs.phases = 1;
+    g->log_len = std::min<int32_t>(hs->iters, g->log_cap);
+    rs.iterations = hs->iters;
+    rs.status = hs->status;
+    rs.delta_l1 = hs->l1;
+    rs.delta_linf = hs->linf;
+    rs.run_launches = ctx.launches - launches0;
+    rs.host_syncs = host_syncs;
+    rs.timed_iterations = timed;
+    rs.gather_ms = gather_ms;
+    rs.scatter_ms = scatter_ms;
+    rs.gather_rows = v.nrows;
+    rs.gather_edges = v.nedges;
+    rs.n_contrib = g->n_contrib;
+    rs.edges_gathered = v.nedges * (int64_t)hs->iters;
     if (iters_out) *iters_out = hs->iters;
     if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
     return hs->status;

@@ -1,0 +1,231 @@
+"""GPU tests of the row-sharded sync iteration (pr_graph_shard / pr_run_sharded;
+SURVEY §8(e) / f3).
+
+There is one GPU here, so P ranks run in ONE process on it: each rank is a
+host thread driving its own pr_graph; the per-sweep exchange is a loopback
+all-gather (device copies between the ranks' buffers after a host barrier).
+No kernel ever waits on another rank's kernel: every wait is on the host.
+The library code under test is exactly what runs across GPUs; only the
+exchange callback differs (torch.distributed / NCCL there).
+
+Pins (none uses the CUDA path as its own reference):
+  * world = 1 is bit-identical to pr_run(PR_MODE_SYNC), whose oracle parity is
+    pinned in test_gpu_parity;
+  * P > 1: the assembled ranks match the oracle (1e-10 per vertex, 1e-9 L1,
+    iteration count within the +/-1 rule), every vertex is owned exactly once,
+    the rows and edges of the shards partition the plain view's.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+from tests import graphs as G
+from tests.test_gpu_parity import D, assert_close, assert_iters, dev
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_09527_b200 as m
+    return m
+
+
+class Loopback:
+    """In-process all-gather of the ranks' chunks (one GPU, host barriers)."""
+
+    def __init__(self, pr, world):
+        self.pr = pr
+        self.world = world
+        self.bufs = [None] * world
+        self.bar = threading.Barrier(world)
+
+    def exchange_for(self, rank):
+        def ex(buf, chunk, world, stream):
+            assert world == self.world
+            torch.cuda.synchronize()
+            self.bufs[rank] = self.pr.device_f64(buf, chunk * world)
+            self.bar.wait()
+            mine = self.bufs[rank]
+            for r in range(world):
+                if r != rank:
+                    mine[r * chunk:(r + 1) * chunk].copy_(self.bufs[r][r * chunk:(r + 1) * chunk])
+            torch.cuda.synchronize()
+            self.bar.wait()
+        return ex
+
+
+def run_world(pr, n, s, t, world, tau, max_iter=1000, mode=0):
+    """Shard one graph over `world` in-process ranks; returns the assembled
+    ranks, per-rank (status, iters, delta) and shard infos."""
+    graphs = [pr.Graph(n, dev(s), dev(t)) for _ in range(world)]
+    try:
+        for r, g in enumerate(graphs):
+            g.shard(r, world)
+        infos = [g.shard_info() for g in graphs]
+        xs = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(world)]
+        lb = Loopback(pr, world)
+        out = [None] * world
+        errs = []
+
+        def work(r):
+            try:
+                out[r] = graphs[r].run_sharded(xs[r], lb.exchange_for(r), D, tau, max_iter, mode)
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+                lb.bar.abort()
+        ths = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        if errs:
+            raise errs[0]
+        torch.cuda.synchronize()
+        x = torch.stack(xs).sum(0).cpu().numpy()     # the sum all-reduce of the owned parts
+        logs = [g.delta_log() for g in graphs]
+        return x, out, infos, logs
+    finally:
+        for g in graphs:
+            g.close()
+
+
+GRAPHS = {
+    "planted": lambda: G.planted_graph(2, n_base=150, chains=(2, 9, 16, 1)),
+    "random": lambda: (400, G.random_edges(400, 1600, 23)),
+    "in_star": lambda: (300, G.in_star(300)),
+    "out_star": lambda: (64, G.out_star(64)),
+    "path": lambda: (50, G.path(50)),
+    "cycle": lambda: (31, G.cycle(31)),
+    "single": lambda: (1, []),
+    "no_edges": lambda: (9, []),
+}
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+def test_world1_is_sync(pr, name):
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        x0 = torch.empty(n, dtype=torch.float64, device="cuda")
+        ref = g.run(x0, D, 1e-12, 1000)
+        ref_log = g.delta_log()
+    x, out, infos, logs = run_world(pr, n, s, t, 1, 1e-12)
+    assert out[0] == ref
+    assert np.array_equal(x, x0.cpu().numpy())
+    assert np.array_equal(logs[0], ref_log)
+    assert infos[0]["owned_vertices"] == n
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_sharded_matches_oracle(pr, name, world):
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    ref_g = oracle.build_csr(n, s, t)
+    tau = 1e-12
+    ref = oracle.pagerank(ref_g, D, tau, 1000)
+    x, out, infos, logs = run_world(pr, n, s, t, world, tau)
+    assert len({o for o in out}) == 1                    # identical status / iterations / delta on every rank
+    st, it, fd = out[0]
+    assert st == ref.status
+    assert_iters(it, ref, tau)
+    assert_close(x, ref.x)
+    assert sum(i["owned_vertices"] for i in infos) == n
+    assert sum(i["edges"] for i in infos) == ref_g.E
+    assert sum(i["rows"] for i in infos) == int((np.diff(ref_g.row_ptr) > 0).sum())
+    assert all(np.array_equal(lg, logs[0]) for lg in logs)
+
+
+@pytest.mark.parametrize("cfg,world", [(2, 2), (2, 4), (3, 3)])
+def test_sharded_configs(pr, cfg, world):
+    gen = graphgen.make_config(cfg)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    ref = oracle.pagerank(ref_g, gen.d, gen.tau, gen.max_iter)
+    x, out, infos, logs = run_world(pr, gen.n, gen.src, gen.dst, world, gen.tau, gen.max_iter)
+    st, it, fd = out[0]
+    assert st == ref.status
+    assert_iters(it, ref, gen.tau)
+    assert_close(x, ref.x)
+    # nnz balance: no shard gathers more than 1.5x its share of the edges (no mega-hub dominates here)
+    share = ref_g.E / world
+    assert max(i["edges"] for i in infos) <= 1.5 * share + 1
+
+
+def test_sharded_linf_and_max_iter(pr):
+    n = 300
+    s, t = G.edges_to_arrays(G.random_edges(n, 1200, 77))
+    ref_g = oracle.build_csr(n, s, t)
+    x, out, _, _ = run_world(pr, n, s, t, 2, 0.0, max_iter=4)
+    assert out[0][:2] == (pr.PR_NOT_CONVERGED, 4)
+    ref = oracle.pagerank(ref_g, D, 0.0, 4)
+    assert np.abs(x - ref.x).max() <= 1e-14
+    x, out, _, _ = run_world(pr, n, s, t, 2, 1e-14, mode=pr.PR_NORM_LINF)
+    ref = oracle.pagerank(ref_g, D, 1e-14, 1000, norm_linf=True)
+    assert out[0][0] == pr.PR_OK
+    assert_iters(out[0][1], ref, 1e-14, linf=True)
+    assert_close(x, ref.x)
+
+
+def test_shard_validation(pr):
+    n = 50
+    s, t = G.edges_to_arrays(G.random_edges(n, 200, 3))
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        with pytest.raises(pr.PRError) as e:
+            g.run_sharded(x, lambda *a: None)
+        assert e.value.code == pr.PR_ESTATE
+        for rank, world in ((0, 0), (2, 2), (-1, 3), (0, 5000)):
+            with pytest.raises(pr.PRError) as e:
+                g.shard(rank, world)
+            assert e.value.code == pr.PR_EINVAL
+        g.shard(0, 1)
+        with pytest.raises(pr.PRError) as e:
+            g.run_sharded(torch.empty(n, dtype=torch.float64), lambda *a: None)     # host ranks
+        assert e.value.code == pr.PR_EINVAL
+        with pytest.raises(pr.PRError) as e:
+            g.run_sharded(x, lambda *a: None, mode=pr.PR_MODE_ASYNC)
+        assert e.value.code == pr.PR_EINVAL
+
+        def boom(*a):
+            raise RuntimeError("exchange failed")
+        with pytest.raises(RuntimeError, match="exchange failed"):
+            g.run_sharded(x, boom)
+        g.run(x, D, 1e-10, 100)     # the whole-graph path still works after sharding
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_multiprocess(pr, tmp_path, world):
+    """The real multi-process path: torchrun, one process per rank, the
+    torch.distributed exchange (gloo here; every rank on cuda:0 -- the waits
+    are host-side collectives, no kernel waits on another rank)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    out = tmp_path / "shard.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "tests", "shard_worker.py"),
+           "2", str(out)]
+    subprocess.run(cmd, check=True, timeout=600, cwd=root)
+    r = json.load(open(out))
+    ranks = r["ranks"]
+    assert len({(x["st"], x["it"], x["fd"]) for x in ranks}) == 1
+    assert ranks[0]["st"] == r["oracle_status"]
+    it, ref_it = ranks[0]["it"], r["oracle_iters"]
+    if it != ref_it:
+        assert abs(it - ref_it) == 1
+        assert abs(r["oracle_log"][min(it, ref_it) - 1] - 1e-10) <= 1e-9 * 1e-10
+    assert r["max_diff"] <= 1e-10 and r["l1_diff"] <= 1e-9
+    assert sum(x["info"]["owned_vertices"] for x in ranks) == graphgen.make_config(2).n

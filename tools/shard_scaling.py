@@ -1,0 +1,58 @@
+"""Per-rank cost of the row-sharded sweep (pr_run_sharded) on ONE GPU: for each
+world size P, every rank's shard is built and swept alone for a fixed number
+of sweeps with a no-op exchange (its gather + finalize + combine kernels are
+exactly those of a P-GPU run; only the all-gather is missing).  Reports the
+slowest rank's sweep time and the exchanged bytes per sweep, from which the
+P-GPU sweep is projected as compute + all-gather at an assumed NVLink rate.
+Usage: python tools/shard_scaling.py [config] [P ...] > out.json"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import graphgen  # noqa: E402
+import paper_2109_09527_b200 as pr  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+Ps = [int(a) for a in sys.argv[2:]] or [1, 2, 4, 8]
+SWEEPS = 20
+NVLINK_GBS = 700.0   # assumed effective all-gather receive rate per GPU (NVLink 5: 900 GB/s per direction)
+gen = graphgen.make_config(cfg)
+s = torch.from_numpy(gen.src).cuda()
+t = torch.from_numpy(gen.dst).cuda()
+x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+st = torch.cuda.current_stream()
+out = {"config": cfg, "workload": gen.name, "sweeps": SWEEPS, "assumed_allgather_GBs": NVLINK_GBS, "P": {}}
+base = None
+for P in Ps:
+    per = []
+    for r in range(P):
+        with pr.Graph(gen.n, s, t) as g:
+            g.shard(r, P)
+            info = g.shard_info()
+            g.run_sharded(x, lambda *a: None, gen.d, 0.0, 3)   # warm
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            g.run_sharded(x, lambda *a: None, gen.d, 0.0, SWEEPS)
+            b.record(st)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / SWEEPS
+            per.append({"rank": r, "sweep_ms": round(ms, 4), "edges": info["edges"], "rows": info["rows"],
+                        "chunk": info["chunk"]})
+    worst = max(p["sweep_ms"] for p in per)
+    chunk = per[0]["chunk"]
+    recv = (P - 1) * chunk * 8
+    comm_ms = recv / (NVLINK_GBS * 1e9) * 1e3
+    if base is None:
+        base = worst
+    rec = {"ranks": per, "slowest_rank_sweep_ms": worst, "allgather_recv_bytes_per_rank": recv,
+           "projected_sweep_ms_no_overlap": round(worst + comm_ms, 4),
+           "projected_speedup_vs_1gpu": round(base / (worst + comm_ms), 2),
+           "edge_imbalance": round(max(p["edges"] for p in per) / (sum(p["edges"] for p in per) / P), 4)}
+    out["P"][P] = rec
+    print(P, json.dumps(rec)[:300], file=sys.stderr, flush=True)
+print(json.dumps(out))
