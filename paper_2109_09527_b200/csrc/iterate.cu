@@ -868,6 +868,16 @@ static int launch_tasks_t(Ctx& ctx, const View& v, const double* y_in, double* y
     return PR_OK;
 }
 
+// PRGPU_TRACE=<file>: every edge-stream gather launch records per-warp
+// (start, end) globaltimer stamps; run() writes the last launch's to <file>
+// (diagnostics of the tail; tools/trace_tail.py).
+static unsigned long long* g_trace = nullptr;
+static int64_t g_trace_n = 0;
+static const char* trace_path() {
+    const char* e = getenv("PRGPU_TRACE");
+    return (e && *e) ? e : nullptr;
+}
+
 static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_out, double* x, pr_graph* g,
                          double c, double d, const IterArgs& ia, const GatherCfg& gc, int finalize,
                          int64_t span_lo = 0, int64_t span_hi = -1) {
@@ -879,6 +889,7 @@ static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_
                 a.span_lo = span_lo;
                 a.span_hi = span_hi;
             }
+            a.trace = g_trace;
             return a;
         };
         if (v.nseg > 0) {  // source-blocked: S = 0, then one accumulating pass per slot segment
@@ -1105,6 +1116,15 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     const View& gv = K > 1 ? *v.phv : v;
     GatherCfg gc;
     PR_TRY(gather_config(ctx, gv, g, async, &gc, phased));
+    if (trace_path()) {
+        const int64_t nwarps = (int64_t)gc.grid * (gc.nt / 32);
+        if (g_trace_n < nwarps) {
+            if (g_trace) cudaFree(g_trace);
+            PR_CUDA(cudaMalloc(&g_trace, sizeof(unsigned long long) * 2 * (size_t)nwarps));
+            g_trace_n = nwarps;
+        }
+        PR_CUDA(cudaMemsetAsync(g_trace, 0, sizeof(unsigned long long) * 2 * (size_t)g_trace_n, s));
+    }
     const int64_t cap4 = (int64_t)ctx.num_sms * 4;
     // K-FINALIZE (stream path): fixed grid per phase, so each CTA's rows and
     // members (and hence its Delta partial) are a fixed set (deterministic)
@@ -1306,6 +1326,15 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         if (batch < 64) batch *= 2;
     }
     for (auto e : ev) cudaEventDestroy(e);
+    if (const char* tp = trace_path()) {
+        std::vector<unsigned long long> ht(2 * (size_t)g_trace_n);
+        PR_CUDA(cudaMemcpyAsync(ht.data(), g_trace, sizeof(unsigned long long) * ht.size(), cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        if (FILE* f = fopen(tp, "w")) {
+            for (int64_t i = 0; i < g_trace_n; ++i) fprintf(f, "%llu %llu\n", ht[2 * i], ht[2 * i + 1]);
+            fclose(f);
+        }
+    }
     if (gc.stream || gc.inplace) {
         const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
         PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,

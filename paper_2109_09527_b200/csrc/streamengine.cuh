@@ -50,7 +50,14 @@ struct StreamArgs {
     uint32_t* bticket;         // [nbound]
     int64_t span_lo = 0;       // this launch runs spans [span_lo, span_hi) (span_hi < 0: nspans);
     int64_t span_hi = -1;      // PR_MODE_PHASED runs a sweep as several span ranges
+    unsigned long long* trace = nullptr;  // diagnostics (PRGPU_TRACE): per warp (start, end) globaltimer ns
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __device__ __forceinline__ int4 ld_stream_v4(const int32_t* p, uint64_t pol) {
     int4 r;
@@ -214,7 +221,12 @@ __device__ __forceinline__ void stream_run(P& p, const StreamArgs& a) {
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint64_t pol = policy_evict_first();
     const int64_t hi = a.span_hi < 0 ? a.nspans : a.span_hi;
+    const unsigned long long t0 = a.trace ? globaltimer_ns() : 0ull;
     for (int64_t span = a.span_lo + w; span < hi; span += nw) stream_span(p, a, span, pol);
+    if (a.trace && (threadIdx.x & 31) == 0) {
+        a.trace[2 * w] = t0;
+        a.trace[2 * w + 1] = globaltimer_ns();
+    }
 }
 
 }  // namespace prgpu

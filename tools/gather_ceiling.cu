@@ -114,6 +114,132 @@ extern "C" int ceiling_run(const int32_t* col, int64_t E, const double* y, int h
     return (int)cudaGetLastError();
 }
 
+// Cluster / distributed-shared-memory variant: contribs [0, HL) replicated in
+// every CTA's shared memory (LDS); [HL, HL + CL*HD) distributed over the CL
+// CTAs of a thread-block cluster (slot HL + i*CL + r lives in CTA r at HL + i,
+// read with mapa + ld.shared::cluster); [.., tier) L1::evict_last; rest
+// L1::no_allocate.
+__device__ __forceinline__ double ld_dsmem(uint32_t laddr, uint32_t rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(laddr), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra));
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+template <int U, int CL>
+__global__ void __launch_bounds__(1024) k_flat_cl(const int32_t* __restrict__ col, int64_t E,
+                                                 const double* __restrict__ y, int HL, int HD, int tier, double* out) {
+    extern __shared__ double hot[];
+    const uint32_t me = cluster_rank();
+    for (int i = threadIdx.x; i < HL; i += blockDim.x) hot[i] = y[i];
+    for (int i = threadIdx.x; i < HD; i += blockDim.x) hot[HL + i] = y[HL + (int64_t)i * CL + me];
+    cluster_sync_all();
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(hot) + (uint32_t)HL * 8u;
+    const int HT = HL + CL * HD;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    constexpr int CH = 32 * 4 * U;
+    const int64_t nch = E / CH;
+    double acc = 0.0;
+    for (int64_t c = warp; c < nch; c += nwarps) {
+        const int4* p = reinterpret_cast<const int4*>(col + c * CH) + lane;
+        int4 ix[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ix[u] = ldg_stream(p + 32 * u);
+        double v[4 * U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q[4] = {ix[u].x, ix[u].y, ix[u].z, ix[u].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int s = q[j];
+                if (s < HL) {
+                    v[4 * u + j] = hot[s];
+                } else if (s < HT) {
+                    const int t = s - HL;
+                    v[4 * u + j] = ld_dsmem(base + (uint32_t)(t / CL) * 8u, (uint32_t)(t % CL));
+                } else {
+                    v[4 * u + j] = s < tier ? ldg_el(y + s) : ldg_na(y + s);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4 * U; ++k) acc += v[k];
+    }
+    out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+    cluster_sync_all();  // peers may still read this CTA's shared memory
+}
+
+extern "C" int ceiling_cluster(const int32_t* col, int64_t E, const double* y, int HL, int HD, int cl, int tier,
+                               int reps, double* out, float* ms_out, int* grid_out) {
+    const size_t smem = (size_t)(HL + HD) * 8;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const void* fn = nullptr;
+    switch (cl) {
+        case 1: fn = (const void*)k_flat_cl<4, 1>; break;
+        case 2: fn = (const void*)k_flat_cl<4, 2>; break;
+        case 4: fn = (const void*)k_flat_cl<4, 4>; break;
+        case 8: fn = (const void*)k_flat_cl<4, 8>; break;
+        default: return -1;
+    }
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cfg.gridDim = dim3(cl);
+    int nclusters = 0;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
+    if (e != cudaSuccess || nclusters < 1) {
+        fprintf(stderr, "occupancy: %s (%d)\n", cudaGetErrorString(e), nclusters);
+        return -2;
+    }
+    cfg.gridDim = dim3(nclusters * cl);
+    *grid_out = nclusters * cl;
+    auto launch = [&]() {
+        switch (cl) {
+            case 1: cudaLaunchKernelEx(&cfg, k_flat_cl<4, 1>, col, E, y, HL, HD, tier, out); break;
+            case 2: cudaLaunchKernelEx(&cfg, k_flat_cl<4, 2>, col, E, y, HL, HD, tier, out); break;
+            case 4: cudaLaunchKernelEx(&cfg, k_flat_cl<4, 4>, col, E, y, HL, HD, tier, out); break;
+            case 8: cudaLaunchKernelEx(&cfg, k_flat_cl<4, 8>, col, E, y, HL, HD, tier, out); break;
+        }
+    };
+    launch();
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "cluster kernel: %s\n", cudaGetErrorString(e));
+        return -3;
+    }
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return (int)cudaGetLastError();
+}
+
 // TMA gather4 variant: y viewed as a 2D tensor [ceil(nsrc/2)][2] of fp64 (16 B
 // rows); each lane issues one cp.async.bulk.tensor ... tile::gather4 for its
 // 4 indices (4 rows x 16 B -> 64 B of shared memory), S stages per warp.

@@ -26,7 +26,12 @@ lib.ceiling_tma.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ct
 lib.ceiling_run.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]
 
+lib.ceiling_cluster.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int)]
+
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+which = sys.argv[2] if len(sys.argv) > 2 else "all"
 gen = graphgen.make_config(cfg)
 dev = torch.device("cuda:0")
 s = torch.from_numpy(gen.src).to(dev)
@@ -90,7 +95,30 @@ def run(colv, hot, unroll, cps, label, threads=256, tier=0):
           f"{gps * 1e9 / (sms * clk):.3f} gathers/SM/cycle@1965MHz", flush=True)
 
 
+def run_cluster(colv, HL, HD, cl, tier=0, label="skewed + cluster DSMEM tier"):
+    ms = ctypes.c_float()
+    grid = ctypes.c_int()
+    out.zero_()
+    E4 = colv.numel() // 512 * 512
+    rc = lib.ceiling_cluster(colv.data_ptr(), E4, y.data_ptr(), HL, HD, cl, tier, 10, out.data_ptr(),
+                             ctypes.byref(ms), ctypes.byref(grid))
+    assert rc == 0, rc
+    gps = E4 / (ms.value * 1e-3) / 1e9
+    print(f"{label:38s} CL={cl} HL={HL:6d} HD={HD:6d} (on-chip {HL + cl * HD:7d}) tier={tier} grid={grid.value}: "
+          f"{ms.value:.4f} ms  {gps:7.1f} G gathers/s  {gps * 1e9 / (sms * clk):.3f} gathers/SM/cycle@1965MHz", flush=True)
+
+
 print(f"{gen.name}: n={n} E={E} sources={nsrc}")
+if which == "cluster":
+    run(col, 16384, 4, 1, "skewed + hot smem + L1 tier (current)", threads=1024, tier=32768)
+    for cl, HL, HD, tier in ((1, 16384, 0, 32768), (2, 16384, 12288, 0), (2, 16384, 12288, 65536),
+                             (2, 8192, 20480, 0), (2, 0, 28672, 0), (4, 16384, 12288, 0), (4, 8192, 20480, 0),
+                             (4, 0, 28672, 0), (8, 8192, 20480, 0), (8, 0, 28672, 0)):
+        try:
+            run_cluster(col, HL, HD, cl, tier)
+        except AssertionError as e:
+            print("cluster variant failed", cl, HL, HD, e, flush=True)
+    sys.exit(0)
 for mb in (4, 8, 16, 24, 32, 48, 64, 96):
     slots = mb * (1 << 20) // 8
     u = torch.randint(0, min(slots, nsrc), (E,), dtype=torch.int32, device=dev)
