@@ -80,9 +80,16 @@ __global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict_
                                                      const int64_t* __restrict__ partial,
                                                      const int64_t* __restrict__ total, int32_t* __restrict__ col,
                                                      int64_t* __restrict__ row_ptr) {
+    // striped: in stripe j, thread t handles tile item j*UQ_NT + t (conflict-
+    // free shared-memory reads, adjacent lanes write adjacent row_ptr
+    // entries); the output rank of a kept key = the kept count of the earlier
+    // (stripe, warp) groups + its rank in the warp's ballot
+    constexpr int NW = UQ_NT / 32;
     __shared__ uint64_t sk[UQ_TILE + 1];
     __shared__ int32_t so[UQ_TILE];
-    __shared__ int64_t sw[33];
+    __shared__ int32_t woff[UQ_IPT * NW + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = lanemask_lt();
     const uint64_t mask = (1ull << b) - 1;
     const int64_t cb = (int64_t)blockIdx.x * per_cta;
     const int64_t ce = min(n, cb + per_cta);
@@ -93,40 +100,60 @@ __global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict_
         for (int i = threadIdx.x; i < tn; i += UQ_NT) sk[i + 1] = k[tb + i];
         if (threadIdx.x == 0) sk[0] = tb > 0 ? k[tb - 1] : ~0ull;
         __syncthreads();
-        // blocked: thread t owns tile items [t*IPT, t*IPT + IPT)
-        const int j0 = threadIdx.x * UQ_IPT;
-        uint32_t keep = 0;
-        int cnt = 0;
+        uint32_t bal[UQ_IPT];
 #pragma unroll
         for (int j = 0; j < UQ_IPT; ++j) {
-            const int i = j0 + j;
+            const int i = j * UQ_NT + threadIdx.x;
+            bool kp = false;
             if (i < tn) {
                 const uint64_t key = sk[i + 1];
-                const bool kp = key != sentinel && (tb + i == 0 || key != sk[i]);
-                keep |= (uint32_t)kp << j;
-                cnt += kp;
+                kp = key != sentinel && (tb + i == 0 || key != sk[i]);
             }
+            bal[j] = __ballot_sync(0xffffffffu, kp);
+            if (lane == 0) woff[j * NW + warp] = __popc(bal[j]);
         }
-        int64_t tile_tot;
-        const int64_t off = block_exclusive_sum((int64_t)cnt, &tile_tot, sw);
-        int64_t q = off;
+        __syncthreads();
+        if (warp == 0) {  // exclusive scan of the UQ_IPT * NW group counts (stripe-major = tile order)
+            constexpr int G = UQ_IPT * NW;
+            constexpr int PER = (G + 31) / 32;
+            int v[PER], run = 0;
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int gi = lane * PER + u;
+                v[u] = gi < G ? woff[gi] : 0;
+                run += v[u];
+            }
+            int incl = run;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += t;
+            }
+            int ex = incl - run;
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int gi = lane * PER + u;
+                if (gi < G) woff[gi] = ex;
+                ex += v[u];
+            }
+            if (lane == 31) woff[G] = incl;
+        }
+        __syncthreads();
+        const int tile_tot = woff[UQ_IPT * NW];
 #pragma unroll
         for (int j = 0; j < UQ_IPT; ++j) {
-            if (keep & (1u << j)) {
-                const int i = j0 + j;
+            const int i = j * UQ_NT + threadIdx.x;
+            if (bal[j] & (1u << lane)) {
+                const int q = woff[j * NW + warp] + __popc(bal[j] & lt);
                 const uint64_t key = sk[i + 1];
                 so[q] = (int32_t)(key & mask);
                 const int64_t d = (int64_t)(key >> b);
                 const int64_t dp = (tb + i == 0) ? -1 : (int64_t)(sk[i] >> b);
                 const int64_t p = base + q;
                 for (int64_t r = dp + 1; r <= d; ++r) row_ptr[r] = p;   // first edge of row d
-                ++q;
             }
-        }
-#pragma unroll
-        for (int j = 0; j < UQ_IPT; ++j) {  // the last real key (kept or a duplicate) closes every later row
-            const int i = j0 + j;
-            if (i < tn) {
+            if (i < tn) {  // the last real key (kept or a duplicate) closes every later row
                 const uint64_t key = sk[i + 1];
                 if (key != sentinel &&
                     (tb + i + 1 == n || (i + 1 < tn ? sk[i + 2] : k[tb + i + 1]) == sentinel))
@@ -134,7 +161,7 @@ __global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict_
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < (int)tile_tot; i += UQ_NT) col[base + i] = so[i];
+        for (int i = threadIdx.x; i < tile_tot; i += UQ_NT) col[base + i] = so[i];
         base += tile_tot;
         __syncthreads();
     }
@@ -185,7 +212,9 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
         bool alt = false;
         PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, 2 * b, &alt)));
         const uint64_t* sorted = alt ? keys_alt : keys;
-        int64_t G = std::min<int64_t>((mk + UQ_TILE - 1) / UQ_TILE, (int64_t)ctx.num_sms * 4);
+        int uq_occ = 0;  // every CTA of the emit pass resident (fixed chunks: no second wave)
+        PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uq_occ, k_uniq_emit, UQ_NT, 0));
+        int64_t G = std::min<int64_t>((mk + UQ_TILE - 1) / UQ_TILE, (int64_t)ctx.num_sms * std::max(1, uq_occ));
         int64_t per = (mk + G - 1) / G;
         per = (per + UQ_TILE - 1) / UQ_TILE * UQ_TILE;
         G = (mk + per - 1) / per;
