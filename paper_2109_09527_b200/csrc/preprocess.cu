@@ -136,19 +136,31 @@ struct ListEmit {
     }
 };
 
-__global__ void k_chain_init(const int32_t* __restrict__ cl, int64_t C, const int64_t* __restrict__ rp,
+// Serial walk first: every chain vertex follows its pred links for up to
+// CH_WALK steps (R-MAT / config-3 chains are short, so nearly all reach their
+// head here); the pointer and distance it stops at are a valid list-ranking
+// state, so pointer jumping only runs if some vertex did not resolve (long
+// chains, pure cycles) -- flagged in *unresolved.
+constexpr int CH_WALK = 64;
+__global__ void k_chain_walk(const int32_t* __restrict__ cl, int64_t C, const int64_t* __restrict__ rp,
                              const int32_t* __restrict__ col, const int32_t* __restrict__ od,
-                             int32_t* __restrict__ nxt, int32_t* __restrict__ dist) {
+                             int32_t* __restrict__ nxt, int32_t* __restrict__ dist, int* __restrict__ unresolved) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < C; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = cl[i];
-        const int32_t p = col[rp[v]];
-        if (is_chain(rp, od, p)) {
-            nxt[v] = p;
-            dist[v] = 1;
-        } else {
-            nxt[v] = v;  // head: root of its list
-            dist[v] = 0;
+        int32_t u = v;
+        int d = 0;
+        bool head = false;
+        for (; d < CH_WALK; ++d) {
+            const int32_t p = col[rp[u]];
+            if (!is_chain(rp, od, p)) {
+                head = true;
+                break;
+            }
+            u = p;
         }
+        nxt[v] = u;
+        dist[v] = d;
+        if (!head) atomicOr(unresolved, 1);
     }
 }
 
@@ -398,9 +410,13 @@ static int find_chains(pr_graph* g, Ctx& ctx) {
         PR_TRY(dalloc(&dist, (size_t)n, s));
         PR_TRY(dalloc(&nxt2, (size_t)n, s));
         PR_TRY(dalloc(&dist2, (size_t)n, s));
-        PR_LAUNCH(ctx, k_chain_init, grid_of(ctx, C), 256, 0, (const int32_t*)cl, C, (const int64_t*)g->row_ptr,
-                  (const int32_t*)g->col, (const int32_t*)g->outdeg, nxt, dist);
-        const int rounds = bits_for((uint64_t)C) + 1;  // ceil(log2 C) + 1 >= enough for any path
+        PR_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t), s));
+        PR_LAUNCH(ctx, k_chain_walk, grid_of(ctx, C), 256, 0, (const int32_t*)cl, C, (const int64_t*)g->row_ptr,
+                  (const int32_t*)g->col, (const int32_t*)g->outdeg, nxt, dist, (int*)cnt);
+        int64_t unresolved = 0;
+        PR_TRY(read_count(ctx, cnt, &unresolved));
+        // ceil(log2 C) + 1 doublings suffice for any path (the walk only shortens them)
+        const int rounds = unresolved ? bits_for((uint64_t)C) + 1 : 0;
         for (int r = 0; r < rounds; ++r) {
             PR_LAUNCH(ctx, k_chain_jump, grid_of(ctx, C), 256, 0, (const int32_t*)cl, C, (const int32_t*)nxt,
                       (const int32_t*)dist, nxt2, dist2);

@@ -130,6 +130,8 @@ HAND = {
     "in_star": (50, G.in_star(50)),
     "out_star": (50, G.out_star(50)),
     "path": (40, G.path(40)),
+    "long_path": (300, G.path(300)),      # chain longer than the 64-link serial walk: pointer jumping resumes
+    "cycle_tail": (90, G.cycle(20) + [(i, i + 1) for i in range(19, 89)]),   # 68-long chain off a cycle
     "complete": (12, G.complete(12)),
     "no_edges": (7, []),
     "loops_only": (5, [(i, i) for i in range(5)] * 3),
