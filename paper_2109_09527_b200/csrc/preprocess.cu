@@ -264,23 +264,31 @@ __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const i
                 hi = mid;
         }
         // rows of the chunk, 32 at a time: every lane fetches one row's
-        // (output start, source start) so the row walk has no dependent loads
+        // (output start, source - output offset); then the batch's output
+        // range is copied element-parallel (lane k finds its row among the 32
+        // by a shuffle binary search), so short rows do not idle the warp and
+        // both the loads and the stores stay coalesced
         int64_t i0 = lo, o = o0;
         while (o < o1) {
             const int64_t ri = i0 + lane;
-            int64_t ostart = 0, sstart = 0;
+            int64_t ostart = ER, delta = 0;
             if (ri < nr) {
                 ostart = rpR[ri];
-                sstart = rp[vid[ri]];
+                delta = rp[vid[ri]] - ostart;
             }
-            for (int q = 0; q < 32 && o < o1; ++q) {
-                const int64_t os = __shfl_sync(0xffffffffu, ostart, q);
-                const int64_t ss = __shfl_sync(0xffffffffu, sstart, q);
-                const int64_t oe = min(o1, (i0 + q + 1 < nr) ? __shfl_sync(0xffffffffu, ostart, (q + 1) & 31) : ER);
-                const int64_t re = (q == 31) ? min(o1, (i0 + 32 < nr) ? rpR[i0 + 32] : ER) : oe;
-                for (int64_t k = o + lane; k < re; k += 32) colR[k] = col[ss + (k - os)];
-                o = re;
+            const int64_t bend = min(o1, (i0 + 32 < nr) ? rpR[i0 + 32] : ER);
+            for (int64_t b0 = o; b0 < bend; b0 += 32) {
+                const int64_t k = b0 + lane;
+                int q = 0;
+#pragma unroll
+                for (int st = 16; st; st >>= 1) {
+                    const int64_t v = __shfl_sync(0xffffffffu, ostart, q + st);
+                    if (v <= k) q += st;
+                }
+                const int64_t dq = __shfl_sync(0xffffffffu, delta, q);
+                if (k < bend) colR[k] = col[k + dq];
             }
+            o = bend;
             i0 += 32;
         }
     }
