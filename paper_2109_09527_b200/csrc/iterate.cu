@@ -1978,7 +1978,7 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
         PR_TRY(read_count(ctx, tot, &B.v.nedges));
         PR_TRY(dalloc(&B.v.col, (size_t)stream_pad(B.v.nedges), s));
         if (nr > 0)
-            PR_LAUNCH(ctx, k_copy_rows, (unsigned)std::min<int64_t>((B.v.nedges + 1023) / 1024 / 8 + 1, cap4 * 4), 256,
+            PR_LAUNCH(ctx, k_copy_rows, (unsigned)std::min<int64_t>((B.v.nedges + 1023) / 1024 / 8 + 1, cap4 * 2), 256,
                       0, (const int32_t*)src_row, nr, (const int64_t*)A.v.row_ptr, (const int32_t*)A.v.col,
                       (const int64_t*)B.v.row_ptr, B.v.col);
         PR_TRY(build_view_stream(B.v, ctx, (int32_t)g->n_contrib, nullptr, nullptr));

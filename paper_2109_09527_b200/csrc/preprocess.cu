@@ -243,18 +243,21 @@ struct PosEmit {
 };
 
 // Reduced view col: rows vid[i] of the plain view's col, packed at rpR[i].
-// Edge-parallel: every warp copies a fixed 1024-edge range of the OUTPUT
-// (binary search for its first row, then row segment by row segment), so a
-// mega-hub row is spread over many warps instead of serialising one.
-constexpr int CR_CHUNK = 1024;
+// Edge-parallel: every warp copies a fixed range of the OUTPUT (binary search
+// for its first row, then batches of 32 rows), so a mega-hub row is spread
+// over many warps instead of serialising one.
 __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const int64_t* __restrict__ rp,
                             const int32_t* __restrict__ col, const int64_t* __restrict__ rpR, int32_t* __restrict__ colR) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t ER = rpR[nr];
-    for (int64_t o0 = w0 * CR_CHUNK; o0 < ER; o0 += nw * CR_CHUNK) {
-        const int64_t o1 = min(ER, o0 + CR_CHUNK);
+    // one contiguous output range per warp: a single binary search, then the
+    // row walk carries over (a search per 1024-edge chunk was the bottleneck:
+    // ~23 dependent loads each)
+    const int64_t per = ((ER + nw - 1) / nw + 31) / 32 * 32;
+    for (int64_t o0 = w0 * per; o0 < ER; o0 += nw * per) {
+        const int64_t o1 = min(ER, o0 + per);
         int64_t lo = 0, hi = nr;  // last row i with rpR[i] <= o0
         while (hi - lo > 1) {
             const int64_t mid = (lo + hi) >> 1;
@@ -269,27 +272,42 @@ __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const i
         // by a shuffle binary search), so short rows do not idle the warp and
         // both the loads and the stores stay coalesced
         int64_t i0 = lo, o = o0;
+        int64_t ostart = ER, delta = 0;
+        if (i0 + lane < nr) {
+            ostart = rpR[i0 + lane];
+            delta = rp[vid[i0 + lane]] - ostart;
+        }
         while (o < o1) {
-            const int64_t ri = i0 + lane;
-            int64_t ostart = ER, delta = 0;
-            if (ri < nr) {
-                ostart = rpR[ri];
-                delta = rp[vid[ri]] - ostart;
-            }
-            const int64_t bend = min(o1, (i0 + 32 < nr) ? rpR[i0 + 32] : ER);
-            for (int64_t b0 = o; b0 < bend; b0 += 32) {
-                const int64_t k = b0 + lane;
-                int q = 0;
+            // the next batch's row metadata is loaded while this one is copied
+            const int64_t rn = i0 + 32 + lane;
+            const int64_t nos = rn < nr ? rpR[rn] : ER;
+            const int32_t nvid = rn < nr ? vid[rn] : 0;
+            const int64_t bend = min(o1, __shfl_sync(0xffffffffu, nos, 0));
+            constexpr int CU = 8;  // 8 independent loads in flight per lane
+            for (int64_t b0 = o; b0 < bend; b0 += 32 * CU) {
+                int32_t val[CU];
 #pragma unroll
-                for (int st = 16; st; st >>= 1) {
-                    const int64_t v = __shfl_sync(0xffffffffu, ostart, q + st);
-                    if (v <= k) q += st;
+                for (int u = 0; u < CU; ++u) {
+                    const int64_t k = b0 + u * 32 + lane;
+                    int q = 0;
+#pragma unroll
+                    for (int st = 16; st; st >>= 1) {
+                        const int64_t v = __shfl_sync(0xffffffffu, ostart, q + st);
+                        if (v <= k) q += st;
+                    }
+                    const int64_t dq = __shfl_sync(0xffffffffu, delta, q);
+                    val[u] = k < bend ? __ldg(col + k + dq) : 0;
                 }
-                const int64_t dq = __shfl_sync(0xffffffffu, delta, q);
-                if (k < bend) colR[k] = col[k + dq];
+#pragma unroll
+                for (int u = 0; u < CU; ++u) {
+                    const int64_t k = b0 + u * 32 + lane;
+                    if (k < bend) colR[k] = val[u];
+                }
             }
             o = bend;
             i0 += 32;
+            ostart = nos;
+            delta = rn < nr ? rp[nvid] - nos : 0;
         }
     }
 }
@@ -498,7 +516,8 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
     PR_TRY(read_count(ctx, cnt, &R.nedges));
     PR_TRY(dalloc(&R.col, (size_t)stream_pad(R.nedges), s));
     if (R.nrows > 0)
-        PR_LAUNCH(ctx, k_copy_rows, grid_of(ctx, R.nrows * 32), 256, 0, (const int32_t*)R.vid, R.nrows,
+        PR_LAUNCH(ctx, k_copy_rows, std::min<unsigned>(grid_of(ctx, R.nrows * 32), (unsigned)ctx.num_sms * 8), 256, 0,
+                  (const int32_t*)R.vid, R.nrows,
                   (const int64_t*)g->row_ptr, (const int32_t*)g->plain.col, (const int64_t*)R.row_ptr, R.col);
     PR_TRY(build_view_stream(R, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx));
     PR_TRY(build_view_blocked(R, ctx, g->n_contrib));

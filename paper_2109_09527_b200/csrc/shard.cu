@@ -183,7 +183,7 @@ int build_shard(pr_graph* g, int rank, int world, Ctx& ctx) {
     PR_TRY(dalloc(&S.col, (size_t)stream_pad(S.nedges), s));
     if (S.nrows > 0) {
         const unsigned gc = (unsigned)std::max<int64_t>(
-            1, std::min<int64_t>((S.nedges + 1023) / 1024 * 32 / 256 + 1, (int64_t)ctx.num_sms * 16));
+            1, std::min<int64_t>((S.nedges + 1023) / 1024 * 32 / 256 + 1, (int64_t)ctx.num_sms * 8));
         PR_LAUNCH(ctx, k_copy_rows, gc, 256, 0, (const int32_t*)S.vid, S.nrows, (const int64_t*)g->row_ptr,
                   (const int32_t*)g->plain.col, (const int64_t*)S.row_ptr, S.col);
         PR_LAUNCH(ctx, k_sh_map_col, sh_grid(ctx, S.nedges), 256, 0, S.col, S.nedges, (const int32_t*)smap);
