@@ -48,6 +48,29 @@ __global__ void k_outdeg(const int32_t* __restrict__ col, int64_t E, int32_t* __
         atomicAdd(&outdeg[col[e]], 1);
 }
 
+// outdeg without per-edge atomics: after the LSD passes over the src bits
+// alone, the keys are grouped by src; a run [s, e) of source v adds e - s
+// (two modular atomics per run: -s at its start, +e at its end).  Self-loop /
+// sentinel keys (all 2b bits set) fall in the run of src = 2^b - 1 and are
+// subtracted when that is a vertex; duplicates are subtracted by k_uniq_emit.
+__global__ void k_src_runs(const uint64_t* __restrict__ k, int64_t m, int b, uint64_t sentinel, int64_t n,
+                           int32_t* __restrict__ outdeg) {
+    const uint64_t maskb = (1ull << b) - 1;
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += T) {
+        const uint64_t key = k[i];
+        const int64_t v = (int64_t)(key & maskb);
+        const bool sent = key == sentinel;
+        if (v < n) {
+            unsigned* o = reinterpret_cast<unsigned*>(outdeg + v);
+            if (i == 0 || (k[i - 1] & maskb) != (uint64_t)v) atomicAdd(o, (unsigned)(-(int64_t)i));
+            if (i == m - 1 || (k[i + 1] & maskb) != (uint64_t)v) atomicAdd(o, (unsigned)(i + 1));
+        }
+        const unsigned ns = __ballot_sync(__activemask(), sent && v < n);
+        if (ns && (threadIdx.x & 31) == __ffs(ns) - 1) atomicSub(reinterpret_cast<unsigned*>(outdeg + v), __popc(ns));
+    }
+}
+
 // ---- dedup + CSR in one pass over the sorted keys --------------------------
 // Key i is kept iff it is not the sentinel and differs from key i-1.
 // Kept key i lands at p = its rank among kept keys: col[p] = src; and when it
@@ -79,7 +102,7 @@ __global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict_
                                                      uint64_t sentinel, int b, int64_t nv,
                                                      const int64_t* __restrict__ partial,
                                                      const int64_t* __restrict__ total, int32_t* __restrict__ col,
-                                                     int64_t* __restrict__ row_ptr) {
+                                                     int64_t* __restrict__ row_ptr, int32_t* __restrict__ od_dup) {
     // striped: in stripe j, thread t handles tile item j*UQ_NT + t (conflict-
     // free shared-memory reads, adjacent lanes write adjacent row_ptr
     // entries); the output rank of a kept key = the kept count of the earlier
@@ -111,6 +134,8 @@ __global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict_
             }
             bal[j] = __ballot_sync(0xffffffffu, kp);
             if (lane == 0) woff[j * NW + warp] = __popc(bal[j]);
+            if (od_dup && i < tn && !kp && sk[i + 1] != sentinel)  // a duplicate: outdeg counted it once too often
+                atomicSub(od_dup + (sk[i + 1] & mask), 1);
         }
         __syncthreads();
         if (warp == 0) {  // exclusive scan of the UQ_IPT * NW group counts (stripe-major = tile order)
@@ -198,6 +223,7 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
     PR_CUDA(cudaMemsetAsync(scratch, 0, 2 * sizeof(int64_t), s));
     // n == 1 (b == 0): every edge is a self-loop, nothing to sort
     const int64_t mk = b > 0 ? m : 0;
+    bool od_runs = false;  // outdeg counted from the src runs of the partial sort
     const uint64_t sentinel = b > 0 ? ((2 * b >= 64) ? ~0ull : ((1ull << (2 * b)) - 1)) : 0ull;
 
     // pack, sort by (dst, src), deduplicate + CSR (row_ptr, col_idx) in one pass
@@ -209,9 +235,26 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
         PR_LAUNCH(ctx, k_pack, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, sentinel, keys,
                   (int*)(scratch + 1));
         PR_TRY(dalloc(&keys_alt, (size_t)mk, s));
-        bool alt = false;
-        PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, 2 * b, &alt)));
-        const uint64_t* sorted = alt ? keys_alt : keys;
+        PR_TRY(dalloc(&g->outdeg, (size_t)n, s));
+        PR_CUDA(cudaMemsetAsync(g->outdeg, 0, sizeof(int32_t) * (size_t)n, s));
+        // sort the src bits, count the src runs (outdeg), then the dst bits --
+        // when splitting costs no extra radix pass; else one sort and atomics
+        od_runs = b >= 8 && 2 * ((b + RS_BITS - 1) / RS_BITS) == (2 * b + RS_BITS - 1) / RS_BITS;
+        const uint64_t* sorted = nullptr;
+        if (od_runs) {
+            bool a1 = false, a2 = false;
+            PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, b, &a1)));
+            uint64_t* cur = a1 ? keys_alt : keys;
+            uint64_t* oth = a1 ? keys : keys_alt;
+            PR_LAUNCH(ctx, k_src_runs, grid_for(ctx, mk, 256), 256, 0, (const uint64_t*)cur, mk, b, sentinel, n,
+                      g->outdeg);
+            PR_TRY((radix_sort<uint64_t, false>(ctx, cur, oth, nullptr, nullptr, mk, b, 2 * b, &a2)));
+            sorted = a2 ? oth : cur;
+        } else {
+            bool alt = false;
+            PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, 2 * b, &alt)));
+            sorted = alt ? keys_alt : keys;
+        }
         int uq_occ = 0;  // every CTA of the emit pass resident (fixed chunks: no second wave)
         PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&uq_occ, k_uniq_emit, UQ_NT, 0));
         int64_t G = std::min<int64_t>((mk + UQ_TILE - 1) / UQ_TILE, (int64_t)ctx.num_sms * std::max(1, uq_occ));
@@ -223,7 +266,7 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
         PR_LAUNCH(ctx, k_uniq_count, (unsigned)G, UQ_NT, 0, sorted, mk, per, sentinel, part);
         PR_LAUNCH(ctx, (k_scan_partials<int64_t>), 1, 1024, 0, part, G, scratch);
         PR_LAUNCH(ctx, k_uniq_emit, (unsigned)G, UQ_NT, 0, sorted, mk, per, sentinel, b, n, (const int64_t*)part,
-                  (const int64_t*)scratch, g->col, g->row_ptr);
+                  (const int64_t*)scratch, g->col, g->row_ptr, od_runs ? g->outdeg : nullptr);
         dfree(part, s);
         dfree(keys, s);
         dfree(keys_alt, s);
@@ -240,10 +283,12 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
     }
     g->E = h[0];
 
-    // outdeg from the sources of the deduplicated edges
-    PR_TRY(dalloc(&g->outdeg, (size_t)n, s));
-    PR_CUDA(cudaMemsetAsync(g->outdeg, 0, sizeof(int32_t) * (size_t)n, s));
-    if (g->E > 0)
+    // outdeg from the sources of the deduplicated edges (unless the src runs gave it)
+    if (!g->outdeg) {
+        PR_TRY(dalloc(&g->outdeg, (size_t)n, s));
+        PR_CUDA(cudaMemsetAsync(g->outdeg, 0, sizeof(int32_t) * (size_t)n, s));
+    }
+    if (g->E > 0 && !od_runs)
         PR_LAUNCH(ctx, k_outdeg, grid_for(ctx, g->E, 256), 256, 0, (const int32_t*)g->col, g->E, g->outdeg);
     dfree(scratch, s);
     return PR_OK;

@@ -306,3 +306,25 @@ def test_config3_async(pr):
     ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
     with gpu_graph(pr, gen.n, gen.src, gen.dst) as g:
         check_async(pr, g, ref_g, gen.n, gen.tau)
+
+
+@pytest.mark.parametrize("n", [256, 300, 1 << 16])
+def test_outdeg_split_sort_edge_cases(pr, n):
+    """Ingest counts outdeg from the src runs of a partial sort when that costs
+    no extra radix pass (b = 8, 16, 24, ...; n = 300 has b = 9 and takes the
+    atomic path): self-loops and duplicates on the LAST vertex (whose src bits
+    equal the sentinel's when n = 2^b) must not be counted."""
+    rng = np.random.default_rng(n)
+    m = 20 * n
+    s = rng.integers(0, n, m, dtype=np.int64)
+    t = rng.integers(0, n, m, dtype=np.int64)
+    last = n - 1
+    extra_s = np.array([last] * 40 + [last] * 30 + [0] * 5, np.int64)
+    extra_t = np.array([last] * 40 + [3] * 30 + [0] * 5, np.int64)        # self-loops, duplicates
+    s = np.concatenate([s, extra_s]).astype(np.int32)
+    t = np.concatenate([t, extra_t]).astype(np.int32)
+    ref_g = oracle.build_csr(n, s, t)
+    with gpu_graph(pr, n, s, t) as g:
+        rp, col, od = gpu_csr(pr, g, n, ref_g.E)
+        assert np.array_equal(od, ref_g.outdeg)
+        assert np.array_equal(rp, ref_g.row_ptr) and np.array_equal(col, ref_g.col_idx)
