@@ -57,7 +57,8 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
 #define PR_NORM_LINF      2u  /* stop when max_v |x_t(v)-x_{t-1}(v)| <= threshold */
 #define PR_USE_REDUCTIONS 4u  /* compute one vertex per identical group, resolve chain
                                  members from their head; needs pr_preprocess */
-#define PR_TIMING         8u  /* record CUDA events around every gather launch (bench) */
+#define PR_TIMING         8u  /* record CUDA events around the gather / finalize launches of
+                                 every 4th sweep (PRGPU_TIMING_STRIDE; bench roofline) */
 #define PR_MODE_NOSYNC   16u  /* persistent barrier-free No-Sync kernel with thread-level
                                  (here: CTA-level) convergence (Alg.3 P:535-565, P:416-418;
                                  SURVEY f1): one launch, every CTA sweeps its own static work

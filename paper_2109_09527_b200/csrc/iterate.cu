@@ -1086,6 +1086,9 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     const bool phased = (mode & PR_MODE_PHASED) != 0;
     const bool reduced = (mode & PR_USE_REDUCTIONS) != 0;
     const bool timing = (mode & PR_TIMING) != 0;
+    // PR_TIMING brackets every tstride-th sweep's launches with events (each
+    // event pair also blocks the programmatic launch overlap of its sweep)
+    const int tstride = std::max(1, env_int("PRGPU_TIMING_STRIDE", 4));
     const int64_t n = g->n;
     const View& v = reduced ? g->reduced : g->plain;
     const int64_t nm = reduced ? g->n_members : 0;
@@ -1235,7 +1238,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
             if (it == 0 && zgrid > 0 && !phased)
                 PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, zper, c, x, y_out,
                           (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
-            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
+            if (timing && it % tstride == tstride - 1) PR_CUDA(cudaEventRecord(ev[4 * j], s));
             if (phased) {
                 // in place, phase by phase: the gather of phase k reads the
                 // contribs phases 0..k-1 of this sweep wrote (block Gauss-Seidel)
@@ -1279,7 +1282,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
             } else {
                 PR_TRY(launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, gather_finalizes));
             }
-            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
+            if (timing && it % tstride == tstride - 1) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
             if (phased) {
                 // the whole sweep is timed as gather_ms
             } else if (gc.fused) {
@@ -1301,7 +1304,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                               (const int32_t*)g->mem_src, (const int32_t*)g->mem_k, nm, sper, (const double*)g->ab, x,
                               y_out, (const int32_t*)g->outdeg, (const int32_t*)g->cidx, ia);
             }
-            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
+            if (timing && it % tstride == tstride - 1) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
             if (it == 0 && nz > 0 && !async && !phased)
                 PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256,
                           0, (const int32_t*)g->zlist, nz, c, (double*)y_in, (const int32_t*)g->outdeg,
@@ -1313,6 +1316,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         if (timing) {
             for (int j = 0; j < nb; ++j) {
                 if (launched + j >= hs->iters) break;
+                if ((launched + j) % tstride != tstride - 1) continue;
                 float a = 0.f, b2 = 0.f;
                 PR_CUDA(cudaEventElapsedTime(&a, ev[4 * j], ev[4 * j + 1]));
                 PR_CUDA(cudaEventElapsedTime(&b2, ev[4 * j + 1], ev[4 * j + 2]));
@@ -1398,6 +1402,9 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
                 pr_exchange_fn exchange, void* exchange_ctx, int32_t* iters_out, double* delta_out) {
     cudaStream_t s = ctx.stream;
     const bool timing = (mode & PR_TIMING) != 0;
+    // PR_TIMING brackets every tstride-th sweep's launches with events (each
+    // event pair also blocks the programmatic launch overlap of its sweep)
+    const int tstride = std::max(1, env_int("PRGPU_TIMING_STRIDE", 4));
     const int64_t n = g->n;
     const View& v = g->shard;
     const int world = g->shard_world, rank = g->shard_rank;
@@ -1481,13 +1488,13 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
             if (it == 0 && zgrid > 0)
                 PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->szlist, nz, zper, c, x, y_out,
                           (const int32_t*)g->outdeg, (const int32_t*)g->scidx, zero_partial);
-            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j], s));
+            if (timing && it % tstride == tstride - 1) PR_CUDA(cudaEventRecord(ev[4 * j], s));
             if (v.nrows > 0) PR_TRY(launch_gather(ctx, v, y_in, y_out, x, g, c, d, ia, gc, 0));
-            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
+            if (timing && it % tstride == tstride - 1) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
             FinArgs f = fa;
             f.y_out = y_out;
             PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
-            if (timing) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
+            if (timing && it % tstride == tstride - 1) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
             if (it == 0 && nz > 0)
                 PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256,
                           0, (const int32_t*)g->szlist, nz, c, y_in, (const int32_t*)g->outdeg,
@@ -1505,6 +1512,7 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
         if (timing) {
             for (int j = 0; j < nb; ++j) {
                 if (launched + j >= hs->iters) break;
+                if ((launched + j) % tstride != tstride - 1) continue;
                 float a = 0.f, b2 = 0.f;
                 PR_CUDA(cudaEventElapsedTime(&a, ev[4 * j], ev[4 * j + 1]));
                 PR_CUDA(cudaEventElapsedTime(&b2, ev[4 * j + 1], ev[4 * j + 2]));
