@@ -449,7 +449,7 @@ def main():
     rows, edges = st0["gather_rows"], st0["gather_edges"]
     g_bytes = 12 * edges + 8 * rows
     achieved = g_bytes / (g_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, l2hit, reqbusy = None, None, None
     prof = os.path.join(ROOT, "profiles", "gather_traffic.json")
     if os.path.exists(prof):
         try:
@@ -457,6 +457,8 @@ def main():
             key = f"{gen.name}:{args.mode}"
             if key in pj:
                 traffic = pj[key]["dram_bytes_per_launch"]
+                l2hit = pj[key].get("l2_hit_rate_pct")
+                reqbusy = pj[key].get("l1tex_to_l2_request_busy_pct")
         except Exception:
             traffic = None
     # whole sweep (K-GATHER + K-FINALIZE) against the north_star per-iteration
@@ -465,6 +467,7 @@ def main():
     model = 12 * E + 8 * (n + 1) + 16 * n
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "l2_hit_rate_pct": l2hit, "l1tex_to_l2_request_busy_pct": reqbusy,
                 "kernel": f"k_stream ({args.mode})", "bytes_per_launch": g_bytes,
                 "launch_ms": round(g_ms, 5), "peak_source": peak_src,
                 "sweep": {"ms": round(sweep_ms, 5), "gather_ms": round(g_ms, 5), "finalize_ms": round(f_ms, 5),

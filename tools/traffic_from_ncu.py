@@ -21,7 +21,14 @@ for vals in rows[2:]:
     wr = float(d["dram__bytes_write.sum"].replace(",", "")) * scale[units[hdr.index("dram__bytes_write.sum")]]
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "gather_traffic.json")
     pj = json.load(open(path)) if os.path.exists(path) else {}
+    def num(k):
+        try:
+            return float(d[k].replace(",", ""))
+        except (KeyError, ValueError):
+            return None
     pj[key] = {"dram_bytes_per_launch": int(rd + wr), "dram_read_bytes": int(rd), "dram_write_bytes": int(wr),
+               "l2_hit_rate_pct": num("lts__t_sector_hit_rate.pct"),
+               "l1tex_to_l2_request_busy_pct": num("l1tex__m_l1tex2xbar_req_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                "kernel": d["Kernel Name"][:80], "source": note}
     json.dump(pj, open(path, "w"), indent=1)
     print(key, pj[key])
