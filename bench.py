@@ -434,6 +434,7 @@ def main():
     value = total_units / (t_max * 1e-3) / 1e9
     phase = {k: statistics.median(r["ev"][i].elapsed_time(r["ev"][i + 1]) for r in recs)
              for k, i in (("create_ms", 0), ("preprocess_ms", 1), ("run_ms", 2))}
+    run_all = [r["ev"][2].elapsed_time(r["ev"][3]) for r in recs]
     st0 = recs[-1]["stats"]
     launches = sum(r["stats"]["total_launches"] for r in recs)
     launches = int(sum_over_ranks(float(launches), ws, dev))
@@ -474,7 +475,8 @@ def main():
                           "model_bytes": model, "achieved_GBs": round(model / (sweep_ms * 1e-3) / 1e9, 1),
                           "frac_measured_peak": round(model / (sweep_ms * 1e-3) / 1e9 / hbm_peak, 4),
                           "frac_nominal_8TBs": round(model / (sweep_ms * 1e-3) / 1e9 / 8000.0, 4),
-                          "gteps_per_iteration": round(E / (sweep_ms * 1e-3) / 1e9, 2)}}
+                          "gteps_per_iteration": round(E / (sweep_ms * 1e-3) / 1e9, 2),
+                          "traversed_gteps_per_iteration": round(edges / (sweep_ms * 1e-3) / 1e9, 2)}}
 
     # plain-mode sweep (the north_star 60 % target), one extra untimed run
     extra = {}
@@ -494,6 +496,28 @@ def main():
                                                      (pg * 1e-3) / 1e9 / hbm_peak, 4),
                                 "gteps_per_iteration": round(E / ((pg + pf) * 1e-3) / 1e9, 2),
                                 "iterations": sp["iterations"]}
+        g.close()
+
+    # t_iter by difference: [T(K2 sweeps) - T(K1 sweeps)] / (K2 - K1) at tau = 0,
+    # fixed costs cancel; median of 3 -- a cross-check of the event-timed sweep
+    if not args.no_plain:
+        g = pr.Graph(n, src_d, dst_d)
+        if flags:
+            g.preprocess(flags)
+        K1, K2 = 10, 40
+
+        def t_run(k):
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            g.run(x_d, gen.d, 0.0, k, mode=mode)
+            b_.record(stream)
+            torch.cuda.synchronize()
+            return a_.elapsed_time(b_)
+        t_run(K1)
+        d_ms = statistics.median((t_run(K2) - t_run(K1)) / (K2 - K1) for _ in range(3))
+        extra["t_iter_difference"] = {"ms": round(d_ms, 5), "K1": K1, "K2": K2, "mode": args.mode,
+                                      "gteps_per_iteration": round(E / (d_ms * 1e-3) / 1e9, 2),
+                                      "frac_measured_peak": round(model / (d_ms * 1e-3) / 1e9 / hbm_peak, 4)}
         g.close()
 
     if not args.no_modes:
@@ -535,7 +559,9 @@ def main():
             "config": {"workload": gen.name, "n": n, "m_raw": m, "E": E, "d": gen.d, "tau": gen.tau,
                        "norm": "L1", "mode": args.mode, "iterations": recs[0]["iters"],
                        "parallelism": f"replicas{ws}", "l2": "inputs larger than L2 (edge list 8m bytes)",
-                       "time_to_converge_ms": round(phase["run_ms"], 3), "create_ms": round(phase["create_ms"], 3),
+                       "time_to_converge_ms": round(phase["run_ms"], 3),
+                       "time_to_converge_min_max_ms": [round(min(run_all), 3), round(max(run_all), 3)],
+                       "create_ms": round(phase["create_ms"], 3),
                        "preprocess_ms": round(phase["preprocess_ms"], 3),
                        "n_members": recs[0]["info"]["n_members"]},
             "roofline": roofline,
