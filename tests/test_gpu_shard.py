@@ -229,3 +229,25 @@ def test_sharded_multiprocess(pr, tmp_path, world):
         assert abs(r["oracle_log"][min(it, ref_it) - 1] - 1e-10) <= 1e-9 * 1e-10
     assert r["max_diff"] <= 1e-10 and r["l1_diff"] <= 1e-9
     assert sum(x["info"]["owned_vertices"] for x in ranks) == graphgen.make_config(2).n
+
+
+def test_nccl_exchange_world1(pr, tmp_path):
+    """The NCCL branch of torch_dist_exchange (in-place all_gather_into_tensor on
+    the library's stream), in a one-rank NCCL process group: bit-identical to
+    the sync run."""
+    import torch.distributed as dist
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    store = dist.FileStore(str(tmp_path / "store"), 1)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1)
+    try:
+        gen = graphgen.make_config(2)
+        with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+            x0 = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+            ref = g.run(x0, gen.d, gen.tau, gen.max_iter)
+            g.shard(0, 1)
+            x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+            out = g.run_sharded(x, pr.torch_dist_exchange(), gen.d, gen.tau, gen.max_iter)
+            assert out == ref and torch.equal(x, x0)
+    finally:
+        dist.destroy_process_group()
