@@ -166,7 +166,8 @@ int pr_get_reductions(const pr_graph *g, int32_t *rep, int32_t *chain_src, int32
 
 /* Per-sweep (L1, L-inf) deltas of the last pr_run: writes min(cap, iters)
  * pairs into host buffer log[2*cap]; returns the number of pairs written
- * (>= 0) or a negative PR_* code. */
+ * (>= 0), or on error a negative value (-PR_EINVAL, PR_ECUDA) with the
+ * message in pr_last_error(). */
 int pr_get_delta_log(const pr_graph *g, double *log, int32_t cap);
 
 /* Statistics of the last pr_run (and of the graph's lifetime). */
@@ -202,6 +203,19 @@ typedef struct {
 } pr_run_stats;
 
 int pr_get_run_stats(const pr_graph *g, pr_run_stats *out);
+
+/*
+ * pr_get_phase_plan -- the phase plan of the last PR_MODE_PHASED run on the
+ * plain (reduced = 0) or reduced view (Q-B): phase k gathers the view's edges
+ * [edge_bounds[k], edge_bounds[k+1]) (view edge order: the view's rows in
+ * vertex order, each row's in-edges in CSR order) and finalizes the view rows
+ * [row_bounds[k], row_bounds[k+1]).  Host arrays of cap >= K+1 entries.
+ * Returns K >= 1, or on error a negative value (-PR_EINVAL: bad arguments or
+ * cap; -PR_ESTATE: no phased run on that view yet) with the message in
+ * pr_last_error().
+ */
+int pr_get_phase_plan(const pr_graph *g, int32_t reduced, int64_t *edge_bounds, int64_t *row_bounds,
+                      int32_t cap);
 
 /*
  * ---- Row sharding over P ranks ----

@@ -150,3 +150,55 @@ def residual_l1(g: CSR, d: float, x: np.ndarray, want_r: bool = False):
     r = np.empty(g.n, np.float64) if want_r else None
     v = _load().or_residual_l1(g.n, _p(g.row_ptr), _p(g.col_idx), _p(g.outdeg), d, _p(x), _p(r))
     return (v, r) if want_r else v
+
+
+def phased_sweeps(g: CSR, d: float, sweeps: int, rows: np.ndarray, edge_bounds, row_bounds):
+    """In-place sweeps in a fixed block order -- reading Q-B of
+    No-Sync's in-place update (Alg.3: "pr(u) <- tmp" is visible to
+    every later read), with Eq.(1) per vertex.  Test model of
+    PR_MODE_PHASED, written from that reading, not from the kernels:
+      * `rows` are the vertices of the view in order; the view's edge stream
+        is each row's in-edges in CSR order, one row after the other;
+      * a sweep runs phases k = 0..K-1 in order: phase k adds y(u) =
+        x(u)/outdeg(u), AS IT STANDS WHEN THE PHASE STARTS, for the stream
+        edges [edge_bounds[k], edge_bounds[k+1]) to their rows' sums, then
+        sets x(v) = (1-d)/n + d * S(v) for the rows [row_bounds[k],
+        row_bounds[k+1]) (a row crossing a phase boundary keeps the sums of
+        both phases);
+      * vertices of in-degree 0 take x = (1-d)/n at the end of sweep 1
+        (after every gather of that sweep; constant afterwards, Q-Z).
+    Returns (x, delta_log[(sweeps, 2)] of (L1, Linf) per sweep)."""
+    n = g.n
+    c = (1.0 - d) / n
+    rows = np.asarray(rows, np.int64)
+    od = g.outdeg.astype(np.float64)
+    x = np.full(n, 1.0 / n)
+    y = np.where(g.outdeg > 0, x / np.where(g.outdeg > 0, od, 1.0), 0.0)
+    deg = (g.row_ptr[rows + 1] - g.row_ptr[rows]).astype(np.int64)
+    src = (np.concatenate([g.col_idx[g.row_ptr[v]:g.row_ptr[v + 1]] for v in rows]) if len(rows)
+           else np.zeros(0, np.int32)).astype(np.int64)
+    row_of_edge = np.repeat(np.arange(len(rows)), deg)
+    zero = np.nonzero(np.diff(g.row_ptr) == 0)[0]
+    K = len(edge_bounds) - 1
+    log = np.zeros((sweeps, 2))
+    for t in range(sweeps):
+        xold = x.copy()
+        S = np.zeros(len(rows))
+        for k in range(K):
+            e0, e1 = int(edge_bounds[k]), int(edge_bounds[k + 1])
+            for e in range(e0, e1):                 # sequential: CSR order within each row
+                S[row_of_edge[e]] += y[src[e]]
+            r0, r1 = int(row_bounds[k]), int(row_bounds[k + 1])
+            for i in range(r0, r1):
+                v = rows[i]
+                x[v] = c + d * S[i]
+                if g.outdeg[v] > 0:
+                    y[v] = x[v] / od[v]
+        if t == 0:
+            for v in zero:
+                x[v] = c
+                if g.outdeg[v] > 0:
+                    y[v] = c / od[v]
+        diff = np.abs(x - xold)
+        log[t] = (diff.sum(), diff.max())
+    return x, log

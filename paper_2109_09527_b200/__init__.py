@@ -43,7 +43,7 @@ PR_MODE_PHASED = 64
 ABI_SYMBOLS = (
     "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_last_error",
     "pr_graph_info", "pr_get_csr", "pr_get_reductions", "pr_get_delta_log", "pr_get_run_stats",
-    "pr_graph_shard", "pr_run_sharded", "pr_get_shard_info",
+    "pr_graph_shard", "pr_run_sharded", "pr_get_shard_info", "pr_get_phase_plan",
 )
 
 
@@ -137,6 +137,8 @@ def _load():
     lib.pr_run_sharded.restype = ctypes.c_int
     lib.pr_get_shard_info.argtypes = [p, ctypes.POINTER(pr_shard_info)]
     lib.pr_get_shard_info.restype = ctypes.c_int
+    lib.pr_get_phase_plan.argtypes = [p, i32, p, p, i32]
+    lib.pr_get_phase_plan.restype = ctypes.c_int
     return lib
 
 
@@ -234,7 +236,7 @@ def pr_get_delta_log(g, cap: int):
     buf = np.zeros((max(cap, 1), 2), np.float64)
     k = lib.pr_get_delta_log(g, buf.ctypes.data, cap)
     if k < 0:
-        raise PRError(k, last_error())
+        raise PRError(-k if k == -PR_EINVAL else k, last_error())
     return buf[:k]
 
 
@@ -242,6 +244,17 @@ def pr_get_run_stats(g) -> dict:
     st = pr_run_stats()
     _check(lib.pr_get_run_stats(g, ctypes.byref(st)))
     return st.as_dict()
+
+
+def pr_get_phase_plan(g, reduced: bool = False):
+    """(edge_bounds, row_bounds) of the last PR_MODE_PHASED run on that view."""
+    import numpy as np
+    eb = np.zeros(65, np.int64)
+    rb = np.zeros(65, np.int64)
+    k = lib.pr_get_phase_plan(g, 1 if reduced else 0, eb.ctypes.data, rb.ctypes.data, 65)
+    if k < 0:
+        raise PRError(-k if k in (-PR_EINVAL, -PR_ESTATE) else k, last_error())
+    return eb[:k + 1].copy(), rb[:k + 1].copy()
 
 
 def pr_graph_shard(g, rank: int, world: int, stream=None) -> None:

@@ -419,6 +419,27 @@ int pr_run_sharded(pr_graph* g, double d, double threshold, int32_t max_iter, vo
     return rc;
 }
 
+int pr_get_phase_plan(const pr_graph* g, int32_t reduced, int64_t* edge_bounds, int64_t* row_bounds, int32_t cap) {
+    if (!g || !edge_bounds || !row_bounds) {
+        set_error("pr_get_phase_plan: bad arguments");
+        return -PR_EINVAL;
+    }
+    const View& v = reduced ? g->reduced : g->plain;
+    if (v.phase_k < 1 || (reduced && !g->pre_done)) {
+        set_error("pr_get_phase_plan: no PR_MODE_PHASED run on this view yet");
+        return -PR_ESTATE;
+    }
+    if (cap < v.phase_k + 1) {
+        set_error("pr_get_phase_plan: cap %d < %d", cap, v.phase_k + 1);
+        return -PR_EINVAL;
+    }
+    for (int k = 0; k <= v.phase_k; ++k) {
+        edge_bounds[k] = v.phase_eb[k];
+        row_bounds[k] = v.phase_rb[k];
+    }
+    return v.phase_k;
+}
+
 int pr_get_shard_info(const pr_graph* g, pr_shard_info* out) {
     if (!g || !out) {
         set_error("pr_get_shard_info: bad arguments");
@@ -518,7 +539,7 @@ int pr_get_reductions(const pr_graph* g, int32_t* rep, int32_t* chain_src, int32
 int pr_get_delta_log(const pr_graph* g, double* log, int32_t cap) {
     if (!g || !log || cap < 0) {
         set_error("pr_get_delta_log: bad arguments");
-        return PR_EINVAL;
+        return -PR_EINVAL;
     }
     int32_t k = g->log_len;
     if (k > cap) k = cap;

@@ -113,6 +113,7 @@ struct View {
     // [k*nspans/K, (k+1)*nspans/K) and finalizes rows [phase_rb[k], phase_rb[k+1])
     int phase_k = 0;
     int64_t phase_rb[SE_MAX_PHASES + 1];
+    int64_t phase_eb[SE_MAX_PHASES + 1];  // first edge (view edge order) of each phase, [K] = nedges
     View* phv = nullptr;            // the view with K-times finer spans (build_phase_view)
     int phv_k = 0;
 };

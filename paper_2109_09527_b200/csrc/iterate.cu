@@ -1045,6 +1045,8 @@ static int phase_plan(pr_graph* g, bool reduced, Ctx& ctx, int* K_out) {
         if (v.phase_k != 1) {
             v.phase_rb[0] = 0;
             v.phase_rb[1] = v.nrows;
+            v.phase_eb[0] = 0;
+            v.phase_eb[1] = v.nedges;
             v.phase_k = 1;
         }
         return PR_OK;
@@ -1059,6 +1061,9 @@ static int phase_plan(pr_graph* g, bool reduced, Ctx& ctx, int* K_out) {
     PR_CUDA(cudaMemcpyAsync(v.phase_rb, rb, sizeof(int64_t) * (size_t)(K + 1), cudaMemcpyDeviceToHost, ctx.stream));
     PR_CUDA(cudaStreamSynchronize(ctx.stream));
     dfree(rb, ctx.stream);
+    for (int k = 0; k <= K; ++k)
+        v.phase_eb[k] = k == K ? v.nedges
+                               : std::min<int64_t>(v.nedges, (int64_t)k * pv.nspans / K * pv.span_steps * SE_STEP);
     v.phase_k = K;
     return PR_OK;
 }

@@ -149,3 +149,36 @@ def test_phased_mode_validation(pr):
             with pytest.raises(pr.PRError) as e:
                 pr.pr_run(g.handle, D, 1e-10, 10, x, mode=pr.PR_MODE_PHASED | bad)
             assert e.value.code == pr.PR_EINVAL
+
+
+@pytest.mark.parametrize("name", ["planted0", "random", "in_star", "path"])
+@pytest.mark.parametrize("phases", ["3", "8"])
+def test_phased_trajectory_matches_block_model(pr, monkeypatch, name, phases):
+    """Element-wise parity of the first sweeps with the oracle's model of the
+    phased sweep (oracle.phased_sweeps, reading Q-B) driven by the library's
+    own phase plan (pr_get_phase_plan): which edges each phase gathers and
+    which rows it updates.  One-step spans put rows across phase boundaries."""
+    monkeypatch.setenv("PRGPU_PHASES", phases)
+    monkeypatch.setenv("PRGPU_SPAN", "1")
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    ref_g = oracle.build_csr(n, s, t)
+    rows = np.nonzero(np.diff(ref_g.row_ptr) > 0)[0]
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        for sweeps in (1, 3):
+            st, it, fd, x = run(pr, g, n, 0.0, pr.PR_MODE_PHASED, max_iter=sweeps)
+            eb, rb = pr.pr_get_phase_plan(g.handle)
+            assert eb[0] == 0 and eb[-1] == ref_g.E and rb[0] == 0 and rb[-1] == len(rows)
+            assert len(eb) - 1 == g.stats()["phases"]
+            xm, log = oracle.phased_sweeps(ref_g, D, sweeps, rows, eb, rb)
+            np.testing.assert_allclose(x, xm, rtol=1e-13, atol=1e-18)
+            np.testing.assert_allclose(g.delta_log()[:, 0], log[:, 0], rtol=1e-9, atol=1e-18)
+
+
+def test_phase_plan_errors(pr):
+    n = 30
+    s, t = G.edges_to_arrays(G.random_edges(n, 90, 4))
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        with pytest.raises(pr.PRError) as e:
+            pr.pr_get_phase_plan(g.handle)
+        assert e.value.code == pr.PR_ESTATE

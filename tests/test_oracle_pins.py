@@ -343,3 +343,55 @@ def test_gauss_seidel_is_in_place_sweep():
     x_1 = c + D * x_0
     x_2 = c + D * x_1
     np.testing.assert_allclose(r.x, [x_0, x_1, x_2], rtol=1e-15)
+
+
+# ---- the phased-sweep model (reading Q-B), pinned to Jacobi and Gauss-Seidel
+def _phased_inputs(n, edges):
+    from tests import graphs as G
+    s, t = G.edges_to_arrays(edges)
+    g = oracle.build_csr(n, s, t)
+    rows = np.nonzero(np.diff(g.row_ptr) > 0)[0]
+    return g, rows
+
+
+def test_phased_model_one_phase_is_jacobi():
+    """One phase over the whole stream = the synchronous sweep (Eq.(1))."""
+    from tests import graphs as G
+    n = 120
+    g, rows = _phased_inputs(n, G.random_edges(n, 500, 5) + [(0, 1)])
+    E = int(g.row_ptr[-1])
+    x, log = oracle.phased_sweeps(g, 0.85, 4, rows, [0, E], [0, len(rows)])
+    ref = oracle.pagerank(g, 0.85, 0.0, 4)
+    assert np.array_equal(x, ref.x)
+    np.testing.assert_allclose(log, ref.delta_log, rtol=1e-12, atol=1e-18)
+
+
+def test_phased_model_one_row_per_phase_is_gauss_seidel():
+    """One row per phase, rows ascending, every vertex with in-edges = the
+    in-place ascending sweep (Alg.3 with one thread), bit for bit."""
+    from tests import graphs as G
+    n = 90
+    edges = G.cycle(n) + G.random_edges(n, 300, 8)     # every vertex has in-degree >= 1
+    g, rows = _phased_inputs(n, edges)
+    assert len(rows) == n
+    eb = list(g.row_ptr)                              # a phase boundary at every row start
+    rb = list(range(n + 1))
+    x, log = oracle.phased_sweeps(g, 0.85, 5, rows, eb, rb)
+    ref = oracle.pagerank(g, 0.85, 0.0, 5, gauss_seidel=True)
+    np.testing.assert_allclose(x, ref.x, rtol=1e-15, atol=0)
+    np.testing.assert_allclose(log[:, 1], ref.delta_log[:, 1], rtol=1e-12, atol=1e-18)
+
+
+def test_phased_model_reaches_the_fixed_point():
+    """Any block order converges to the same fixed point (Lemma 2)."""
+    from tests import graphs as G
+    n = 150
+    g, rows = _phased_inputs(n, G.random_edges(n, 600, 13))
+    E = int(g.row_ptr[-1])
+    eb = [0, E // 3, (2 * E) // 3, E]
+    # rows ending in each edge range
+    ends = g.row_ptr[rows + 1]
+    rb = [0] + [int(np.searchsorted(ends, b, side="right")) for b in eb[1:-1]] + [len(rows)]
+    x, _ = oracle.phased_sweeps(g, 0.85, 200, rows, eb, rb)
+    tight = oracle.pagerank(g, 0.85, 1e-15, 2000)
+    assert np.abs(x - tight.x).max() <= 1e-12
