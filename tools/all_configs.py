@@ -59,17 +59,23 @@ for k in cfgs:
     w = pr.Graph(gen.n, s, t)  # warm-up build (the first one in a process also grows the memory pool)
     w.preprocess()
     w.close()
-    a, b, c_ = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-    a.record(st)
-    g = pr.Graph(gen.n, s, t)
-    b.record(st)
-    g.preprocess()
-    c_.record(st)
-    torch.cuda.synchronize()
+    cts, pts = [], []
+    for rep in range(3):       # median of 3 builds
+        a, b, c_ = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(st)
+        g = pr.Graph(gen.n, s, t)
+        b.record(st)
+        g.preprocess()
+        c_.record(st)
+        torch.cuda.synchronize()
+        cts.append(a.elapsed_time(b))
+        pts.append(b.elapsed_time(c_))
+        if rep < 2:
+            g.close()
     info = g.info()
     E, n = info["E"], gen.n
     rec = {"config": k, "workload": gen.name, "n": n, "E": E, "tau": gen.tau,
-           "create_ms": round(a.elapsed_time(b), 3), "preprocess_ms": round(b.elapsed_time(c_), 3)}
+           "create_ms": round(sorted(cts)[1], 3), "preprocess_ms": round(sorted(pts)[1], 3)}
     for name, mode in (("plain", 0), ("reduced", pr.PR_USE_REDUCTIONS), ("phased", pr.PR_MODE_PHASED),
                        ("async", pr.PR_MODE_ASYNC), ("nosync", pr.PR_MODE_NOSYNC)):
         (ms, it, rc), stt, gms, fms = timed_run(g, x, gen, mode)
