@@ -53,21 +53,39 @@ __global__ void k_outdeg(const int32_t* __restrict__ col, int64_t E, int32_t* __
 // (two modular atomics per run: -s at its start, +e at its end).  Self-loop /
 // sentinel keys (all 2b bits set) fall in the run of src = 2^b - 1 and are
 // subtracted when that is a vertex; duplicates are subtracted by k_uniq_emit.
-__global__ void k_src_runs(const uint64_t* __restrict__ k, int64_t m, int b, uint64_t sentinel, int64_t n,
-                           int32_t* __restrict__ outdeg) {
+// Tiles of SR_TILE keys staged through shared memory (coalesced loads, one
+// halo key each side), SR_IPT keys per thread.
+constexpr int SR_NT = 256, SR_IPT = 8, SR_TILE = SR_NT * SR_IPT;
+__global__ void __launch_bounds__(SR_NT) k_src_runs(const uint64_t* __restrict__ k, int64_t m, int b,
+                                                    uint64_t sentinel, int64_t n, int32_t* __restrict__ outdeg) {
+    __shared__ uint64_t sk[SR_TILE + 2];
     const uint64_t maskb = (1ull << b) - 1;
-    const int64_t T = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += T) {
-        const uint64_t key = k[i];
-        const int64_t v = (int64_t)(key & maskb);
-        const bool sent = key == sentinel;
-        if (v < n) {
-            unsigned* o = reinterpret_cast<unsigned*>(outdeg + v);
-            if (i == 0 || (k[i - 1] & maskb) != (uint64_t)v) atomicAdd(o, (unsigned)(-(int64_t)i));
-            if (i == m - 1 || (k[i + 1] & maskb) != (uint64_t)v) atomicAdd(o, (unsigned)(i + 1));
+    for (int64_t tb = (int64_t)blockIdx.x * SR_TILE; tb < m; tb += (int64_t)gridDim.x * SR_TILE) {
+        const int tn = (int)min((int64_t)SR_TILE, m - tb);
+        for (int i = threadIdx.x; i < tn; i += SR_NT) sk[i + 1] = __ldcs(k + tb + i);
+        if (threadIdx.x == 0) sk[0] = tb > 0 ? k[tb - 1] : ~0ull;
+        if (threadIdx.x == 1) sk[tn + 1] = tb + tn < m ? k[tb + tn] : ~0ull;
+        __syncthreads();
+        unsigned nsent = 0;
+#pragma unroll
+        for (int j = 0; j < SR_IPT; ++j) {
+            const int i = j * SR_NT + threadIdx.x;  // striped: conflict-free shared-memory reads
+            if (i < tn) {
+                const uint64_t key = sk[i + 1];
+                const uint64_t v = key & maskb;
+                if ((int64_t)v < n) {
+                    const int64_t gi = tb + i;
+                    unsigned* o = reinterpret_cast<unsigned*>(outdeg + v);
+                    // a missing neighbour (~0) never matches: its masked bits
+                    // are all ones only for the sentinel's run, handled below
+                    if (gi == 0 || (sk[i] & maskb) != v) atomicAdd(o, (unsigned)(-gi));
+                    if (gi == m - 1 || (sk[i + 2] & maskb) != v) atomicAdd(o, (unsigned)(gi + 1));
+                    nsent += key == sentinel;
+                }
+            }
         }
-        const unsigned ns = __ballot_sync(__activemask(), sent && v < n);
-        if (ns && (threadIdx.x & 31) == __ffs(ns) - 1) atomicSub(reinterpret_cast<unsigned*>(outdeg + v), __popc(ns));
+        if (nsent) atomicSub(reinterpret_cast<unsigned*>(outdeg + maskb), nsent);
+        __syncthreads();
     }
 }
 
@@ -246,8 +264,8 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
             PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, b, &a1)));
             uint64_t* cur = a1 ? keys_alt : keys;
             uint64_t* oth = a1 ? keys : keys_alt;
-            PR_LAUNCH(ctx, k_src_runs, grid_for(ctx, mk, 256), 256, 0, (const uint64_t*)cur, mk, b, sentinel, n,
-                      g->outdeg);
+            PR_LAUNCH(ctx, k_src_runs, grid_for(ctx, (mk + SR_IPT - 1) / SR_IPT, SR_NT), SR_NT, 0, (const uint64_t*)cur,
+                      mk, b, sentinel, n, g->outdeg);
             PR_TRY((radix_sort<uint64_t, false>(ctx, cur, oth, nullptr, nullptr, mk, b, 2 * b, &a2)));
             sorted = a2 ? oth : cur;
         } else {
