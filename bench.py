@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--parallel", choices=["replicas", "shard"], default="replicas",
                    help="N>1: independent replicas (weak scaling, default) or ONE graph row-sharded over the "
                         "ranks with a per-sweep all-gather (pr_run_sharded, strong scaling; plain sync mode)")
+    p.add_argument("--exchange", choices=["allgather", "peers"], default="allgather",
+                   help="--parallel shard: NCCL all-gather per sweep, or the exchange fused into the kernels "
+                        "(every new contrib stored into every rank's buffer through CUDA IPC, host barrier per sweep)")
     p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                    help="process-group backend of our arm (gloo + PRGPU_BENCH_ONE_GPU=1: test the sharded "
                         "multi-process plumbing with every rank on cuda:0)")
@@ -287,6 +290,8 @@ def run_shard_bench(args, ws, rank, local, dev, pr, torch, gen, W, K):
         e[0].record(stream)
         g = pr.Graph(n, src, dst)
         g.shard(rank, ws)
+        if ws > 1 and args.exchange == "peers":
+            pr.torch_dist_peer_setup(g.handle)
         e[1].record(stream)
         st, it, fd = g.run_sharded(x_d, exchange, gen.d, gen.tau, gen.max_iter,
                                    mode=pr.PR_TIMING if timing else 0)
@@ -342,7 +347,7 @@ def run_shard_bench(args, ws, rank, local, dev, pr, torch, gen, W, K):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": gen.name, "n": n, "m_raw": gen.m, "E": E, "d": gen.d, "tau": gen.tau,
                        "norm": "L1", "mode": "plain", "iterations": iters, "parallelism": f"shard{ws}",
-                       "backend": args.backend if ws > 1 else None,
+                       "backend": args.backend if ws > 1 else None, "exchange": args.exchange,
                        "l2": "inputs larger than L2 (edge list 8m bytes)",
                        "time_to_converge_ms": round(run_ms, 3), "create_and_shard_ms": round(setup_ms, 3),
                        "rank0_shard": recs[0]["info"]},

@@ -261,6 +261,29 @@ int pr_run_sharded(pr_graph *g, double d, double threshold, int32_t max_iter, vo
                    double *ranks, pr_exchange_fn exchange, void *exchange_ctx, int32_t *iters_out,
                    double *final_delta_out);
 
+/*
+ * Peer buffers -- the exchange fused into K-FINALIZE: with every rank's two
+ * contrib buffers addressable from this device (same device, peer access, or
+ * CUDA IPC below), each new contrib, zero-in-degree contrib and the rank's
+ * (L1, L-inf) pair are stored straight into every peer's buffer by the
+ * kernels that produce them, and pr_run_sharded calls the exchange with
+ * buf = NULL, meaning only: return when every rank has finished its work
+ * enqueued so far (e.g. stream synchronize + a host barrier) -- once after
+ * the initialisation and once per sweep.
+ *   pr_shard_buffers     this rank's buffers (device pointers, len doubles each)
+ *   pr_shard_set_peers   y0s[r], y1s[r] = rank r's buffers as addressable here
+ *                        (host arrays of world device pointers; [rank] unused);
+ *                        world = 0 or NULL arrays: back to the all-gather
+ *   pr_shard_export_ipc  2 cudaIpcMemHandle_t (64 B each) of this rank's buffers
+ *   pr_shard_open_ipc    handles = world x 2 such handles (rank-major); opens
+ *                        the peers' and sets them (closed by pr_destroy)
+ * All return PR_OK, PR_EINVAL, PR_ESTATE (no pr_graph_shard) or PR_ECUDA.
+ */
+int pr_shard_buffers(const pr_graph *g, void **y0, void **y1, int64_t *len);
+int pr_shard_set_peers(pr_graph *g, void *const *y0s, void *const *y1s, int32_t world);
+int pr_shard_export_ipc(const pr_graph *g, void *handles);
+int pr_shard_open_ipc(pr_graph *g, const void *handles, int32_t world);
+
 typedef struct {
     int32_t rank;
     int32_t world;

@@ -44,6 +44,7 @@ ABI_SYMBOLS = (
     "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_last_error",
     "pr_graph_info", "pr_get_csr", "pr_get_reductions", "pr_get_delta_log", "pr_get_run_stats",
     "pr_graph_shard", "pr_run_sharded", "pr_get_shard_info", "pr_get_phase_plan",
+    "pr_shard_buffers", "pr_shard_set_peers", "pr_shard_export_ipc", "pr_shard_open_ipc",
 )
 
 
@@ -139,6 +140,14 @@ def _load():
     lib.pr_get_shard_info.restype = ctypes.c_int
     lib.pr_get_phase_plan.argtypes = [p, i32, p, p, i32]
     lib.pr_get_phase_plan.restype = ctypes.c_int
+    lib.pr_shard_buffers.argtypes = [p, pp, pp, ctypes.POINTER(i64)]
+    lib.pr_shard_buffers.restype = ctypes.c_int
+    lib.pr_shard_set_peers.argtypes = [p, pp, pp, i32]
+    lib.pr_shard_set_peers.restype = ctypes.c_int
+    lib.pr_shard_export_ipc.argtypes = [p, p]
+    lib.pr_shard_export_ipc.restype = ctypes.c_int
+    lib.pr_shard_open_ipc.argtypes = [p, p, i32]
+    lib.pr_shard_open_ipc.restype = ctypes.c_int
     return lib
 
 
@@ -278,6 +287,47 @@ def device_f64(ptr: int, count: int):
     return torch.as_tensor(_CAI(), device="cuda")
 
 
+def pr_shard_buffers(g):
+    """(y0_ptr, y1_ptr, length in doubles) of this rank's contrib buffers."""
+    a, b, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+    _check(lib.pr_shard_buffers(g, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
+    return a.value, b.value, n.value
+
+
+def pr_shard_set_peers(g, y0s, y1s) -> None:
+    """Peer buffers (lists of world device pointers; this rank's entry unused);
+    None: back to the all-gather exchange."""
+    if y0s is None:
+        _check(lib.pr_shard_set_peers(g, None, None, 0))
+        return
+    w = len(y0s)
+    A = (ctypes.c_void_p * w)(*[v or 0 for v in y0s])
+    B = (ctypes.c_void_p * w)(*[v or 0 for v in y1s])
+    _check(lib.pr_shard_set_peers(g, A, B, w))
+
+
+def pr_shard_export_ipc(g) -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.pr_shard_export_ipc(g, buf))
+    return buf.raw
+
+
+def pr_shard_open_ipc(g, handles) -> None:
+    """handles: the world ranks' pr_shard_export_ipc bytes, in rank order."""
+    blob = b"".join(handles)
+    _check(lib.pr_shard_open_ipc(g, blob, len(handles)))
+
+
+def torch_dist_peer_setup(g, group=None) -> None:
+    """Exchange this rank's buffer IPC handles over torch.distributed and open
+    the peers' (the fused peer-store exchange, one process per GPU)."""
+    import torch.distributed as dist
+    mine = pr_shard_export_ipc(g)
+    allh = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allh, mine, group=group)
+    pr_shard_open_ipc(g, allh)
+
+
 def torch_dist_exchange(group=None):
     """The per-sweep exchange of pr_run_sharded through torch.distributed
     (NCCL over NVLink on a GPU node): an in-place all_gather_into_tensor of the
@@ -288,6 +338,10 @@ def torch_dist_exchange(group=None):
     nccl = dist.get_backend(group) == "nccl"
 
     def exchange(buf: int, chunk: int, world: int, stream: int):
+        if buf is None:  # peer buffers: the kernels already stored everything; only synchronise
+            (torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()).synchronize()
+            dist.barrier(group=group)
+            return
         full = device_f64(buf, chunk * world)
         rank = dist.get_rank(group)
         # stream 0 (ctypes passes it as None) is the legacy default stream
@@ -347,6 +401,12 @@ class Graph:
 
     def shard_info(self):
         return pr_get_shard_info(self.handle)
+
+    def shard_buffers(self):
+        return pr_shard_buffers(self.handle)
+
+    def set_peers(self, y0s, y1s=None):
+        pr_shard_set_peers(self.handle, y0s, y1s)
 
     def run_sharded(self, ranks, exchange, d=0.85, threshold=1e-10, max_iter=1000, mode=0, stream=None):
         return pr_run_sharded(self.handle, d, threshold, max_iter, ranks, exchange, stream, mode)

@@ -7,6 +7,7 @@
 // in ingest.cu / preprocess.cu / iterate.cu.
 #include <math.h>
 #include <stdarg.h>
+#include <vector>
 #include <string.h>
 
 #include <new>
@@ -417,6 +418,85 @@ int pr_run_sharded(pr_graph* g, double d, double threshold, int32_t max_iter, vo
     g->launches += ctx.launches;
     g->last.total_launches = g->launches;
     return rc;
+}
+
+int pr_shard_buffers(const pr_graph* g, void** y0, void** y1, int64_t* len) {
+    if (!g || !y0 || !y1 || !len) {
+        set_error("pr_shard_buffers: bad arguments");
+        return PR_EINVAL;
+    }
+    if (g->shard_world < 1) {
+        set_error("pr_shard_buffers: pr_graph_shard has not run");
+        return PR_ESTATE;
+    }
+    *y0 = g->sy[0];
+    *y1 = g->sy[1];
+    *len = g->shard_hot + (int64_t)g->shard_world * g->shard_chunk + 1;
+    return PR_OK;
+}
+
+int pr_shard_set_peers(pr_graph* g, void* const* y0s, void* const* y1s, int32_t world) {
+    g_err[0] = 0;
+    if (!g) {
+        set_error("pr_shard_set_peers: NULL graph");
+        return PR_EINVAL;
+    }
+    if (g->shard_world < 1) {
+        set_error("pr_shard_set_peers: pr_graph_shard has not run");
+        return PR_ESTATE;
+    }
+    if (world == 0 || !y0s || !y1s) {  // back to the all-gather exchange
+        clear_peers(g);
+        return PR_OK;
+    }
+    if (world != g->shard_world) {
+        set_error("pr_shard_set_peers: world %d != the shard's %d", world, g->shard_world);
+        return PR_EINVAL;
+    }
+    for (int r = 0; r < world; ++r)
+        if (r != g->shard_rank && (!y0s[r] || !y1s[r])) {
+            set_error("pr_shard_set_peers: NULL buffer for rank %d", r);
+            return PR_EINVAL;
+        }
+    return set_peers(g, (double* const*)y0s, (double* const*)y1s, world);
+}
+
+int pr_shard_export_ipc(const pr_graph* g, void* handles) {
+    if (!g || !handles) {
+        set_error("pr_shard_export_ipc: bad arguments");
+        return PR_EINVAL;
+    }
+    if (g->shard_world < 1) {
+        set_error("pr_shard_export_ipc: pr_graph_shard has not run");
+        return PR_ESTATE;
+    }
+    cudaIpcMemHandle_t* h = reinterpret_cast<cudaIpcMemHandle_t*>(handles);
+    PR_CUDA(cudaIpcGetMemHandle(&h[0], g->sy[0]));
+    PR_CUDA(cudaIpcGetMemHandle(&h[1], g->sy[1]));
+    return PR_OK;
+}
+
+int pr_shard_open_ipc(pr_graph* g, const void* handles, int32_t world) {
+    g_err[0] = 0;
+    if (!g || !handles) {
+        set_error("pr_shard_open_ipc: bad arguments");
+        return PR_EINVAL;
+    }
+    if (g->shard_world < 1 || world != g->shard_world) {
+        set_error("pr_shard_open_ipc: world %d does not match the shard", world);
+        return g->shard_world < 1 ? PR_ESTATE : PR_EINVAL;
+    }
+    clear_peers(g);
+    const cudaIpcMemHandle_t* h = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+    std::vector<void*> y0(world, nullptr), y1(world, nullptr);
+    for (int r = 0; r < world; ++r) {
+        if (r == g->shard_rank) continue;
+        PR_CUDA(cudaIpcOpenMemHandle(&y0[r], h[2 * r], cudaIpcMemLazyEnablePeerAccess));
+        g->speer_ipc.push_back(y0[r]);
+        PR_CUDA(cudaIpcOpenMemHandle(&y1[r], h[2 * r + 1], cudaIpcMemLazyEnablePeerAccess));
+        g->speer_ipc.push_back(y1[r]);
+    }
+    return set_peers(g, (double* const*)y0.data(), (double* const*)y1.data(), world);
 }
 
 int pr_get_phase_plan(const pr_graph* g, int32_t reduced, int64_t* edge_bounds, int64_t* row_bounds, int32_t cap) {

@@ -1,5 +1,6 @@
 // internal.h -- library-private state of libprgpu.
 #pragma once
+#include <vector>
 #include "common.cuh"
 
 namespace prgpu {
@@ -179,7 +180,9 @@ struct pr_graph {
     int32_t* shot_src = nullptr;    // [H] chunk slot of each hot copy
     int64_t snz = 0;
     prgpu::View shard;              // owned rows of in-degree > 0, columns in sharded slots
-    double* sy[2] = {nullptr, nullptr};  // [H + world * chunk + 1] ping-pong, last slot = +0.0
+    double* sy[2] = {nullptr, nullptr};  // [H + world * chunk + 1] ping-pong, last slot = +0.0 (cudaMalloc: IPC-exportable)
+    double** speer_dev = nullptr;   // [2][world-1] peers' sy[parity] (pr_shard_set_peers / pr_shard_open_ipc)
+    std::vector<void*> speer_ipc;   // IPC-opened peer bases to close
     // iteration buffers (allocated lazily by pr_run)
     double* x = nullptr;            // fp64[n] (used when the caller's ranks are on the host)
     double* xr = nullptr;           // sync sweeps: x of the view's rows, row order (unpermuted at the end)
@@ -219,6 +222,8 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
 int read_count(Ctx& ctx, const int64_t* dev, int64_t* host);
 int build_shard(pr_graph* g, int rank, int world, Ctx& ctx);
 void clear_shard(pr_graph* g, cudaStream_t s);
+void clear_peers(pr_graph* g);
+int set_peers(pr_graph* g, double* const* y0s, double* const* y1s, int world);
 int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
                 pr_exchange_fn exchange, void* exchange_ctx, int32_t* iters_out, double* delta_out);
 }  // namespace prgpu

@@ -154,8 +154,12 @@ struct IterArgs {
     int64_t nhubs;
     double* delta_log;
     // sharded run: the last CTA writes this rank's (L1, Linf) here (the tail
-    // of its exchanged chunk) instead of taking the stop decision
+    // of its exchanged chunk) instead of taking the stop decision; with peer
+    // buffers (pr_shard_set_peers) also at peer_y[q] + shard_off of every peer
     double* shard_out = nullptr;
+    double* const* peer_y = nullptr;
+    int npeer = 0;
+    int64_t shard_off = 0;
 };
 
 // The stop test on a sweep's (L1, Linf): iteration count, delta log, done /
@@ -215,6 +219,10 @@ __device__ void global_finalize(const IterArgs& ia, double* red) {
         if (ia.shard_out) {
             ia.shard_out[0] = l1;
             ia.shard_out[1] = li;
+            for (int q = 0; q < ia.npeer; ++q) {
+                ia.peer_y[q][ia.shard_off] = l1;
+                ia.peer_y[q][ia.shard_off + 1] = li;
+            }
         } else {
             stop_test(ia, l1, li);
         }
@@ -316,6 +324,10 @@ struct FinArgs {
     int64_t row0 = 0;
     int64_t part_off = 0;
     int last = 1;
+    // sharded run with peer buffers: every new contrib is also stored into
+    // the same slot of each peer's buffer (the all-gather fused into K-FINALIZE)
+    double* const* peer_y = nullptr;
+    int npeer = 0;
 };
 
 // Rows are visited grid-stride (all CTAs sweep the row space together, which
@@ -356,7 +368,11 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
             if (r < f.nrows) {
                 const double xn = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
                 xr[r] = xn;
-                if (inf[u].x > 0) y[inf[u].y] = xn / (double)inf[u].x;
+                if (inf[u].x > 0) {
+                    const double yv = xn / (double)inf[u].x;
+                    y[inf[u].y] = yv;
+                    for (int q = 0; q < f.npeer; ++q) f.peer_y[q][inf[u].y] = yv;
+                }
                 const double dl = fabs(xn - xo[u]);
                 l1 += dl;
                 linf = fmax(linf, dl);
@@ -516,6 +532,18 @@ __global__ void k_zero_y(const int32_t* __restrict__ zl, int64_t nz, double c, d
         const int32_t v = zl[i];
         const int32_t o = od[v];
         if (o > 0) y[cidx[v]] = c / (double)o;
+    }
+}
+
+// Sharded run with peer buffers: the constant contribs of this rank's
+// in-degree-0 vertices into every peer's buffer (sweep 1).
+__global__ void k_peer_zero(const int32_t* __restrict__ zl, int64_t nz, double c, const int32_t* __restrict__ od,
+                            const int32_t* __restrict__ cidx, double* const* peers, int np) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = zl[i];
+        const int32_t o = od[v];
+        if (o > 0)
+            for (int q = 0; q < np; ++q) peers[q][cidx[v]] = c / (double)o;
     }
 }
 
@@ -1414,6 +1442,7 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
     const View& v = g->shard;
     const int world = g->shard_world, rank = g->shard_rank;
     const int64_t chunk = g->shard_chunk, H = g->shard_hot;
+    const bool peers = g->speer_dev != nullptr && world > 1;
     const int64_t launches0 = ctx.launches;
     PR_TRY(reset_tickets(v, s));
     if (!g->x) PR_TRY(dalloc(&g->x, (size_t)n, s));
@@ -1463,6 +1492,12 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
     IterArgs ia0{g->st, g->cta_partial, 0, 0, 0, nullptr, 0, g->delta_log};
     const unsigned cgrid = (unsigned)std::max<int64_t>(1, (H + 255) / 256);
     PR_LAUNCH(ctx, k_shard_combine, cgrid, 256, 0, ia0, g->sy[0], (const int32_t*)g->shot_src, H, world, chunk, 0);
+    // peer buffers: no rank may store into another's buffers before that rank
+    // has initialised them (sweep 1's stores would be overwritten)
+    if (peers && exchange(exchange_ctx, nullptr, chunk, world, (void*)s) != 0) {
+        set_error("pr_run_sharded: the exchange callback failed before sweep 1");
+        return PR_ECUDA;
+    }
     const unsigned fg = (unsigned)std::min<int64_t>((v.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
     PR_LAUNCH(ctx, k_fill_f64, fg, 256, 0, g->xr, v.nrows, 1.0 / (double)n);
     IterArgs ia_rest{g->st, g->cta_partial, fgrid, 0, 0, nullptr, 0, g->delta_log};
@@ -1490,6 +1525,10 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
             double* y_out = g->sy[(it + 1) & 1];
             IterArgs ia = it == 0 ? ia_first : ia_rest;
             ia.shard_out = y_out + H + (int64_t)rank * chunk + chunk - 2;
+            double* const* pout = peers ? g->speer_dev + ((it + 1) & 1) * (world - 1) : nullptr;
+            ia.peer_y = pout;
+            ia.npeer = peers ? world - 1 : 0;
+            ia.shard_off = H + (int64_t)rank * chunk + chunk - 2;
             if (it == 0 && zgrid > 0)
                 PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->szlist, nz, zper, c, x, y_out,
                           (const int32_t*)g->outdeg, (const int32_t*)g->scidx, zero_partial);
@@ -1498,13 +1537,27 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
             if (timing && it % tstride == tstride - 1) PR_CUDA(cudaEventRecord(ev[4 * j + 1], s));
             FinArgs f = fa;
             f.y_out = y_out;
+            f.peer_y = pout;
+            f.npeer = peers ? world - 1 : 0;
             PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
             if (timing && it % tstride == tstride - 1) PR_CUDA(cudaEventRecord(ev[4 * j + 2], s));
-            if (it == 0 && nz > 0)
-                PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256,
-                          0, (const int32_t*)g->szlist, nz, c, y_in, (const int32_t*)g->outdeg,
-                          (const int32_t*)g->scidx);
-            if (exchange(exchange_ctx, y_out + H, chunk, world, (void*)s) != 0) {
+            if (it == 0 && nz > 0) {
+                const unsigned zg = (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8);
+                PR_LAUNCH(ctx, k_zero_y, zg, 256, 0, (const int32_t*)g->szlist, nz, c, y_in,
+                          (const int32_t*)g->outdeg, (const int32_t*)g->scidx);
+                if (peers)  // peers' sweep-1 output buffer (their gathers read the other one)
+                    PR_LAUNCH(ctx, k_peer_zero, zg, 256, 0, (const int32_t*)g->szlist, nz, c,
+                              (const int32_t*)g->outdeg, (const int32_t*)g->scidx, pout, world - 1);
+            }
+            // ...and their other buffer only in sweep 2 (their sweep-2 output):
+            // in sweep 1 it is what they gather from
+            if (it == 1 && nz > 0 && peers)
+                PR_LAUNCH(ctx, k_peer_zero, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8),
+                          256, 0, (const int32_t*)g->szlist, nz, c, (const int32_t*)g->outdeg,
+                          (const int32_t*)g->scidx, pout, world - 1);
+            // all-gather of the chunks (or, with peer buffers, only the
+            // cross-rank barrier: every rank's stores landed in every buffer)
+            if (exchange(exchange_ctx, peers ? nullptr : y_out + H, chunk, world, (void*)s) != 0) {
                 set_error("pr_run_sharded: the exchange callback failed at sweep %lld", (long long)it + 1);
                 for (auto e : ev) cudaEventDestroy(e);
                 return PR_ECUDA;

@@ -114,6 +114,16 @@ struct ShPosEmit {
     __device__ void operator()(int64_t i, int64_t pos, int64_t) const { out[i] = pos; }
 };
 
+void clear_peers(pr_graph* g) {
+    if (g->speer_dev) {
+        cudaFree(g->speer_dev);
+        g->speer_dev = nullptr;
+    }
+    for (void* p : g->speer_ipc)
+        if (p) cudaIpcCloseMemHandle(p);
+    g->speer_ipc.clear();
+}
+
 void clear_shard(pr_graph* g, cudaStream_t s) {
     free_view(g->shard, s);
     dfree(g->sowner, s);
@@ -121,8 +131,13 @@ void clear_shard(pr_graph* g, cudaStream_t s) {
     dfree(g->szlist, s);
     dfree(g->shot_src, s);
     g->shard_hot = 0;
-    dfree(g->sy[0], s);
-    dfree(g->sy[1], s);
+    clear_peers(g);
+    for (int b = 0; b < 2; ++b)
+        if (g->sy[b]) {
+            cudaStreamSynchronize(s);
+            cudaFree(g->sy[b]);
+            g->sy[b] = nullptr;
+        }
     g->shard_rank = -1;
     g->shard_world = 0;
     g->shard_chunk = 0;
@@ -190,14 +205,35 @@ int build_shard(pr_graph* g, int rank, int world, Ctx& ctx) {
     }
     PR_TRY(build_view_stream(S, ctx, (int32_t)(H + (int64_t)world * chunk), g->outdeg, g->scidx));
     const int64_t ny = H + (int64_t)world * chunk + 1;
-    for (int b = 0; b < 2; ++b) {
-        PR_TRY(dalloc(&g->sy[b], (size_t)ny, s));
+    for (int b = 0; b < 2; ++b) {  // plain cudaMalloc: exportable by cudaIpcGetMemHandle (pr_shard_export_ipc)
+        PR_CUDA(cudaMalloc(&g->sy[b], sizeof(double) * (size_t)ny));
         PR_CUDA(cudaMemsetAsync(g->sy[b], 0, sizeof(double) * (size_t)ny, s));
     }
     g->shard_rank = rank;
     g->shard_world = world;
     g->shard_chunk = chunk;
     g->shard_hot = H;
+    return PR_OK;
+}
+
+// Peer buffers: y0s[r] / y1s[r] = rank r's sy[0] / sy[1] as addressable from
+// this device (same device, peer access or IPC-opened); entry [rank] unused.
+int set_peers(pr_graph* g, double* const* y0s, double* const* y1s, int world) {
+    if (g->speer_dev) {
+        cudaFree(g->speer_dev);
+        g->speer_dev = nullptr;
+    }
+    if (world <= 1) return PR_OK;
+    std::vector<double*> h(2 * (size_t)(world - 1));
+    int q = 0;
+    for (int r = 0; r < world; ++r) {
+        if (r == g->shard_rank) continue;
+        h[q] = y0s[r];
+        h[(world - 1) + q] = y1s[r];
+        ++q;
+    }
+    PR_CUDA(cudaMalloc(&g->speer_dev, sizeof(double*) * h.size()));
+    PR_CUDA(cudaMemcpy(g->speer_dev, h.data(), sizeof(double*) * h.size(), cudaMemcpyHostToDevice));
     return PR_OK;
 }
 

@@ -18,12 +18,15 @@ import oracle  # noqa: E402
 import paper_2109_09527_b200 as pr  # noqa: E402
 
 cfg, out = int(sys.argv[1]), sys.argv[2]
+peers = len(sys.argv) > 3 and sys.argv[3] == "peers"
 dist.init_process_group("gloo")
 rank, world = dist.get_rank(), dist.get_world_size()
 torch.cuda.set_device(0)
 gen = graphgen.make_config(cfg)
 with pr.Graph(gen.n, torch.from_numpy(gen.src).cuda(), torch.from_numpy(gen.dst).cuda()) as g:
     g.shard(rank, world)
+    if peers:  # the exchange fused into the kernels: CUDA IPC buffers, barrier-only exchange
+        pr.torch_dist_peer_setup(g.handle)
     x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
     st, it, fd = g.run_sharded(x, pr.torch_dist_exchange(), gen.d, gen.tau, gen.max_iter)
     info = g.shard_info()

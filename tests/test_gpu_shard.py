@@ -61,9 +61,26 @@ class Loopback:
         return ex
 
 
-def run_world(pr, n, s, t, world, tau, max_iter=1000, mode=0):
+class PeerBarrier:
+    """The exchange of the peer-store form: the kernels already wrote every
+    rank's buffers; only wait until all ranks' stores of the sweep are done."""
+
+    def __init__(self, world):
+        self.bar = threading.Barrier(world)
+
+    def exchange_for(self, rank):
+        def ex(buf, chunk, world, stream):
+            assert buf is None
+            torch.cuda.synchronize()
+            self.bar.wait()
+        return ex
+
+
+def run_world(pr, n, s, t, world, tau, max_iter=1000, mode=0, peers=False):
     """Shard one graph over `world` in-process ranks; returns the assembled
-    ranks, per-rank (status, iters, delta) and shard infos."""
+    ranks, per-rank (status, iters, delta) and shard infos.  peers=True: the
+    exchange fused into the kernels (every rank stores into every rank's
+    buffers; pr_shard_set_peers with the other graphs' device pointers)."""
     graphs = [pr.Graph(n, dev(s), dev(t)) for _ in range(world)]
     try:
         for r, g in enumerate(graphs):
@@ -71,6 +88,11 @@ def run_world(pr, n, s, t, world, tau, max_iter=1000, mode=0):
         infos = [g.shard_info() for g in graphs]
         xs = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(world)]
         lb = Loopback(pr, world)
+        if peers:
+            bufs = [g.shard_buffers() for g in graphs]
+            for g in graphs:
+                g.set_peers([b[0] for b in bufs], [b[1] for b in bufs])
+            lb = PeerBarrier(world)
         out = [None] * world
         errs = []
 
@@ -251,3 +273,50 @@ def test_nccl_exchange_world1(pr, tmp_path):
             assert out == ref and torch.equal(x, x0)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["planted", "random", "in_star", "no_edges"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_store_exchange_matches_allgather(pr, name, world):
+    """The exchange fused into K-FINALIZE (peer stores) gives bit-identically
+    the ranks, sweeps and deltas of the all-gather exchange, and the oracle's."""
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    a = run_world(pr, n, s, t, world, 1e-12)
+    b = run_world(pr, n, s, t, world, 1e-12, peers=True)
+    assert a[1] == b[1] and np.array_equal(a[0], b[0])
+    assert all(np.array_equal(x, y) for x, y in zip(a[3], b[3]))
+    ref = oracle.pagerank(oracle.build_csr(n, s, t), D, 1e-12, 1000)
+    assert_close(b[0], ref.x)
+
+
+def test_peer_store_config(pr):
+    gen = graphgen.make_config(2)
+    ref = oracle.pagerank(oracle.build_csr(gen.n, gen.src, gen.dst), gen.d, gen.tau, gen.max_iter)
+    x, out, _, _ = run_world(pr, gen.n, gen.src, gen.dst, 4, gen.tau, gen.max_iter, peers=True)
+    assert_iters(out[0][1], ref, gen.tau)
+    assert_close(x, ref.x)
+
+
+@pytest.mark.parametrize("world", [2])
+def test_peer_store_multiprocess_ipc(pr, tmp_path, world):
+    """One process per rank, buffers shared by CUDA IPC handles exchanged over
+    torch.distributed (every rank on cuda:0 here), the exchange reduced to a
+    barrier."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    out = tmp_path / "shard_ipc.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "tests", "shard_worker.py"),
+           "2", str(out), "peers"]
+    subprocess.run(cmd, check=True, timeout=600, cwd=root)
+    r = json.load(open(out))
+    assert len({(x["st"], x["it"], x["fd"]) for x in r["ranks"]}) == 1
+    assert r["max_diff"] <= 1e-10 and r["l1_diff"] <= 1e-9
