@@ -43,13 +43,37 @@ for P in Ps:
             ms = a.elapsed_time(b) / SWEEPS
             per.append({"rank": r, "sweep_ms": round(ms, 4), "edges": info["edges"], "rows": info["rows"],
                         "chunk": info["chunk"]})
+    # the fused exchange's kernel-side cost: rank 0 storing every contrib into
+    # P - 1 peer buffers (scratch buffers on this GPU stand in for the peers;
+    # over NVLink the stores are remote, which this cannot measure)
+    if P > 1:
+        with pr.Graph(gen.n, s, t) as g:
+            g.shard(0, P)
+            y0, y1, ln = g.shard_buffers()
+            scratch = [(torch.zeros(ln, dtype=torch.float64, device="cuda"),
+                        torch.zeros(ln, dtype=torch.float64, device="cuda")) for _ in range(P - 1)]
+            p0 = [y0] + [a.data_ptr() for a, _ in scratch]
+            p1 = [y1] + [b_.data_ptr() for _, b_ in scratch]
+            g.set_peers(p0, p1)
+            g.run_sharded(x, lambda *a: None, gen.d, 0.0, 3)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            g.run_sharded(x, lambda *a: None, gen.d, 0.0, SWEEPS)
+            b.record(st)
+            torch.cuda.synchronize()
+            peer_ms = round(a.elapsed_time(b) / SWEEPS, 4)
+            del scratch
+    else:
+        peer_ms = None
     worst = max(p["sweep_ms"] for p in per)
     chunk = per[0]["chunk"]
     recv = (P - 1) * chunk * 8
     comm_ms = recv / (NVLINK_GBS * 1e9) * 1e3
     if base is None:
         base = worst
-    rec = {"ranks": per, "slowest_rank_sweep_ms": worst, "allgather_recv_bytes_per_rank": recv,
+    rec = {"ranks": per, "slowest_rank_sweep_ms": worst, "rank0_sweep_ms_with_peer_stores_local": peer_ms,
+           "allgather_recv_bytes_per_rank": recv,
            "projected_sweep_ms_no_overlap": round(worst + comm_ms, 4),
            "projected_speedup_vs_1gpu": round(base / (worst + comm_ms), 2),
            "edge_imbalance": round(max(p["edges"] for p in per) / (sum(p["edges"] for p in per) / P), 4)}
