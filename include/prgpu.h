@@ -238,10 +238,11 @@ typedef int (*pr_exchange_fn)(void *ctx, double *buf, int64_t chunk, int32_t wor
 
 /*
  * pr_graph_shard -- make g (created from the SAME edge list on every rank) the
- * rank's share of a world-rank row partition: contrib-carrying vertices are cut
- * into world ranges of the internal contrib order balanced by
- * sum(in-degree + 1), dangling vertices by id range.  Deterministic: every
- * rank derives the same partition.  1 <= world <= 4096, 0 <= rank < world
+ * rank's share of a world-rank row partition: contrib-carrying vertices are
+ * dealt round-robin in the internal contrib (out-degree) order, so every rank
+ * owns an equal share of the contribs and of each degree class; dangling
+ * vertices round-robin by id.  Deterministic: every rank derives the same
+ * partition.  1 <= world <= 4096, 0 <= rank < world
  * (else PR_EINVAL).  pr_run / pr_preprocess keep working on the whole graph.
  */
 int pr_graph_shard(pr_graph *g, int32_t rank, int32_t world, void *stream);
