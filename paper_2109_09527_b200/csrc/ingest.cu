@@ -532,6 +532,7 @@ void free_view(View& v, cudaStream_t s) {
         return;
     }
     free_phase_view(v, s);
+    free_dyn_view(v, s);
     if (v.owns_row_ptr) dfree(v.row_ptr, s);
     v.row_ptr = nullptr;
     dfree(v.col, s);
@@ -738,6 +739,8 @@ int build_phase_view(View& v, Ctx& ctx, int K) {
     }
     p->alias = true;  // owns only its span tables (free_phase_view)
     p->phv = nullptr;
+    p->dynv = nullptr;
+    p->dyn_ctr = nullptr;
     p->seg = nullptr;
     p->nseg = 0;
     p->bin = p->bout = p->b_row = p->b_s0 = p->b_s1 = nullptr;
@@ -755,6 +758,42 @@ int build_phase_view(View& v, Ctx& ctx, int K) {
     v.phv = p;
     v.phv_k = K;
     return build_spans(*p, ctx, ss);
+}
+
+// PRGPU_DYN_SPAN: a shallow copy of v with spans of span_steps steps, handed
+// out to warps by an atomic counter (k_stream_dyn).
+int build_dyn_view(View& v, Ctx& ctx, int64_t ss) {
+    if (v.dynv && v.dyn_ss == ss) return PR_OK;
+    free_dyn_view(v, ctx.stream);
+    View* p = new (std::nothrow) View(v);
+    if (!p) {
+        set_error("build_dyn_view: host allocation failed");
+        return PR_ENOMEM;
+    }
+    p->alias = true;
+    p->phv = nullptr;
+    p->dynv = nullptr;
+    p->dyn_ctr = nullptr;
+    p->seg = nullptr;
+    p->nseg = 0;
+    p->bin = p->bout = p->b_row = p->b_s0 = p->b_s1 = nullptr;
+    p->part_in = p->part_out = nullptr;
+    p->bticket = nullptr;
+    p->phase_k = 0;
+    v.dynv = p;
+    v.dyn_ss = ss;
+    PR_TRY(dalloc(&v.dyn_ctr, 1, ctx.stream));
+    PR_CUDA(cudaMemsetAsync(v.dyn_ctr, 0, sizeof(uint32_t), ctx.stream));
+    return build_spans(*p, ctx, ss);
+}
+
+void free_dyn_view(View& v, cudaStream_t s) {
+    if (!v.dynv) return;
+    free_spans(*v.dynv, s);
+    delete v.dynv;
+    v.dynv = nullptr;
+    v.dyn_ss = 0;
+    dfree(v.dyn_ctr, s);
 }
 
 void free_phase_view(View& v, cudaStream_t s) {

@@ -117,6 +117,9 @@ struct View {
     int64_t phase_eb[SE_MAX_PHASES + 1];  // first edge (view edge order) of each phase, [K] = nedges
     View* phv = nullptr;            // the view with K-times finer spans (build_phase_view)
     int phv_k = 0;
+    View* dynv = nullptr;           // finer spans handed out dynamically (PRGPU_DYN_SPAN, build_dyn_view)
+    int64_t dyn_ss = 0;
+    uint32_t* dyn_ctr = nullptr;    // its span counter
 };
 
 // Device-resident iteration state (one per graph).
@@ -210,6 +213,8 @@ int build_spans(View& v, Ctx& ctx, int64_t span_steps);
 void free_spans(View& v, cudaStream_t s);
 int build_phase_view(View& v, Ctx& ctx, int K);
 void free_phase_view(View& v, cudaStream_t s);
+int build_dyn_view(View& v, Ctx& ctx, int64_t span_steps);
+void free_dyn_view(View& v, cudaStream_t s);
 int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib);
 void free_view(View& v, cudaStream_t s);
 __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const int64_t* __restrict__ rp,

@@ -294,6 +294,26 @@ __global__ void __launch_bounds__(SE_NT, 1) k_stream(P p, StreamArgs a, const De
     stream_run(p, a);
 }
 
+// K-GATHER with dynamically handed-out spans (PRGPU_DYN_SPAN; a finer span
+// layout of the view, DESIGN.md §9 "Tail of the gather").
+template <class P>
+__global__ void __launch_bounds__(SE_NT, 1) k_stream_dyn(P p, StreamArgs a, const DevState* st) {
+    extern __shared__ __align__(16) double hot_smem[];
+    pdl_wait();
+    pdl_trigger();
+    if (st->done) return;
+    p.pol_last = policy_evict_last();
+    if (P::kHot) {
+        const double2* src = reinterpret_cast<const double2*>(p.y_in);
+        double2* dst = reinterpret_cast<double2*>(hot_smem);
+        for (int i = threadIdx.x; i < (p.hot_n >> 1); i += blockDim.x) dst[i] = __ldcg(src + i);
+        if ((p.hot_n & 1) && threadIdx.x == 0) hot_smem[p.hot_n - 1] = __ldcg(p.y_in + p.hot_n - 1);
+        p.hot = hot_smem;
+        __syncthreads();
+    }
+    stream_run_dyn(p, a);
+}
+
 // K-FINALIZE (sync sweeps): for every row r of the view
 //   x_t(v) = c + d*S(r)  (Eq.(1) in the "sum, then times d" form; Q-F),
 //   y_t(v) = x_t(v)/outdeg(v) into the next contrib buffer (fused contrib),
@@ -328,6 +348,7 @@ struct FinArgs {
     // the same slot of each peer's buffer (the all-gather fused into K-FINALIZE)
     double* const* peer_y = nullptr;
     int npeer = 0;
+    uint32_t* dyn_reset = nullptr;  // the gather's span counter, zeroed for the next sweep
 };
 
 // Rows are visited grid-stride (all CTAs sweep the row space together, which
@@ -342,6 +363,7 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     __shared__ int flag;
     pdl_wait();
     pdl_trigger();
+    if (f.dyn_reset && blockIdx.x == 0 && threadIdx.x == 0) *f.dyn_reset = 0u;  // the gather has completed
     if (ia.st->done) return;
     double l1 = 0.0, linf = 0.0;
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
@@ -877,6 +899,7 @@ __global__ void __launch_bounds__(SE_NT_IP, 1) k_nosync_stream(InPlacePolicy p, 
 // ------------------------------------------------------------------- host --
 
 struct GatherCfg {
+    bool dyn = false;  // sync: spans handed out dynamically (PRGPU_DYN_SPAN)
     bool stream;  // sync: edge-stream gather + K-FINALIZE; async (or PRGPU_ENGINE=tasks): row-task engine
     bool inplace; // async on the edge-stream engine (k_stream_async; PRGPU_ENGINE=tasks: row-task engine)
     bool fused;   // sync stream sweep with the finalize fused into the gather (k_stream_fused)
@@ -927,6 +950,18 @@ static int launch_gather(Ctx& ctx, const View& v, const double* y_in, double* y_
                 if (sv.nspans == 0) continue;
                 AccumPolicy p{y_in, v.sums, sv.vid, nullptr, 0, 0, 0, {}};
                 PR_LAUNCH_PDL(ctx, k_stream<AccumPolicy>, gc.grid, gc.nt, 0, p, args(sv), (const DevState*)g->st);
+            }
+        } else if (gc.dyn && v.dynv && span_hi < 0 && span_lo == 0) {  // dynamic spans on the finer layout
+            StreamArgs a = args(*v.dynv);
+            a.dyn_ctr = v.dyn_ctr;
+            if (gc.hot_n > 0) {
+                StreamPolicy<true> p{y_in, v.sums, nullptr, gc.hot_n, 0};
+                PR_LAUNCH_PDL(ctx, k_stream_dyn<StreamPolicy<true>>, gc.grid, gc.nt, gc.smem, p, a,
+                              (const DevState*)g->st);
+            } else {
+                StreamPolicy<false> p{y_in, v.sums, nullptr, 0, 0};
+                PR_LAUNCH_PDL(ctx, k_stream_dyn<StreamPolicy<false>>, gc.grid, gc.nt, gc.smem, p, a,
+                              (const DevState*)g->st);
             }
         } else if (gc.hot_n > 0) {
             StreamPolicy<true> p{y_in, v.sums, nullptr, gc.hot_n, 0};
@@ -1104,12 +1139,34 @@ static int reset_tickets(const View& v, cudaStream_t s) {
     if (v.hub_ticket && v.nhubs > 0) PR_CUDA(cudaMemsetAsync(v.hub_ticket, 0, sizeof(uint32_t) * (size_t)v.nhubs, s));
     for (int q = 0; q < v.nseg; ++q) PR_TRY(reset_tickets(v.seg[q], s));
     if (v.phv) PR_TRY(reset_tickets(*v.phv, s));
+    if (v.dynv) {
+        PR_TRY(reset_tickets(*v.dynv, s));
+        PR_CUDA(cudaMemsetAsync(v.dyn_ctr, 0, sizeof(uint32_t), s));
+    }
     return PR_OK;
+}
+
+// PRGPU_DYN_SPAN=F > 0: the sync gather hands out spans of F steps
+// dynamically (built on first use; an aliased reduced view shares the plain
+// view's).  0 / unset: static spans.
+static int ensure_dyn(pr_graph* g, bool reduced, Ctx& ctx, int64_t F) {
+    View& v = reduced ? g->reduced : g->plain;
+    if (v.alias) {
+        PR_TRY(ensure_dyn(g, false, ctx, F));
+        g->reduced = g->plain;
+        g->reduced.alias = true;
+        return PR_OK;
+    }
+    if (v.nseg > 0 || v.nspans == 0) return PR_OK;
+    return build_dyn_view(v, ctx, F);
 }
 
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
         int32_t* iters_out, double* delta_out) {
     if (tasks_engine_requested()) PR_TRY(ensure_tasks(g, (mode & PR_USE_REDUCTIONS) != 0, ctx));
+    const int dyn_f = env_int("PRGPU_DYN_SPAN", 0);
+    const bool dyn = dyn_f > 0 && !(mode & (PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_PERFORATE | PR_MODE_PHASED));
+    if (dyn) PR_TRY(ensure_dyn(g, (mode & PR_USE_REDUCTIONS) != 0, ctx, dyn_f));
     PR_TRY(reset_tickets(g->plain, ctx.stream));
     if (g->pre_done) PR_TRY(reset_tickets(g->reduced, ctx.stream));
     if (mode & PR_MODE_NOSYNC) return run_nosync(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
@@ -1152,6 +1209,13 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     const View& gv = K > 1 ? *v.phv : v;
     GatherCfg gc;
     PR_TRY(gather_config(ctx, gv, g, async, &gc, phased));
+    gc.dyn = dyn && v.dynv != nullptr && gc.stream && !gc.fused;
+    if (gc.dyn) {
+        PR_CUDA(cudaFuncSetAttribute(k_stream_dyn<StreamPolicy<true>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)gc.smem));
+        PR_CUDA(cudaFuncSetAttribute(k_stream_dyn<StreamPolicy<false>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)gc.smem));
+    }
     if (trace_path()) {
         const int64_t nwarps = (int64_t)gc.grid * (gc.nt / 32);
         if (g_trace_n < nwarps) {
@@ -1326,6 +1390,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
             } else if (gc.stream) {
                 FinArgs f = fa;
                 f.y_out = y_out;
+                if (gc.dyn) f.dyn_reset = v.dyn_ctr;
                 PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
             } else if (!gather_finalizes && !gc.inplace) {
                 if (async)
