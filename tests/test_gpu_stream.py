@@ -204,3 +204,35 @@ def test_perforation_can_freeze_everything(pr):
         st, it, fd, x = gpu_run(pr, g, n, 1e-13, max_iter=5000, mode=pr.PR_PERFORATE)
         assert st == pr.PR_OK
         assert np.abs(x - ref.x).max() <= 1e-12
+
+
+@pytest.mark.parametrize("F", [1, 3, 8])
+def test_dynamic_spans_match_oracle(pr, monkeypatch, F):
+    """PRGPU_DYN_SPAN (spans handed out by an atomic counter, next span
+    prefetched): parity with the oracle, plain and reduced, bit-identical
+    across runs (the sums do not depend on which warp takes a span)."""
+    monkeypatch.setenv("PRGPU_DYN_SPAN", str(F))
+    n, edges = G.planted_graph(3, n_base=150, chains=(2, 9, 16, 1))
+    s, t = G.edges_to_arrays(edges)
+    ref_g = oracle.build_csr(n, s, t)
+    ref = oracle.pagerank(ref_g, D, 1e-12, 1000)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        st, it, fd, x = gpu_run(pr, g, n, 1e-12)
+        assert_iters(it, ref, 1e-12)
+        assert_close(x, ref.x)
+        again = gpu_run(pr, g, n, 1e-12)
+        assert again[1] == it and np.array_equal(again[3], x)
+        g.preprocess()
+        rep = oracle.identical(ref_g)
+        _, ck, _ = oracle.chains(ref_g, rep)
+        ref_r = oracle.pagerank(ref_g, D, 1e-12, 1000, reduced=True, rep=rep, chain_k=ck)
+        st, it, fd, xr = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS)
+        assert_iters(it, ref_r, 1e-12)
+        assert_close(xr, ref_r.x)
+    gen = graphgen.make_config(4, scale_override=14)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    ref = oracle.pagerank(ref_g, D, 1e-10, 1000)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        st, it, fd, x = gpu_run(pr, g, gen.n, 1e-10)
+        assert_iters(it, ref, 1e-10)
+        assert_close(x, ref.x)
