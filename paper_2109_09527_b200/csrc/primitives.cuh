@@ -150,9 +150,10 @@ int device_scan(Ctx& ctx, int64_t n, Get get, Emit emit, T* total_dev) {
 // ------------------------------------------------------------ radix sort --
 // LSD radix sort, 8-bit digits, "reduce-then-scan" per pass with a fixed
 // number G of CTAs, each owning a contiguous chunk of the array (stable and
-// deterministic, no look-back).  Large tiles (RS_TILE = 8192 keys per CTA
-// step) keep the number of block barriers per key low and make each digit's
-// run in a tile ~32 keys long, so the write-out is coalesced.
+// deterministic, no look-back).  Tiles of RS_TILE = 4096 keys per CTA step at
+// 2 CTAs/SM (measured best against 3072 / 6144 / 8192) keep the block
+// barriers per key low and each digit's run in a tile ~16 keys long, so the
+// write-out is coalesced.
 #ifndef PRGPU_RS_NT
 #define PRGPU_RS_NT 512
 #endif
