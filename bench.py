@@ -80,7 +80,8 @@ class Clocks:
     """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,timestamp")
+    window = None  # (t0, t1) host times of the timed region: only samples inside count
 
     def __init__(self, index: int):
         self.index = index
@@ -105,7 +106,21 @@ class Clocks:
         self.f.seek(0)
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
+        lines = self.f.read().splitlines()
+        if self.window is not None:
+            import datetime
+            inside = []
+            for line in lines:
+                c = [x.strip() for x in line.split(",")]
+                try:
+                    ts = datetime.datetime.strptime(c[9], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except (IndexError, ValueError):
+                    continue
+                if self.window[0] - 0.05 <= ts <= self.window[1] + 0.05:
+                    inside.append(line)
+            if inside:
+                lines = inside
+        for line in lines:
             c = [x.strip() for x in line.split(",")]
             if len(c) < 9:
                 continue
@@ -416,19 +431,21 @@ def main():
         g.close()
         return {"iters": it, "status": st, "delta": fd, "stats": stats, "info": info, "ev": evs}
 
+    clocks = Clocks(local)
+    clocks.start()  # during the warm-up already: nvidia-smi takes a while to produce its first sample
     for _ in range(W):
         step(src_d, dst_d, x_d)
     torch.cuda.synchronize()
-    clocks = Clocks(local)
     barrier(ws)
     torch.cuda.synchronize()
-    clocks.start()
     e_start = torch.cuda.Event(enable_timing=True)
     e_end = torch.cuda.Event(enable_timing=True)
+    t_wall0 = time.time()
     e_start.record(stream)
     recs = [step(src_d, dst_d, x_d) for _ in range(K)]
     e_end.record(stream)
     torch.cuda.synchronize()
+    clocks.window = (t_wall0, time.time())
     barrier(ws)
     clk = clocks.stop()
     t_ms = e_start.elapsed_time(e_end)
