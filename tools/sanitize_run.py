@@ -35,7 +35,7 @@ MODES = [0, pr.PR_USE_REDUCTIONS, pr.PR_MODE_ASYNC, pr.PR_MODE_ASYNC | pr.PR_USE
          pr.PR_MODE_PHASED | pr.PR_USE_REDUCTIONS]
 
 env_sets = [{}, {"PRGPU_SEG_BITS": "5"}, {"PRGPU_ENGINE": "tasks"}, {"PRGPU_SPAN": "1", "PRGPU_PHASES": "16"},
-            {"PRGPU_FUSED": "1"}]
+            {"PRGPU_FUSED": "1"}, {"PRGPU_DYN_SPAN": "2"}]
 runs = 0
 for envs in env_sets:
     for k, v in envs.items():
