@@ -1319,6 +1319,8 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     int host_syncs = 0;
     int64_t launched = 0;
     int batch = 8;
+    int32_t prev_it = 0;
+    double prev_dn = 0.0;
     while (true) {
         int nb = batch;
         if (launched + nb > max_iter) nb = (int)(max_iter - launched);
@@ -1425,7 +1427,21 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         }
         launched += nb;
         if (hs->done || launched >= max_iter) break;
-        if (batch < 64) batch *= 2;
+        // next batch: the sweeps a geometric fit of the last two batch-end
+        // deltas predicts until the stop test, + 1 (capped at 64; doubling
+        // while there is no fit), so few no-op sweeps are launched past it
+        {
+            const double dn = hs->norm_linf ? hs->linf : hs->l1;
+            int next = batch < 64 ? batch * 2 : 64;
+            if (prev_it > 0 && hs->iters > prev_it && prev_dn > 0.0 && dn > 0.0 && dn < prev_dn && tau > 0.0) {
+                const double rho = pow(dn / prev_dn, 1.0 / (double)(hs->iters - prev_it));
+                const double rem = log(tau / dn) / log(rho);
+                if (rem > 0.0 && rem < 64.0) next = (int)ceil(rem) + 1;
+            }
+            prev_it = hs->iters;
+            prev_dn = dn;
+            batch = next;
+        }
     }
     for (auto e : ev) cudaEventDestroy(e);
     if (const char* tp = trace_path()) {
