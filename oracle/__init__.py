@@ -25,6 +25,8 @@ _lib = None
 NORM_LINF = 1
 REDUCED = 2
 GAUSS_SEIDEL = 4
+BLOCK_GS = 8
+PERFORATE = 16
 
 
 def build(force: bool = False) -> str:
@@ -49,8 +51,10 @@ def _load():
         lib.or_chains.restype = ctypes.c_int
         lib.or_jacobi_step.argtypes = [i64, p, p, p, dbl, p, p]
         lib.or_jacobi_step.restype = None
-        lib.or_pagerank.argtypes = [i64, p, p, p, dbl, dbl, i32, i32, p, p, p, p, p, p]
+        lib.or_pagerank.argtypes = [i64, p, p, p, dbl, dbl, i32, i32, p, p, i32, dbl, p, p, p, p, p, p]
         lib.or_pagerank.restype = ctypes.c_int
+        lib.or_block_bounds.argtypes = [i64, p, p, p, i32, i32, p, p]
+        lib.or_block_bounds.restype = i64
         lib.or_residual_l1.argtypes = [i64, p, p, p, dbl, p, p]
         lib.or_residual_l1.restype = dbl
         _lib = lib
@@ -122,26 +126,47 @@ class Result:
     delta: float
     delta_log: np.ndarray   # (iters, 2): L1, Linf
     seconds: float
+    frozen: np.ndarray | None = None   # perforate: the threshold_check flags at exit
 
 
 def pagerank(g: CSR, d: float = 0.85, tau: float = 1e-10, max_iter: int = 1000, *,
              norm_linf: bool = False, reduced: bool = False, gauss_seidel: bool = False,
+             blocks: int = 0, perforate: bool = False, perf_thr: float = -1.0,
+             x0: np.ndarray | None = None,
              rep: np.ndarray | None = None, chain_k: np.ndarray | None = None) -> Result:
-    """Eq.(1) power iteration (Alg.1); see oracle.c."""
+    """Eq.(1) power iteration (Alg.1); see oracle.c.
+    blocks=K > 0: block Gauss-Seidel in K blocks (reading Q-B); perforate:
+    loop perforation (Alg.5, reading Q-P) with the threshold tau * 1e-5
+     unless perf_thr >= 0; x0: resume from this state."""
     mode = (NORM_LINF if norm_linf else 0) | (REDUCED if reduced else 0) | \
-        (GAUSS_SEIDEL if gauss_seidel else 0)
+        (GAUSS_SEIDEL if gauss_seidel else 0) | (BLOCK_GS if blocks > 0 else 0) | \
+        (PERFORATE if perforate else 0)
     x = np.empty(g.n, np.float64)
     log = np.zeros((max_iter, 2), np.float64)
+    fz = np.zeros(g.n, np.uint8) if perforate else None
+    xi = None if x0 is None else np.ascontiguousarray(x0, np.float64)
     it = ctypes.c_int32(0)
     dl = ctypes.c_double(0.0)
     t0 = time.perf_counter()
     st = _load().or_pagerank(g.n, _p(g.row_ptr), _p(g.col_idx), _p(g.outdeg), d, tau, max_iter,
-                             mode, _p(rep), _p(chain_k), _p(x), _p(log),
-                             ctypes.byref(it), ctypes.byref(dl))
+                             mode, _p(rep), _p(chain_k), int(blocks), float(perf_thr), _p(xi), _p(x), _p(log),
+                             ctypes.byref(it), ctypes.byref(dl), _p(fz))
     sec = time.perf_counter() - t0
     if st not in (0, 2):
         raise ValueError(f"or_pagerank status {st}")
-    return Result(x, it.value, st, dl.value, log[: it.value].copy(), sec)
+    return Result(x, it.value, st, dl.value, log[: it.value].copy(), sec, fz)
+
+
+def block_bounds(g: CSR, K: int, reduced: bool = False, rep=None, chain_k=None):
+    """(rows, bounds): the rows a block Gauss-Seidel sweep gathers, in order,
+    and the K+1 row bounds of its blocks (reading Q-B; see oracle.c)."""
+    rows = np.empty(g.n, np.int32)
+    b = np.empty(K + 1, np.int64)
+    R = _load().or_block_bounds(g.n, _p(g.row_ptr), _p(rep), _p(chain_k), REDUCED if reduced else 0, K,
+                                _p(rows), _p(b))
+    if R < 0:
+        raise ValueError("or_block_bounds: bad arguments")
+    return rows[:R].copy(), b
 
 
 def residual_l1(g: CSR, d: float, x: np.ndarray, want_r: bool = False):
@@ -150,55 +175,3 @@ def residual_l1(g: CSR, d: float, x: np.ndarray, want_r: bool = False):
     r = np.empty(g.n, np.float64) if want_r else None
     v = _load().or_residual_l1(g.n, _p(g.row_ptr), _p(g.col_idx), _p(g.outdeg), d, _p(x), _p(r))
     return (v, r) if want_r else v
-
-
-def phased_sweeps(g: CSR, d: float, sweeps: int, rows: np.ndarray, edge_bounds, row_bounds):
-    """In-place sweeps in a fixed block order -- reading Q-B of
-    No-Sync's in-place update (Alg.3: "pr(u) <- tmp" is visible to
-    every later read), with Eq.(1) per vertex.  Test model of
-    PR_MODE_PHASED, written from that reading, not from the kernels:
-      * `rows` are the vertices of the view in order; the view's edge stream
-        is each row's in-edges in CSR order, one row after the other;
-      * a sweep runs phases k = 0..K-1 in order: phase k adds y(u) =
-        x(u)/outdeg(u), AS IT STANDS WHEN THE PHASE STARTS, for the stream
-        edges [edge_bounds[k], edge_bounds[k+1]) to their rows' sums, then
-        sets x(v) = (1-d)/n + d * S(v) for the rows [row_bounds[k],
-        row_bounds[k+1]) (a row crossing a phase boundary keeps the sums of
-        both phases);
-      * vertices of in-degree 0 take x = (1-d)/n at the end of sweep 1
-        (after every gather of that sweep; constant afterwards, Q-Z).
-    Returns (x, delta_log[(sweeps, 2)] of (L1, Linf) per sweep)."""
-    n = g.n
-    c = (1.0 - d) / n
-    rows = np.asarray(rows, np.int64)
-    od = g.outdeg.astype(np.float64)
-    x = np.full(n, 1.0 / n)
-    y = np.where(g.outdeg > 0, x / np.where(g.outdeg > 0, od, 1.0), 0.0)
-    deg = (g.row_ptr[rows + 1] - g.row_ptr[rows]).astype(np.int64)
-    src = (np.concatenate([g.col_idx[g.row_ptr[v]:g.row_ptr[v + 1]] for v in rows]) if len(rows)
-           else np.zeros(0, np.int32)).astype(np.int64)
-    row_of_edge = np.repeat(np.arange(len(rows)), deg)
-    zero = np.nonzero(np.diff(g.row_ptr) == 0)[0]
-    K = len(edge_bounds) - 1
-    log = np.zeros((sweeps, 2))
-    for t in range(sweeps):
-        xold = x.copy()
-        S = np.zeros(len(rows))
-        for k in range(K):
-            e0, e1 = int(edge_bounds[k]), int(edge_bounds[k + 1])
-            for e in range(e0, e1):                 # sequential: CSR order within each row
-                S[row_of_edge[e]] += y[src[e]]
-            r0, r1 = int(row_bounds[k]), int(row_bounds[k + 1])
-            for i in range(r0, r1):
-                v = rows[i]
-                x[v] = c + d * S[i]
-                if g.outdeg[v] > 0:
-                    y[v] = x[v] / od[v]
-        if t == 0:
-            for v in zero:
-                x[v] = c
-                if g.outdeg[v] > 0:
-                    y[v] = c / od[v]
-        diff = np.abs(x - xold)
-        log[t] = (diff.sum(), diff.max())
-    return x, log

@@ -176,7 +176,7 @@ int or_chains(int64_t n, const int64_t *rp, const int32_t *col, const int32_t *o
 }
 
 /* --------------------------------------------------------------- PageRank -- */
-enum { OR_NORM_LINF = 1, OR_REDUCED = 2, OR_GAUSS_SEIDEL = 4 };
+enum { OR_NORM_LINF = 1, OR_REDUCED = 2, OR_GAUSS_SEIDEL = 4, OR_BLOCK_GS = 8, OR_PERFORATE = 16 };
 
 /*
  * One synchronous (Jacobi) sweep over all vertices, Eq.(1) in the
@@ -196,8 +196,49 @@ void or_jacobi_step(int64_t n, const int64_t *rp, const int32_t *col, const int3
 }
 
 /*
+ * Blocks of the block Gauss-Seidel sweep (reading Q-B: No-Sync's
+ * in-place update, Alg.3, in a FIXED order).  The rows are the
+ * vertices the sweep gathers, in ascending id: every vertex of in-degree > 0
+ * (plain), or (OR_REDUCED) those that are their class representative and not a
+ * chain member.  With E_R the rows' in-edges and off(i) the in-edges of the
+ * rows before row i, block k of K is the rows [b_k, b_{k+1}):
+ *     b_0 = 0,  b_K = R,  b_k = the first i with off(i) * K >= k * E_R,
+ * i.e. a block starts at the first row starting at or after the k-th K-th of
+ * the edges, so no row is split between blocks.
+ * rows_out (nullable, n entries) receives the rows; bounds_out K+1 entries.
+ * Returns R, or -1 on bad arguments.
+ */
+int64_t or_block_bounds(int64_t n, const int64_t *rp, const int32_t *rep, const int32_t *chain_k,
+                        int32_t mode, int32_t K, int32_t *rows_out, int64_t *bounds_out) {
+    if (K < 1 || ((mode & OR_REDUCED) && (!rep || !chain_k))) return -1;
+    int64_t R = 0, ER = 0;
+    for (int64_t v = 0; v < n; ++v) {
+        if (rp[v + 1] == rp[v]) continue;
+        if ((mode & OR_REDUCED) && (rep[v] != v || chain_k[v] > 0)) continue;
+        if (rows_out) rows_out[R] = (int32_t)v;
+        ++R;
+        ER += rp[v + 1] - rp[v];
+    }
+    bounds_out[0] = 0;
+    for (int32_t k = 1; k < K; ++k) bounds_out[k] = R;
+    bounds_out[K] = R;
+    int64_t off = 0, i = 0;
+    for (int64_t v = 0; v < n; ++v) {
+        if (rp[v + 1] == rp[v]) continue;
+        if ((mode & OR_REDUCED) && (rep[v] != v || chain_k[v] > 0)) continue;
+        for (int32_t k = 1; k < K; ++k)
+            if (bounds_out[k] == R && off * (int64_t)K >= (int64_t)k * ER) bounds_out[k] = i;
+        off += rp[v + 1] - rp[v];
+        ++i;
+    }
+    return R;
+}
+
+/*
  * Power iteration to convergence.
- *   x_0 = 1/n ("prPrev(u_i) <- 1/n").
+ *   x_0 = 1/n ("prPrev(u_i) <- 1/n"), or x_init when given (a resumed
+ *   run: the sweeps are memoryless, so running to tau1 and then resuming to
+ *   tau2 < tau1 gives exactly the iterates of one run to tau2).
  *   iterate "while err > threshold" (Q-S): stop at the first t with
  *   Delta_t <= tau, or at t = max_iter (status 2).
  *   Delta_t = sum_v |x_t(v) - x_{t-1}(v)| (L1, BASELINE configs; Q-N) or
@@ -213,21 +254,56 @@ void or_jacobi_step(int64_t n, const int64_t *rp, const int32_t *col, const int3
  *                   increasing distance from the head (Q-C)
  *   OR_GAUSS_SEIDEL in-place ascending sweep (No-Sync with one thread,
  *                   Alg.3)
+ *   OR_BLOCK_GS     block Gauss-Seidel in `nblocks` blocks (or_block_bounds;
+ *                   reading Q-B): block by block, every row of the block gathers
+ *                   x(u)/outdeg(u) as x stands when the block starts (the
+ *                   updates of the earlier blocks of the same sweep visible,
+ *                   Alg.3's in-place pr(u) <- tmp), then the block's
+ *                   rows are updated; after the last block, (with OR_REDUCED)
+ *                   the members as in the reduced mode, then the vertices of
+ *                   in-degree 0 take (1-d)/n (Eq.(1) with an empty sum).
+ *                   nblocks = 1 is the synchronous sweep.
+ *   OR_PERFORATE    loop perforation (Alg.5; reading Q-P), plain
+ *                   synchronous only: a vertex whose change in a sweep is
+ *                   0 != |delta| < tau * 0.00001 (or perf_thr, if >= 0) gets its
+ *                   threshold_check flag set after that sweep, and from the
+ *                   next sweep on is not computed: it keeps its value
+ *                   (|delta| = 0)
  *   | OR_NORM_LINF  use the max norm for the stop test
  * delta_log (nullable) receives (L1, Linf) per iteration: 2*max_iter doubles.
+ * frozen_out (nullable, OR_PERFORATE) receives the flags (0/1 per vertex).
  * Returns 0 converged, 2 max_iter reached, -2 out of memory, 1 bad args.
  */
 int or_pagerank(int64_t n, const int64_t *rp, const int32_t *col, const int32_t *od,
                 double d, double tau, int32_t max_iter, int32_t mode,
-                const int32_t *rep, const int32_t *chain_k,
-                double *x_out, double *delta_log, int32_t *iters_out, double *final_delta) {
+                const int32_t *rep, const int32_t *chain_k, int32_t nblocks, double perf_thr,
+                const double *x_init,
+                double *x_out, double *delta_log, int32_t *iters_out, double *final_delta,
+                uint8_t *frozen_out) {
     if (n < 1 || !(d > 0.0 && d < 1.0) || !(tau >= 0.0) || max_iter < 1) return 1;
     if ((mode & OR_REDUCED) && (!rep || !chain_k)) return 1;
+    if ((mode & OR_BLOCK_GS) && nblocks < 1) return 1;
+    if ((mode & OR_PERFORATE) && (mode & (OR_REDUCED | OR_GAUSS_SEIDEL | OR_BLOCK_GS))) return 1;
     const double c = (1.0 - d) / (double)n;
+    const double tau_f = perf_thr >= 0.0 ? perf_thr : tau * 1e-5;   /* "threshold*0.00001" */
     double *xp = (double *)malloc(sizeof(double) * (size_t)n);
     double *xn = (double *)malloc(sizeof(double) * (size_t)n);
+    double *sb = NULL;                 /* block GS: the sums of one block */
+    int32_t *rows = NULL; int64_t *bb = NULL;
+    uint8_t *frozen = NULL;
     int32_t *by_k = NULL; int64_t *k_start = NULL; int maxk = 0;
     if (!xp || !xn) { free(xp); free(xn); return -2; }
+    if (mode & OR_BLOCK_GS) {
+        rows = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+        bb = (int64_t *)malloc(sizeof(int64_t) * ((size_t)nblocks + 1));
+        sb = (double *)malloc(sizeof(double) * (size_t)n);
+        if (!rows || !bb || !sb) { free(xp); free(xn); free(rows); free(bb); free(sb); return -2; }
+        or_block_bounds(n, rp, rep, chain_k, mode, nblocks, rows, bb);
+    }
+    if (mode & OR_PERFORATE) {
+        frozen = (uint8_t *)calloc((size_t)n, 1);
+        if (!frozen) { free(xp); free(xn); return -2; }
+    }
     if (mode & OR_REDUCED) {
         /* chain members bucketed by distance k from their head */
         for (int64_t v = 0; v < n; ++v) if (chain_k[v] > maxk) maxk = chain_k[v];
@@ -240,7 +316,7 @@ int or_pagerank(int64_t n, const int64_t *rp, const int32_t *col, const int32_t 
         for (int64_t v = 0; v < n; ++v) if (chain_k[v] > 0) by_k[f[chain_k[v]]++] = (int32_t)v;
         free(f);
     }
-    for (int64_t v = 0; v < n; ++v) xp[v] = 1.0 / (double)n;
+    for (int64_t v = 0; v < n; ++v) xp[v] = x_init ? x_init[v] : 1.0 / (double)n;
     int status = 2; int32_t t = 0; double delta = 0.0;
     for (t = 1; t <= max_iter; ++t) {
         nsum_t l1 = { 0.0, 0.0 }; double linf = 0.0;
@@ -254,11 +330,26 @@ int or_pagerank(int64_t n, const int64_t *rp, const int32_t *col, const int32_t 
             }
             memcpy(xn, xp, sizeof(double) * (size_t)n);
         } else {
-            for (int64_t v = 0; v < n; ++v) {
-                if ((mode & OR_REDUCED) && (rep[v] != v || chain_k[v] > 0)) continue;
-                double s = 0.0;
-                for (int64_t e = rp[v]; e < rp[v + 1]; ++e) s += xp[col[e]] / (double)od[col[e]];
-                xn[v] = c + d * s;
+            if (mode & OR_BLOCK_GS) {
+                /* xn is updated in place, block by block; xp keeps x_{t-1} for Delta */
+                memcpy(xn, xp, sizeof(double) * (size_t)n);
+                for (int32_t k = 0; k < nblocks; ++k) {
+                    for (int64_t i = bb[k]; i < bb[k + 1]; ++i) {
+                        int32_t v = rows[i];
+                        double s = 0.0;
+                        for (int64_t e = rp[v]; e < rp[v + 1]; ++e) s += xn[col[e]] / (double)od[col[e]];
+                        sb[i] = s;
+                    }
+                    for (int64_t i = bb[k]; i < bb[k + 1]; ++i) xn[rows[i]] = c + d * sb[i];
+                }
+            } else {
+                for (int64_t v = 0; v < n; ++v) {
+                    if ((mode & OR_REDUCED) && (rep[v] != v || chain_k[v] > 0)) continue;
+                    if (frozen && frozen[v]) { xn[v] = xp[v]; continue; }   /* skipped (Alg.5) */
+                    double s = 0.0;
+                    for (int64_t e = rp[v]; e < rp[v + 1]; ++e) s += xp[col[e]] / (double)od[col[e]];
+                    xn[v] = c + d * s;
+                }
             }
             if (mode & OR_REDUCED) {
                 for (int64_t v = 0; v < n; ++v)          /* identical members */
@@ -269,9 +360,13 @@ int or_pagerank(int64_t n, const int64_t *rp, const int32_t *col, const int32_t 
                         xn[v] = c + d * (xn[p] / (double)od[p]);
                     }
             }
+            if (mode & OR_BLOCK_GS)                      /* in-degree 0: Eq.(1), empty sum */
+                for (int64_t v = 0; v < n; ++v)
+                    if (rp[v + 1] == rp[v]) xn[v] = c;
             for (int64_t v = 0; v < n; ++v) {
                 double a = fabs(xn[v] - xp[v]);
                 nsum_add(&l1, a); if (a > linf) linf = a;
+                if (frozen && !frozen[v] && a != 0.0 && a < tau_f) frozen[v] = 1;
             }
             double *sw = xp; xp = xn; xn = sw;           /* prPrev = pr */
         }
@@ -284,7 +379,8 @@ int or_pagerank(int64_t n, const int64_t *rp, const int32_t *col, const int32_t 
     memcpy(x_out, xp, sizeof(double) * (size_t)n);
     if (iters_out) *iters_out = t;
     if (final_delta) *final_delta = delta;
-    free(xp); free(xn); free(by_k); free(k_start);
+    if (frozen_out && frozen) memcpy(frozen_out, frozen, (size_t)n);
+    free(xp); free(xn); free(by_k); free(k_start); free(rows); free(bb); free(sb); free(frozen);
     return status;
 }
 

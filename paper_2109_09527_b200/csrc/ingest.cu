@@ -1,7 +1,7 @@
 // ingest.cu -- K-INGEST: raw edge list -> deduplicated in-CSR + out-degrees
 // (§5.2 "converted later to Compressed Sparse Row (CSR)
 // format"; SPEC S:69-77 build_csr; readings Q-L, Q-V in DESIGN.md), plus the
-// contrib relabelling and the row-block task lists of the gather engine.
+// contrib relabelling, the plain view and the edge-stream tables of a view.
 //
 // Pipeline (all hand-written kernels):
 //   pack    validate ids, drop self-loops, key = dst << b | src   (b = bits(n-1))
@@ -450,99 +450,17 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
     return PR_OK;
 }
 
-// ------------------------------------------------------------ view tasks --
-// Row blocks: a row r of in-degree <= WT_LONG starts a block iff r == 0, r-1
-// is a long row, or the running weight P(r) (edges + ROW_W per row; long rows
-// weigh 0) crosses a multiple of WT_CAP.  Hence a block has < WT_CAP/ROW_W + 1
-// rows and < WT_CAP + WT_LONG edges.  A long row (in-degree > WT_LONG) becomes
-// ceil(deg / WT_HCH) chunk tasks; rows with several chunks get a Hub record.
-struct WGet {
-    const int64_t* rp;
-    __device__ int64_t operator()(int64_t r) const {
-        int64_t d = rp[r + 1] - rp[r];
-        return d > WT_LONG ? 0 : d + WT_ROW_W;
-    }
-};
-struct WEmit {
-    int64_t* P;
-    __device__ void operator()(int64_t r, int64_t pos, int64_t) const { P[r] = pos; }
-};
-struct StartGet {
-    const int64_t* rp;
-    const int64_t* P;
-    __device__ bool is_long(int64_t r) const { return rp[r + 1] - rp[r] > WT_LONG; }
-    __device__ int64_t operator()(int64_t r) const {
-        if (r == 0 || is_long(r) || is_long(r - 1)) return 1;
-        return (P[r] / WT_CAP) != (P[r - 1] / WT_CAP) ? 1 : 0;
-    }
-};
-struct StartEmit {
-    int64_t* starts;
-    __device__ void operator()(int64_t r, int64_t pos, int64_t f) const {
-        if (f) starts[pos] = r;
-    }
-};
-// per start: low 40 bits = number of tasks, high bits = 1 if the row needs a Hub record
-struct TaskCountGet {
-    const int64_t* rp;
-    const int64_t* starts;
-    __device__ int64_t operator()(int64_t i) const {
-        int64_t r = starts[i];
-        int64_t d = rp[r + 1] - rp[r];
-        if (d > WT_LONG) {
-            int64_t nch = (d + WT_HCH - 1) / WT_HCH;
-            return nch | (nch > 1 ? (1ll << 40) : 0ll);
-        }
-        return 1;
-    }
-};
-struct TaskFillEmit {
-    const int64_t* rp;
-    const int64_t* starts;
-    int64_t nstarts;
-    int64_t nrows;
-    Task* tasks;
-    Hub* hubs;
-    __device__ void operator()(int64_t i, int64_t pos, int64_t v) const {
-        const int64_t r = starts[i];
-        const int64_t toff = pos & ((1ll << 40) - 1);
-        const int64_t hid = pos >> 40;
-        const int64_t rs = rp[r], d = rp[r + 1] - rs;
-        if (d > WT_LONG) {
-            const int32_t nch = (int32_t)(v & ((1ll << 40) - 1));
-            const bool hub = nch > 1;
-            if (hub) hubs[hid] = Hub{(int32_t)rs, nch, (int32_t)toff, 0};
-            for (int32_t j = 0; j < nch; ++j) {
-                const int64_t e0 = rs + (int64_t)j * WT_HCH;
-                const int64_t nnz = min((int64_t)WT_HCH, d - (int64_t)j * WT_HCH);
-                tasks[toff + j] = Task{(int32_t)e0, (int32_t)r, (int32_t)(0x80000000u | (uint32_t)nnz),
-                                       hub ? (int32_t)hid : -1};
-            }
-        } else {
-            const int64_t rend = i + 1 < nstarts ? starts[i + 1] : nrows;
-            const int64_t nnz = rp[rend] - rs;
-            tasks[toff] = Task{(int32_t)rs, (int32_t)r, (int32_t)(((rend - r) << 16) | nnz), -1};
-        }
-    }
-};
-
 void free_view(View& v, cudaStream_t s) {
     if (v.alias) {
         v = View{};
         return;
     }
     free_phase_view(v, s);
-    free_dyn_view(v, s);
     if (v.owns_row_ptr) dfree(v.row_ptr, s);
     v.row_ptr = nullptr;
     dfree(v.col, s);
     dfree(v.vid, s);
-    dfree(v.tasks, s);
-    dfree(v.hubs, s);
-    dfree(v.hub_partial, s);
-    dfree(v.hub_delta, s);
-    dfree(v.hub_ticket, s);
-    v.nrows = v.nedges = v.ntasks = v.nhubs = v.hub_slots = 0;
+    v.nrows = v.nedges = 0;
     dfree(v.sflags, s);
     dfree(v.step_row, s);
     free_spans(v, s);
@@ -556,44 +474,6 @@ void free_view(View& v, cudaStream_t s) {
         v.seg = nullptr;
     }
     v.nseg = 0;
-}
-
-int build_view_tasks(View& v, Ctx& ctx) {
-    cudaStream_t s = ctx.stream;
-    v.ntasks = 0;
-    v.nhubs = 0;
-    if (v.nrows == 0) return PR_OK;
-    int64_t* P = nullptr;
-    int64_t* starts = nullptr;
-    int64_t* scratch = nullptr;
-    PR_TRY(dalloc(&scratch, 2, s));
-    PR_TRY(dalloc(&P, (size_t)v.nrows, s));
-    PR_TRY((device_scan<int64_t>(ctx, v.nrows, WGet{v.row_ptr}, WEmit{P}, (int64_t*)nullptr)));
-    PR_TRY(dalloc(&starts, (size_t)v.nrows, s));
-    PR_TRY((device_scan<int64_t>(ctx, v.nrows, StartGet{v.row_ptr, P}, StartEmit{starts}, scratch)));
-    int64_t nstarts = 0;
-    PR_TRY(read_count(ctx, scratch, &nstarts));
-    // upper bound on tasks: nstarts + sum over hubs of chunks <= nstarts + E / HUB_CHUNK + 1
-    int64_t cap_tasks = nstarts + v.nedges / WT_HCH + 1;
-    int64_t cap_hubs = v.nedges / (WT_HCH + 1) + 1;
-    PR_TRY(dalloc(&v.tasks, (size_t)cap_tasks, s));
-    PR_TRY(dalloc(&v.hubs, (size_t)cap_hubs, s));
-    PR_TRY((device_scan<int64_t>(ctx, nstarts, TaskCountGet{v.row_ptr, starts},
-                                 TaskFillEmit{v.row_ptr, starts, nstarts, v.nrows, v.tasks, v.hubs}, scratch + 1)));
-    int64_t packed = 0;
-    PR_TRY(read_count(ctx, scratch + 1, &packed));
-    v.ntasks = packed & ((1ll << 40) - 1);
-    v.nhubs = packed >> 40;
-    v.hub_slots = v.ntasks;  // slot index == task index of the chunk
-    PR_TRY(dalloc(&v.hub_partial, (size_t)(v.ntasks > 0 ? v.ntasks : 1), s));
-    PR_TRY(dalloc(&v.hub_delta, (size_t)(v.nhubs > 0 ? v.nhubs : 1), s));
-    PR_TRY(dalloc(&v.hub_ticket, (size_t)(v.nhubs > 0 ? v.nhubs : 1), s));
-    PR_CUDA(cudaMemsetAsync(v.hub_ticket, 0, sizeof(uint32_t) * (size_t)(v.nhubs > 0 ? v.nhubs : 1), s));
-    PR_CUDA(cudaMemsetAsync(v.hub_delta, 0, sizeof(double) * (size_t)(v.nhubs > 0 ? v.nhubs : 1), s));
-    dfree(P, s);
-    dfree(starts, s);
-    dfree(scratch, s);
-    return PR_OK;
 }
 
 // ------------------------------------------------------------ view stream --
@@ -726,82 +606,98 @@ void free_spans(View& v, cudaStream_t s) {
     v.nspans = v.nbound = 0;
 }
 
-// PR_MODE_PHASED: a shallow copy of v (sharing its edge stream, rows and sums)
-// with spans K times finer, so each phase's 1/K of the spans still gives every
-// resident warp one span.
-int build_phase_view(View& v, Ctx& ctx, int K) {
+// PR_MODE_PHASED (reading Q-B): K row-aligned phases.  Phase k owns the rows
+// [b_k, b_{k+1}) of the view, b_k = the first row whose first edge e satisfies
+// e * K >= k * E (rows in view order, E the view's edges), so no row is split
+// between phases.  Each phase is its own edge-stream sub-view (a padded copy of
+// its rows' edges with its own row-start bits, steps and spans: one span per
+// resident warp); its gather emits into the parent's sums + b_k.
+__global__ void k_phase_bounds(const int64_t* __restrict__ rp, int64_t nrows, int K, int64_t* __restrict__ rb) {
+    const int k = threadIdx.x;
+    if (k > K) return;
+    const int64_t E = rp[nrows];
+    if (k == 0) {
+        rb[0] = 0;
+        return;
+    }
+    if (k == K) {
+        rb[K] = nrows;
+        return;
+    }
+    int64_t lo = 0, hi = nrows;  // first row r with rp[r] * K >= k * E
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (rp[mid] * (int64_t)K >= (int64_t)k * E)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    rb[k] = lo;
+}
+__global__ void k_rebase_rp(const int64_t* __restrict__ rp, int64_t r0, int64_t cnt, int64_t* __restrict__ out) {
+    const int64_t base = rp[r0];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= cnt; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = rp[r0 + i] - base;
+}
+
+static void free_stream_subview(View& p, cudaStream_t s) {
+    dfree(p.col, s);
+    dfree(p.sflags, s);
+    dfree(p.step_row, s);
+    free_spans(p, s);
+    p = View{};
+}
+
+int build_phase_view(View& v, Ctx& ctx, int K, int32_t pad_slot) {
     if (v.phv && v.phv_k == K) return PR_OK;
     free_phase_view(v, ctx.stream);
-    View* p = new (std::nothrow) View(v);
-    if (!p) {
+    cudaStream_t s = ctx.stream;
+    int64_t* rb = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(rb);
+    PR_TRY(dalloc(&rb, (size_t)K + 1, s));
+    PR_LAUNCH(ctx, k_phase_bounds, 1, 128, 0, (const int64_t*)v.row_ptr, v.nrows, K, rb);
+    PR_CUDA(cudaMemcpyAsync(v.phase_rb, rb, sizeof(int64_t) * (size_t)(K + 1), cudaMemcpyDeviceToHost, s));
+    std::vector<int64_t> eb(K + 1);
+    PR_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k <= K; ++k)  // first edge of each phase: row_ptr at the bounds
+        PR_CUDA(cudaMemcpyAsync(&eb[k], v.row_ptr + v.phase_rb[k], sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k <= K; ++k) v.phase_eb[k] = eb[k];
+    View* ph = new (std::nothrow) View[K];
+    if (!ph) {
         set_error("build_phase_view: host allocation failed");
         return PR_ENOMEM;
     }
-    p->alias = true;  // owns only its span tables (free_phase_view)
-    p->phv = nullptr;
-    p->dynv = nullptr;
-    p->dyn_ctr = nullptr;
-    p->seg = nullptr;
-    p->nseg = 0;
-    p->bin = p->bout = p->b_row = p->b_s0 = p->b_s1 = nullptr;
-    p->part_in = p->part_out = nullptr;
-    p->bticket = nullptr;
-    p->phase_k = 0;
-    const int64_t warps = (int64_t)ctx.num_sms * (SE_NT / 32);
-    int64_t ss = (v.nsteps + warps * K - 1) / (warps * K);
-    if (ss < 1) ss = 1;
-    if (v.span_steps < ss) ss = v.span_steps;  // PRGPU_SPAN overrides stay as fine
-    if (const char* e = getenv("PRGPU_PHASE_SPAN")) {  // tuning override
-        const int64_t o = atoll(e);
-        if (o >= 1) ss = o;
-    }
-    v.phv = p;
+    v.phv = ph;
     v.phv_k = K;
-    return build_spans(*p, ctx, ss);
-}
-
-// PRGPU_DYN_SPAN: a shallow copy of v with spans of span_steps steps, handed
-// out to warps by an atomic counter (k_stream_dyn).
-int build_dyn_view(View& v, Ctx& ctx, int64_t ss) {
-    if (v.dynv && v.dyn_ss == ss) return PR_OK;
-    free_dyn_view(v, ctx.stream);
-    View* p = new (std::nothrow) View(v);
-    if (!p) {
-        set_error("build_dyn_view: host allocation failed");
-        return PR_ENOMEM;
+    for (int k = 0; k < K; ++k) {
+        View& p = ph[k];
+        p.nrows = v.phase_rb[k + 1] - v.phase_rb[k];
+        p.nedges = eb[k + 1] - eb[k];
+        if (p.nrows == 0 || p.nedges == 0) continue;
+        PR_TRY(dalloc(&p.row_ptr, (size_t)p.nrows + 1, s));
+        p.owns_row_ptr = true;
+        PR_LAUNCH(ctx, k_rebase_rp, grid_for(ctx, p.nrows + 1, 256), 256, 0, (const int64_t*)v.row_ptr,
+                  v.phase_rb[k], p.nrows, p.row_ptr);
+        PR_TRY(dalloc(&p.col, (size_t)stream_pad(p.nedges), s));
+        PR_CUDA(cudaMemcpyAsync(p.col, v.col + eb[k], sizeof(int32_t) * (size_t)p.nedges, cudaMemcpyDeviceToDevice,
+                                s));
+        PR_TRY(build_view_stream(p, ctx, pad_slot, nullptr, nullptr));
+        dfree(p.row_ptr, s);  // the stream engine does not read row_ptr
+        p.owns_row_ptr = false;
     }
-    p->alias = true;
-    p->phv = nullptr;
-    p->dynv = nullptr;
-    p->dyn_ctr = nullptr;
-    p->seg = nullptr;
-    p->nseg = 0;
-    p->bin = p->bout = p->b_row = p->b_s0 = p->b_s1 = nullptr;
-    p->part_in = p->part_out = nullptr;
-    p->bticket = nullptr;
-    p->phase_k = 0;
-    v.dynv = p;
-    v.dyn_ss = ss;
-    PR_TRY(dalloc(&v.dyn_ctr, 1, ctx.stream));
-    PR_CUDA(cudaMemsetAsync(v.dyn_ctr, 0, sizeof(uint32_t), ctx.stream));
-    return build_spans(*p, ctx, ss);
-}
-
-void free_dyn_view(View& v, cudaStream_t s) {
-    if (!v.dynv) return;
-    free_spans(*v.dynv, s);
-    delete v.dynv;
-    v.dynv = nullptr;
-    v.dyn_ss = 0;
-    dfree(v.dyn_ctr, s);
+    v.phase_k = K;
+    return PR_OK;
 }
 
 void free_phase_view(View& v, cudaStream_t s) {
     if (!v.phv) return;
-    free_spans(*v.phv, s);
-    delete v.phv;
+    for (int k = 0; k < v.phv_k; ++k) free_stream_subview(v.phv[k], s);
+    delete[] v.phv;
     v.phv = nullptr;
     v.phv_k = 0;
+    v.phase_k = 0;
 }
 
 }  // namespace prgpu

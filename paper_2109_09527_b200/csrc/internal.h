@@ -5,17 +5,6 @@
 
 namespace prgpu {
 
-// Warp-task engine tuning (see rowengine.cuh and DESIGN.md "K-GATHER").
-#ifndef PRGPU_NT
-#define PRGPU_NT 256
-#endif
-#ifndef PRGPU_MIN_CTAS
-#define PRGPU_MIN_CTAS 3
-#endif
-// Contribs with index < GT_L1_TIER (the highest out-degrees) are gathered
-// with L1::evict_last, the rest with L1::no_allocate (measured: 1.57 -> 1.39
-// ms per R-MAT-24 sweep; insensitive to the tier size between 2K and 128K).
-constexpr int GT_L1_TIER = 8192;
 // Edge-stream engine (streamengine.cuh): SE_V edges per lane per step.
 constexpr int SE_V = 8;
 constexpr int SE_STEP = 32 * SE_V;
@@ -35,39 +24,12 @@ constexpr int SE_HOT_MAX = 16384;           // 128 KB of fp64
 constexpr int SE_HOT_IP = 2048;
 constexpr int SE_MAX_PHASES = 64;   // PR_MODE_PHASED: most phases per sweep
 constexpr int SE_L1_TIER = 32768;
+// Source-blocked views (blocked.cu): the sub-view row -> parent row map has this
+// bit set on the row's last segment (the in-place blocked sweep finalizes there).
+constexpr int32_t SEG_LAST = (int32_t)0x80000000u;
 inline int64_t stream_pad(int64_t E) { return ((E > 0 ? E : 1) + SE_STEP - 1) / SE_STEP * SE_STEP; }
-constexpr int GT_NT = PRGPU_NT;              // threads per CTA (independent warps)
-constexpr int GT_MIN_CTAS = PRGPU_MIN_CTAS;  // __launch_bounds__ min CTAs/SM of the gather
-constexpr int WT_CAP = 256;                  // weight budget per row-block task (edges + ROW_W*rows)
-constexpr int WT_ROW_W = 8;                  // per-row weight in edge units
-constexpr int WT_LONG = 128;                 // rows with in-degree > LONG become chunk tasks
-constexpr int WT_HCH = 4096;                 // edges per chunk task (a chunk is <= 11 pieces)
-constexpr int WT_PIECE = 384;                // edges staged per pipeline step (one TMA copy)
-constexpr int WT_SHORT = 16;                 // rows up to this length: one lane sums serially
-constexpr int WT_MAXROWS = WT_CAP / WT_ROW_W + 1;
-constexpr int WT_VALS = WT_PIECE;
-constexpr int WT_COLBUF = WT_PIECE + 8;      // staged col_idx: 3 lead + piece + rounding to 16 B
-static_assert(WT_CAP + WT_LONG <= WT_PIECE, "a row block is one piece");
-static_assert(WT_HCH < 65536 && WT_PIECE % 32 == 0, "task edge bound");
-static_assert(WT_MAXROWS <= 64, "phase B handles rows lane and lane+32");
-
-// A unit of work for one warp (16 bytes).
-//   info >= 0: row block, rows [r0, r0 + (info >> 16)), edges [e0, e0 + (info & 0xffff)).
-//   info <  0: chunk of one long row r0, edges [e0, e0 + (info & 0xffff));
-//              hub = index into View::hubs if the row has several chunks, else -1.
-struct Task {
-    int32_t e0;
-    int32_t r0;
-    int32_t info;
-    int32_t hub;
-};
-
-struct Hub {
-    int32_t row_e0;   // first edge of the row
-    int32_t nchunks;
-    int32_t slot;     // first partial slot of this hub in View::hub_partial
-    int32_t pad;
-};
+// Threads per CTA of the row-parallel kernels (K-FINALIZE, K-ZERO, ...).
+constexpr int GT_NT = 256;
 
 // A set of rows over which the gather runs: all vertices (plain) or the
 // computed representatives R (reduced).  Rows are in increasing vertex id.
@@ -79,14 +41,6 @@ struct View {
     int32_t* col = nullptr;         // int32[nedges] contrib indices (relabelled sources)
     int32_t* vid = nullptr;         // int32[nrows] vertex id of each row (nullptr: identity)
     bool owns_row_ptr = false;
-    Task* tasks = nullptr;
-    int64_t ntasks = 0;
-    Hub* hubs = nullptr;
-    int64_t nhubs = 0;
-    double* hub_partial = nullptr;  // [sum of nchunks]
-    double* hub_delta = nullptr;    // [nhubs] |delta| of each hub row (fixed-order reduce)
-    uint32_t* hub_ticket = nullptr; // [nhubs]
-    int64_t hub_slots = 0;
     // edge-stream engine (build_view_stream; col is padded to nsteps * SE_STEP)
     int64_t nsteps = 0;
     int64_t span_steps = 1;
@@ -110,16 +64,13 @@ struct View {
     int seg_bits = 0;
     View* seg = nullptr;
     int2* rinfo = nullptr;          // [nrows] (outdeg, contrib slot) of the row's vertex, row order
-    // PR_MODE_PHASED (cached per phase count): phase k runs spans
-    // [k*nspans/K, (k+1)*nspans/K) and finalizes rows [phase_rb[k], phase_rb[k+1])
+    // PR_MODE_PHASED (cached per phase count K): phase k gathers and finalizes
+    // the rows [phase_rb[k], phase_rb[k+1]) (row-aligned, build_phase_view)
     int phase_k = 0;
     int64_t phase_rb[SE_MAX_PHASES + 1];
     int64_t phase_eb[SE_MAX_PHASES + 1];  // first edge (view edge order) of each phase, [K] = nedges
-    View* phv = nullptr;            // the view with K-times finer spans (build_phase_view)
+    View* phv = nullptr;            // [phv_k] edge-stream sub-view of each phase's rows
     int phv_k = 0;
-    View* dynv = nullptr;           // finer spans handed out dynamically (PRGPU_DYN_SPAN, build_dyn_view)
-    int64_t dyn_ss = 0;
-    uint32_t* dyn_ctr = nullptr;    // its span counter
 };
 
 // Device-resident iteration state (one per graph).
@@ -207,14 +158,11 @@ struct pr_graph {
 namespace prgpu {
 int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx);
 int build_relabel(pr_graph* g, Ctx& ctx);
-int build_view_tasks(View& v, Ctx& ctx);
 int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx);
 int build_spans(View& v, Ctx& ctx, int64_t span_steps);
 void free_spans(View& v, cudaStream_t s);
-int build_phase_view(View& v, Ctx& ctx, int K);
+int build_phase_view(View& v, Ctx& ctx, int K, int32_t pad_slot);
 void free_phase_view(View& v, cudaStream_t s);
-int build_dyn_view(View& v, Ctx& ctx, int64_t span_steps);
-void free_dyn_view(View& v, cudaStream_t s);
 int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib);
 void free_view(View& v, cudaStream_t s);
 __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const int64_t* __restrict__ rp,

@@ -18,7 +18,6 @@
 
 #include "internal.h"
 #include "primitives.cuh"
-#include "rowengine.cuh"
 #include "streamengine.cuh"
 
 namespace prgpu {

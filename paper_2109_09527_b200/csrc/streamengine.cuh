@@ -48,17 +48,7 @@ struct StreamArgs {
     double* part_in;           // [nspans] (8-byte pieces; reinterpreted for non-fp64 sums)
     double* part_out;          // [nspans]
     uint32_t* bticket;         // [nbound]
-    int64_t span_lo = 0;       // this launch runs spans [span_lo, span_hi) (span_hi < 0: nspans);
-    int64_t span_hi = -1;      // PR_MODE_PHASED runs a sweep as several span ranges
-    unsigned long long* trace = nullptr;  // diagnostics (PRGPU_TRACE): per warp (start, end) globaltimer ns
-    uint32_t* dyn_ctr = nullptr;          // stream_run_dyn: next span to hand out (zeroed before the launch)
 };
-
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 
 __device__ __forceinline__ int4 ld_stream_v4(const int32_t* p, uint64_t pol) {
     int4 r;
@@ -145,13 +135,11 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
         // row starts: warp-exclusive rank of this lane's first start
         const int nf = __popc(f);
         int incl = nf;
-#ifndef PRGPU_ABL_NOISCAN
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const int t = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += t;
         }
-#endif
         const int rank0 = incl - nf;
         const int nst = __shfl_sync(0xffffffffu, incl, 31);
         p.prep((int64_t)R0 - 1 + rank0, f);  // policy may prefetch per-row data of this lane's closures
@@ -177,7 +165,6 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
         if (lane == 0 && nf == 0) o = carry + o;
         T S = o;
         int F = nf > 0;
-#ifndef PRGPU_ABL_NODSCAN
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const T tS = __shfl_up_sync(0xffffffffu, S, d);
@@ -187,7 +174,6 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
                 F = tF;
             }
         }
-#endif
         T I = __shfl_up_sync(0xffffffffu, S, 1);
         if (lane == 0) I = carry;
         carry = __shfl_sync(0xffffffffu, S, 31);
@@ -216,150 +202,12 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
     }
 }
 
-// Dynamic variant of stream_span: the first step's indices, flags and
-// step_row arrive preloaded, and during the last step the first step of the
-// warp's NEXT span (handed out by an atomic counter; t_next = lane 0's
-// ticket) is prefetched, so a warp runs through its spans with no pipeline
-// ramp between them.  Sums are identical to stream_span's for the same span.
-template <class P>
-__device__ __forceinline__ void stream_span_dyn(P& p, const StreamArgs& a, int64_t span, uint64_t pol_stream,
-                                                int4& c0, int4& c1, uint32_t& fn, int32_t& Rn, uint32_t t_next,
-                                                int64_t* next_out, int64_t hi) {
-    const int lane = threadIdx.x & 31;
-    const int64_t sb = span * a.span_steps;
-    const int64_t se = min(a.nsteps, sb + a.span_steps);
-    const int32_t bin = a.bin[span];
-    bool first_closure = true;
-    using T = typename P::T;
-    T carry = T(0);
-    for (int64_t s = sb; s < se; ++s) {
-        T v[SE_V];
-        v[0] = p.load(c0.x);
-        v[1] = p.load(c0.y);
-        v[2] = p.load(c0.z);
-        v[3] = p.load(c0.w);
-        v[4] = p.load(c1.x);
-        v[5] = p.load(c1.y);
-        v[6] = p.load(c1.z);
-        v[7] = p.load(c1.w);
-        const uint32_t f = fn;
-        const int32_t R0 = Rn;
-        int64_t s1 = s + 1;
-        if (s1 >= se) {  // last step: prefetch the next span's first step
-            const int64_t nx = a.span_lo + (int64_t)__shfl_sync(0xffffffffu, t_next, 0);
-            *next_out = nx;
-            s1 = nx < hi ? nx * a.span_steps : -1;
-        }
-        if (s1 >= 0) {
-            const int64_t e1 = s1 * SE_STEP + (int64_t)lane * SE_V;
-            c0 = ld_stream_v4(a.col + e1, pol_stream);
-            c1 = ld_stream_v4(a.col + e1 + 4, pol_stream);
-            fn = ld_stream_u8(a.flags8 + s1 * 32 + lane);
-            Rn = a.step_row[s1];
-        }
-        const int nf = __popc(f);
-        int incl = nf;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += t;
-        }
-        const int rank0 = incl - nf;
-        const int nst = __shfl_sync(0xffffffffu, incl, 31);
-        p.prep((int64_t)R0 - 1 + rank0, f);
-        T run = T(0), head = T(0);
-        int i = 0;
-#pragma unroll
-        for (int j = 0; j < SE_V; ++j) {
-            if (f & (1u << j)) {
-                if (i == 0) {
-                    head = run;
-                } else {
-                    p.emit_at(j, (int64_t)R0 - 1 + rank0 + i, run);
-                }
-                ++i;
-                run = T(0);
-            }
-            run += v[j];
-        }
-        T o = run;
-        if (lane == 0 && nf == 0) o = carry + o;
-        T S = o;
-        int F = nf > 0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const T tS = __shfl_up_sync(0xffffffffu, S, d);
-            const int tF = __shfl_up_sync(0xffffffffu, F, d);
-            if (lane >= d && !F) {
-                S = tS + S;
-                F = tF;
-            }
-        }
-        T I = __shfl_up_sync(0xffffffffu, S, 1);
-        if (lane == 0) I = carry;
-        carry = __shfl_sync(0xffffffffu, S, 31);
-        if (nf > 0) {
-            const T val = I + head;
-            if (rank0 == 0 && first_closure) {
-                if (bin >= 0) stream_piece(p, a, bin, span, val, false);
-            } else {
-                p.emit_first((int64_t)R0 - 1 + rank0, val);
-            }
-        }
-        if (nst > 0) first_closure = false;
-    }
-    if (lane == 0) {
-        if (first_closure) {
-            stream_piece(p, a, bin, span, carry, false);
-        } else {
-            const int32_t bo = a.bout[span];
-            if (bo >= 0) {
-                stream_piece(p, a, bo, span, carry, true);
-            } else {
-                p.emit((int64_t)a.step_row[se] - 1, carry);
-            }
-        }
-    }
-}
-
-// Spans handed out dynamically (a.dyn_ctr), so warps that finish early take
-// more of them and the sweep has no static tail.
-template <class P>
-__device__ __forceinline__ void stream_run_dyn(P& p, const StreamArgs& a) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t pol = policy_evict_first();
-    const int64_t hi = a.span_hi < 0 ? a.nspans : a.span_hi;
-    uint32_t t = 0;
-    if (lane == 0) t = atomicAdd(a.dyn_ctr, 1u);
-    int64_t span = a.span_lo + (int64_t)__shfl_sync(0xffffffffu, t, 0);
-    if (span >= hi) return;
-    const int64_t sb = span * a.span_steps;
-    int4 c0 = ld_stream_v4(a.col + sb * SE_STEP + (int64_t)lane * SE_V, pol);
-    int4 c1 = ld_stream_v4(a.col + sb * SE_STEP + (int64_t)lane * SE_V + 4, pol);
-    uint32_t fn = ld_stream_u8(a.flags8 + sb * 32 + lane);
-    int32_t Rn = a.step_row[sb];
-    while (true) {
-        uint32_t tn = 0;
-        if (lane == 0) tn = atomicAdd(a.dyn_ctr, 1u);  // consumed in the span's last step
-        int64_t nx = hi;
-        stream_span_dyn(p, a, span, pol, c0, c1, fn, Rn, tn, &nx, hi);
-        if (nx >= hi) break;
-        span = nx;
-    }
-}
-
 template <class P>
 __device__ __forceinline__ void stream_run(P& p, const StreamArgs& a) {
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const uint64_t pol = policy_evict_first();
-    const int64_t hi = a.span_hi < 0 ? a.nspans : a.span_hi;
-    const unsigned long long t0 = a.trace ? globaltimer_ns() : 0ull;
-    for (int64_t span = a.span_lo + w; span < hi; span += nw) stream_span(p, a, span, pol);
-    if (a.trace && (threadIdx.x & 31) == 0) {
-        a.trace[2 * w] = t0;
-        a.trace[2 * w + 1] = globaltimer_ns();
-    }
+    for (int64_t span = w; span < a.nspans; span += nw) stream_span(p, a, span, pol);
 }
 
 }  // namespace prgpu

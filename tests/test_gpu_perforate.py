@@ -1,9 +1,11 @@
 """GPU tests of PR_PERFORATE: loop perforation (Barriers-Opt, Alg.5 P:670-707;
-SURVEY §8 f2).  Approximate by design: rows whose change falls to
-0 < |delta| < tau * 1e-5 keep their value and are no longer gathered.  Pinned:
-the work really shrinks (edges gathered over the run < E * sweeps), the frozen
-values are exactly the values the rows had, and the result stays close to the
-oracle's fixed point (the analogue of the paper's L1-norm of Figs.5-6)."""
+SURVEY §8 f2).  Approximate by design: a vertex whose change falls to
+0 < |delta| < tau * 1e-5 gets its sticky threshold_check flag and keeps its
+value from the next sweep on (reading Q-P); flagged rows are compacted out of
+the gather (a performance step only).  Pinned: element-wise parity with the
+oracle's perforated run (oracle.pagerank(perforate=True)), the work really
+shrinks (edges gathered over the run < E * sweeps), and the result stays close
+to the fixed point (the analogue of the paper's L1-norm of Figs.5-6)."""
 import numpy as np
 import pytest
 
@@ -40,6 +42,12 @@ def test_perforation_saves_work_and_stays_close(pr, cfg, scale):
     assert s["compactions"] >= 1 and s["frozen_rows"] > 0
     assert s["edges_gathered"] < s["gather_edges"] * it_p
     assert s["edges_gathered"] < full_work
+    # element-wise parity with the oracle's perforated run (same flags rule);
+    # a flag decided differently near the threshold moves a value by < tau*1e-5
+    ref_p = oracle.pagerank(ref_g, D, gen.tau, 1000, perforate=True)
+    assert abs(it_p - ref_p.iters) <= 1, (it_p, ref_p.iters)
+    assert np.abs(xp - ref_p.x).max() <= 1e-10 and np.abs(xp - ref_p.x).sum() <= 1e-9
+    assert abs(s["frozen_rows"] - int(ref_p.frozen.sum())) <= max(10, 0.01 * ref_p.frozen.sum())
     l1 = np.abs(xp - tight.x).sum()
     l1_exact = np.abs(exact - tight.x).sum()
     # approximate, but within a few thousand times the exact run's own error

@@ -1,8 +1,11 @@
-"""GPU tests of PR_MODE_PHASED: in-place sweeps in K ordered phases (block
-Gauss-Seidel, DESIGN.md Q-B; the in-place reads of Alg.3 P:545-565 in a fixed
-order).
+"""GPU tests of PR_MODE_PHASED: in-place sweeps in K ordered, row-aligned
+phases (block Gauss-Seidel, DESIGN.md Q-B; the in-place reads of Alg.3
+P:545-565 in a fixed order).
 
 Pins, none of which uses the CUDA path as its own reference:
+  * element-wise parity with the oracle's block Gauss-Seidel sweep
+    (oracle.pagerank(blocks=K), which derives its blocks itself from the rule
+    of reading Q-B), sweep by sweep and converged, plain and reduced;
   * one phase is an in-place Jacobi sweep: bit-identical to PR_MODE_SYNC
     (ranks and sweep count), whose parity with the oracle is pinned elsewhere;
   * K phases reach the oracle's fixed point (residual certificate of the
@@ -151,28 +154,61 @@ def test_phased_mode_validation(pr):
             assert e.value.code == pr.PR_EINVAL
 
 
-@pytest.mark.parametrize("name", ["planted0", "random", "in_star", "path"])
-@pytest.mark.parametrize("phases", ["3", "8"])
-def test_phased_trajectory_matches_block_model(pr, monkeypatch, name, phases):
-    """Element-wise parity of the first sweeps with the oracle's model of the
-    phased sweep (oracle.phased_sweeps, reading Q-B) driven by the library's
-    own phase plan (pr_get_phase_plan): which edges each phase gathers and
-    which rows it updates.  One-step spans put rows across phase boundaries."""
+def _oracle_reductions(ref_g):
+    rep = oracle.identical(ref_g)
+    _, ck, _ = oracle.chains(ref_g, rep)
+    return rep, ck
+
+
+@pytest.mark.parametrize("name", ["planted0", "planted3", "random", "in_star", "path"])
+@pytest.mark.parametrize("phases", ["2", "3", "8", "64"])
+def test_phased_matches_oracle_block_gs(pr, monkeypatch, name, phases):
+    """Sweep by sweep (tau = 0, 1 and 3 sweeps) and converged, plain and
+    reduced: the GPU's phased run equals the oracle's block Gauss-Seidel run
+    with the same K element by element; the GPU's phase plan equals the blocks
+    the oracle derives from the rule (row bounds)."""
     monkeypatch.setenv("PRGPU_PHASES", phases)
-    monkeypatch.setenv("PRGPU_SPAN", "1")
+    monkeypatch.setenv("PRGPU_SPAN", "1")  # many spans: boundary rows inside the phases
+    K = int(phases)
     n, edges = GRAPHS[name]()
     s, t = G.edges_to_arrays(edges)
     ref_g = oracle.build_csr(n, s, t)
-    rows = np.nonzero(np.diff(ref_g.row_ptr) > 0)[0]
+    rep, ck = _oracle_reductions(ref_g)
     with pr.Graph(n, dev(s), dev(t)) as g:
-        for sweeps in (1, 3):
-            st, it, fd, x = run(pr, g, n, 0.0, pr.PR_MODE_PHASED, max_iter=sweeps)
-            eb, rb = pr.pr_get_phase_plan(g.handle)
-            assert eb[0] == 0 and eb[-1] == ref_g.E and rb[0] == 0 and rb[-1] == len(rows)
-            assert len(eb) - 1 == g.stats()["phases"]
-            xm, log = oracle.phased_sweeps(ref_g, D, sweeps, rows, eb, rb)
-            np.testing.assert_allclose(x, xm, rtol=1e-13, atol=1e-18)
-            np.testing.assert_allclose(g.delta_log()[:, 0], log[:, 0], rtol=1e-9, atol=1e-18)
+        g.preprocess()
+        for reduced in (False, True):
+            extra = pr.PR_USE_REDUCTIONS if reduced else 0
+            kw = {"reduced": True, "rep": rep, "chain_k": ck} if reduced else {}
+            for sweeps in (1, 3):
+                st, it, fd, x = run(pr, g, n, 0.0, pr.PR_MODE_PHASED | extra, max_iter=sweeps)
+                assert it == sweeps and g.stats()["phases"] == K
+                ref = oracle.pagerank(ref_g, D, 0.0, sweeps, blocks=K, **kw)
+                np.testing.assert_allclose(x, ref.x, rtol=1e-13, atol=1e-18)
+                np.testing.assert_allclose(g.delta_log()[:, 0], ref.delta_log[:, 0], rtol=1e-9, atol=1e-18)
+            eb, rb = pr.pr_get_phase_plan(g.handle, reduced)
+            _, ob = oracle.block_bounds(ref_g, K, reduced, rep, ck)
+            assert rb.tolist() == ob.tolist()
+            st, it, fd, x = run(pr, g, n, 1e-12, pr.PR_MODE_PHASED | extra)
+            ref = oracle.pagerank(ref_g, D, 1e-12, 2000, blocks=K, **kw)
+            assert st == pr.PR_OK and abs(it - ref.iters) <= 1
+            if it != ref.iters:
+                assert abs(ref.delta - 1e-12) <= 1e-3 * 1e-12
+            assert np.abs(x - ref.x).max() <= TOL_V and np.abs(x - ref.x).sum() <= 1e-9
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_phased_configs_match_oracle_block_gs(pr, monkeypatch, cfg):
+    """Configs 2 and 3 at their tau, 8 phases: iteration count within +/-1
+    and ranks within 1e-10 of the oracle's block Gauss-Seidel run (plain)."""
+    monkeypatch.setenv("PRGPU_PHASES", "8")
+    gen = graphgen.make_config(cfg)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    ref = oracle.pagerank(ref_g, D, gen.tau, gen.max_iter, blocks=8)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        st, it, fd, x = run(pr, g, gen.n, gen.tau, pr.PR_MODE_PHASED)
+        assert st == pr.PR_OK and g.stats()["phases"] == 8
+        assert abs(it - ref.iters) <= 1
+        assert np.abs(x - ref.x).max() <= TOL_V and np.abs(x - ref.x).sum() <= 1e-9
 
 
 def test_phase_plan_errors(pr):

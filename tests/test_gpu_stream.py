@@ -7,7 +7,7 @@ K-FINALIZE.  Its result must not depend on how the edge array is cut:
     association -> oracle tolerance, iteration count +/-1 rule;
   * the shared-memory hot tier (PRGPU_HOT) changes only WHERE a contrib is
     read from -> bit-identical ranks and Delta logs;
-  * the legacy row-task engine (PRGPU_ENGINE=tasks) -> oracle tolerance.
+  * source-blocked views (PRGPU_SEG_BITS) -> oracle tolerance, in every mode.
 """
 import numpy as np
 import pytest
@@ -93,21 +93,6 @@ def test_hot_tier_is_bit_identical(pr, monkeypatch):
             assert np.array_equal(r[4], rs[0][4])
 
 
-def test_task_engine_agrees(pr, monkeypatch):
-    gen = graphgen.make_config(4, scale_override=13)
-    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
-    ref = oracle.pagerank(ref_g, D, 1e-10, 1000)
-    out = {}
-    for eng in ("stream", "tasks"):
-        monkeypatch.setenv("PRGPU_ENGINE", eng)
-        with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
-            st, it, fd, x = gpu_run(pr, g, gen.n, 1e-10)
-            assert_iters(it, ref, 1e-10)
-            assert_close(x, ref.x)
-            out[eng] = x
-    assert np.abs(out["stream"] - out["tasks"]).max() <= 1e-15
-
-
 def test_stream_deterministic_across_graph_builds(pr):
     gen = graphgen.make_config(2, scale_override=16)
     xs = []
@@ -152,31 +137,12 @@ def test_blocked_rmat(pr, monkeypatch):
         assert_close(x, ref.x)
 
 
-def test_fused_sweep_matches_split(pr, monkeypatch):
-    """K-GATHER with the finalize fused in (PRGPU_FUSED=1, measured slower) vs
-    the default split K-GATHER + K-FINALIZE: same S per row, same update
-    formula, so the ranks are bit-identical (the Delta sums may differ in their
-    last bits)."""
-    gen = graphgen.make_config(4, scale_override=15)
-    out = {}
-    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
-        g.preprocess()
-        for fused in ("1", "0"):
-            monkeypatch.setenv("PRGPU_FUSED", fused)
-            for mode in (0, pr.PR_USE_REDUCTIONS):
-                out[(fused, mode)] = gpu_run(pr, g, gen.n, 0.0, max_iter=40, mode=mode)
-    for mode in (0, pr.PR_USE_REDUCTIONS):
-        a, b = out[("1", mode)], out[("0", mode)]
-        assert a[1] == b[1] == 40
-        assert np.array_equal(a[3], b[3])
-
-
 @pytest.mark.parametrize("bits", [4, 8])
 def test_blocked_views_with_every_mode(pr, monkeypatch, bits):
-    """Source-blocked views only change the synchronous gather; the in-place
-    modes (which use the unblocked tables), the No-Sync certificate (a blocked
-    sync gather) and perforation (blocked first, unblocked after compaction)
-    must all still reach the oracle's fixed point."""
+    """Source-blocked views: the in-place modes run the in-place blocked sweep
+    (rows finalized in their last segment's pass), No-Sync adds its
+    certificate (a blocked sync gather), perforation runs blocked first,
+    unblocked after compaction -- all must reach the oracle's fixed point."""
     monkeypatch.setenv("PRGPU_SEG_BITS", str(bits))
     n, s, t = hub_graph(seed=11)
     ref_g = oracle.build_csr(n, s, t)
@@ -204,35 +170,3 @@ def test_perforation_can_freeze_everything(pr):
         st, it, fd, x = gpu_run(pr, g, n, 1e-13, max_iter=5000, mode=pr.PR_PERFORATE)
         assert st == pr.PR_OK
         assert np.abs(x - ref.x).max() <= 1e-12
-
-
-@pytest.mark.parametrize("F", [1, 3, 8])
-def test_dynamic_spans_match_oracle(pr, monkeypatch, F):
-    """PRGPU_DYN_SPAN (spans handed out by an atomic counter, next span
-    prefetched): parity with the oracle, plain and reduced, bit-identical
-    across runs (the sums do not depend on which warp takes a span)."""
-    monkeypatch.setenv("PRGPU_DYN_SPAN", str(F))
-    n, edges = G.planted_graph(3, n_base=150, chains=(2, 9, 16, 1))
-    s, t = G.edges_to_arrays(edges)
-    ref_g = oracle.build_csr(n, s, t)
-    ref = oracle.pagerank(ref_g, D, 1e-12, 1000)
-    with pr.Graph(n, dev(s), dev(t)) as g:
-        st, it, fd, x = gpu_run(pr, g, n, 1e-12)
-        assert_iters(it, ref, 1e-12)
-        assert_close(x, ref.x)
-        again = gpu_run(pr, g, n, 1e-12)
-        assert again[1] == it and np.array_equal(again[3], x)
-        g.preprocess()
-        rep = oracle.identical(ref_g)
-        _, ck, _ = oracle.chains(ref_g, rep)
-        ref_r = oracle.pagerank(ref_g, D, 1e-12, 1000, reduced=True, rep=rep, chain_k=ck)
-        st, it, fd, xr = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS)
-        assert_iters(it, ref_r, 1e-12)
-        assert_close(xr, ref_r.x)
-    gen = graphgen.make_config(4, scale_override=14)
-    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
-    ref = oracle.pagerank(ref_g, D, 1e-10, 1000)
-    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
-        st, it, fd, x = gpu_run(pr, g, gen.n, 1e-10)
-        assert_iters(it, ref, 1e-10)
-        assert_close(x, ref.x)

@@ -345,53 +345,136 @@ def test_gauss_seidel_is_in_place_sweep():
     np.testing.assert_allclose(r.x, [x_0, x_1, x_2], rtol=1e-15)
 
 
-# ---- the phased-sweep model (reading Q-B), pinned to Jacobi and Gauss-Seidel
-def _phased_inputs(n, edges):
-    from tests import graphs as G
-    s, t = G.edges_to_arrays(edges)
-    g = oracle.build_csr(n, s, t)
-    rows = np.nonzero(np.diff(g.row_ptr) > 0)[0]
-    return g, rows
+# ---- block Gauss-Seidel (reading Q-B) and loop perforation (Alg.5, Q-P) --
+BGS = json.load(open(os.path.join(HERE, "golden", "block_gs_examples.json")))
 
 
-def test_phased_model_one_phase_is_jacobi():
-    """One phase over the whole stream = the synchronous sweep (Eq.(1))."""
-    from tests import graphs as G
-    n = 120
-    g, rows = _phased_inputs(n, G.random_edges(n, 500, 5) + [(0, 1)])
-    E = int(g.row_ptr[-1])
-    x, log = oracle.phased_sweeps(g, 0.85, 4, rows, [0, E], [0, len(rows)])
-    ref = oracle.pagerank(g, 0.85, 0.0, 4)
-    assert np.array_equal(x, ref.x)
-    np.testing.assert_allclose(log, ref.delta_log, rtol=1e-12, atol=1e-18)
+def _frac(s):
+    from fractions import Fraction
+    return float(Fraction(s))
 
 
-def test_phased_model_one_row_per_phase_is_gauss_seidel():
-    """One row per phase, rows ascending, every vertex with in-edges = the
-    in-place ascending sweep (Alg.3 with one thread), bit for bit."""
-    from tests import graphs as G
+@pytest.mark.parametrize("ex", BGS["block_gs"], ids=lambda e: e["name"])
+def test_block_gs_hand_examples(ex):
+    """Hand-derived sweeps (tests/golden/block_gs_examples.json): block bounds
+    (no row split at a boundary), in-place reads of the earlier blocks, Jacobi
+    reads inside a block, in-degree-0 vertices after the blocks, and Delta."""
+    g = csr_of(ex["n"], ex["edges"])
+    _, b = oracle.block_bounds(g, ex["K"])
+    assert b.tolist() == ex["bounds"]
+    r = oracle.pagerank(g, ex["d"], 0.0, ex["sweeps"], blocks=ex["K"])
+    assert r.iters == ex["sweeps"]
+    np.testing.assert_allclose(r.x, [_frac(s) for s in ex["x"]], rtol=1e-15)
+    np.testing.assert_allclose(r.delta_log[:, 0], [_frac(s) for s in ex["l1"]], rtol=1e-14)
+    np.testing.assert_allclose(r.delta_log[:, 1], [_frac(s) for s in ex["linf"]], rtol=1e-14)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_block_bounds_rule_brute_force(seed):
+    """b_k = the first row whose first edge e has e*K >= k*E, over the rows a
+    sweep gathers (in-degree > 0; reduced: representatives, not chain
+    members), checked against a direct scan of every row start."""
+    n, edges = G.planted_graph(300 + seed, n_base=60, chains=(4, 7))
+    g = csr_of(n, edges)
+    rep = oracle.identical(g)
+    _, ck, _ = oracle.chains(g, rep)
+    deg = np.diff(g.row_ptr)
+    for reduced in (False, True):
+        keep = deg > 0
+        if reduced:
+            keep &= (rep == np.arange(n)) & (ck == 0)
+        rows_bf = np.nonzero(keep)[0]
+        starts = np.concatenate([[0], np.cumsum(deg[rows_bf])])
+        E = int(starts[-1])
+        for K in (1, 2, 3, 5, 17, E + 3):
+            rows, b = oracle.block_bounds(g, K, reduced, rep, ck)
+            assert rows.tolist() == rows_bf.tolist()
+            want = [0] + [next((i for i in range(len(rows_bf)) if starts[i] * K >= k * E), len(rows_bf))
+                          for k in range(1, K)] + [len(rows_bf)]
+            assert b.tolist() == want
+
+
+def test_block_gs_one_block_is_jacobi():
+    """K = 1 is the synchronous sweep, bit for bit (plain and reduced)."""
+    n, edges = G.planted_graph(5, n_base=120, chains=(9, 3))
+    g = csr_of(n, edges)
+    rep = oracle.identical(g)
+    _, ck, _ = oracle.chains(g, rep)
+    for kw in ({}, {"reduced": True, "rep": rep, "chain_k": ck}):
+        a = oracle.pagerank(g, D, 1e-13, 500, **kw)
+        b = oracle.pagerank(g, D, 1e-13, 500, blocks=1, **kw)
+        assert a.iters == b.iters and np.array_equal(a.x, b.x)
+        np.testing.assert_allclose(a.delta_log, b.delta_log, rtol=1e-12, atol=1e-18)
+
+
+def test_block_gs_one_row_per_block_is_gauss_seidel():
+    """A block per row (K = E puts a boundary at every row start) on a graph
+    where every vertex has in-edges = the ascending in-place sweep (Alg.3 with
+    one thread), bit for bit."""
     n = 90
-    edges = G.cycle(n) + G.random_edges(n, 300, 8)     # every vertex has in-degree >= 1
-    g, rows = _phased_inputs(n, edges)
-    assert len(rows) == n
-    eb = list(g.row_ptr)                              # a phase boundary at every row start
-    rb = list(range(n + 1))
-    x, log = oracle.phased_sweeps(g, 0.85, 5, rows, eb, rb)
-    ref = oracle.pagerank(g, 0.85, 0.0, 5, gauss_seidel=True)
-    np.testing.assert_allclose(x, ref.x, rtol=1e-15, atol=0)
-    np.testing.assert_allclose(log[:, 1], ref.delta_log[:, 1], rtol=1e-12, atol=1e-18)
+    g = csr_of(n, G.cycle(n) + G.random_edges(n, 300, 8))
+    assert (np.diff(g.row_ptr) > 0).all()
+    r = oracle.pagerank(g, D, 0.0, 6, blocks=g.E)
+    gs = oracle.pagerank(g, D, 0.0, 6, gauss_seidel=True)
+    assert np.array_equal(r.x, gs.x)
 
 
-def test_phased_model_reaches_the_fixed_point():
-    """Any block order converges to the same fixed point (Lemma 2)."""
-    from tests import graphs as G
-    n = 150
-    g, rows = _phased_inputs(n, G.random_edges(n, 600, 13))
-    E = int(g.row_ptr[-1])
-    eb = [0, E // 3, (2 * E) // 3, E]
-    # rows ending in each edge range
-    ends = g.row_ptr[rows + 1]
-    rb = [0] + [int(np.searchsorted(ends, b, side="right")) for b in eb[1:-1]] + [len(rows)]
-    x, _ = oracle.phased_sweeps(g, 0.85, 200, rows, eb, rb)
-    tight = oracle.pagerank(g, 0.85, 1e-15, 2000)
-    assert np.abs(x - tight.x).max() <= 1e-12
+@pytest.mark.parametrize("case", _dense_cases()[:5], ids=lambda c: c[0])
+@pytest.mark.parametrize("K", [2, 3, 8])
+def test_block_gs_reaches_dense_solve(case, K):
+    """Any block order reaches the fixed point of (I - dM)x = c1 (Lemma 2,
+    P:607-628), plain and reduced."""
+    _, n, edges = case
+    xs, _ = G.dense_pagerank(n, edges, D)
+    g = csr_of(n, edges)
+    rep = oracle.identical(g)
+    _, ck, _ = oracle.chains(g, rep)
+    for kw in ({}, {"reduced": True, "rep": rep, "chain_k": ck}):
+        r = oracle.pagerank(g, D, 1e-14, 5000, blocks=K, **kw)
+        assert r.status == 0 and np.abs(r.x - xs).sum() <= 1e-12
+
+
+@pytest.mark.parametrize("ex", BGS["perforate"], ids=lambda e: e["name"])
+def test_perforate_hand_example(ex):
+    g = csr_of(ex["n"], ex["edges"])
+    r = oracle.pagerank(g, ex["d"], ex["tau"], ex["max_iter"], perforate=True, perf_thr=ex["perf_thr"])
+    assert r.iters == ex["iters"] and r.status == 0
+    np.testing.assert_allclose(r.x, [_frac(s) for s in ex["x"]], rtol=1e-15)
+    assert r.frozen.tolist() == ex["frozen"]
+    np.testing.assert_allclose(r.delta_log[:, 0], [_frac(s) for s in ex["l1"]], rtol=1e-14, atol=1e-17)
+
+
+def test_perforate_default_threshold_and_no_freeze_is_jacobi():
+    """The threshold is tau * 1e-5: with tau = 0 nothing can freeze
+    and the run is the synchronous one bit for bit; with perf_thr = 0 too."""
+    n, edges = G.planted_graph(9, n_base=150, chains=(5,))
+    g = csr_of(n, edges)
+    a = oracle.pagerank(g, D, 0.0, 60)
+    for kw in ({}, {"perf_thr": 0.0}):
+        b = oracle.pagerank(g, D, 0.0, 60, perforate=True, **kw)
+        assert np.array_equal(a.x, b.x) and not b.frozen.any()
+    # tau > 0: the default threshold is tau * 1e-5 exactly
+    t = 1e-9
+    c1 = oracle.pagerank(g, D, t, 500, perforate=True)
+    c2 = oracle.pagerank(g, D, t, 500, perforate=True, perf_thr=t * 1e-5)
+    assert c1.iters == c2.iters and np.array_equal(c1.x, c2.x) and np.array_equal(c1.frozen, c2.frozen)
+
+
+def test_perforate_frozen_values_are_constant():
+    """A flagged vertex keeps the value of the sweep that flagged it: the
+    flags of a run cut at sweep t are a subset of those at t + k, and the
+    vertices flagged at t have the same value at t + k."""
+    import graphgen
+    s, t = graphgen.rmat(14, 16 << 14, seed=3)
+    g = oracle.build_csr(1 << 14, s, t)
+    tau = 1e-10
+    runs = [oracle.pagerank(g, D, tau, m, perforate=True) for m in (80, 90, 100, 500)]
+    for a, b in zip(runs, runs[1:]):
+        fa = a.frozen.astype(bool)
+        assert (b.frozen.astype(bool) | ~fa).all()
+        assert np.array_equal(a.x[fa], b.x[fa])
+    assert runs[-1].frozen.sum() > 0
+    # approximate: near, not at, the fixed point
+    exact = oracle.pagerank(g, D, 1e-14, 2000)
+    err = np.abs(runs[-1].x - exact.x).sum()
+    assert err <= 1e-6

@@ -34,8 +34,7 @@ MODES = [0, pr.PR_USE_REDUCTIONS, pr.PR_MODE_ASYNC, pr.PR_MODE_ASYNC | pr.PR_USE
          pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS, pr.PR_PERFORATE, pr.PR_NORM_LINF, pr.PR_MODE_PHASED,
          pr.PR_MODE_PHASED | pr.PR_USE_REDUCTIONS]
 
-env_sets = [{}, {"PRGPU_SEG_BITS": "5"}, {"PRGPU_ENGINE": "tasks"}, {"PRGPU_SPAN": "1", "PRGPU_PHASES": "16"},
-            {"PRGPU_FUSED": "1"}, {"PRGPU_DYN_SPAN": "2"}]
+env_sets = [{}, {"PRGPU_SEG_BITS": "5"}, {"PRGPU_SPAN": "1", "PRGPU_PHASES": "16"}, {"PRGPU_PHASES": "3"}]
 runs = 0
 for envs in env_sets:
     for k, v in envs.items():
@@ -46,8 +45,6 @@ for envs in env_sets:
             g.preprocess()
             x = torch.empty(n, dtype=torch.float64, device="cuda")
             for m in MODES:
-                if envs.get("PRGPU_ENGINE") and m & pr.PR_PERFORATE:
-                    continue
                 g.run(x, 0.85, 1e-12, 300, mode=m)
                 runs += 1
             rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
