@@ -13,7 +13,7 @@ region (E = deduplicated edges).  Multi-GPU is "replicas only":
 each rank runs its own replica, scaling is weak.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4]
-       python bench.py --impl reference ...   (the CPU fp64 oracle, bounded sample)
+       python bench.py --impl reference ...   (the CPU fp64 oracle: whole sweeps of the full graph)
 """
 from __future__ import annotations
 
@@ -176,58 +176,85 @@ def barrier(ws):
 
 
 # --------------------------------------------------------------- reference --
-def cpu_sample(gen, iters_whole: int, sweeps: int, warm: int = 0, frac: int = 4):
-    """Bounded oracle sample (~10-30 s of one core): the oracle's CSR build and
-    `sweeps` timed Jacobi sweeps on the graph made of the first 1/frac of the
-    raw edges (same n, same generator order, so the same degree and locality
-    structure), extrapolated linearly in edges to the full edge list and to a
-    whole job of `iters_whole` iterations."""
-    import oracle
-    ms = gen.m // frac
-    src, dst = gen.src[:ms], gen.dst[:ms]
-    t0 = time.perf_counter()
-    c = oracle.build_csr(gen.n, src, dst)
-    t_build = time.perf_counter() - t0
-    if warm:
-        oracle.pagerank(c, gen.d, 0.0, warm)
-    per = []
-    for _ in range(sweeps):
-        r = oracle.pagerank(c, gen.d, 0.0, 1)
-        per.append(r.seconds)
-    t_sweep = statistics.mean(per)
-    scale = gen.m / max(1, ms)
-    t_job = scale * (t_build + iters_whole * t_sweep)
-    E_full = c.E * scale
-    return {"E_sample": c.E, "t_build": t_build, "t_sweep": t_sweep, "t_job": t_job, "frac": frac,
-            "value": E_full * iters_whole / t_job / 1e9, "sweeps": sweeps, "raw_edges": ms}
+class OracleBaseline:
+    """The CPU oracle (oracle/oracle.c: single-threaded fp64 C, -O2, as it
+    stands) on the FULL graph of the workload, measured on this host: its CSR
+    build, (reduced mode) its identical-group and chain preprocessing, then
+    whole Jacobi sweeps, each timed (no sampling, no scaling).  GTEPS per
+    iteration = E / sweep time."""
+
+    def __init__(self, gen, mode: str):
+        import oracle
+        self.oracle = oracle
+        self.gen = gen
+        self.mode = mode
+        t0 = time.perf_counter()
+        self.g = oracle.build_csr(gen.n, gen.src, gen.dst)
+        self.t_build = time.perf_counter() - t0
+        self.kw = {}
+        self.t_pre = 0.0
+        if mode == "reduced":
+            t0 = time.perf_counter()
+            rep = oracle.identical(self.g)
+            _, ck, _ = oracle.chains(self.g, rep)
+            self.t_pre = time.perf_counter() - t0
+            self.kw = {"reduced": True, "rep": rep, "chain_k": ck}
+        self.x = None
+        self.sweeps = []
+
+    def sweep(self):
+        """One whole sweep from the current state (x_0 = 1/n first)."""
+        r = self.oracle.pagerank(self.g, self.gen.d, 0.0, 1, x0=self.x, **self.kw)
+        self.x = r.x
+        self.sweeps.append(r.seconds)
+        return r.seconds
+
+    def gteps(self, times):
+        return self.g.E / statistics.mean(times) / 1e9
+
+    def describe(self, times):
+        return (f"oracle (oracle/oracle.c, single-threaded C -O2 fp64, 1 core of this host's {os.cpu_count()}) on "
+                f"the full {self.gen.name} graph (E={self.g.E}): CSR build {self.t_build:.2f} s"
+                + (f", identical groups + chains {self.t_pre:.2f} s" if self.mode == "reduced" else "")
+                + f", then {len(times)} whole {self.mode} Jacobi sweeps timed one by one "
+                  f"(mean {statistics.mean(times):.3f} s, min {min(times):.3f} s, max {max(times):.3f} s); "
+                  f"value = E / mean sweep time (GTEPS per iteration); nothing scaled or extrapolated")
 
 
-def describe_sample(s, gen, iters):
-    return (f"oracle (single-threaded C, -O2, 1 core; host has {os.cpu_count()} cores): CSR build "
-            f"({s['t_build']:.2f} s) and {s['sweeps']} Jacobi sweeps ({s['t_sweep']:.3f} s each) on the graph of "
-            f"the first 1/{s['frac']} of the {gen.name} raw edges ({s['raw_edges']} edges, E={s['E_sample']}), "
-            f"scaled x{s['frac']} to the full edge list and extrapolated to {iters} iterations (the oracle's "
-            f"own count, tests/golden/config_iters.json); preprocessing not included")
+def workload_config(gen, args, ws):
+    """The workload identity both arms report (measured quantities go elsewhere)."""
+    return {"workload": gen.name, "n": gen.n, "m_raw": gen.m, "d": gen.d, "tau": gen.tau, "norm": "L1",
+            "mode": args.mode, "parallelism": f"replicas{ws}" if args.parallel == "replicas" else f"shard{ws}",
+            "l2": "inputs larger than L2 (edge list 8m bytes)"}
 
 
 def run_reference(args, ws, rank):
+    """--impl reference: the oracle as it stands, on the host cores, on our
+    arm's config and metric.  Setup (untimed, reported): graph generation, the
+    oracle's CSR build (+ preprocessing in reduced mode).  Then W warm-up and K
+    timed steps, one step = one whole oracle sweep of the full graph."""
     import graphgen
     if rank != 0:
         return 0
     gen = graphgen.make_config(args.config)
-    red_it, plain_it = oracle_iters(args.config)
-    iters = red_it or plain_it or 100
-    s = cpu_sample(gen, iters, sweeps=max(1, args.steps), warm=max(0, min(args.warmup, 1)))
+    ob = OracleBaseline(gen, args.mode)
+    for _ in range(args.warmup):
+        ob.sweep()
+    t0 = time.perf_counter()
+    times = [ob.sweep() for _ in range(max(1, args.steps))]
+    t_all = time.perf_counter() - t0
+    value = ob.g.E * len(times) / t_all / 1e9
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(s["value"], 5), "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(s["t_job"] * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+        "ms_per_step": round(t_all / len(times) * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": gen.name, "n": gen.n, "m_raw": gen.m, "tau": gen.tau, "d": gen.d,
-                   "iterations": iters, "mode": "plain sync (oracle)"},
-        "cpu_baseline": {"value": round(s["value"], 5), "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": describe_sample(s, gen, iters)},
-        "e2e": {"value": round(s["value"], 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": workload_config(gen, args, 1),
+        "run": {"E": ob.g.E, "oracle_csr_build_s": round(ob.t_build, 3),
+                "oracle_preprocess_s": round(ob.t_pre, 3), "timed_region_s": round(t_all, 3)},
+        "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": ob.describe(times)},
+        "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -360,12 +387,10 @@ def run_shard_bench(args, ws, rank, local, dev, pr, torch, gen, W, K):
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": round(t / K, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": gen.name, "n": n, "m_raw": gen.m, "E": E, "d": gen.d, "tau": gen.tau,
-                       "norm": "L1", "mode": "plain", "iterations": iters, "parallelism": f"shard{ws}",
-                       "backend": args.backend if ws > 1 else None, "exchange": args.exchange,
-                       "l2": "inputs larger than L2 (edge list 8m bytes)",
-                       "time_to_converge_ms": round(run_ms, 3), "create_and_shard_ms": round(setup_ms, 3),
-                       "rank0_shard": recs[0]["info"]},
+            "config": dict(workload_config(gen, args, ws), mode="plain", backend=args.backend if ws > 1 else None,
+                           exchange=args.exchange),
+            "run": {"E": E, "iterations": iters, "time_to_converge_ms": round(run_ms, 3),
+                    "create_and_shard_ms": round(setup_ms, 3), "rank0_shard": recs[0]["info"]},
             "roofline": roofline,
             "cpu_baseline": None,
             "e2e": {"value": round(E * er["iters"] / (te * 1e-3) / 1e9, 4), "unit": UNIT,
@@ -567,25 +592,36 @@ def main():
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        red_it, plain_it = oracle_iters(args.config)
-        iters = (red_it if args.mode == "reduced" else plain_it) or recs[0]["iters"]
-        s = cpu_sample(gen, iters, sweeps=2)
-        cpu = {"value": round(s["value"], 5), "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": describe_sample(s, gen, iters)}
+        ob = OracleBaseline(gen, args.mode if args.mode != "async" else "plain")
+        times = [ob.sweep() for _ in range(2)]
+        cpu = {"value": round(ob.gteps(times), 6), "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": ob.describe(times), "csr_build_s": round(ob.t_build, 3),
+               "preprocess_s": round(ob.t_pre, 3)}
+
+    # every timed step must have converged with the oracle's iteration count
+    # (+/-1: SURVEY c3; the count of the config, tests/golden/config_iters.json)
+    red_it, plain_it = oracle_iters(args.config)
+    ref_it = red_it if args.mode == "reduced" else (plain_it if args.mode == "plain" else None)
+    bad = [r for r in recs if r["status"] != pr.PR_OK]
+    if ref_it is not None:
+        bad += [r for r in recs if abs(r["iters"] - ref_it) > 1]
+    check = {"status_ok": all(r["status"] == pr.PR_OK for r in recs),
+             "oracle_iterations": ref_it, "iterations": sorted({r["iters"] for r in recs}),
+             "valid": not bad}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": round(t_max / K, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": gen.name, "n": n, "m_raw": m, "E": E, "d": gen.d, "tau": gen.tau,
-                       "norm": "L1", "mode": args.mode, "iterations": recs[0]["iters"],
-                       "parallelism": f"replicas{ws}", "l2": "inputs larger than L2 (edge list 8m bytes)",
-                       "time_to_converge_ms": round(phase["run_ms"], 3),
-                       "time_to_converge_min_max_ms": [round(min(run_all), 3), round(max(run_all), 3)],
-                       "create_ms": round(phase["create_ms"], 3),
-                       "preprocess_ms": round(phase["preprocess_ms"], 3),
-                       "n_members": recs[0]["info"]["n_members"]},
+            "config": workload_config(gen, args, ws),
+            "run": {"E": E, "iterations": recs[0]["iters"],
+                    "time_to_converge_ms": round(phase["run_ms"], 3),
+                    "time_to_converge_min_max_ms": [round(min(run_all), 3), round(max(run_all), 3)],
+                    "create_ms": round(phase["create_ms"], 3),
+                    "preprocess_ms": round(phase["preprocess_ms"], 3),
+                    "n_members": recs[0]["info"]["n_members"]},
+            "check": check,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -598,6 +634,10 @@ def main():
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if bad:
+        print(f"bench: INVALID -- {len(bad)} timed step(s) did not converge with the oracle's iteration count "
+              f"({check})", file=sys.stderr)
+        return 1
     return 0
 
 

@@ -139,8 +139,18 @@ int pr_preprocess(pr_graph *g, uint32_t flags, void *stream);
 int pr_run(pr_graph *g, double d, double threshold, int32_t max_iter, void *stream,
            uint32_t mode, double *ranks, int32_t *iters_out, double *final_delta_out);
 
-/* pr_destroy -- release every device buffer of g.  NULL-safe. */
+/* pr_destroy -- release every device buffer of g.  NULL-safe.  Waits for the
+ * work the last call on g enqueued (on whatever stream it used) to finish, then
+ * returns the buffers to the library's memory pool. */
 void pr_destroy(pr_graph *g);
+
+/* pr_release_memory -- return the device memory the library's private pool
+ * keeps for reuse (all library allocations come from that pool, never from the
+ * process's default pool; freed blocks stay reserved in it so a later
+ * pr_graph_create does not map memory mid-call) to the device.  Synchronises
+ * the device.  Safe with live graphs (only unused blocks are released).
+ * Returns PR_OK or PR_ECUDA. */
+int pr_release_memory(void);
 
 /* pr_last_error -- message for the last failing call on this thread ("" if none). */
 const char *pr_last_error(void);

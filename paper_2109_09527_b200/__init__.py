@@ -41,7 +41,7 @@ PR_MODE_PHASED = 64
 
 # every symbol include/prgpu.h declares (tests check the .so exports them)
 ABI_SYMBOLS = (
-    "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_last_error",
+    "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_release_memory", "pr_last_error",
     "pr_graph_info", "pr_get_csr", "pr_get_reductions", "pr_get_delta_log", "pr_get_run_stats",
     "pr_graph_shard", "pr_run_sharded", "pr_get_shard_info", "pr_get_phase_plan",
     "pr_shard_buffers", "pr_shard_set_peers", "pr_shard_export_ipc", "pr_shard_open_ipc",
@@ -119,6 +119,8 @@ def _load():
     lib.pr_run.restype = ctypes.c_int
     lib.pr_destroy.argtypes = [p]
     lib.pr_destroy.restype = None
+    lib.pr_release_memory.argtypes = []
+    lib.pr_release_memory.restype = ctypes.c_int
     lib.pr_last_error.argtypes = []
     lib.pr_last_error.restype = ctypes.c_char_p
     lib.pr_graph_info.argtypes = [p, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32)]
@@ -169,6 +171,26 @@ def _ptr(a) -> int | None:
     raise TypeError(type(a))
 
 
+def _numel(a) -> int:
+    if hasattr(a, "numel"):
+        return int(a.numel())
+    return int(a.size)
+
+
+def _out(a, dtype: str, need: int, what: str):
+    """Address of a caller-owned output buffer the library writes `need`
+    elements of `dtype` into: checked for dtype, contiguity and length (a
+    float32 or short buffer would be a silent out-of-bounds write)."""
+    if a is None:
+        return None
+    dt = str(getattr(a, "dtype", ""))
+    if not dt.endswith(dtype):
+        raise TypeError(f"{what} must be {dtype}, got {dt}")
+    if _numel(a) < need:
+        raise ValueError(f"{what} holds {_numel(a)} elements, needs {need}")
+    return _ptr(a)
+
+
 def _stream(stream) -> int | None:
     if stream is None:
         try:
@@ -216,7 +238,8 @@ def pr_run(g, d: float, threshold: float, max_iter: int, ranks, stream=None, mod
     """Iterate to convergence; returns (status, iterations, final_delta)."""
     it = ctypes.c_int32(0)
     fd = ctypes.c_double(0.0)
-    rc = _check(lib.pr_run(g, d, threshold, max_iter, _stream(stream), mode, _ptr(ranks),
+    rptr = _out(ranks, "float64", pr_graph_info(g)["n"], "ranks")
+    rc = _check(lib.pr_run(g, d, threshold, max_iter, _stream(stream), mode, rptr,
                            ctypes.byref(it), ctypes.byref(fd)), ok=(PR_OK, PR_NOT_CONVERGED))
     return rc, it.value, fd.value
 
@@ -233,11 +256,20 @@ def pr_graph_info(g):
 
 
 def pr_get_csr(g, row_ptr, col_idx, outdeg, stream=None) -> None:
-    _check(lib.pr_get_csr(g, _ptr(row_ptr), _ptr(col_idx), _ptr(outdeg), _stream(stream)))
+    inf = pr_graph_info(g)
+    _check(lib.pr_get_csr(g, _out(row_ptr, "int64", inf["n"] + 1, "row_ptr"), _out(col_idx, "int32", inf["E"], "col_idx"),
+                          _out(outdeg, "int32", inf["n"], "outdeg"), _stream(stream)))
 
 
 def pr_get_reductions(g, rep, chain_src, chain_k, stream=None) -> None:
-    _check(lib.pr_get_reductions(g, _ptr(rep), _ptr(chain_src), _ptr(chain_k), _stream(stream)))
+    n = pr_graph_info(g)["n"]
+    _check(lib.pr_get_reductions(g, _out(rep, "int32", n, "rep"), _out(chain_src, "int32", n, "chain_src"),
+                                 _out(chain_k, "int32", n, "chain_k"), _stream(stream)))
+
+
+def pr_release_memory() -> None:
+    """Return the library pool's unused device memory to the device."""
+    _check(lib.pr_release_memory())
 
 
 def pr_get_delta_log(g, cap: int):
@@ -373,7 +405,8 @@ def pr_run_sharded(g, d: float, threshold: float, max_iter: int, ranks, exchange
     cb = EXCHANGE_FN(_cb)
     it = ctypes.c_int32(0)
     fd = ctypes.c_double(0.0)
-    rc = lib.pr_run_sharded(g, d, threshold, max_iter, _stream(stream), mode, _ptr(ranks), cb, None,
+    rptr = _out(ranks, "float64", pr_graph_info(g)["n"], "ranks")
+    rc = lib.pr_run_sharded(g, d, threshold, max_iter, _stream(stream), mode, rptr, cb, None,
                             ctypes.byref(it), ctypes.byref(fd))
     if err:
         raise err[0]

@@ -35,39 +35,57 @@ bool pdl_enabled() {  // PRGPU_PDL=0 turns programmatic dependent launch off (me
     return on;
 }
 
+// One private pool per device (created on first use, release threshold
+// UINT64_MAX: freed memory is kept for the next graph instead of being
+// unmapped at every synchronisation -- re-mapping GBs costs tens of ms per
+// pr_graph_create).  The process's default pool is left as the caller set it.
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pools[64] = {};
+
+cudaMemPool_t lib_pool() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (!g_pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool;
+        if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        cudaGetLastError();
+        g_pools[dev] = pool;
+    }
+    return g_pools[dev];
+}
+
 static int make_ctx(Ctx& ctx, void* stream) {
     ctx.stream = (cudaStream_t)stream;
     ctx.launches = 0;
     int dev = 0;
     PR_CUDA(cudaGetDevice(&dev));
     PR_CUDA(cudaDeviceGetAttribute(&ctx.num_sms, cudaDevAttrMultiProcessorCount, dev));
-    // Keep freed stream-ordered memory in the device pool instead of returning
-    // it to the OS at every synchronisation (re-mapping GBs per call otherwise
-    // costs tens of ms per pr_graph_create).
-    static bool pool_tuned[64] = {false};
-    if (dev >= 0 && dev < 64 && !pool_tuned[dev]) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        cudaGetLastError();
-        pool_tuned[dev] = true;
-    }
     return PR_OK;
 }
 
-// Grow the device pool once to `bytes` (allocate + free), so that later
+// Grow the library pool once to `bytes` (allocate + free), so that later
 // stream-ordered allocations are carved from memory the pool already holds
 // instead of mapping new memory in the middle of a call (measured: up to
 // 60 ms per pr_graph_create under allocation churn otherwise).
 static void pool_reserve(cudaStream_t s, size_t bytes) {
     const char* e = getenv("PRGPU_POOL_RESERVE");
     if (e && e[0] == '0') return;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    cudaMemPool_t pool = lib_pool();
+    if (!pool) return;
     uint64_t have = 0;
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &have);
     if (have >= bytes) return;
@@ -75,8 +93,22 @@ static void pool_reserve(cudaStream_t s, size_t bytes) {
     cudaMemGetInfo(&fr, &tot);
     if (bytes > have + fr / 2) bytes = have + fr / 2;  // never take more than half of what is free
     void* p = nullptr;
-    if (bytes > have && cudaMallocAsync(&p, bytes - have, s) == cudaSuccess) cudaFreeAsync(p, s);
+    if (bytes > have && cudaMallocFromPoolAsync(&p, bytes - have, pool, s) == cudaSuccess) cudaFreeAsync(p, s);
     cudaGetLastError();
+}
+
+// Every call that enqueues work records the graph's event on its stream at the
+// end; pr_destroy waits for it before releasing the buffers (the caller's
+// stream may be non-blocking, and pr_run may return with k_unpermute still
+// reading them when the ranks are in device memory).
+static void mark_done(pr_graph* g, cudaStream_t s) {
+    if (!g) return;
+    if (!g->fin_ev && cudaEventCreateWithFlags(&g->fin_ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        g->fin_ev = nullptr;
+        return;
+    }
+    if (cudaEventRecord(g->fin_ev, s) != cudaSuccess) cudaGetLastError();
 }
 
 // Pinned host copies of the per-graph DevState come from one process-wide
@@ -194,6 +226,18 @@ extern "C" {
 
 const char* pr_last_error(void) { return g_err; }
 
+int pr_release_memory(void) {
+    g_err[0] = 0;
+    cudaMemPool_t pool = lib_pool();
+    if (!pool) {
+        set_error("pr_release_memory: no library pool on this device");
+        return PR_ECUDA;
+    }
+    PR_CUDA(cudaDeviceSynchronize());  // frees still pending on some stream land first
+    PR_CUDA(cudaMemPoolTrimTo(pool, 0));
+    return PR_OK;
+}
+
 int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst, void* stream, pr_graph** out) {
     g_err[0] = 0;
     if (!out) {
@@ -280,9 +324,11 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
     if (rc != PR_OK) {
         dfree(dsrc, ctx.stream);
         dfree(ddst, ctx.stream);
+        mark_done(g, ctx.stream);
         pr_destroy(g);
         return rc;
     }
+    mark_done(g, ctx.stream);
     *out = g;
     return PR_OK;
 }
@@ -301,6 +347,7 @@ int pr_preprocess(pr_graph* g, uint32_t flags, void* stream) {
     PR_TRY(make_ctx(ctx, stream));
     int rc = preprocess(g, flags, ctx);
     g->launches += ctx.launches;
+    mark_done(g, ctx.stream);
     if (rc == PR_OK) PR_CUDA(cudaStreamSynchronize(ctx.stream));
     return rc;
 }
@@ -349,6 +396,7 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
     PR_TRY(make_ctx(ctx, stream));
     int rc = run(g, d, threshold, max_iter, mode, ranks, ctx, iters_out, final_delta_out);
     g->launches += ctx.launches;
+    mark_done(g, ctx.stream);
     g->last.total_launches = g->launches;
     return rc;
 }
@@ -367,6 +415,7 @@ int pr_graph_shard(pr_graph* g, int32_t rank, int32_t world, void* stream) {
     PR_TRY(make_ctx(ctx, stream));
     int rc = build_shard(g, rank, world, ctx);
     g->launches += ctx.launches;
+    mark_done(g, ctx.stream);
     if (rc != PR_OK) {
         clear_shard(g, ctx.stream);
         return rc;
@@ -416,6 +465,7 @@ int pr_run_sharded(pr_graph* g, double d, double threshold, int32_t max_iter, vo
     int rc = run_sharded(g, d, threshold, max_iter, mode, ranks, ctx, exchange, exchange_ctx, iters_out,
                          final_delta_out);
     g->launches += ctx.launches;
+    mark_done(g, ctx.stream);
     g->last.total_launches = g->launches;
     return rc;
 }
@@ -540,6 +590,14 @@ int pr_get_shard_info(const pr_graph* g, pr_shard_info* out) {
 
 void pr_destroy(pr_graph* g) {
     if (!g) return;
+    // the last call's work on its stream must be complete before its buffers
+    // return to the pool (they are then freed, stream-ordered, on stream 0)
+    if (g->fin_ev) {
+        cudaEventSynchronize(g->fin_ev);
+        cudaEventDestroy(g->fin_ev);
+        g->fin_ev = nullptr;
+    }
+    cudaGetLastError();
     cudaStream_t s = 0;
     PhaseTimer pt(s, "destroy");
     clear_shard(g, s);

@@ -77,13 +77,20 @@ struct Ctx {
     int64_t launches;
 };
 
+// The library's own stream-ordered memory pool on the current device (api.cu):
+// freed blocks stay in it for later graphs (no re-mapping in the middle of a
+// call) without touching the process's default pool; pr_release_memory()
+// returns them to the device.
+cudaMemPool_t lib_pool();
+
 // Stream-ordered allocation; all library memory comes from here.
 template <class T>
 int dalloc(T** p, size_t count, cudaStream_t s) {
     *p = nullptr;
     size_t bytes = count * sizeof(T) + 64;  // +64: vector tails may read past the end
     const auto t0 = std::chrono::steady_clock::now();
-    cudaError_t e = cudaMallocAsync((void**)p, bytes, s);
+    cudaMemPool_t pool = lib_pool();
+    cudaError_t e = pool ? cudaMallocFromPoolAsync((void**)p, bytes, pool, s) : cudaMallocAsync((void**)p, bytes, s);
     g_alloc_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (e != cudaSuccess) {
         set_error("cudaMallocAsync(%zu bytes): %s", bytes, cudaGetErrorString(e));

@@ -153,6 +153,7 @@ struct pr_graph {
     prgpu::DevState* st_host = nullptr;  // pinned
     int64_t launches = 0;
     pr_run_stats last{};
+    cudaEvent_t fin_ev = nullptr;   // recorded at the end of every call (pr_destroy waits for it)
 };
 
 namespace prgpu {

@@ -154,9 +154,12 @@ def test_blocked_views_with_every_mode(pr, monkeypatch, bits):
             st, it, fd, x = gpu_run(pr, g, n, 1e-12, max_iter=5000, mode=mode)
             assert st == pr.PR_OK
             assert np.abs(x - tight.x).max() <= 1e-10, mode
+        # perforation (Alg.5): a vertex can freeze where its change crosses zero,
+        # so the result is compared with the oracle's perforated run, not x*
         st, it, fd, x = gpu_run(pr, g, n, 1e-12, mode=pr.PR_PERFORATE)
-        assert st == pr.PR_OK
-        assert np.abs(x - tight.x).sum() <= 1e-6
+        ref_p = oracle.pagerank(ref_g, D, 1e-12, 1000, perforate=True)
+        assert st == pr.PR_OK and abs(it - ref_p.iters) <= 1
+        assert np.abs(x - ref_p.x).max() <= 1e-10 and np.abs(x - ref_p.x).sum() <= 1e-9
 
 
 def test_perforation_can_freeze_everything(pr):
