@@ -35,9 +35,22 @@ __device__ __forceinline__ int4 ldg_stream(const int4* p) {
 
 // Each warp handles chunks of 32*4*U edges; per step a lane loads U int4 of
 // indices and then issues 4U independent gathers.
+// cold-tier gathers: 0 = L1::no_allocate, 1 = L1::evict_first (allocated, first
+// to go: a lane's next gathers to the same sector hit), 2 = default caching
+__device__ __forceinline__ double ldg_cold(const double* p, int cold) {
+    double r;
+    if (cold == 1)
+        asm volatile("ld.global.nc.L1::evict_first.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    else if (cold == 2)
+        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    else
+        asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+
 template <int U, bool HOT>
 __global__ void __launch_bounds__(1024) k_flat(const int32_t* __restrict__ col, int64_t E, const double* __restrict__ y,
-                                              int hot_n, int tier, double* out) {
+                                              int hot_n, int tier, double* out, int cold) {
     extern __shared__ double hot[];
     if (HOT) {
         for (int i = threadIdx.x; i < hot_n; i += blockDim.x) hot[i] = y[i];
@@ -66,9 +79,9 @@ __global__ void __launch_bounds__(1024) k_flat(const int32_t* __restrict__ col, 
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (HOT) {
-                    v[4 * u + j] = q[j] < hot_n ? hot[q[j]] : (q[j] < tier ? ldg_el(y + q[j]) : ldg_na(y + q[j]));
+                    v[4 * u + j] = q[j] < hot_n ? hot[q[j]] : (q[j] < tier ? ldg_el(y + q[j]) : ldg_cold(y + q[j], cold));
                 } else {
-                    v[4 * u + j] = q[j] < tier ? ldg_el(y + q[j]) : ldg_na(y + q[j]);
+                    v[4 * u + j] = q[j] < tier ? ldg_el(y + q[j]) : ldg_cold(y + q[j], cold);
                 }
             }
         }
@@ -77,6 +90,9 @@ __global__ void __launch_bounds__(1024) k_flat(const int32_t* __restrict__ col, 
     }
     out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
+
+static int g_cold = 0;
+extern "C" void ceiling_set_cold(int c) { g_cold = c; }
 
 extern "C" int ceiling_run(const int32_t* col, int64_t E, const double* y, int hot_n, int unroll, int ctas_per_sm,
                            int reps, int threads, int tier, double* out, float* ms_out) {
@@ -92,9 +108,9 @@ extern "C" int ceiling_run(const int32_t* col, int64_t E, const double* y, int h
     if (unroll == U) {                                                                                  \
         if (hot_n > 0) {                                                                                \
             cudaFuncSetAttribute(k_flat<U, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-            k_flat<U, true><<<grid, threads, smem>>>(col, E, y, hot_n, tier, out);                                \
+            k_flat<U, true><<<grid, threads, smem>>>(col, E, y, hot_n, tier, out, g_cold);                                \
         } else {                                                                                        \
-            k_flat<U, false><<<grid, threads, 0>>>(col, E, y, 0, tier, out);                                      \
+            k_flat<U, false><<<grid, threads, 0>>>(col, E, y, 0, tier, out, g_cold);                                      \
         }                                                                                               \
     }
         L(1) L(2) L(4) L(8)
