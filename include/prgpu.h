@@ -73,6 +73,16 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
                                  is 0 < |delta| < threshold * 1e-5 keeps its value from then on
                                  and is no longer gathered (APPROXIMATE: the result is not the
                                  fixed point; the stop test counts frozen vertices as 0). */
+#define PR_CHAIN_EAGER  128u  /* with PR_USE_REDUCTIONS in the synchronous mode: resolve chain
+                                 members in the SAME sweep from their head's new value (reading
+                                 Q-C as first written; information crosses a chain in one sweep,
+                                 but the sweep no longer conserves the plain iteration's
+                                 invariants, e.g. sum(x) = 1 without dangling vertices).  Default
+                                 (delayed, reading Q-C2): x_t(v_k) = alpha_j + beta_j *
+                                 x_{t-j}(source), j = min(k, t) -- Eq.(1) unrolled along the chain,
+                                 so the reduced sweep reproduces the plain (Jacobi) trajectory
+                                 while still gathering no chain member.  The phased, async and
+                                 No-Sync modes always resolve members eagerly (in place). */
 #define PR_MODE_PHASED   64u  /* in-place sweeps in K ordered phases (block Gauss-Seidel; Q-B):
                                  one contrib buffer; phase k gathers a contiguous 1/K of the
                                  edge stream and finalizes the rows ending in it, so it reads

@@ -38,6 +38,7 @@ PR_TIMING = 8
 PR_MODE_NOSYNC = 16
 PR_PERFORATE = 32
 PR_MODE_PHASED = 64
+PR_CHAIN_EAGER = 128
 
 # every symbol include/prgpu.h declares (tests check the .so exports them)
 ABI_SYMBOLS = (

@@ -372,7 +372,7 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
         return PR_EINVAL;
     }
     if (mode & ~(PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_NORM_LINF | PR_USE_REDUCTIONS | PR_TIMING | PR_PERFORATE |
-                 PR_MODE_PHASED)) {
+                 PR_MODE_PHASED | PR_CHAIN_EAGER)) {
         set_error("pr_run: unknown mode bits 0x%x", mode);
         return PR_EINVAL;
     }
@@ -616,6 +616,7 @@ void pr_destroy(pr_graph* g) {
     dfree(g->mem_k, s);
     dfree(g->mem_srow, s);
     dfree(g->mem_info, s);
+    dfree(g->mem_h, s);
     dfree(g->xr, s);
     dfree(g->xm, s);
     dfree(g->x, s);
@@ -623,6 +624,7 @@ void pr_destroy(pr_graph* g) {
     dfree(g->y[1], s);
     dfree(g->cta_partial, s);
     dfree(g->ab, s);
+    dfree(g->hist, s);
     dfree(g->delta_log, s);
     dfree(g->st, s);
     pinned_state_free(g->st_host);

@@ -77,18 +77,6 @@ struct SegRunEmit {
 
 __global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
 
-// last[parent row] = q for every row of segment q (launched in segment order,
-// so the final value is the row's last segment)
-__global__ void k_seg_last(const int32_t* __restrict__ vid, int64_t nr, uint8_t q, uint8_t* __restrict__ last) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x)
-        last[vid[i]] = q;
-}
-// mark the rows of segment q whose last segment it is (SEG_LAST)
-__global__ void k_seg_mark(int32_t* __restrict__ vid, int64_t nr, uint8_t q, const uint8_t* __restrict__ last) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x)
-        if (last[vid[i]] == q) vid[i] |= SEG_LAST;
-}
-
 int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib) {
     cudaStream_t s = ctx.stream;
     v.nseg = 0;
@@ -171,19 +159,6 @@ int build_view_blocked(View& v, Ctx& ctx, int64_t n_contrib) {
         dfree(sv.row_ptr, s);  // the stream engine does not read row_ptr
         sv.owns_row_ptr = false;
     }
-    // the in-place blocked sweep (iterate.cu) finalizes a row in its last segment
-    uint8_t* last = nullptr;
-    tg_.track(last);
-    PR_TRY(dalloc(&last, (size_t)v.nrows, s));
-    for (int q = 0; q < nseg; ++q)
-        if (v.seg[q].nrows > 0)
-            PR_LAUNCH(ctx, k_seg_last, (unsigned)std::min<int64_t>((v.seg[q].nrows + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, (const int32_t*)v.seg[q].vid,
-                      v.seg[q].nrows, (uint8_t)q, last);
-    for (int q = 0; q < nseg; ++q)
-        if (v.seg[q].nrows > 0)
-            PR_LAUNCH(ctx, k_seg_mark, (unsigned)std::min<int64_t>((v.seg[q].nrows + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0, v.seg[q].vid, v.seg[q].nrows,
-                      (uint8_t)q, (const uint8_t*)last);
-    dfree(last, s);
     dfree(cnt, s);
     dfree(keys, s);
     dfree(keys_alt, s);

@@ -24,9 +24,6 @@ constexpr int SE_HOT_MAX = 16384;           // 128 KB of fp64
 constexpr int SE_HOT_IP = 2048;
 constexpr int SE_MAX_PHASES = 64;   // PR_MODE_PHASED: most phases per sweep
 constexpr int SE_L1_TIER = 32768;
-// Source-blocked views (blocked.cu): the sub-view row -> parent row map has this
-// bit set on the row's last segment (the in-place blocked sweep finalizes there).
-constexpr int32_t SEG_LAST = (int32_t)0x80000000u;
 inline int64_t stream_pad(int64_t E) { return ((E > 0 ? E : 1) + SE_STEP - 1) / SE_STEP * SE_STEP; }
 // Threads per CTA of the row-parallel kernels (K-FINALIZE, K-ZERO, ...).
 constexpr int GT_NT = 256;
@@ -121,6 +118,8 @@ struct pr_graph {
     int32_t* mem_k = nullptr;
     int32_t* mem_srow = nullptr;    // reduced-view row of mem_src (K-FINALIZE reads its S)
     int2* mem_info = nullptr;       // (outdeg, contrib slot) of each member
+    int32_t* mem_h = nullptr;       // chain member: index of its source among the chain sources (else -1)
+    int64_t n_hsrc = 0;             // distinct chain sources (delayed chain resolution)
     prgpu::View reduced;
     // row sharding over P ranks (pr_graph_shard, shard.cu)
     int32_t shard_rank = -1;
@@ -146,6 +145,8 @@ struct pr_graph {
     double* cta_partial = nullptr;  // [2 * (gather grid + scatter grid)] (L1, Linf)
     int64_t partial_cap = 0;
     double* ab = nullptr;           // chain alpha/beta [2 * (max_chain+1)]
+    double* hist = nullptr;         // [(max_chain+1) * n_hsrc] last values of the chain sources (ring)
+    int64_t hist_cap = 0;
     double* delta_log = nullptr;    // [2 * log_cap]
     int32_t log_cap = 0;
     int32_t log_len = 0;            // entries of delta_log written by the last pr_run

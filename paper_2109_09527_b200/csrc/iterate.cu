@@ -41,10 +41,6 @@ struct StreamPolicy {
     __device__ __forceinline__ void emit_first(int64_t r, double s) const { sums[r] = s; }
 };
 
-// Sub-view row -> parent row of a source-blocked view (blocked.cu); the top bit
-// (SEG_LAST) marks the row's last segment (used by the in-place blocked sweep).
-__device__ __forceinline__ int32_t seg_row(int32_t m) { return m & 0x7fffffff; }
-
 __device__ __forceinline__ void red_add_f64(double* p, double v) {
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -56,7 +52,7 @@ struct AccumPolicy {
     static constexpr bool kHot = false;
     const double* y_in;
     double* sums;
-    const int32_t* map;  // sub-view row -> parent view row (| SEG_LAST)
+    const int32_t* map;  // sub-view row -> parent view row
     uint64_t pol_last;
 
     // the slice is re-read ~20x per pass: keep it in L2 against the streams
@@ -73,12 +69,12 @@ struct AccumPolicy {
     int32_t m_first;
     int32_t m[SE_V];
     __device__ __forceinline__ void prep(int64_t base, uint32_t f) {
-        if (f) m_first = seg_row(__ldg(map + base));
+        if (f) m_first = __ldg(map + base);
 #pragma unroll
         for (int j = 0; j < SE_V; ++j)
-            if (f & (1u << j)) m[j] = seg_row(__ldg(map + base + __popc(f & ((1u << j) - 1))));
+            if (f & (1u << j)) m[j] = __ldg(map + base + __popc(f & ((1u << j) - 1)));
     }
-    __device__ __forceinline__ void emit(int64_t r, double s) const { red_add_f64(sums + seg_row(map[r]), s); }
+    __device__ __forceinline__ void emit(int64_t r, double s) const { red_add_f64(sums + map[r], s); }
     __device__ __forceinline__ void emit_at(int j, int64_t, double s) const { red_add_f64(sums + m[j], s); }
     __device__ __forceinline__ void emit_first(int64_t, double s) const { red_add_f64(sums + m_first, s); }
 };
@@ -262,6 +258,14 @@ struct FinArgs {
     // the same slot of each peer's buffer (the all-gather fused into K-FINALIZE)
     double* const* peer_y = nullptr;
     int npeer = 0;
+    // delayed chain resolution (sync reduced mode without PR_CHAIN_EAGER):
+    // hist[(t mod L) * nh + h] = x_t of chain source h (L = max_chain + 1
+    // sweeps, slot 0 = x_0 = 1/n); chain member m at distance k takes
+    // x_t(m) = alpha_j + beta_j * x_{t-j}(h), j = min(k, t)
+    double* hist = nullptr;
+    const int32_t* mh = nullptr;
+    int64_t nh = 0;
+    int L = 1;
 };
 
 // Rows are visited grid-stride (all CTAs sweep the row space together, which
@@ -326,6 +330,7 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
         if ((threadIdx.x & 31) == 0 && nfrozen) atomicAdd(f.nfz, (unsigned long long)nfrozen);
     }
     double* __restrict__ xm = f.xm;
+    const int t_sw = f.hist ? ia.st->iters + 1 : 0;  // this sweep's number (delayed chains)
     for (int64_t i0 = t0; i0 < f.nm; i0 += FIN_U * T) {
         double S[FIN_U], xo[FIN_U];
         int32_t k[FIN_U];
@@ -345,7 +350,15 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
             const int64_t i = i0 + u * T;
             if (i < f.nm) {
                 const double xs = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
-                const double xn = __dadd_rn(f.ab[2 * k[u]], __dmul_rn(f.ab[2 * k[u] + 1], xs));
+                int j = k[u];
+                double xsrc = xs;
+                if (f.hist && j > 0) {  // delayed: the source's value j sweeps ago (Eq.(1) along the chain)
+                    const int64_t h = __ldg(f.mh + i);
+                    if (j == 1) f.hist[(int64_t)(t_sw % f.L) * f.nh + h] = xs;  // one writer value per source
+                    j = min(j, t_sw);
+                    xsrc = f.hist[(int64_t)((t_sw - j) % f.L) * f.nh + h];
+                }
+                const double xn = __dadd_rn(f.ab[2 * j], __dmul_rn(f.ab[2 * j + 1], xsrc));
                 xm[i] = xn;
                 if (inf[u].x > 0) y[inf[u].y] = xn / (double)inf[u].x;
                 const double dl = fabs(xn - xo[u]);
@@ -625,90 +638,6 @@ __global__ void k_residual(const double* __restrict__ sums, int64_t nrows, const
     }
 }
 
-// ----------------------------------- in-place sweeps on source-blocked views --
-// (SURVEY f4 + a9.)  A contrib
-// vector far larger than L2 is gathered one L2-resident slice at a time
-// (blocked.cu); a row's sum is complete only in the pass of the LAST segment
-// holding one of its edges.  The in-place sweep therefore accumulates like the
-// synchronous blocked sweep, but finalizes each row IN PLACE the moment its
-// last segment's piece closes: x and y are stored at once (relaxed), so every
-// later pass -- and later gathers of the same pass -- read the new value
-// (Alg.3's pr(u) <- tmp).  Loads are relaxed (y is written during
-// the sweep).  Rows whose edges all lie in earlier segments were finalized in
-// their own last pass.
-struct AccumIPPolicy {
-    using T = double;
-    static constexpr bool kHot = false;
-    double* y;
-    double* sums;
-    const int32_t* map;  // sub-view row -> parent row | SEG_LAST
-    double* xr;
-    const int2* rinfo;
-    double c, d;
-    uint64_t pol_last;
-    double l1, linf;
-    int32_t m_first;
-    int32_t m[SE_V];
-
-    __device__ __forceinline__ double load(int32_t u) const {
-        double r;
-        asm volatile("ld.relaxed.gpu.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(y + u), "l"(pol_last));
-        return r;
-    }
-    __device__ __forceinline__ void prep(int64_t base, uint32_t f) {
-        if (f) m_first = __ldg(map + base);
-#pragma unroll
-        for (int j = 0; j < SE_V; ++j)
-            if (f & (1u << j)) m[j] = __ldg(map + base + __popc(f & ((1u << j) - 1)));
-    }
-    __device__ __forceinline__ void close(int32_t mm, double s) {
-        const int32_t r = seg_row(mm);
-        if (mm >= 0) {
-            red_add_f64(sums + r, s);
-            return;
-        }
-        // S of the earlier segments (previous launches) + this piece, in segment order
-        const double S = __ldcg(sums + r) + s;
-        const double xn = __dadd_rn(c, __dmul_rn(d, S));
-        const double xo = xr[r];
-        xr[r] = xn;
-        const int2 q = __ldg(rinfo + r);
-        if (q.x > 0) st_relaxed_f64(y + q.y, xn / (double)q.x);
-        const double dl = fabs(xn - xo);
-        l1 += dl;
-        linf = fmax(linf, dl);
-    }
-    __device__ __forceinline__ void emit(int64_t r, double s) { close(map[r], s); }
-    __device__ __forceinline__ void emit_at(int j, int64_t, double s) { close(m[j], s); }
-    __device__ __forceinline__ void emit_first(int64_t, double s) { close(m_first, s); }
-};
-
-__global__ void __launch_bounds__(SE_NT_IP, 1)
-    k_blocked_inplace(AccumIPPolicy p, StreamArgs a, IterArgs ia, int64_t part_off) {
-    __shared__ double red[64];
-    pdl_wait();
-    pdl_trigger();
-    if (ia.st->done) return;
-    p.pol_last = policy_evict_last();
-    p.l1 = 0.0;
-    p.linf = 0.0;
-    stream_run(p, a);
-    block_delta(p.l1, p.linf, red, ia.cta_partial + 2 * (part_off + blockIdx.x));
-}
-
-// Members in place after an in-place blocked sweep (x of the sources as
-// visible), then the sweep's global reduction and stop test.
-__global__ void __launch_bounds__(GT_NT) k_members_tail(MemArgs ma, const double* xr, double* y, IterArgs ia) {
-    __shared__ double red[64];
-    __shared__ int flag;
-    pdl_wait();
-    pdl_trigger();
-    if (ia.st->done) return;
-    double l1 = 0.0, linf = 0.0;
-    members_inplace(ma, xr, y, l1, linf);
-    partial_and_ticket(ia, l1, linf, red, ia.gather_ctas + blockIdx.x, &ia.st->ticket_scatter, &flag);
-}
-
 // ------------------------------------------------------------------- host --
 
 struct GatherCfg {
@@ -729,9 +658,9 @@ static StreamArgs stream_args(const View& w) {
 }
 
 // Kernel, dynamic shared memory and persistent grid (resident CTAs, capped by
-// the spans to run) of a gather over v: synchronous (k_stream), in place
-// (k_stream_async / k_nosync_stream) or in-place blocked (k_blocked_inplace).
-enum GatherKind { G_SYNC, G_INPLACE, G_BLOCKED_IP };
+// the spans to run) of a gather over v: synchronous (k_stream) or in place
+// (k_stream_async / k_nosync_stream).
+enum GatherKind { G_SYNC, G_INPLACE };
 static int gather_config(Ctx& ctx, const View& v, pr_graph* g, GatherKind kind, GatherCfg* gc) {
     const void* fn = nullptr;
     if (kind == G_SYNC) {
@@ -740,15 +669,11 @@ static int gather_config(Ctx& ctx, const View& v, pr_graph* g, GatherKind kind, 
         gc->nt = SE_NT;
         fn = gc->hot_n > 0 ? (const void*)k_stream<StreamPolicy<true>> : (const void*)k_stream<StreamPolicy<false>>;
         if (v.nseg > 0) fn = (const void*)k_stream<AccumPolicy>;
-    } else if (kind == G_INPLACE) {
+    } else {
         int hot = env_int("PRGPU_HOT", SE_HOT_IP);
         gc->hot_n = std::max(0, std::min<int>(std::min(hot, SE_HOT_MAX), (int)g->n_contrib));
         gc->nt = SE_NT_IP;
         fn = (const void*)k_stream_async;
-    } else {
-        gc->hot_n = 0;
-        gc->nt = SE_NT_IP;
-        fn = (const void*)k_blocked_inplace;
     }
     gc->smem = (size_t)gc->hot_n * sizeof(double);
     PR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gc->smem));
@@ -963,7 +888,6 @@ static int sweep_loop(pr_graph* g, Ctx& ctx, int32_t max_iter, double tau, F&& s
     }
     return PR_OK;
 }
-static int no_after(int64_t) { return PR_OK; }
 
 // PR_TIMING: CUDA events around the gather and the finalize of every
 // stride-th sweep (each event pair also blocks the programmatic launch overlap
@@ -1032,8 +956,8 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
                       int32_t* iters_out, double* delta_out);
 static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
                           Ctx& ctx, int32_t* iters_out, double* delta_out);
-static int run_blocked_inplace(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
-                               Ctx& ctx, int32_t* iters_out, double* delta_out);
+static int residual_check(pr_graph* g, Ctx& ctx, double c, double d, const double* x, const double* y, double* resid,
+                          double* out2, int32_t done);
 
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
         int32_t* iters_out, double* delta_out) {
@@ -1041,8 +965,16 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     if (g->pre_done) PR_TRY(reset_tickets(g->reduced, ctx.stream));
     const bool reduced = (mode & PR_USE_REDUCTIONS) != 0;
     const View& v = reduced ? g->reduced : g->plain;
-    if ((mode & (PR_MODE_ASYNC | PR_MODE_NOSYNC)) && v.nseg > 0)
-        return run_blocked_inplace(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
+    // Source-blocked views (contrib vector beyond L2) run the asynchronous
+    // modes on the Jacobi schedule -- a valid No-Sync schedule in which every
+    // read sees the previous sweep's value (reading Q-Y2): measured on config
+    // 5, slice passes finalizing rows in place in their last segment needed
+    // 88 sweeps against Jacobi's 14 (the in-place updates break the plain
+    // iteration's mass conservation on this dangling-free graph).  No-Sync keeps
+    // its certificate of the original system.
+    const bool blocked_async = (mode & (PR_MODE_ASYNC | PR_MODE_NOSYNC)) && v.nseg > 0;
+    const uint32_t mode_in = mode;
+    if (blocked_async) mode &= ~(PR_MODE_ASYNC | PR_MODE_NOSYNC);
     if (mode & PR_MODE_NOSYNC) return run_nosync(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     if (mode & PR_PERFORATE) return run_perforated(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     cudaStream_t s = ctx.stream;
@@ -1088,8 +1020,24 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     ia_first.zero_ctas = zgrid;
     double* zero_partial = g->cta_partial + 2 * ggrid;
     const MemArgs ma{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, nm > 0 ? (nm + gc.grid - 1) / gc.grid : 0, g->ab};
-    const FinArgs fa{v.sums, v.nrows, v.rinfo, g->xr, g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, g->ab, nullptr,
-                     c, d};
+    FinArgs fa{v.sums, v.nrows, v.rinfo, g->xr, g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, g->ab, nullptr, c, d};
+    // delayed chain resolution (sync reduced, reading Q-C2): the last
+    // max_chain + 1 values of every chain source, slot 0 = x_0 = 1/n
+    if (reduced && nm > 0 && !async && !phased && !(mode & PR_CHAIN_EAGER) && g->n_hsrc > 0) {
+        const int L = g->max_chain + 1;
+        const int64_t need = (int64_t)L * g->n_hsrc;
+        if (g->hist_cap < need) {
+            dfree(g->hist, s);
+            PR_TRY(dalloc(&g->hist, (size_t)need, s));
+            g->hist_cap = need;
+        }
+        PR_LAUNCH(ctx, k_fill_f64, (unsigned)std::min<int64_t>((need + 255) / 256, (int64_t)ctx.num_sms * 16), 256, 0,
+                  g->hist, need, 1.0 / (double)n);
+        fa.hist = g->hist;
+        fa.mh = g->mem_h;
+        fa.nh = g->n_hsrc;
+        fa.L = L;
+    }
 
     SweepTimer tmr;
     tmr.on = timing;
@@ -1172,19 +1120,30 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     rs.gather_ms = tmr.gather_ms;
     rs.scatter_ms = tmr.scatter_ms;
     DevState* hs = g->st_host;
+    if (blocked_async && (mode_in & PR_MODE_NOSYNC)) {
+        // No-Sync's certificate: ||F(x) - x|| of the original system over the
+        // final contribs (a converged Jacobi run has it <= d * tau)
+        double cert[2] = {0.0, 0.0};
+        PR_TRY(ensure_partials(g, ctx, 2 * (ggrid + zgrid) + 2));
+        const double* yfin = g->y[hs->iters & 1];
+        PR_TRY(residual_check(g, ctx, c, d, x, yfin, g->cta_partial + 2 * (ggrid + zgrid), cert, 1));
+        rs.nosync_launches = 1;
+        rs.nosync_min_iters = rs.nosync_median_iters = hs->iters;
+        rs.residual = (mode_in & PR_NORM_LINF) ? cert[1] : cert[0];
+        rs.host_syncs += 1;
+        if (rs.residual > tau && hs->status == PR_OK) hs->status = PR_NOT_CONVERGED;
+        if (iters_out) *iters_out = hs->iters;
+        if (delta_out) *delta_out = rs.residual;
+        return hs->status;
+    }
     if (iters_out) *iters_out = hs->iters;
     if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
     return hs->status;
 }
 
-// ------------------------------------ in-place sweeps on blocked views --
-// PR_MODE_ASYNC on a source-blocked view: launch-level in-place sweeps, each
-// = one k_blocked_inplace pass per slot segment (rows finalized in place in
-// their last segment's pass) + k_members_tail (members in place, reduction,
-// stop test).  PR_MODE_NOSYNC on a blocked view runs the same sweeps (a
-// persistent kernel cannot order the slice passes without a grid barrier) and
-// then certifies the result like the persistent kernel: ||F(x) - x|| of the
-// original system by one synchronous gather; above tau, more sweeps follow.
+// ------------------------------------------------------- certificate --
+// ||F(x) - x|| of the original system (F = Eq.(1)) over the contribs y, by one
+// synchronous gather of the plain view + k_residual (No-Sync's exit check).
 __global__ void k_set_done(DevState* st, int32_t v) { st->done = v; }
 
 static int residual_check(pr_graph* g, Ctx& ctx, double c, double d, const double* x, const double* y, double* resid,
@@ -1204,108 +1163,6 @@ static int residual_check(pr_graph* g, Ctx& ctx, double c, double d, const doubl
     PR_LAUNCH(ctx, k_set_done, 1, 1, 0, g->st, done);
     PR_CUDA(cudaStreamSynchronize(s));
     return PR_OK;
-}
-
-static int run_blocked_inplace(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
-                               Ctx& ctx, int32_t* iters_out, double* delta_out) {
-    cudaStream_t s = ctx.stream;
-    const bool reduced = (mode & PR_USE_REDUCTIONS) != 0;
-    const bool nosync = (mode & PR_MODE_NOSYNC) != 0;
-    const int64_t n = g->n;
-    const View& v = reduced ? g->reduced : g->plain;
-    const int64_t nm = reduced ? g->n_members : 0;
-    const int64_t launches0 = ctx.launches;
-    RunBufs rb;
-    PR_TRY(run_buffers(g, ctx, ranks, max_iter, &rb));
-    double* x = rb.x;
-    double* y = g->y[0];
-    GatherCfg gc;
-    PR_TRY(gather_config(ctx, v, g, G_BLOCKED_IP, &gc));
-    int nact = 0;  // segments with edges (each pass writes gc.grid partials)
-    for (int q = 0; q < v.nseg; ++q) nact += v.seg[q].nspans > 0 ? 1 : 0;
-    const int64_t cap4 = (int64_t)ctx.num_sms * 4;
-    const int64_t mgrid = std::max<int64_t>(1, std::min<int64_t>((nm + GT_NT - 1) / GT_NT, cap4));
-    const int64_t nz = g->nz;
-    const int64_t zgrid = nz > 0 ? std::min<int64_t>((nz + GT_NT * 4 - 1) / (GT_NT * 4), cap4) : 0;
-    const int64_t pgrid = (int64_t)nact * gc.grid;
-    PR_TRY(ensure_partials(g, ctx, 2 * (pgrid + mgrid + zgrid) + 2));
-    const double c = (1.0 - d) / (double)n;
-    if (reduced && nm > 0) PR_TRY(upload_ab(g, ctx, c, d));
-    PR_TRY(init_state(g, ctx, tau, max_iter, mode, x, g->cidx, y, v, nm));
-    IterArgs ia_rest{g->st, g->cta_partial, pgrid, mgrid, 0, g->delta_log};
-    IterArgs ia_first = ia_rest;
-    ia_first.zero_ctas = zgrid;
-    double* zero_partial = g->cta_partial + 2 * (pgrid + mgrid);
-    double* resid = g->cta_partial + 2 * (pgrid + mgrid + zgrid);
-    const MemArgs ma{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, nm > 0 ? (nm + mgrid - 1) / mgrid : 0, g->ab};
-    int32_t sweeps_before = 0;  // No-Sync: sweeps of earlier certified rounds
-    auto sweep = [&](int64_t it) -> int {
-        const IterArgs& ia = it == 0 ? ia_first : ia_rest;
-        if (it == 0 && zgrid > 0 && sweeps_before == 0)
-            PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, c, x, y,
-                      (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
-        PR_CUDA(cudaMemsetAsync(v.sums, 0, sizeof(double) * (size_t)v.nrows, s));
-        int a = 0;
-        for (int q = 0; q < v.nseg; ++q) {
-            const View& sv = v.seg[q];
-            if (sv.nspans == 0) continue;
-            AccumIPPolicy p{};
-            p.y = y;
-            p.sums = v.sums;
-            p.map = sv.vid;
-            p.xr = g->xr;
-            p.rinfo = v.rinfo;
-            p.c = c;
-            p.d = d;
-            PR_LAUNCH_PDL(ctx, k_blocked_inplace, gc.grid, gc.nt, 0, p, stream_args(sv), ia, (int64_t)a * gc.grid);
-            ++a;
-        }
-        PR_LAUNCH_PDL(ctx, k_members_tail, (unsigned)mgrid, GT_NT, 0, ma, (const double*)g->xr, y, ia);
-        return PR_OK;
-    };
-    LoopStats ls;
-    DevState* hs = g->st_host;
-    double cert[2] = {0.0, 0.0};
-    int checks = 0;
-    while (true) {
-        PR_TRY(sweep_loop(g, ctx, max_iter - sweeps_before, tau, sweep, no_after, ls));
-        const int32_t total = sweeps_before + hs->iters;
-        if (!nosync) break;
-        // No-Sync: certify (x in vertex order first)
-        const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
-        PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
-                  (const double*)g->xm, (const int32_t*)g->mem_vid, nm, x);
-        PR_TRY(residual_check(g, ctx, c, d, x, y, resid, cert, 1));
-        ++checks;
-        const double rn = (mode & PR_NORM_LINF) ? cert[1] : cert[0];
-        if (rn <= tau || total >= max_iter) {
-            hs->status = rn <= tau ? PR_OK : PR_NOT_CONVERGED;
-            hs->iters = total;
-            break;
-        }
-        // continue from the current state: reset the sweep counter and done
-        sweeps_before = total;
-        hs->done = 0;
-        hs->iters = 0;
-        hs->max_iter = max_iter - total;
-        PR_CUDA(cudaMemcpyAsync(g->st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
-    }
-    const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
-    PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
-              (const double*)g->xm, (const int32_t*)g->mem_vid, nm, x);
-    if (!rb.ranks_dev) PR_CUDA(cudaMemcpyAsync(ranks, x, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
-    PR_CUDA(cudaStreamSynchronize(s));
-    fill_stats(g, ctx, launches0, v, nm, ls.host_syncs + checks, 1);
-    pr_run_stats& rs = g->last;
-    if (nosync) {
-        rs.nosync_launches = checks;
-        rs.nosync_min_iters = rs.nosync_median_iters = hs->iters;
-        rs.residual = (mode & PR_NORM_LINF) ? cert[1] : cert[0];
-        g->log_len = std::min<int32_t>(std::min<int32_t>(hs->iters, g->log_cap), hs->iters - sweeps_before);
-    }
-    if (iters_out) *iters_out = hs->iters;
-    if (delta_out) *delta_out = nosync ? rs.residual : ((mode & PR_NORM_LINF) ? hs->linf : hs->l1);
-    return hs->status;
 }
 
 // -------------------------------------------------------- sharded (f3) --

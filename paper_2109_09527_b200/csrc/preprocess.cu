@@ -311,6 +311,29 @@ __global__ void k_copy_rows(const int32_t* __restrict__ vid, int64_t nr, const i
     }
 }
 
+// chain sources (the distinct source rows of chain members, k >= 1): compact
+// index per row, and per member (-1 for identical members).  The synchronous
+// reduced sweep keeps the last max_chain + 1 values of each chain source
+// (delayed chain resolution, iterate.cu K-FINALIZE).
+__global__ void k_mark_chain_src(const int32_t* __restrict__ mk, const int32_t* __restrict__ msrow, int64_t nm,
+                                 int32_t* __restrict__ mark) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += (int64_t)gridDim.x * blockDim.x)
+        if (mk[i] > 0) mark[msrow[i]] = 1;
+}
+struct MarkGet {
+    const int32_t* mark;
+    __device__ int64_t operator()(int64_t r) const { return mark[r] ? 1 : 0; }
+};
+struct MarkEmit {
+    int32_t* idx;
+    __device__ void operator()(int64_t r, int64_t pos, int64_t f) const { idx[r] = f ? (int32_t)pos : -1; }
+};
+__global__ void k_member_hist(const int32_t* __restrict__ mk, const int32_t* __restrict__ msrow, int64_t nm,
+                              const int32_t* __restrict__ idx, int32_t* __restrict__ mh) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += (int64_t)gridDim.x * blockDim.x)
+        mh[i] = mk[i] > 0 ? idx[msrow[i]] : -1;
+}
+
 __global__ void k_rowof(const int32_t* __restrict__ vid, int64_t nrows, int32_t* __restrict__ rowof) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x)
         rowof[vid[r]] = (int32_t)r;
@@ -338,6 +361,8 @@ static void clear_reductions(pr_graph* g, cudaStream_t s) {
     dfree(g->mem_k, s);
     dfree(g->mem_srow, s);
     dfree(g->mem_info, s);
+    dfree(g->mem_h, s);
+    g->n_hsrc = 0;
     dfree(g->xm, s);
     free_view(g->reduced, s);
     g->n_members = 0;
@@ -533,6 +558,24 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
         PR_TRY(dalloc(&g->mem_info, (size_t)g->n_members, s));
         PR_LAUNCH(ctx, k_rinfo, grid_of(ctx, g->n_members), 256, 0, (const int32_t*)g->mem_vid, g->n_members,
                   (const int32_t*)g->outdeg, (const int32_t*)g->cidx, g->mem_info);
+        if (g->max_chain > 0) {
+            int32_t* mark = nullptr;
+            int32_t* idx = nullptr;
+            tg_.track(mark);
+            tg_.track(idx);
+            PR_TRY(dalloc(&mark, (size_t)std::max<int64_t>(R.nrows, 1), s));
+            PR_TRY(dalloc(&idx, (size_t)std::max<int64_t>(R.nrows, 1), s));
+            PR_CUDA(cudaMemsetAsync(mark, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(R.nrows, 1), s));
+            PR_LAUNCH(ctx, k_mark_chain_src, grid_of(ctx, g->n_members), 256, 0, (const int32_t*)g->mem_k,
+                      (const int32_t*)g->mem_srow, g->n_members, mark);
+            PR_TRY((device_scan<int64_t>(ctx, R.nrows, MarkGet{mark}, MarkEmit{idx}, cnt)));
+            PR_TRY(read_count(ctx, cnt, &g->n_hsrc));
+            PR_TRY(dalloc(&g->mem_h, (size_t)g->n_members, s));
+            PR_LAUNCH(ctx, k_member_hist, grid_of(ctx, g->n_members), 256, 0, (const int32_t*)g->mem_k,
+                      (const int32_t*)g->mem_srow, g->n_members, (const int32_t*)idx, g->mem_h);
+            dfree(mark, s);
+            dfree(idx, s);
+        }
     }
     dfree(cnt, s);
     g->pre_done = true;

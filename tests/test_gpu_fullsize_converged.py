@@ -12,7 +12,8 @@ stands):
   * reduced Jacobi to tau (identical groups + chains, Q-G / Q-C);
   * block Gauss-Seidel with the phase count the GPU uses (reading Q-B).
 Checks (tolerances of SURVEY c3):
-  * sync plain / reduced / phased against the matching oracle run: per-vertex
+  * sync plain, reduced (delayed chains: the plain run; eager: the oracle's
+    reduced run) and phased against the matching oracle run: per-vertex
     |diff| <= 1e-10, L1 <= 1e-9, iterations within +/-1 (a difference only
     where the oracle's last delta sits at the threshold);
   * async, No-Sync (plain and reduced) and phased-reduced against the tau/100
@@ -163,6 +164,7 @@ def _converged(pr, k):
         # (in-degree-0 vertices are written once, in sweep 1)
         assert g.info()["n_members"] == int(((np.diff(ref_g.row_ptr) > 0) & ((rep != np.arange(n)) | (ck > 0))).sum())
         out["reduced"] = _run(pr, g, n, d, tau, gen.max_iter, pr.PR_USE_REDUCTIONS)
+        out["reduced_eager"] = _run(pr, g, n, d, tau, gen.max_iter, pr.PR_USE_REDUCTIONS | pr.PR_CHAIN_EAGER)
         out["phased_reduced"] = _run(pr, g, n, d, tau, gen.max_iter, pr.PR_MODE_PHASED | pr.PR_USE_REDUCTIONS)
         out["async_reduced"] = _run(pr, g, n, d, tau, gen.max_iter, pr.PR_MODE_ASYNC | pr.PR_USE_REDUCTIONS)
         out["nosync_reduced"] = _run(pr, g, n, d, tau, gen.max_iter, pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS)
@@ -181,10 +183,13 @@ def _converged(pr, k):
     _close(x, ref["plain"]["x"], "sync plain vs oracle plain")
     if str(k) in ITERS:
         assert ref["plain"]["iters"] == ITERS[str(k)]["plain_iters"]
+    st, it, fd, x = out["reduced"]             # delayed chains: the plain trajectory (Q-C2)
+    assert st == pr.PR_OK and _iters_ok(it, ref["plain"], tau), (it, ref["plain"]["iters"])
+    _close(x, ref["plain"]["x"], "sync reduced (delayed chains) vs oracle plain")
     red_ref = ref.get("reduced", ref["plain"])   # no members: the reduced run IS the plain run (Q-G)
-    st, it, fd, x = out["reduced"]
+    st, it, fd, x = out["reduced_eager"]
     assert st == pr.PR_OK and _iters_ok(it, red_ref, tau), (it, red_ref["iters"])
-    _close(x, red_ref["x"], "sync reduced vs oracle reduced")
+    _close(x, red_ref["x"], "sync reduced (eager chains) vs oracle reduced")
     blk_ref = ref.get("blocks", ref["plain"])    # one phase: the phased run IS the sync run
     st, it, fd, x = out["phased"]
     assert st == pr.PR_OK and _iters_ok(it, blk_ref, tau), (it, blk_ref["iters"])

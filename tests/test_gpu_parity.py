@@ -99,12 +99,18 @@ def check_all(pr, n, src, dst, tau=1e-12, reductions=True, async_mode=True):
             assert np.array_equal(cs, cs_o)
             assert np.array_equal(ck, ck_o)
             assert g.info()["max_chain"] == mk
-            ref_r = oracle.pagerank(ref_g, D, tau, 1000, reduced=True, rep=rep_o, chain_k=ck_o)
+            # delayed chain resolution (default, Q-C2): the plain trajectory
             st, it, fd, xr = gpu_run(pr, g, n, tau, mode=pr.PR_USE_REDUCTIONS)
-            assert_iters(it, ref_r, tau)
-            assert_close(xr, ref_r.x)
+            assert_iters(it, ref, tau)
+            assert_close(xr, ref.x)
             members = np.nonzero(rep_o != np.arange(n))[0]
             assert np.array_equal(xr[members], xr[rep_o[members]])  # exact copies
+            # eager (same-sweep) chain resolution: the oracle's reduced mode (Q-C)
+            ref_r = oracle.pagerank(ref_g, D, tau, 1000, reduced=True, rep=rep_o, chain_k=ck_o)
+            st, it, fd, xe = gpu_run(pr, g, n, tau, mode=pr.PR_USE_REDUCTIONS | pr.PR_CHAIN_EAGER)
+            assert_iters(it, ref_r, tau)
+            assert_close(xe, ref_r.x)
+            assert np.array_equal(xe[members], xe[rep_o[members]])
         if async_mode:
             check_async(pr, g, ref_g, n, tau)
     return ref_g
@@ -299,6 +305,27 @@ def test_config3_structured(pr):
         for a, b in zip(starts, np.r_[starts[1:], len(gs)]):
             if gs[a] >= 0:
                 assert (rs[a:b] == rs[a]).all()
+
+
+def test_config3_delayed_chains_keep_the_plain_sweep_count(pr):
+    """Config 3 (dangling-free, 5 % of the vertices on chains): eager chain
+    resolution breaks the plain iteration's mass conservation and needs about
+    twice the sweeps (finding about Q-C); the delayed resolution
+    reproduces the plain trajectory, so the reduced run takes the plain sweep
+    count while gathering fewer edges per sweep."""
+    gen = graphgen.make_config(3)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    ref = oracle.pagerank(ref_g, D, gen.tau, gen.max_iter)
+    with gpu_graph(pr, gen.n, gen.src, gen.dst) as g:
+        st, it_p, fd, xp = gpu_run(pr, g, gen.n, gen.tau)
+        g.preprocess()
+        st, it_r, fd, xr = gpu_run(pr, g, gen.n, gen.tau, mode=pr.PR_USE_REDUCTIONS)
+        s = g.stats()
+        st, it_e, fd, xe = gpu_run(pr, g, gen.n, gen.tau, mode=pr.PR_USE_REDUCTIONS | pr.PR_CHAIN_EAGER)
+    assert_iters(it_r, ref, gen.tau)
+    assert_close(xr, ref.x)
+    assert it_r <= it_p + 1 and it_e > it_r
+    assert s["gather_edges"] < ref_g.E
 
 
 def test_config3_async(pr):

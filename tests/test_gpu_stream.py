@@ -56,7 +56,7 @@ def test_span_sizes_match_oracle(pr, monkeypatch, span):
         assert_iters(it, ref, 1e-12)
         assert_close(x, ref.x)
         g.preprocess()
-        st, it, fd, xr = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS)
+        st, it, fd, xr = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS | pr.PR_CHAIN_EAGER)
         assert_iters(it, ref_r, 1e-12)
         assert_close(xr, ref_r.x)
 
@@ -121,9 +121,12 @@ def test_blocked_segments_match_oracle(pr, monkeypatch, bits):
         a = gpu_run(pr, g, n, 1e-12)[3]
         assert np.array_equal(a, x)                      # deterministic
         g.preprocess()
-        st, it, fd, xr = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS)
+        st, it, fd, xr = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS | pr.PR_CHAIN_EAGER)
         assert_iters(it, ref_r, 1e-12)
         assert_close(xr, ref_r.x)
+        st, it, fd, xd = gpu_run(pr, g, n, 1e-12, mode=pr.PR_USE_REDUCTIONS)   # delayed: the plain run
+        assert_iters(it, ref, 1e-12)
+        assert_close(xd, ref.x)
 
 
 def test_blocked_rmat(pr, monkeypatch):

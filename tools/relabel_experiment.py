@@ -65,10 +65,18 @@ ord2 = torch.sort(key).indices
 first_rank = torch.empty(n, dtype=torch.int64, device=dev)
 first_rank[ord2] = torch.arange(n, device=dev)
 
+# cold sources in vertex-id order (rows and slots both ascending: K-FINALIZE's
+# contrib stores of the cold rows would be coalesced)
+key3 = torch.where(cold, H + torch.arange(n, device=dev), deg_rank)
+key3 = torch.where(od > 0, key3, torch.full_like(key3, 1 << 62))
+ord3 = torch.sort(key3).indices
+id_rank = torch.empty(n, dtype=torch.int64, device=dev)
+id_rank[ord3] = torch.arange(n, device=dev)
+
 y = torch.rand(nsrc, dtype=torch.float64, device=dev)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 out = torch.empty(sms * 8 * 1024, dtype=torch.float64, device=dev)
-for name, rank in (("degree", deg_rank), ("first", first_rank)):
+for name, rank in (("degree", deg_rank), ("first", first_rank), ("idorder", id_rank)):
     col = rank[ci64].to(torch.int32).contiguous()
     # sectors per warp instruction (32 lanes x 1 gather, lane L = edges 8L..8L+7
     # of a step) for the cold gathers: distinct 32-byte sectors of one lane's 8
