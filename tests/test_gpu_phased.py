@@ -75,7 +75,8 @@ def test_one_phase_is_sync(pr, monkeypatch, name, span):
     with pr.Graph(n, dev(s), dev(t)) as g:
         g.preprocess()
         for extra in (0, pr.PR_USE_REDUCTIONS, pr.PR_NORM_LINF):
-            a = run(pr, g, n, 1e-12, extra)
+            # (the phased mode resolves chains eagerly, Q-C: compare with the eager sync form)
+            a = run(pr, g, n, 1e-12, extra | (pr.PR_CHAIN_EAGER if extra & pr.PR_USE_REDUCTIONS else 0))
             b = run(pr, g, n, 1e-12, pr.PR_MODE_PHASED | extra)
             assert a[:3] == b[:3] and np.array_equal(a[3], b[3]), (extra, a[:3], b[:3])
             assert g.stats()["phases"] == 1
