@@ -169,24 +169,6 @@ __device__ __forceinline__ double ld_gather_f64(const double* ptr, uint64_t pol)
     return r;
 }
 
-// Gather with the L1 policy chosen per tier: evict_last (hot), default
-// allocation, or no_allocate (streaming).
-__device__ __forceinline__ double ld_gather_l1last_f64(const double* ptr, uint64_t pol) {
-    double r;
-    asm("ld.global.nc.L1::evict_last.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ double ld_gather_l1def_f64(const double* ptr, uint64_t pol) {
-    double r;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-__device__ __forceinline__ double ld_gather_l1na_f64(const double* ptr, uint64_t pol) {
-    double r;
-    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(ptr), "l"(pol));
-    return r;
-}
-
 // Two-tier gather: hot contribs (small index = high out-degree) stay in L1
 // (evict_last), cold ones bypass it (no_allocate) so they cannot evict the
 // hot lines.  One predicated load each, branch-free.

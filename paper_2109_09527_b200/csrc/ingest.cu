@@ -381,22 +381,6 @@ struct NonZeroEmit {
     }
 };
 
-// PRGPU_RELABEL=hotid: the hot tiers ([0, H) by degree) stay, the cold
-// sources take slots H.. in vertex-id order, so the contrib stores of
-// K-FINALIZE's consecutive rows land in consecutive slots.
-struct ColdGet {
-    const int32_t* cidx;
-    int32_t H;
-    __device__ int64_t operator()(int64_t v) const { return cidx[v] >= H ? 1 : 0; }
-};
-struct ColdEmit {
-    int32_t* cidx;
-    int32_t H;
-    __device__ void operator()(int64_t v, int64_t pos, int64_t f) const {
-        if (f) cidx[v] = H + (int32_t)pos;
-    }
-};
-
 int build_relabel(pr_graph* g, Ctx& ctx) {
     cudaStream_t s = ctx.stream;
     const int64_t n = g->n;
@@ -437,8 +421,6 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
     if (cnt > 0)
         PR_LAUNCH(ctx, k_set_cidx, grid_for(ctx, cnt, 256), 256, 0, sorted, cnt,
                   b ? ((1ull << b) - 1) : 0ull, g->cidx);
-    if (by_degree && mode && mode[0] == 'h' && cnt > SE_L1_TIER)
-        PR_TRY((device_scan<int64_t>(ctx, n, ColdGet{g->cidx, SE_L1_TIER}, ColdEmit{g->cidx, SE_L1_TIER}, scratch)));
     // zero in-degree vertices (written once, in sweep 1) and the plain view:
     // the rows of in-degree > 0 (identity view when there are no empty rows)
     View& v = g->plain;

@@ -30,12 +30,10 @@ struct StreamPolicy {
     const double* hot;
     int32_t hot_n;
     uint64_t pol_last;
-    int cold_alloc;  // cold tier (slots >= SE_L1_TIER): 1 = L1 default allocation, 0 = L1::no_allocate
 
     __device__ __forceinline__ double load(int32_t u) const {
         if (HOT && u < hot_n) return hot[u];
-        if (u < SE_L1_TIER) return ld_gather_l1last_f64(y_in + u, pol_last);
-        return cold_alloc ? ld_gather_l1def_f64(y_in + u, pol_last) : ld_gather_l1na_f64(y_in + u, pol_last);
+        return ld_gather_tiered_f64(y_in + u, u < SE_L1_TIER, pol_last);
     }
     __device__ __forceinline__ void emit(int64_t r, double s) const { sums[r] = s; }
     __device__ __forceinline__ void prep(int64_t, uint32_t) {}
@@ -643,7 +641,6 @@ __global__ void k_residual(const double* __restrict__ sums, int64_t nrows, const
 // ------------------------------------------------------------------- host --
 
 struct GatherCfg {
-    int cold_alloc = 0;
     int hot_n = 0;
     size_t smem = 0;
     int grid = 1;
@@ -666,7 +663,6 @@ static StreamArgs stream_args(const View& w) {
 enum GatherKind { G_SYNC, G_INPLACE };
 static int gather_config(Ctx& ctx, const View& v, pr_graph* g, GatherKind kind, GatherCfg* gc) {
     const void* fn = nullptr;
-    gc->cold_alloc = env_int("PRGPU_COLD_ALLOC", 0);
     if (kind == G_SYNC) {
         int hot = v.nseg > 0 ? 0 : env_int("PRGPU_HOT", SE_HOT_MAX);
         gc->hot_n = std::max(0, std::min<int>(std::min(hot, SE_HOT_MAX), (int)g->n_contrib));
@@ -716,11 +712,11 @@ static int launch_gather(Ctx& ctx, pr_graph* g, const View& v, const double* y_i
         }
     } else if (v.nspans > 0) {
         if (gc.hot_n > 0) {
-            StreamPolicy<true> p{y_in, sums, nullptr, gc.hot_n, 0, gc.cold_alloc};
+            StreamPolicy<true> p{y_in, sums, nullptr, gc.hot_n, 0};
             PR_LAUNCH_PDL(ctx, k_stream<StreamPolicy<true>>, gc.grid, gc.nt, gc.smem, p, stream_args(v),
                           (const DevState*)g->st);
         } else {
-            StreamPolicy<false> p{y_in, sums, nullptr, 0, 0, gc.cold_alloc};
+            StreamPolicy<false> p{y_in, sums, nullptr, 0, 0};
             PR_LAUNCH_PDL(ctx, k_stream<StreamPolicy<false>>, gc.grid, gc.nt, gc.smem, p, stream_args(v),
                           (const DevState*)g->st);
         }

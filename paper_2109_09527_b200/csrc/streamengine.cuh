@@ -132,16 +132,20 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
             fn = ld_stream_u8(a.flags8 + (s + 1) * 32 + lane);
             Rn = a.step_row[s + 1];
         }
-        // row starts: warp-exclusive rank of this lane's first start
+        // row starts: warp-exclusive rank of this lane's first start and the
+        // step's total, from ballots of the bit planes of the per-lane count
+        // (nf <= 8: 4 planes; no shuffles on the MIO pipe)
         const int nf = __popc(f);
-        int incl = nf;
+        const uint32_t lt = lanemask_lt();
+        int rank0 = 0, nst = 0;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= d) incl += t;
+        for (int b = 0; b < 4; ++b) {
+            const uint32_t m = __ballot_sync(0xffffffffu, (nf >> b) & 1);
+            rank0 += __popc(m & lt) << b;
+            nst += __popc(m) << b;
         }
-        const int rank0 = incl - nf;
-        const int nst = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t smask = __ballot_sync(0xffffffffu, nf > 0);   // lanes holding a row start
+        const uint32_t le = lt | (1u << lane);
         p.prep((int64_t)R0 - 1 + rank0, f);  // policy may prefetch per-row data of this lane's closures
         // in-lane segments: the i-th start (i >= 1) of this lane closes slot
         // rank0 + i, i.e. row R0 - 1 + rank0 + i, with the lane-local segment
@@ -163,16 +167,17 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
         // open segment of each lane flows right until the next lane with a start
         T o = run;
         if (lane == 0 && nf == 0) o = carry + o;
+        // segmented inclusive scan; F = a row starts within the lanes the
+        // running sum already covers ([lane - 2d + 1, lane] after the round
+        // with distance d), read off the start mask instead of shuffled
         T S = o;
-        int F = nf > 0;
+        bool F = nf > 0;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const T tS = __shfl_up_sync(0xffffffffu, S, d);
-            const int tF = __shfl_up_sync(0xffffffffu, F, d);
-            if (lane >= d && !F) {
-                S = tS + S;
-                F = tF;
-            }
+            if (lane >= d && !F) S = tS + S;
+            const int lo = lane - 2 * d + 1;
+            F = ((smask & le) >> (lo > 0 ? lo : 0)) != 0;
         }
         T I = __shfl_up_sync(0xffffffffu, S, 1);
         if (lane == 0) I = carry;
