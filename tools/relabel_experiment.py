@@ -76,8 +76,16 @@ id_rank[ord3] = torch.arange(n, device=dev)
 y = torch.rand(nsrc, dtype=torch.float64, device=dev)
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 out = torch.empty(sms * 8 * 1024, dtype=torch.float64, device=dev)
-for name, rank in (("degree", deg_rank), ("first", first_rank), ("idorder", id_rank)):
+rows = torch.repeat_interleave(torch.arange(n, device=dev), (rp[1:] - rp[:-1]))
+variants = (("degree", deg_rank, False), ("rowsorted", deg_rank, True))
+if len(sys.argv) > 3:
+    variants = variants + (("first", first_rank, False), ("idorder", id_rank, False))
+for name, rank, rowsort in variants:
     col = rank[ci64].to(torch.int32).contiguous()
+    if rowsort:   # each row's edges ascending by contrib slot (sum order only)
+        key = rows * (1 << 32) + col.to(torch.int64)
+        col = (torch.sort(key).values & 0xffffffff).to(torch.int32).contiguous()
+        del key
     # sectors per warp instruction (32 lanes x 1 gather, lane L = edges 8L..8L+7
     # of a step) for the cold gathers: distinct 32-byte sectors of one lane's 8
     # gathers (what L1 allocation can merge)
