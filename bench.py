@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--exchange", choices=["allgather", "peers"], default="allgather",
                    help="--parallel shard: NCCL all-gather per sweep, or the exchange fused into the kernels "
                         "(every new contrib stored into every rank's buffer through CUDA IPC, host barrier per sweep)")
+    p.add_argument("--ingest", choices=["full", "local"], default="local",
+                   help="--parallel shard: every rank ingests the whole edge list then shards (full), or only "
+                        "the edges into its own vertices with one out-degree all-reduce (pr_graph_create_sharded)")
     p.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                    help="process-group backend of our arm (gloo + PRGPU_BENCH_ONE_GPU=1: test the sharded "
                         "multi-process plumbing with every rank on cuda:0)")
@@ -314,13 +317,15 @@ def compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags):
 # ------------------------------------------------------------ ours, sharded --
 def run_shard_bench(args, ws, rank, local, dev, pr, torch, gen, W, K):
     """--parallel shard: one R-MAT-24 graph row-sharded over the ranks
-    (SURVEY f3).  Step = pr_graph_create (every rank ingests the same edge
-    list) + pr_graph_shard + pr_run_sharded (plain sync, one in-place
+    (SURVEY f3).  Step = pr_graph_create_sharded (--ingest local: the rank's
+    edges only + one out-degree all-reduce; --ingest full: pr_graph_create of
+    the whole list + pr_graph_shard) + pr_run_sharded (plain sync, one in-place
     all-gather of the contrib chunks per sweep) + pr_destroy.  value = E *
     iterations / max-over-ranks time (ONE graph: strong scaling)."""
     n = gen.n
     stream = torch.cuda.current_stream(dev)
     exchange = pr.torch_dist_exchange() if ws > 1 else (lambda *a: None)
+    allreduce = pr.torch_dist_allreduce() if ws > 1 else (lambda *a: None)
     src_h = torch.from_numpy(gen.src).pin_memory()
     dst_h = torch.from_numpy(gen.dst).pin_memory()
     src_d, dst_d = src_h.to(dev), dst_h.to(dev)
@@ -330,8 +335,11 @@ def run_shard_bench(args, ws, rank, local, dev, pr, torch, gen, W, K):
     def step(src, dst, to_host=False, timing=False):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record(stream)
-        g = pr.Graph(n, src, dst)
-        g.shard(rank, ws)
+        if args.ingest == "local":   # this rank's edges only + one out-degree all-reduce
+            g = pr.Graph.sharded(n, src, dst, rank, ws, allreduce)
+        else:
+            g = pr.Graph(n, src, dst)
+            g.shard(rank, ws)
         if ws > 1 and args.exchange == "peers":
             pr.torch_dist_peer_setup(g.handle)
         e[1].record(stream)
@@ -388,7 +396,7 @@ def run_shard_bench(args, ws, rank, local, dev, pr, torch, gen, W, K):
             "ms_per_step": round(t / K, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": dict(workload_config(gen, args, ws), mode="plain", backend=args.backend if ws > 1 else None,
-                           exchange=args.exchange),
+                           exchange=args.exchange, ingest=args.ingest),
             "run": {"E": E, "iterations": iters, "time_to_converge_ms": round(run_ms, 3),
                     "create_and_shard_ms": round(setup_ms, 3), "rank0_shard": recs[0]["info"]},
             "roofline": roofline,

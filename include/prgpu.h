@@ -257,6 +257,35 @@ int pr_get_phase_plan(const pr_graph *g, int32_t reduced, int64_t *edge_bounds, 
 typedef int (*pr_exchange_fn)(void *ctx, double *buf, int64_t chunk, int32_t world, void *stream);
 
 /*
+ * pr_allreduce_fn -- caller-supplied sum all-reduce, in place, of `count` int32
+ * values of the device buffer `buf` over the `world` ranks, ordered on
+ * `stream` (e.g. torch.distributed / NCCL all_reduce).  Returns 0, or nonzero
+ * to abort with PR_ECUDA.
+ */
+typedef int (*pr_allreduce_fn)(void *ctx, int32_t *buf, int64_t count, int32_t world, void *stream);
+
+/*
+ * pr_graph_create_sharded -- build ONLY this rank's share of a world-rank row
+ * partition straight from the raw edge list (the same list on every rank,
+ * host or device, as pr_graph_create): vertex v is owned by rank v mod world,
+ * rows and contribs alike; the rank sorts and deduplicates only the edges into
+ * its vertices (1/world of them), sums the partial out-degrees with one
+ * `allreduce` over n int32 (every deduplicated edge lives on exactly one rank:
+ * the owner of its dst), then derives the contrib order and the sharded layout
+ * identically on every rank (a rank's contribs sit in its chunk in contrib
+ * order).  Must be called on every rank (the all-reduce is collective).  The
+ * graph is for pr_run_sharded / pr_get_shard_info / the peer calls only:
+ * pr_run, pr_preprocess and pr_graph_shard return PR_ESTATE; pr_graph_info's
+ * E and pr_get_csr describe the rank's edges (rows of other ranks' vertices
+ * are empty).  world = 1 equals pr_graph_create + pr_graph_shard(0, 1).
+ * Errors as pr_graph_create, plus PR_EINVAL for a bad rank / world or a NULL
+ * allreduce and PR_ECUDA when the all-reduce fails.
+ */
+int pr_graph_create_sharded(int64_t n, int64_t m, const int32_t *src, const int32_t *dst, int32_t rank,
+                            int32_t world, pr_allreduce_fn allreduce, void *allreduce_ctx, void *stream,
+                            pr_graph **out);
+
+/*
  * pr_graph_shard -- make g (created from the SAME edge list on every rank) the
  * rank's share of a world-rank row partition: contrib-carrying vertices are
  * dealt round-robin in the internal contrib (out-degree) order, so every rank

@@ -44,7 +44,7 @@ PR_CHAIN_EAGER = 128
 ABI_SYMBOLS = (
     "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_release_memory", "pr_last_error",
     "pr_graph_info", "pr_get_csr", "pr_get_reductions", "pr_get_delta_log", "pr_get_run_stats",
-    "pr_graph_shard", "pr_run_sharded", "pr_get_shard_info", "pr_get_phase_plan",
+    "pr_graph_shard", "pr_graph_create_sharded", "pr_run_sharded", "pr_get_shard_info", "pr_get_phase_plan",
     "pr_shard_buffers", "pr_shard_set_peers", "pr_shard_export_ipc", "pr_shard_open_ipc",
 )
 
@@ -103,6 +103,8 @@ class pr_shard_info(ctypes.Structure):
 # int (*pr_exchange_fn)(void *ctx, double *buf, int64_t chunk, int32_t world, void *stream)
 EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                ctypes.c_void_p)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                ctypes.c_void_p)
 
 
 def _load():
@@ -136,6 +138,8 @@ def _load():
     lib.pr_get_run_stats.restype = ctypes.c_int
     lib.pr_graph_shard.argtypes = [p, i32, i32, p]
     lib.pr_graph_shard.restype = ctypes.c_int
+    lib.pr_graph_create_sharded.argtypes = [i64, i64, p, p, i32, i32, ALLREDUCE_FN, p, p, pp]
+    lib.pr_graph_create_sharded.restype = ctypes.c_int
     lib.pr_run_sharded.argtypes = [p, dbl, dbl, i32, p, u32, p, EXCHANGE_FN, p, ctypes.POINTER(i32),
                                    ctypes.POINTER(dbl)]
     lib.pr_run_sharded.restype = ctypes.c_int
@@ -361,6 +365,69 @@ def torch_dist_peer_setup(g, group=None) -> None:
     pr_shard_open_ipc(g, allh)
 
 
+def device_i32(ptr: int, count: int):
+    """A torch view (no copy) of `count` int32 of device memory at `ptr`."""
+    import torch
+
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (int(count),), "typestr": "<i4", "data": (int(ptr), False),
+                                    "version": 2, "strides": None}
+    return torch.as_tensor(_CAI(), device="cuda")
+
+
+def pr_graph_create_sharded(n: int, src, dst, rank: int, world: int, allreduce, stream=None) -> ctypes.c_void_p:
+    """This rank's share of a world-rank row partition, ingesting only the
+    edges into its vertices (v mod world == rank); `allreduce(buf_ptr, count,
+    world, stream_ptr)` sums `count` int32 in place over the ranks."""
+    m = int(src.shape[0])
+    if int(dst.shape[0]) != m:
+        raise ValueError("src and dst lengths differ")
+    for a in (src, dst):
+        dt = str(getattr(a, "dtype", ""))
+        if "int32" not in dt:
+            raise TypeError(f"edge arrays must be int32, got {dt}")
+    err = []
+
+    def _cb(ctx, buf, count, world_, strm):
+        try:
+            allreduce(buf, count, world_, strm)
+            return 0
+        except BaseException as e:  # reported after the call returns
+            err.append(e)
+            return 1
+    cb = ALLREDUCE_FN(_cb)
+    out = ctypes.c_void_p()
+    rc = lib.pr_graph_create_sharded(n, m, _ptr(src) if m else None, _ptr(dst) if m else None, rank, world, cb,
+                                     None, _stream(stream), ctypes.byref(out))
+    if err:
+        raise err[0]
+    _check(rc)
+    return out
+
+
+def torch_dist_allreduce(group=None):
+    """The out-degree all-reduce of pr_graph_create_sharded through
+    torch.distributed (NCCL, or gloo through a host copy)."""
+    import torch
+    import torch.distributed as dist
+
+    nccl = dist.get_backend(group) == "nccl"
+
+    def allreduce(buf: int, count: int, world: int, stream: int):
+        t = device_i32(buf, count)
+        s = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+        with torch.cuda.stream(s):
+            if nccl:
+                dist.all_reduce(t, group=group)
+            else:
+                s.synchronize()
+                h = t.cpu()
+                dist.all_reduce(h, group=group)
+                t.copy_(h)
+                torch.cuda.synchronize()
+    return allreduce
+
+
 def torch_dist_exchange(group=None):
     """The per-sweep exchange of pr_run_sharded through torch.distributed
     (NCCL over NVLink on a GPU node): an in-place all_gather_into_tensor of the
@@ -418,9 +485,14 @@ def pr_run_sharded(g, d: float, threshold: float, max_iter: int, ranks, exchange
 class Graph:
     """RAII convenience wrapper around one pr_graph (still only marshalling)."""
 
-    def __init__(self, n: int, src, dst, stream=None):
+    def __init__(self, n: int, src, dst, stream=None, handle=None):
         self.n = n
-        self.handle = pr_graph_create(n, src, dst, stream)
+        self.handle = handle if handle is not None else pr_graph_create(n, src, dst, stream)
+
+    @classmethod
+    def sharded(cls, n: int, src, dst, rank: int, world: int, allreduce, stream=None):
+        """pr_graph_create_sharded: only this rank's rows are ingested."""
+        return cls(n, None, None, handle=pr_graph_create_sharded(n, src, dst, rank, world, allreduce, stream))
 
     def preprocess(self, flags: int = PR_PRE_IDENTICAL | PR_PRE_CHAIN, stream=None):
         pr_preprocess(self.handle, flags, stream)

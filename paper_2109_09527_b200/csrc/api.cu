@@ -238,23 +238,23 @@ int pr_release_memory(void) {
     return PR_OK;
 }
 
-int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst, void* stream, pr_graph** out) {
-    g_err[0] = 0;
+static int create_graph(const char* fn, int64_t n, int64_t m, const int32_t* src, const int32_t* dst, void* stream,
+                        pr_graph** out, int rank, int world, pr_allreduce_fn allreduce, void* allreduce_ctx) {
     if (!out) {
-        set_error("pr_graph_create: out is NULL");
+        set_error("%s: out is NULL", fn);
         return PR_EINVAL;
     }
     *out = nullptr;
     if (n < 1 || n > 2147483647LL) {
-        set_error("pr_graph_create: n=%lld outside [1, 2^31-1]", (long long)n);
+        set_error("%s: n=%lld outside [1, 2^31-1]", fn, (long long)n);
         return PR_EINVAL;
     }
     if (m < 0 || m > 2147483647LL) {
-        set_error("pr_graph_create: m=%lld outside [0, 2^31-1]", (long long)m);
+        set_error("%s: m=%lld outside [0, 2^31-1]", fn, (long long)m);
         return PR_EINVAL;
     }
     if (m > 0 && (!src || !dst)) {
-        set_error("pr_graph_create: NULL edge array");
+        set_error("%s: NULL edge array", fn);
         return PR_EINVAL;
     }
     Ctx ctx;
@@ -262,10 +262,10 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
     PhaseTimer pt0(ctx.stream, "create");
     // peak of create + preprocess + run: ~ 4 x 8 B per raw edge (sort ping-pong,
     // views) + ~ 80 B per vertex
-    pool_reserve(ctx.stream, (size_t)m * 40 + (size_t)n * 96 + ((size_t)64 << 20));
+    pool_reserve(ctx.stream, (size_t)m * (world > 1 ? 24 : 40) + (size_t)n * 96 + ((size_t)64 << 20));
     pr_graph* g = new (std::nothrow) pr_graph();
     if (!g) {
-        set_error("pr_graph_create: host allocation failed");
+        set_error("%s: host allocation failed", fn);
         return PR_ENOMEM;
     }
     g->n = n;
@@ -304,18 +304,35 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
         }
         pt0.mark("setup");
         PhaseTimer pt(ctx.stream, "create");
-        if ((rc = ingest(g, s, t, ctx)) != PR_OK) break;
+        if ((rc = ingest(g, s, t, ctx, rank, world)) != PR_OK) break;
         pt.mark("ingest");
         dfree(dsrc, ctx.stream);
         dfree(ddst, ctx.stream);
+        if (allreduce) {
+            // the rank ingested only the edges into its vertices: its out-degrees
+            // are partial; their sum over the ranks is the graph's (every
+            // deduplicated edge lives on exactly one rank, the owner of its dst)
+            if (cudaStreamSynchronize(ctx.stream) != cudaSuccess ||
+                allreduce(allreduce_ctx, g->outdeg, n, world, (void*)ctx.stream) != 0) {
+                set_error("%s: the out-degree all-reduce failed", fn);
+                rc = PR_ECUDA;
+                break;
+            }
+            pt.mark("allreduce");
+        }
         if ((rc = build_relabel(g, ctx)) != PR_OK) break;
         pt.mark("relabel");
-
-        if ((rc = build_view_stream(g->plain, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx)) != PR_OK) break;
-        if ((rc = build_view_blocked(g->plain, ctx, g->n_contrib)) != PR_OK) break;
-        pt.mark("stream");
+        if (world > 1 || allreduce) {
+            g->shard_only = true;
+            if ((rc = build_shard(g, rank, world, ctx, true)) != PR_OK) break;
+            pt.mark("shard");
+        } else {
+            if ((rc = build_view_stream(g->plain, ctx, (int32_t)g->n_contrib, g->outdeg, g->cidx)) != PR_OK) break;
+            if ((rc = build_view_blocked(g->plain, ctx, g->n_contrib)) != PR_OK) break;
+            pt.mark("stream");
+        }
         if (cudaStreamSynchronize(ctx.stream) != cudaSuccess) {
-            set_error("pr_graph_create: %s", cudaGetErrorString(cudaGetLastError()));
+            set_error("%s: %s", fn, cudaGetErrorString(cudaGetLastError()));
             rc = PR_ECUDA;
             break;
         }
@@ -333,6 +350,25 @@ int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst
     return PR_OK;
 }
 
+int pr_graph_create(int64_t n, int64_t m, const int32_t* src, const int32_t* dst, void* stream, pr_graph** out) {
+    g_err[0] = 0;
+    return create_graph("pr_graph_create", n, m, src, dst, stream, out, 0, 1, nullptr, nullptr);
+}
+
+int pr_graph_create_sharded(int64_t n, int64_t m, const int32_t* src, const int32_t* dst, int32_t rank,
+                            int32_t world, pr_allreduce_fn allreduce, void* allreduce_ctx, void* stream,
+                            pr_graph** out) {
+    g_err[0] = 0;
+    if (out) *out = nullptr;
+    if (world < 1 || world > 4096 || rank < 0 || rank >= world || !allreduce) {
+        set_error("pr_graph_create_sharded: rank=%d world=%d allreduce=%p (need 0 <= rank < world <= 4096, "
+                  "an all-reduce)", rank, world, (void*)allreduce);
+        return PR_EINVAL;
+    }
+    return create_graph("pr_graph_create_sharded", n, m, src, dst, stream, out, rank, world, allreduce,
+                        allreduce_ctx);
+}
+
 int pr_preprocess(pr_graph* g, uint32_t flags, void* stream) {
     g_err[0] = 0;
     if (!g) {
@@ -342,6 +378,10 @@ int pr_preprocess(pr_graph* g, uint32_t flags, void* stream) {
     if (flags & ~(PR_PRE_IDENTICAL | PR_PRE_CHAIN)) {
         set_error("pr_preprocess: unknown flag bits 0x%x", flags);
         return PR_EINVAL;
+    }
+    if (g->shard_only) {
+        set_error("pr_preprocess: a graph from pr_graph_create_sharded holds one rank's rows only");
+        return PR_ESTATE;
     }
     Ctx ctx;
     PR_TRY(make_ctx(ctx, stream));
@@ -392,6 +432,10 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
         set_error("pr_run: PR_USE_REDUCTIONS before pr_preprocess");
         return PR_ESTATE;
     }
+    if (g->shard_only) {
+        set_error("pr_run: a graph from pr_graph_create_sharded holds one rank's rows only (pr_run_sharded)");
+        return PR_ESTATE;
+    }
     Ctx ctx;
     PR_TRY(make_ctx(ctx, stream));
     int rc = run(g, d, threshold, max_iter, mode, ranks, ctx, iters_out, final_delta_out);
@@ -410,6 +454,10 @@ int pr_graph_shard(pr_graph* g, int32_t rank, int32_t world, void* stream) {
     if (world < 1 || world > 4096 || rank < 0 || rank >= world) {
         set_error("pr_graph_shard: rank=%d world=%d (need 0 <= rank < world <= 4096)", rank, world);
         return PR_EINVAL;
+    }
+    if (g->shard_only) {
+        set_error("pr_graph_shard: the graph is already one rank's share (pr_graph_create_sharded)");
+        return PR_ESTATE;
     }
     Ctx ctx;
     PR_TRY(make_ctx(ctx, stream));

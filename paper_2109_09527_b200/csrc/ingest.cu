@@ -22,15 +22,19 @@ namespace prgpu {
 // become the sentinel 2^(2b) - 1, which sorts last and is dropped by the
 // unique pass (a real key equals it only for the self-loop (2^b-1, 2^b-1)).
 // No compaction here: the sort and the unique pass do not care about order.
+// Sharded create (world > 1): edges into vertices another rank owns (dst mod
+// world != rank) become the sentinel too -- every id is still validated.
 __global__ void k_pack(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m, int64_t n,
-                       int b, uint64_t sentinel, uint64_t* __restrict__ keys, int* __restrict__ err) {
+                       int b, uint64_t sentinel, uint64_t* __restrict__ keys, int* __restrict__ err, int rank,
+                       int world) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     bool any_bad = false;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
         const int32_t s = src[i], t = dst[i];
         const bool bad = s < 0 || (int64_t)s >= n || t < 0 || (int64_t)t >= n;
         any_bad |= bad;
-        keys[i] = (bad || s == t) ? sentinel : (((uint64_t)(uint32_t)t << b) | (uint32_t)s);
+        const bool other = world > 1 && (t % world) != rank;
+        keys[i] = (bad || s == t || other) ? sentinel : (((uint64_t)(uint32_t)t << b) | (uint32_t)s);
     }
     if (__any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
 }
@@ -224,7 +228,7 @@ static unsigned grid_for(const Ctx& ctx, int64_t work, int nt) {
     return (unsigned)g;
 }
 
-int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
+int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank, int world) {
     const int64_t n = g->n, m = g->m_raw;
     const int b = bits_for((uint64_t)(n - 1));
     cudaStream_t s = ctx.stream;
@@ -251,7 +255,7 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx) {
     if (mk > 0) {
         PR_TRY(dalloc(&keys, (size_t)mk, s));
         PR_LAUNCH(ctx, k_pack, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, sentinel, keys,
-                  (int*)(scratch + 1));
+                  (int*)(scratch + 1), rank, world);
         PR_TRY(dalloc(&keys_alt, (size_t)mk, s));
         PR_TRY(dalloc(&g->outdeg, (size_t)n, s));
         PR_CUDA(cudaMemsetAsync(g->outdeg, 0, sizeof(int32_t) * (size_t)n, s));

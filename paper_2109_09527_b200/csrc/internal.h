@@ -122,6 +122,7 @@ struct pr_graph {
     int64_t n_hsrc = 0;             // distinct chain sources (delayed chain resolution)
     prgpu::View reduced;
     // row sharding over P ranks (pr_graph_shard, shard.cu)
+    bool shard_only = false;        // created by pr_graph_create_sharded: only pr_run_sharded applies
     int32_t shard_rank = -1;
     int32_t shard_world = 0;
     int64_t shard_chunk = 0;        // doubles per rank in the exchanged buffer (owned contribs + (L1, Linf))
@@ -158,7 +159,7 @@ struct pr_graph {
 };
 
 namespace prgpu {
-int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx);
+int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank = 0, int world = 1);
 int build_relabel(pr_graph* g, Ctx& ctx);
 int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx);
 int build_spans(View& v, Ctx& ctx, int64_t span_steps);
@@ -175,7 +176,7 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx);
 int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks,
         Ctx& ctx, int32_t* iters_out, double* delta_out);
 int read_count(Ctx& ctx, const int64_t* dev, int64_t* host);
-int build_shard(pr_graph* g, int rank, int world, Ctx& ctx);
+int build_shard(pr_graph* g, int rank, int world, Ctx& ctx, bool by_id = false);
 void clear_shard(pr_graph* g, cudaStream_t s);
 void clear_peers(pr_graph* g);
 int set_peers(pr_graph* g, double* const* y0s, double* const* y1s, int world);

@@ -114,6 +114,46 @@ struct ShPosEmit {
     __device__ void operator()(int64_t i, int64_t pos, int64_t) const { out[i] = pos; }
 };
 
+// ---- id ownership (pr_graph_create_sharded): owner(v) = v mod P, for rows
+// and contribs alike, so a rank can ingest only the edges into its vertices.
+// A rank's contribs sit in its chunk in contrib (degree) order.
+__global__ void k_sh_inv(const int32_t* __restrict__ cidx, int64_t n, int32_t* __restrict__ inv) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        if (cidx[v] >= 0) inv[cidx[v]] = (int32_t)v;
+}
+__global__ void k_sh_idkeys(const int32_t* __restrict__ inv, int64_t nc, int P, uint64_t* __restrict__ keys) {
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x)
+        keys[c] = ((uint64_t)(uint32_t)(inv[c] % P) << 32) | (uint64_t)c;
+}
+// first sorted position of every owner (start[P] = nc); keys sorted by owner
+__global__ void k_sh_starts(const uint64_t* __restrict__ keys, int64_t nc, int P, int64_t* __restrict__ start) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(keys[i] >> 32);
+        const int rp = i == 0 ? -1 : (int)(keys[i - 1] >> 32);
+        for (int q = rp + 1; q <= r; ++q) start[q] = i;
+        if (i == nc - 1)
+            for (int q = r + 1; q <= P; ++q) start[q] = nc;
+    }
+}
+__global__ void k_sh_owner_mod(int64_t n, int P, int32_t* __restrict__ owner, int32_t* __restrict__ scidx) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        owner[v] = (int32_t)(v % P);
+        scidx[v] = -1;
+    }
+}
+__global__ void k_sh_idslots(const uint64_t* __restrict__ keys, int64_t nc, const int64_t* __restrict__ start,
+                             const int32_t* __restrict__ inv, int64_t H, int64_t chunk, int32_t* __restrict__ scidx,
+                             int32_t* __restrict__ smap, int32_t* __restrict__ hot_src) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(keys[i] >> 32);
+        const int64_t c = (int64_t)(keys[i] & 0xffffffffu);
+        const int64_t cs = H + r * chunk + (i - start[r]);
+        scidx[inv[c]] = (int32_t)cs;
+        smap[c] = (int32_t)(c < H ? c : cs);
+        if (c < H) hot_src[c] = (int32_t)cs;
+    }
+}
+
 void clear_peers(pr_graph* g) {
     if (g->speer_dev) {
         cudaFree(g->speer_dev);
@@ -145,39 +185,80 @@ void clear_shard(pr_graph* g, cudaStream_t s) {
     g->shard_owned = 0;
 }
 
-int build_shard(pr_graph* g, int rank, int world, Ctx& ctx) {
+int build_shard(pr_graph* g, int rank, int world, Ctx& ctx, bool by_id) {
     cudaStream_t s = ctx.stream;
     clear_shard(g, s);
     const int64_t n = g->n, nc = g->n_contrib;
     TmpGuard tg_(s);
     int32_t* smap = nullptr;
     int64_t* cnt = nullptr;
+    int32_t* inv = nullptr;
+    uint64_t* keys = nullptr;
+    uint64_t* keys_alt = nullptr;
+    int64_t* start = nullptr;
     tg_.track(smap);
     tg_.track(cnt);
+    tg_.track(inv);
+    tg_.track(keys);
+    tg_.track(keys_alt);
+    tg_.track(start);
     PR_TRY(dalloc(&cnt, 2, s));
-    // chunk = most slots any rank owns, + (L1, Linf)
-    const int64_t nb = (nc + SH_BLOCK - 1) / SH_BLOCK;
-    int64_t cmax = 0;
-    for (int r = 0; r < world && r < nb; ++r) {
-        const int64_t blocks = (nb - r + world - 1) / world;  // blocks r, r + world, ...
-        int64_t cr = blocks * SH_BLOCK;
-        if ((nb - 1) % world == r) cr -= nb * SH_BLOCK - nc;  // the last block is partial
-        cmax = std::max(cmax, cr);
-    }
-    const int64_t chunk = cmax + 2;
     const int64_t H = std::min<int64_t>(SE_L1_TIER, nc);  // hot copy: the smem and L1 tiers of the gather
-    if (H + (int64_t)world * chunk + 1 > INT32_MAX) {
-        set_error("pr_graph_shard: sharded contrib layout exceeds int32 slots");
-        return PR_EINVAL;
-    }
     PR_TRY(dalloc(&g->sowner, (size_t)n, s));
     PR_TRY(dalloc(&g->scidx, (size_t)n, s));
-    PR_LAUNCH(ctx, k_sh_owner, sh_grid(ctx, n), 256, 0, (const int32_t*)g->cidx, n, world, H, chunk, g->sowner,
-              g->scidx);
     if (nc > 0) {
         PR_TRY(dalloc(&smap, (size_t)nc, s));
         PR_TRY(dalloc(&g->shot_src, (size_t)std::max<int64_t>(H, 1), s));
-        PR_LAUNCH(ctx, k_sh_smap, sh_grid(ctx, nc), 256, 0, nc, world, H, chunk, smap, g->shot_src);
+    }
+    int64_t chunk = 2;
+    if (!by_id) {
+        // chunk = most slots any rank owns, + (L1, Linf)
+        const int64_t nb = (nc + SH_BLOCK - 1) / SH_BLOCK;
+        int64_t cmax = 0;
+        for (int r = 0; r < world && r < nb; ++r) {
+            const int64_t blocks = (nb - r + world - 1) / world;  // blocks r, r + world, ...
+            int64_t cr = blocks * SH_BLOCK;
+            if ((nb - 1) % world == r) cr -= nb * SH_BLOCK - nc;  // the last block is partial
+            cmax = std::max(cmax, cr);
+        }
+        chunk = cmax + 2;
+        if (H + (int64_t)world * chunk + 1 > INT32_MAX) {
+            set_error("pr_graph_shard: sharded contrib layout exceeds int32 slots");
+            return PR_EINVAL;
+        }
+        PR_LAUNCH(ctx, k_sh_owner, sh_grid(ctx, n), 256, 0, (const int32_t*)g->cidx, n, world, H, chunk, g->sowner,
+                  g->scidx);
+        if (nc > 0) PR_LAUNCH(ctx, k_sh_smap, sh_grid(ctx, nc), 256, 0, nc, world, H, chunk, smap, g->shot_src);
+    } else {
+        // owner(v) = v mod P; a rank's contribs in contrib order inside its chunk:
+        // sort the contrib slots by owner (stable: slots stay ascending)
+        PR_LAUNCH(ctx, k_sh_owner_mod, sh_grid(ctx, n), 256, 0, n, world, g->sowner, g->scidx);
+        std::vector<int64_t> hs(world + 1, 0);
+        if (nc > 0) {
+            PR_TRY(dalloc(&inv, (size_t)nc, s));
+            PR_TRY(dalloc(&keys, (size_t)nc, s));
+            PR_TRY(dalloc(&keys_alt, (size_t)nc, s));
+            PR_TRY(dalloc(&start, (size_t)world + 1, s));
+            PR_LAUNCH(ctx, k_sh_inv, sh_grid(ctx, n), 256, 0, (const int32_t*)g->cidx, n, inv);
+            PR_LAUNCH(ctx, k_sh_idkeys, sh_grid(ctx, nc), 256, 0, (const int32_t*)inv, nc, world, keys);
+            bool alt = false;
+            if (world > 1)
+                PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, nc, 32,
+                                                    32 + bits_for((uint64_t)(world - 1)), &alt)));
+            const uint64_t* sk = alt ? keys_alt : keys;
+            PR_LAUNCH(ctx, k_sh_starts, sh_grid(ctx, nc), 256, 0, sk, nc, world, start);
+            PR_CUDA(cudaMemcpyAsync(hs.data(), start, sizeof(int64_t) * (size_t)(world + 1), cudaMemcpyDeviceToHost, s));
+            PR_CUDA(cudaStreamSynchronize(s));
+            int64_t cmax = 0;
+            for (int r = 0; r < world; ++r) cmax = std::max(cmax, hs[r + 1] - hs[r]);
+            chunk = cmax + 2;
+            if (H + (int64_t)world * chunk + 1 > INT32_MAX) {
+                set_error("pr_graph_create_sharded: sharded contrib layout exceeds int32 slots");
+                return PR_EINVAL;
+            }
+            PR_LAUNCH(ctx, k_sh_idslots, sh_grid(ctx, nc), 256, 0, sk, nc, (const int64_t*)start,
+                      (const int32_t*)inv, H, chunk, g->scidx, smap, g->shot_src);
+        }
     }
 
     // owned rows (vertex order) and owned in-degree-0 vertices

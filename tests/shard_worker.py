@@ -2,7 +2,7 @@
 torchrun job (gloo process group, every rank on cuda:0) running the sharded
 iteration through the real torch.distributed exchange, then checking the
 assembled ranks against the oracle on rank 0.  Usage (torchrun):
-  shard_worker.py <config> <out.json>"""
+  shard_worker.py <config> <out.json> [peers|local]"""
 import json
 import os
 import sys
@@ -19,12 +19,19 @@ import paper_2109_09527_b200 as pr  # noqa: E402
 
 cfg, out = int(sys.argv[1]), sys.argv[2]
 peers = len(sys.argv) > 3 and sys.argv[3] == "peers"
+local = len(sys.argv) > 3 and sys.argv[3] == "local"   # pr_graph_create_sharded: per-rank ingest
 dist.init_process_group("gloo")
 rank, world = dist.get_rank(), dist.get_world_size()
 torch.cuda.set_device(0)
 gen = graphgen.make_config(cfg)
-with pr.Graph(gen.n, torch.from_numpy(gen.src).cuda(), torch.from_numpy(gen.dst).cuda()) as g:
-    g.shard(rank, world)
+src_d, dst_d = torch.from_numpy(gen.src).cuda(), torch.from_numpy(gen.dst).cuda()
+if local:
+    graph = pr.Graph.sharded(gen.n, src_d, dst_d, rank, world, pr.torch_dist_allreduce())
+else:
+    graph = pr.Graph(gen.n, src_d, dst_d)
+with graph as g:
+    if not local:
+        g.shard(rank, world)
     if peers:  # the exchange fused into the kernels: CUDA IPC buffers, barrier-only exchange
         pr.torch_dist_peer_setup(g.handle)
     x = torch.empty(gen.n, dtype=torch.float64, device="cuda")

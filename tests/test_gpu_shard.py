@@ -76,15 +76,66 @@ class PeerBarrier:
         return ex
 
 
-def run_world(pr, n, s, t, world, tau, max_iter=1000, mode=0, peers=False):
+class LoopAllreduce:
+    """In-process sum all-reduce of int32 device buffers (host copies after a
+    host barrier; no kernel waits on another rank)."""
+
+    def __init__(self, pr, world):
+        self.pr = pr
+        self.world = world
+        self.host = [None] * world
+        self.bar = threading.Barrier(world)
+
+    def for_rank(self, rank):
+        def ar(buf, count, world, stream):
+            assert world == self.world
+            torch.cuda.synchronize()
+            t = self.pr.device_i32(buf, count)
+            self.host[rank] = t.cpu()
+            self.bar.wait()
+            tot = torch.stack(self.host).sum(0, dtype=torch.int64).to(torch.int32)
+            self.bar.wait()
+            t.copy_(tot)
+            torch.cuda.synchronize()
+        return ar
+
+
+def create_local(pr, n, s, t, world):
+    """pr_graph_create_sharded on `world` in-process ranks (threads: the
+    out-degree all-reduce is collective)."""
+    ar = LoopAllreduce(pr, world)
+    graphs = [None] * world
+    errs = []
+
+    def work(r):
+        try:
+            graphs[r] = pr.Graph.sharded(n, dev(s), dev(t), r, world, ar.for_rank(r))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+            ar.bar.abort()
+    ths = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    if errs:
+        for g in graphs:
+            if g is not None:
+                g.close()
+        raise errs[0]
+    return graphs
+
+
+def run_world(pr, n, s, t, world, tau, max_iter=1000, mode=0, peers=False, local=False):
     """Shard one graph over `world` in-process ranks; returns the assembled
     ranks, per-rank (status, iters, delta) and shard infos.  peers=True: the
     exchange fused into the kernels (every rank stores into every rank's
     buffers; pr_shard_set_peers with the other graphs' device pointers)."""
-    graphs = [pr.Graph(n, dev(s), dev(t)) for _ in range(world)]
+    graphs = create_local(pr, n, s, t, world) if local else [pr.Graph(n, dev(s), dev(t)) for _ in range(world)]
     try:
-        for r, g in enumerate(graphs):
-            g.shard(r, world)
+        if not local:
+            for r, g in enumerate(graphs):
+                g.shard(r, world)
         infos = [g.shard_info() for g in graphs]
         xs = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(world)]
         lb = Loopback(pr, world)
@@ -316,6 +367,147 @@ def test_peer_store_multiprocess_ipc(pr, tmp_path, world):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "tests", "shard_worker.py"),
            "2", str(out), "peers"]
+    subprocess.run(cmd, check=True, timeout=600, cwd=root)
+    r = json.load(open(out))
+    assert len({(x["st"], x["it"], x["fd"]) for x in r["ranks"]}) == 1
+    assert r["max_diff"] <= 1e-10 and r["l1_diff"] <= 1e-9
+
+
+# ------------------------------------------- per-rank ingest (create_sharded) --
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+def test_local_ingest_world1_is_sync(pr, name):
+    """pr_graph_create_sharded with world = 1 equals pr_graph_create +
+    pr_graph_shard(0, 1), hence pr_run(PR_MODE_SYNC), bit for bit."""
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        x0 = torch.empty(n, dtype=torch.float64, device="cuda")
+        ref = g.run(x0, D, 1e-12, 1000)
+    x, out, infos, logs = run_world(pr, n, s, t, 1, 1e-12, local=True)
+    assert out[0] == ref
+    assert np.array_equal(x, x0.cpu().numpy())
+    assert infos[0]["owned_vertices"] == n
+
+
+@pytest.mark.parametrize("name", sorted(GRAPHS))
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_local_ingest_matches_oracle(pr, name, world):
+    """Every rank ingests only the edges into its vertices (v mod world):
+    the shards partition the edges, rows and vertices, and the assembled
+    ranks match the oracle (1e-10 / 1e-9, the +/-1 rule)."""
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    ref_g = oracle.build_csr(n, s, t)
+    tau = 1e-12
+    ref = oracle.pagerank(ref_g, D, tau, 1000)
+    x, out, infos, logs = run_world(pr, n, s, t, world, tau, local=True)
+    assert len({o for o in out}) == 1
+    st, it, fd = out[0]
+    assert st == ref.status
+    assert_iters(it, ref, tau)
+    assert_close(x, ref.x)
+    assert sum(i["owned_vertices"] for i in infos) == n
+    assert [i["owned_vertices"] for i in infos] == [len(range(r, n, world)) for r in range(world)]
+    assert sum(i["edges"] for i in infos) == ref_g.E
+    assert sum(i["rows"] for i in infos) == int((np.diff(ref_g.row_ptr) > 0).sum())
+
+
+def test_local_ingest_rank_csr_and_outdeg(pr):
+    """A rank's CSR holds exactly the rows of its vertices (bit-exact with the
+    oracle's rows), and the all-reduced out-degrees are the graph's."""
+    n, edges = G.planted_graph(4, n_base=150, chains=(3, 7))
+    s, t = G.edges_to_arrays(edges)
+    ref_g = oracle.build_csr(n, s, t)
+    world = 3
+    graphs = create_local(pr, n, s, t, world)
+    try:
+        for r, g in enumerate(graphs):
+            E = g.info()["E"]
+            rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+            col = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
+            od = torch.empty(n, dtype=torch.int32, device="cuda")
+            pr.pr_get_csr(g.handle, rp, col, od)
+            rp, col, od = rp.cpu().numpy(), col[:E].cpu().numpy(), od.cpu().numpy()
+            assert np.array_equal(od, ref_g.outdeg)
+            mine = [v for v in range(n) if v % world == r]
+            assert E == sum(int(ref_g.row_ptr[v + 1] - ref_g.row_ptr[v]) for v in mine)
+            for v in range(n):
+                got = col[rp[v]:rp[v + 1]]
+                want = ref_g.col_idx[ref_g.row_ptr[v]:ref_g.row_ptr[v + 1]] if v % world == r else []
+                assert np.array_equal(got, want)
+    finally:
+        for g in graphs:
+            g.close()
+
+
+def test_local_ingest_validation(pr):
+    n = 40
+    s, t = G.edges_to_arrays(G.random_edges(n, 160, 5))
+    for rank, world in ((0, 0), (2, 2), (-1, 3), (0, 5000)):
+        with pytest.raises(pr.PRError) as e:
+            pr.Graph.sharded(n, dev(s), dev(t), rank, world, lambda *a: None)
+        assert e.value.code == pr.PR_EINVAL
+    with pytest.raises(RuntimeError, match="allreduce failed"):
+        def boom(*a):
+            raise RuntimeError("allreduce failed")
+        pr.Graph.sharded(n, dev(s), dev(t), 0, 1, boom)
+    bad = t.copy()
+    bad[3] = n                                           # ids are validated on every rank
+    with pytest.raises(pr.PRError) as e:
+        pr.Graph.sharded(n, dev(s), dev(bad), 0, 1, lambda *a: None)
+    assert e.value.code == pr.PR_EINVAL
+    g = pr.Graph.sharded(n, dev(s), dev(t), 0, 1, lambda *a: None)
+    try:
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        for call in (lambda: g.run(x, D, 1e-10, 10), lambda: g.preprocess(), lambda: g.shard(0, 1)):
+            with pytest.raises(pr.PRError) as e:
+                call()
+            assert e.value.code == pr.PR_ESTATE
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("cfg,world", [(2, 4), (3, 3)])
+def test_local_ingest_configs(pr, cfg, world):
+    gen = graphgen.make_config(cfg)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    ref = oracle.pagerank(ref_g, gen.d, gen.tau, gen.max_iter)
+    x, out, infos, logs = run_world(pr, gen.n, gen.src, gen.dst, world, gen.tau, gen.max_iter, local=True)
+    st, it, fd = out[0]
+    assert st == ref.status
+    assert_iters(it, ref, gen.tau)
+    assert_close(x, ref.x)
+    share = ref_g.E / world
+    assert max(i["edges"] for i in infos) <= 1.5 * share + 1
+
+
+@pytest.mark.parametrize("name", ["planted", "random"])
+def test_local_ingest_peer_stores(pr, name):
+    """The fused peer-store exchange on locally ingested shards: bit-identical
+    to their all-gather exchange."""
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    a = run_world(pr, n, s, t, 3, 1e-12, local=True)
+    b = run_world(pr, n, s, t, 3, 1e-12, local=True, peers=True)
+    assert a[1] == b[1] and np.array_equal(a[0], b[0])
+
+
+def test_local_ingest_multiprocess(pr, tmp_path):
+    """torchrun, one process per rank, the torch.distributed all-reduce and
+    exchange (gloo; every rank on cuda:0, host-side collectives only)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    out = tmp_path / "shard_local.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(root, "tests", "shard_worker.py"),
+           "2", str(out), "local"]
     subprocess.run(cmd, check=True, timeout=600, cwd=root)
     r = json.load(open(out))
     assert len({(x["st"], x["it"], x["fd"]) for x in r["ranks"]}) == 1
