@@ -330,6 +330,28 @@ int pr_run_sharded(pr_graph *g, double d, double threshold, int32_t max_iter, vo
  * All return PR_OK, PR_EINVAL, PR_ESTATE (no pr_graph_shard) or PR_ECUDA.
  */
 int pr_shard_buffers(const pr_graph *g, void **y0, void **y1, int64_t *len);
+
+/*
+ * pr_shard_device_barrier -- with peer buffers set, on != 0 replaces the
+ * per-sweep host barrier (the exchange callback with buf = NULL) by a
+ * device-side one: after the rank's finalize and peer stores, one thread
+ * stores the barrier epoch into every peer's arrival flags (st.release.sys,
+ * slot = this rank) and spins until every peer's epoch has arrived in its own
+ * flags (ld.acquire.sys) -- no host synchronisation inside the sweep loop.
+ * Every rank must make the same calls in the same order (the epochs count
+ * barriers).  A wait over ~20 s aborts the run with PR_ECUDA.  world <= 65.
+ * PR_ESTATE without peer buffers (world > 1).  Not measured across GPUs here.
+ */
+int pr_shard_device_barrier(pr_graph *g, int32_t on);
+
+/*
+ * pr_selftest_peer_barrier -- diagnostic: the barrier protocol above run by
+ * `world` emulated ranks = the blocks of ONE cooperative launch on this
+ * device (launches that wait on one another must not share a GPU), `epochs`
+ * barriers, each checking that every rank sees every other rank's write of
+ * that epoch.  PR_OK, or PR_ECUDA with the count in pr_last_error().
+ */
+int pr_selftest_peer_barrier(int32_t world, int32_t epochs, void *stream);
 int pr_shard_set_peers(pr_graph *g, void *const *y0s, void *const *y1s, int32_t world);
 int pr_shard_export_ipc(const pr_graph *g, void *handles);
 int pr_shard_open_ipc(pr_graph *g, const void *handles, int32_t world);

@@ -45,7 +45,7 @@ ABI_SYMBOLS = (
     "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_release_memory", "pr_last_error",
     "pr_graph_info", "pr_get_csr", "pr_get_reductions", "pr_get_delta_log", "pr_get_run_stats",
     "pr_graph_shard", "pr_graph_create_sharded", "pr_run_sharded", "pr_get_shard_info", "pr_get_phase_plan",
-    "pr_shard_buffers", "pr_shard_set_peers", "pr_shard_export_ipc", "pr_shard_open_ipc",
+    "pr_shard_buffers", "pr_shard_set_peers", "pr_shard_device_barrier", "pr_selftest_peer_barrier", "pr_shard_export_ipc", "pr_shard_open_ipc",
 )
 
 
@@ -138,6 +138,10 @@ def _load():
     lib.pr_get_run_stats.restype = ctypes.c_int
     lib.pr_graph_shard.argtypes = [p, i32, i32, p]
     lib.pr_graph_shard.restype = ctypes.c_int
+    lib.pr_shard_device_barrier.argtypes = [p, i32]
+    lib.pr_shard_device_barrier.restype = ctypes.c_int
+    lib.pr_selftest_peer_barrier.argtypes = [i32, i32, p]
+    lib.pr_selftest_peer_barrier.restype = ctypes.c_int
     lib.pr_graph_create_sharded.argtypes = [i64, i64, p, p, i32, i32, ALLREDUCE_FN, p, p, pp]
     lib.pr_graph_create_sharded.restype = ctypes.c_int
     lib.pr_run_sharded.argtypes = [p, dbl, dbl, i32, p, u32, p, EXCHANGE_FN, p, ctypes.POINTER(i32),
@@ -341,6 +345,16 @@ def pr_shard_set_peers(g, y0s, y1s) -> None:
     A = (ctypes.c_void_p * w)(*[v or 0 for v in y0s])
     B = (ctypes.c_void_p * w)(*[v or 0 for v in y1s])
     _check(lib.pr_shard_set_peers(g, A, B, w))
+
+
+def pr_shard_device_barrier(g, on: bool = True) -> None:
+    """Per-sweep synchronisation of the peer-store exchange on the device."""
+    _check(lib.pr_shard_device_barrier(g, 1 if on else 0))
+
+
+def pr_selftest_peer_barrier(world: int, epochs: int = 64, stream=None) -> None:
+    """The device barrier's protocol on emulated ranks (one cooperative launch)."""
+    _check(lib.pr_selftest_peer_barrier(world, epochs, _stream(stream)))
 
 
 def pr_shard_export_ipc(g) -> bytes:

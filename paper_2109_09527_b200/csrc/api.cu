@@ -559,6 +559,37 @@ int pr_shard_set_peers(pr_graph* g, void* const* y0s, void* const* y1s, int32_t 
     return set_peers(g, (double* const*)y0s, (double* const*)y1s, world);
 }
 
+int pr_shard_device_barrier(pr_graph* g, int32_t on) {
+    g_err[0] = 0;
+    if (!g) {
+        set_error("pr_shard_device_barrier: NULL graph");
+        return PR_EINVAL;
+    }
+    if (on && (g->shard_world < 1 || (g->shard_world > 1 && !g->speer_flags))) {
+        set_error("pr_shard_device_barrier: needs the peer buffers (pr_shard_set_peers / pr_shard_open_ipc)");
+        return PR_ESTATE;
+    }
+    if (on && g->shard_world > 65) {
+        set_error("pr_shard_device_barrier: world %d > 65", g->shard_world);
+        return PR_EINVAL;
+    }
+    g->sdev_barrier = on != 0;
+    return PR_OK;
+}
+
+int pr_selftest_peer_barrier(int32_t world, int32_t epochs, void* stream) {
+    g_err[0] = 0;
+    Ctx ctx;
+    PR_TRY(make_ctx(ctx, stream));
+    int bad = 0;
+    PR_TRY(barrier_selftest(world, epochs, ctx, &bad));
+    if (bad != 0) {
+        set_error("pr_selftest_peer_barrier: %d mismatches / timeouts (x1e6)", bad);
+        return PR_ECUDA;
+    }
+    return PR_OK;
+}
+
 int pr_shard_export_ipc(const pr_graph* g, void* handles) {
     if (!g || !handles) {
         set_error("pr_shard_export_ipc: bad arguments");

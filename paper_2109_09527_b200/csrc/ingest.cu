@@ -39,6 +39,35 @@ __global__ void k_pack(const int32_t* __restrict__ src, const int32_t* __restric
     if (__any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicOr(err, 1);
 }
 
+// Sharded create: the rank's own edges (dst mod world == rank, no self-loops)
+// appended compactly (warp-aggregated counter; the order is irrelevant: the
+// sort that follows fixes it), every id validated.
+__global__ void k_pack_own(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m, int64_t n,
+                           int b, uint64_t* __restrict__ keys, unsigned long long* __restrict__ cnt,
+                           int* __restrict__ err, int rank, int world) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    bool any_bad = false;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < m; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        bool keep = false;
+        uint64_t key = 0;
+        if (i < m) {
+            const int32_t s = src[i], t = dst[i];
+            const bool bad = s < 0 || (int64_t)s >= n || t < 0 || (int64_t)t >= n;
+            any_bad |= bad;
+            keep = !bad && s != t && (t % world) == rank;
+            key = ((uint64_t)(uint32_t)t << b) | (uint32_t)s;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        unsigned long long base = 0;
+        if (lane == 0 && bal) base = atomicAdd(cnt, (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) keys[base + __popc(bal & ((1u << lane) - 1))] = key;
+    }
+    if (__any_sync(0xffffffffu, any_bad) && lane == 0) atomicOr(err, 1);
+}
+
 __global__ void k_check_ids(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m, int64_t n,
                             int* __restrict__ err) {
     bool any_bad = false;
@@ -244,18 +273,34 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
     PR_TRY(dalloc(&scratch, 2, s));
     PR_CUDA(cudaMemsetAsync(scratch, 0, 2 * sizeof(int64_t), s));
     // n == 1 (b == 0): every edge is a self-loop, nothing to sort
-    const int64_t mk = b > 0 ? m : 0;
+    int64_t mk = b > 0 ? m : 0;
     bool od_runs = false;  // outdeg counted from the src runs of the partial sort
     const uint64_t sentinel = b > 0 ? ((2 * b >= 64) ? ~0ull : ((1ull << (2 * b)) - 1)) : 0ull;
 
     // pack, sort by (dst, src), deduplicate + CSR (row_ptr, col_idx) in one pass
-    PR_TRY(dalloc(&g->col, (size_t)(mk > 0 ? mk : 1), s));
     PR_TRY(dalloc(&g->row_ptr, (size_t)n + 1, s));
     PR_CUDA(cudaMemsetAsync(g->row_ptr, 0, sizeof(int64_t) * (size_t)(n + 1), s));  // E == 0: all rows empty
     if (mk > 0) {
         PR_TRY(dalloc(&keys, (size_t)mk, s));
-        PR_LAUNCH(ctx, k_pack, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, sentinel, keys,
-                  (int*)(scratch + 1), rank, world);
+        if (world > 1) {  // sharded create: only this rank's edges, compacted (the sort sees 1/world of them)
+            PR_LAUNCH(ctx, k_pack_own, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, keys,
+                      (unsigned long long*)scratch, (int*)(scratch + 1), rank, world);
+            int64_t h2[2];
+            PR_CUDA(cudaMemcpyAsync(h2, scratch, sizeof(h2), cudaMemcpyDeviceToHost, s));
+            PR_CUDA(cudaStreamSynchronize(s));
+            if (h2[1] != 0) {
+                set_error("pr_graph_create: vertex id outside [0, n)");
+                return PR_EINVAL;
+            }
+            mk = h2[0];
+            PR_CUDA(cudaMemsetAsync(scratch, 0, sizeof(int64_t), s));
+        } else {
+            PR_LAUNCH(ctx, k_pack, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, sentinel, keys,
+                      (int*)(scratch + 1), rank, world);
+        }
+    }
+    PR_TRY(dalloc(&g->col, (size_t)(mk > 0 ? mk : 1), s));
+    if (mk > 0) {
         PR_TRY(dalloc(&keys_alt, (size_t)mk, s));
         PR_TRY(dalloc(&g->outdeg, (size_t)n, s));
         PR_CUDA(cudaMemsetAsync(g->outdeg, 0, sizeof(int32_t) * (size_t)n, s));

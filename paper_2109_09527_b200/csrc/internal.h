@@ -83,6 +83,7 @@ struct DevState {
     uint32_t ticket_scatter;
     int32_t status;
     int32_t log_cap;
+    int32_t peer_err;   // the device-side peer barrier timed out
 };
 
 }  // namespace prgpu
@@ -136,6 +137,9 @@ struct pr_graph {
     prgpu::View shard;              // owned rows of in-degree > 0, columns in sharded slots
     double* sy[2] = {nullptr, nullptr};  // [H + world * chunk + 1] ping-pong, last slot = +0.0 (cudaMalloc: IPC-exportable)
     double** speer_dev = nullptr;   // [2][world-1] peers' sy[parity] (pr_shard_set_peers / pr_shard_open_ipc)
+    unsigned long long** speer_flags = nullptr;  // [world-1] peers' arrival flags (after their sy[0])
+    bool sdev_barrier = false;      // per-sweep synchronisation by the device-side peer barrier
+    uint64_t bar_epoch = 0;         // epochs of that barrier so far (the same sequence on every rank)
     std::vector<void*> speer_ipc;   // IPC-opened peer bases to close
     // iteration buffers (allocated lazily by pr_run)
     double* x = nullptr;            // fp64[n] (used when the caller's ranks are on the host)
@@ -180,6 +184,8 @@ int build_shard(pr_graph* g, int rank, int world, Ctx& ctx, bool by_id = false);
 void clear_shard(pr_graph* g, cudaStream_t s);
 void clear_peers(pr_graph* g);
 int set_peers(pr_graph* g, double* const* y0s, double* const* y1s, int world);
+int device_barrier(pr_graph* g, Ctx& ctx);
+int barrier_selftest(int world, int epochs, Ctx& ctx, int* bad_out);
 int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
                 pr_exchange_fn exchange, void* exchange_ctx, int32_t* iters_out, double* delta_out);
 }  // namespace prgpu

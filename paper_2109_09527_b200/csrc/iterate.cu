@@ -1238,7 +1238,10 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
     PR_LAUNCH(ctx, k_shard_combine, cgrid, 256, 0, ia0, g->sy[0], (const int32_t*)g->shot_src, H, world, chunk, 0);
     // peer buffers: no rank may store into another's buffers before that rank
     // has initialised them (sweep 1's stores would be overwritten)
-    if (peers && exchange(exchange_ctx, nullptr, chunk, world, (void*)s) != 0) {
+    const bool dev_bar = peers && g->sdev_barrier;
+    if (dev_bar) {
+        PR_TRY(device_barrier(g, ctx));
+    } else if (peers && exchange(exchange_ctx, nullptr, chunk, world, (void*)s) != 0) {
         set_error("pr_run_sharded: the exchange callback failed before sweep 1");
         return PR_ECUDA;
     }
@@ -1287,8 +1290,11 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
                       0, (const int32_t*)g->szlist, nz, c, (const int32_t*)g->outdeg, (const int32_t*)g->scidx, pout,
                       world - 1);
         // all-gather of the chunks (or, with peer buffers, only the
-        // cross-rank barrier: every rank's stores landed in every buffer)
-        if (exchange(exchange_ctx, peers ? nullptr : y_out + H, chunk, world, (void*)s) != 0) {
+        // cross-rank barrier: every rank's stores landed in every buffer --
+        // on the device when the device-side barrier is on: no host sync)
+        if (dev_bar) {
+            PR_TRY(device_barrier(g, ctx));
+        } else if (exchange(exchange_ctx, peers ? nullptr : y_out + H, chunk, world, (void*)s) != 0) {
             set_error("pr_run_sharded: the exchange callback failed at sweep %lld", (long long)it + 1);
             return PR_ECUDA;
         }
@@ -1296,7 +1302,13 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
         return PR_OK;
     };
     LoopStats ls;  // (tau = 0: doubling batches)
-    PR_TRY(sweep_loop(g, ctx, max_iter, 0.0, sweep, [&](int64_t) { return tmr.harvest(g->st_host->iters); }, ls));
+    PR_TRY(sweep_loop(g, ctx, max_iter, 0.0, sweep, [&](int64_t) {
+        if (g->st_host->peer_err) {
+            set_error("pr_run_sharded: the device-side peer barrier timed out (a peer stopped)");
+            return (int)PR_ECUDA;
+        }
+        return tmr.harvest(g->st_host->iters);
+    }, ls));
     const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
     PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
               (const double*)nullptr, (const int32_t*)nullptr, (int64_t)0, x);

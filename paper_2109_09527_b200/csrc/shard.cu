@@ -159,6 +159,11 @@ void clear_peers(pr_graph* g) {
         cudaFree(g->speer_dev);
         g->speer_dev = nullptr;
     }
+    if (g->speer_flags) {
+        cudaFree(g->speer_flags);
+        g->speer_flags = nullptr;
+    }
+    g->sdev_barrier = false;
     for (void* p : g->speer_ipc)
         if (p) cudaIpcCloseMemHandle(p);
     g->speer_ipc.clear();
@@ -286,10 +291,15 @@ int build_shard(pr_graph* g, int rank, int world, Ctx& ctx, bool by_id) {
     }
     PR_TRY(build_view_stream(S, ctx, (int32_t)(H + (int64_t)world * chunk), g->outdeg, g->scidx));
     const int64_t ny = H + (int64_t)world * chunk + 1;
-    for (int b = 0; b < 2; ++b) {  // plain cudaMalloc: exportable by cudaIpcGetMemHandle (pr_shard_export_ipc)
-        PR_CUDA(cudaMalloc(&g->sy[b], sizeof(double) * (size_t)ny));
-        PR_CUDA(cudaMemsetAsync(g->sy[b], 0, sizeof(double) * (size_t)ny, s));
+    // plain cudaMalloc: exportable by cudaIpcGetMemHandle (pr_shard_export_ipc);
+    // sy[0] carries `world` uint64 arrival flags of the device-side peer
+    // barrier after its ny doubles (slot r written by rank r)
+    for (int b = 0; b < 2; ++b) {
+        const int64_t cnt = ny + (b == 0 ? world : 0);
+        PR_CUDA(cudaMalloc(&g->sy[b], sizeof(double) * (size_t)cnt));
+        PR_CUDA(cudaMemsetAsync(g->sy[b], 0, sizeof(double) * (size_t)cnt, s));
     }
+    g->bar_epoch = 0;
     g->shard_rank = rank;
     g->shard_world = world;
     g->shard_chunk = chunk;
@@ -304,17 +314,151 @@ int set_peers(pr_graph* g, double* const* y0s, double* const* y1s, int world) {
         cudaFree(g->speer_dev);
         g->speer_dev = nullptr;
     }
+    if (g->speer_flags) {
+        cudaFree(g->speer_flags);
+        g->speer_flags = nullptr;
+    }
     if (world <= 1) return PR_OK;
+    const int64_t ny = g->shard_hot + (int64_t)g->shard_world * g->shard_chunk + 1;
     std::vector<double*> h(2 * (size_t)(world - 1));
+    std::vector<unsigned long long*> f(world - 1);
     int q = 0;
     for (int r = 0; r < world; ++r) {
         if (r == g->shard_rank) continue;
         h[q] = y0s[r];
         h[(world - 1) + q] = y1s[r];
+        f[q] = reinterpret_cast<unsigned long long*>(y0s[r] + ny);  // rank r's arrival flags
         ++q;
     }
     PR_CUDA(cudaMalloc(&g->speer_dev, sizeof(double*) * h.size()));
     PR_CUDA(cudaMemcpy(g->speer_dev, h.data(), sizeof(double*) * h.size(), cudaMemcpyHostToDevice));
+    PR_CUDA(cudaMalloc(&g->speer_flags, sizeof(unsigned long long*) * f.size()));
+    PR_CUDA(cudaMemcpy(g->speer_flags, f.data(), sizeof(unsigned long long*) * f.size(), cudaMemcpyHostToDevice));
+    return PR_OK;
+}
+
+// ---- device-side peer barrier (the exchange's per-sweep synchronisation
+// without the host): rank r stores `epoch` into slot r of every peer's
+// arrival flags (release, system scope), then waits until every peer has
+// stored it into its own flags (acquire).  Every write the rank's earlier
+// kernels made (stream order: they happen before this kernel) -- the peer
+// stores of K-FINALIZE in particular -- is visible to a peer that has seen the
+// flag.  Epochs only grow (every rank runs the same sequence of barriers), so
+// the flags never need resetting.  A wait longer than ~20 s sets *err and
+// returns (no hang on a dead peer).
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ bool peer_barrier(unsigned long long* mine, unsigned long long* const* peers, const int* peer_rank, int npeer,
+                             int rank, unsigned long long epoch) {
+    __threadfence_system();
+    for (int q = 0; q < npeer; ++q) st_release_sys_u64(peers[q] + rank, epoch);
+    const long long t0 = clock64();
+    for (int q = 0; q < npeer; ++q) {
+        const int r = peer_rank[q];
+        while (ld_acquire_sys_u64(mine + r) < epoch) {
+            if (clock64() - t0 > 40000000000ll) return false;  // ~20 s at 2 GHz
+            __nanosleep(64);
+        }
+    }
+    __threadfence_system();
+    return true;
+}
+__global__ void k_peer_barrier(unsigned long long* mine, unsigned long long* const* peers, int npeer, int rank,
+                               int world, unsigned long long epoch, int* err) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int prank[64];
+    int q = 0;
+    for (int r = 0; r < world && q < 64; ++r)
+        if (r != rank) prank[q++] = r;
+    if (!peer_barrier(mine, peers, prank, npeer, rank, epoch)) atomicExch(err, 1);
+}
+
+int device_barrier(pr_graph* g, Ctx& ctx) {
+    const int world = g->shard_world;
+    if (world <= 1 || !g->speer_flags) return PR_OK;
+    if (world > 65) {
+        set_error("device peer barrier: world %d > 65", world);
+        return PR_EINVAL;
+    }
+    const int64_t ny = g->shard_hot + (int64_t)world * g->shard_chunk + 1;
+    g->bar_epoch += 1;
+    PR_LAUNCH(ctx, k_peer_barrier, 1, 32, 0, reinterpret_cast<unsigned long long*>(g->sy[0] + ny),
+              (unsigned long long* const*)g->speer_flags, world - 1, g->shard_rank, world,
+              (unsigned long long)g->bar_epoch, &g->st->peer_err);
+    return PR_OK;
+}
+
+// Self-test of the barrier protocol on one GPU: the guide forbids separate
+// launches that wait on one another, so `world` emulated ranks are the blocks
+// of ONE cooperative launch (co-resident by construction), each running the
+// same peer_barrier over its own flag array; per epoch every block writes its
+// value, passes the barrier and checks every other block's value of that
+// epoch (two parities: a block can only overwrite parity p after the next
+// barrier, which every reader of p has passed).  *bad counts mismatches and
+// timeouts.
+__global__ void k_barrier_selftest(unsigned long long* flags, double* data, int world, int epochs, int* bad) {
+    const int r = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    unsigned long long* peers[64];
+    int prank[64];
+    int q = 0;
+    for (int o = 0; o < world; ++o)
+        if (o != r) {
+            peers[q] = flags + (int64_t)o * world;
+            prank[q] = o;
+            ++q;
+        }
+    for (int e = 1; e <= epochs; ++e) {
+        double* d = data + (int64_t)(e & 1) * world;
+        d[r] = (double)e * 1000.0 + r;
+        if (!peer_barrier(flags + (int64_t)r * world, peers, prank, world - 1, r, (unsigned long long)e)) {
+            atomicAdd(bad, 1000000);
+            return;
+        }
+        for (int o = 0; o < world; ++o) {
+            const double v = *(volatile double*)(d + o);
+            if (v != (double)e * 1000.0 + o) atomicAdd(bad, 1);
+        }
+    }
+}
+
+int barrier_selftest(int world, int epochs, Ctx& ctx, int* bad_out) {
+    if (world < 1 || world > 64 || epochs < 1) {
+        set_error("pr_selftest_peer_barrier: world in [1, 64], epochs >= 1");
+        return PR_EINVAL;
+    }
+    int dev = 0, coop = 0, sms = 0;
+    PR_CUDA(cudaGetDevice(&dev));
+    PR_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    PR_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (!coop || world > sms) {
+        set_error("pr_selftest_peer_barrier: no cooperative launch of %d blocks on this device", world);
+        return PR_ECUDA;
+    }
+    unsigned long long* flags = nullptr;
+    double* data = nullptr;
+    int* bad = nullptr;
+    TmpGuard tg_(ctx.stream);
+    tg_.track(flags);
+    tg_.track(data);
+    tg_.track(bad);
+    PR_TRY(dalloc(&flags, (size_t)world * world, ctx.stream));
+    PR_TRY(dalloc(&data, 2 * (size_t)world, ctx.stream));
+    PR_TRY(dalloc(&bad, 1, ctx.stream));
+    PR_CUDA(cudaMemsetAsync(flags, 0, sizeof(unsigned long long) * (size_t)world * world, ctx.stream));
+    PR_CUDA(cudaMemsetAsync(data, 0, sizeof(double) * 2 * (size_t)world, ctx.stream));
+    PR_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx.stream));
+    void* args[] = {&flags, &data, &world, &epochs, &bad};
+    PR_CUDA(cudaLaunchCooperativeKernel((const void*)k_barrier_selftest, dim3(world), dim3(32), args, 0, ctx.stream));
+    ctx.launches += 1;
+    PR_CUDA(cudaMemcpyAsync(bad_out, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    PR_CUDA(cudaStreamSynchronize(ctx.stream));
     return PR_OK;
 }
 

@@ -512,3 +512,39 @@ def test_local_ingest_multiprocess(pr, tmp_path):
     r = json.load(open(out))
     assert len({(x["st"], x["it"], x["fd"]) for x in r["ranks"]}) == 1
     assert r["max_diff"] <= 1e-10 and r["l1_diff"] <= 1e-9
+
+
+# ------------------------------------------------------ device-side barrier --
+@pytest.mark.parametrize("world", [2, 3, 8, 32])
+def test_peer_barrier_protocol_selftest(pr, world):
+    """The device-side peer barrier (release store of the epoch into every
+    peer's flags, acquire spin on one's own) run by `world` emulated ranks =
+    the blocks of one cooperative launch (separate launches that wait on one
+    another must not share a GPU): every rank sees every other rank's write
+    of each epoch after passing that epoch's barrier."""
+    pr.pr_selftest_peer_barrier(world, 300)
+
+
+def test_device_barrier_world1_and_validation(pr):
+    n, edges = GRAPHS["planted"]()
+    s, t = G.edges_to_arrays(edges)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        with pytest.raises(pr.PRError) as e:
+            pr.pr_shard_device_barrier(g.handle, True)          # not sharded yet
+        assert e.value.code == pr.PR_ESTATE
+        x0 = torch.empty(n, dtype=torch.float64, device="cuda")
+        ref = g.run(x0, D, 1e-12, 1000)
+        g.shard(0, 1)
+        pr.pr_shard_device_barrier(g.handle, True)               # world 1: nothing to wait for
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        assert g.run_sharded(x, lambda *a: None, D, 1e-12, 1000) == ref
+        assert torch.equal(x, x0)
+    graphs = [pr.Graph(n, dev(s), dev(t)) for _ in range(2)]
+    try:
+        graphs[0].shard(0, 2)
+        with pytest.raises(pr.PRError) as e:
+            pr.pr_shard_device_barrier(graphs[0].handle, True)   # world 2 without peer buffers
+        assert e.value.code == pr.PR_ESTATE
+    finally:
+        for g in graphs:
+            g.close()
