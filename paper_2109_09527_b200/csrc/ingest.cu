@@ -40,30 +40,57 @@ __global__ void k_pack(const int32_t* __restrict__ src, const int32_t* __restric
 }
 
 // Sharded create: the rank's own edges (dst mod world == rank, no self-loops)
-// appended compactly (warp-aggregated counter; the order is irrelevant: the
-// sort that follows fixes it), every id validated.
-__global__ void k_pack_own(const int32_t* __restrict__ src, const int32_t* __restrict__ dst, int64_t m, int64_t n,
-                           int b, uint64_t* __restrict__ keys, unsigned long long* __restrict__ cnt,
-                           int* __restrict__ err, int rank, int world) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int lane = threadIdx.x & 31;
+// appended compactly, every id validated.  One atomic per tile of PO_TILE
+// edges (a single counter hit once per warp serialised: 4 ms on R-MAT-24);
+// the order of the appended keys is irrelevant -- the sort that follows fixes it.
+constexpr int PO_NT = 256, PO_IPT = 8, PO_TILE = PO_NT * PO_IPT;
+__global__ void __launch_bounds__(PO_NT) k_pack_own(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                                                    int64_t m, int64_t n, int b, uint64_t* __restrict__ keys,
+                                                    unsigned long long* __restrict__ cnt, int* __restrict__ err,
+                                                    int rank, int world) {
+    __shared__ uint32_t wtot[PO_NT / 32];
+    __shared__ unsigned long long tbase;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = lanemask_lt();
     bool any_bad = false;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < m; i0 += stride) {
-        const int64_t i = i0 + threadIdx.x;
-        bool keep = false;
-        uint64_t key = 0;
-        if (i < m) {
-            const int32_t s = src[i], t = dst[i];
-            const bool bad = s < 0 || (int64_t)s >= n || t < 0 || (int64_t)t >= n;
-            any_bad |= bad;
-            keep = !bad && s != t && (t % world) == rank;
-            key = ((uint64_t)(uint32_t)t << b) | (uint32_t)s;
+    for (int64_t t0 = (int64_t)blockIdx.x * PO_TILE; t0 < m; t0 += (int64_t)gridDim.x * PO_TILE) {
+        uint64_t key[PO_IPT];
+        uint32_t rk[PO_IPT];
+        uint32_t keepm = 0, wcount = 0;
+#pragma unroll
+        for (int j = 0; j < PO_IPT; ++j) {  // item j of the tile: warp-contiguous runs of 32
+            const int64_t i = t0 + (int64_t)(j * PO_NT) + threadIdx.x;
+            bool keep = false;
+            key[j] = 0;
+            if (i < m) {
+                const int32_t s = src[i], t = dst[i];
+                const bool bad = s < 0 || (int64_t)s >= n || t < 0 || (int64_t)t >= n;
+                any_bad |= bad;
+                keep = !bad && s != t && (t % world) == rank;
+                key[j] = ((uint64_t)(uint32_t)t << b) | (uint32_t)s;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            rk[j] = wcount + __popc(bal & lt);
+            wcount += __popc(bal);
+            keepm |= (keep ? 1u : 0u) << j;
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        unsigned long long base = 0;
-        if (lane == 0 && bal) base = atomicAdd(cnt, (unsigned long long)__popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (keep) keys[base + __popc(bal & ((1u << lane) - 1))] = key;
+        if (lane == 0) wtot[warp] = wcount;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < PO_NT / 32; ++w) {
+                const uint32_t c = wtot[w];
+                wtot[w] = tot;
+                tot += c;
+            }
+            tbase = tot ? atomicAdd(cnt, (unsigned long long)tot) : 0ull;
+        }
+        __syncthreads();
+        const unsigned long long base = tbase + wtot[warp];
+#pragma unroll
+        for (int j = 0; j < PO_IPT; ++j)
+            if (keepm & (1u << j)) keys[base + rk[j]] = key[j];
+        __syncthreads();
     }
     if (__any_sync(0xffffffffu, any_bad) && lane == 0) atomicOr(err, 1);
 }
@@ -283,8 +310,8 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
     if (mk > 0) {
         PR_TRY(dalloc(&keys, (size_t)mk, s));
         if (world > 1) {  // sharded create: only this rank's edges, compacted (the sort sees 1/world of them)
-            PR_LAUNCH(ctx, k_pack_own, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, keys,
-                      (unsigned long long*)scratch, (int*)(scratch + 1), rank, world);
+            PR_LAUNCH(ctx, k_pack_own, grid_for(ctx, (mk + PO_IPT - 1) / PO_IPT, PO_NT), PO_NT, 0, src, dst, mk, n, b,
+                      keys, (unsigned long long*)scratch, (int*)(scratch + 1), rank, world);
             int64_t h2[2];
             PR_CUDA(cudaMemcpyAsync(h2, scratch, sizeof(h2), cudaMemcpyDeviceToHost, s));
             PR_CUDA(cudaStreamSynchronize(s));
