@@ -9,3 +9,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 600 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"k_stream|k_finalize" -s 20 -c 2 -o gpurun_out/stream_rmat24_reduced_warm python tools/step_once.py 4 reduced > gpurun_out/ncu_stream.log 2>&1; tail -1 gpurun_out/ncu_stream.log
 timeout 1500 python tools/all_configs.py > gpurun_out/all_configs.json 2> gpurun_out/all_configs.err; tail -c 200 gpurun_out/all_configs.err
 timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; tail -c 300 gpurun_out/bench_reference.json
+timeout 600 python tools/shard_scaling.py 4 1 2 4 8 local > gpurun_out/shard_scaling_local.json 2> gpurun_out/shard_scaling_local.err
+PRGPU_PROFILE=2 timeout 300 python tools/profile_create_sharded.py 4 8 0 > gpurun_out/create_sharded_profile.log 2>&1
