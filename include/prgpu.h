@@ -332,6 +332,32 @@ int pr_run_sharded(pr_graph *g, double d, double threshold, int32_t max_iter, vo
 int pr_shard_buffers(const pr_graph *g, void **y0, void **y1, int64_t *len);
 
 /*
+ * NVLS multicast team -- the B200 form of the
+ * fused exchange: the rank's two contrib buffers (+ the barrier flags) become
+ * one physical allocation bound to a multicast object whose team is the
+ * world's GPUs; K-FINALIZE stores every new contrib (and the delta pair, and
+ * the in-degree-0 contribs) with ONE multimem.st into the multicast address,
+ * which the switch replicates into every rank's buffer; pr_run_sharded then
+ * calls the exchange with buf = NULL (a barrier only, as with peer buffers;
+ * pr_shard_device_barrier makes it a device-side one).  Collective setup, in
+ * this order across the ranks:
+ *   pr_shard_mc_create  rank 0: creates the object (team size = world) and
+ *                       writes its 64-byte fabric handle to handle_out
+ *                       (NULL allowed when world = 1)
+ *   pr_shard_mc_attach  every rank (rank 0 with NULL): imports the handle and
+ *                       adds its device to the team
+ *   pr_shard_mc_bind    every rank, after EVERY rank attached: binds its
+ *                       memory and maps the unicast and multicast addresses
+ *                       (the buffers are zeroed; exclusive with the IPC peer
+ *                       buffers; released by pr_graph_shard / pr_destroy)
+ * PR_ESTATE on an unsharded graph, PR_ECUDA when the device or driver lacks
+ * multicast (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED) or fabric handles.
+ */
+int pr_shard_mc_create(pr_graph *g, void *handle_out);
+int pr_shard_mc_attach(pr_graph *g, const void *handle);
+int pr_shard_mc_bind(pr_graph *g, void *stream);
+
+/*
  * pr_shard_device_barrier -- with peer buffers set, on != 0 replaces the
  * per-sweep host barrier (the exchange callback with buf = NULL) by a
  * device-side one: after the rank's finalize and peer stores, one thread

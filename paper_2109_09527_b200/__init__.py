@@ -45,7 +45,8 @@ ABI_SYMBOLS = (
     "pr_graph_create", "pr_preprocess", "pr_run", "pr_destroy", "pr_release_memory", "pr_last_error",
     "pr_graph_info", "pr_get_csr", "pr_get_reductions", "pr_get_delta_log", "pr_get_run_stats",
     "pr_graph_shard", "pr_graph_create_sharded", "pr_run_sharded", "pr_get_shard_info", "pr_get_phase_plan",
-    "pr_shard_buffers", "pr_shard_set_peers", "pr_shard_device_barrier", "pr_selftest_peer_barrier", "pr_shard_export_ipc", "pr_shard_open_ipc",
+    "pr_shard_buffers", "pr_shard_set_peers", "pr_shard_device_barrier", "pr_selftest_peer_barrier",
+    "pr_shard_mc_create", "pr_shard_mc_attach", "pr_shard_mc_bind", "pr_shard_export_ipc", "pr_shard_open_ipc",
 )
 
 
@@ -138,6 +139,12 @@ def _load():
     lib.pr_get_run_stats.restype = ctypes.c_int
     lib.pr_graph_shard.argtypes = [p, i32, i32, p]
     lib.pr_graph_shard.restype = ctypes.c_int
+    lib.pr_shard_mc_create.argtypes = [p, p]
+    lib.pr_shard_mc_create.restype = ctypes.c_int
+    lib.pr_shard_mc_attach.argtypes = [p, p]
+    lib.pr_shard_mc_attach.restype = ctypes.c_int
+    lib.pr_shard_mc_bind.argtypes = [p, p]
+    lib.pr_shard_mc_bind.restype = ctypes.c_int
     lib.pr_shard_device_barrier.argtypes = [p, i32]
     lib.pr_shard_device_barrier.restype = ctypes.c_int
     lib.pr_selftest_peer_barrier.argtypes = [i32, i32, p]
@@ -345,6 +352,43 @@ def pr_shard_set_peers(g, y0s, y1s) -> None:
     A = (ctypes.c_void_p * w)(*[v or 0 for v in y0s])
     B = (ctypes.c_void_p * w)(*[v or 0 for v in y1s])
     _check(lib.pr_shard_set_peers(g, A, B, w))
+
+
+def pr_shard_mc_create(g) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib.pr_shard_mc_create(g, buf))
+    return buf.raw
+
+
+def pr_shard_mc_attach(g, handle) -> None:
+    _check(lib.pr_shard_mc_attach(g, handle))
+
+
+def pr_shard_mc_bind(g, stream=None) -> None:
+    _check(lib.pr_shard_mc_bind(g, _stream(stream)))
+
+
+def shard_multicast_local(g) -> None:
+    """The NVLS team of a world-1 shard (create + attach + bind in one process)."""
+    _check(lib.pr_shard_mc_create(g, None))
+    _check(lib.pr_shard_mc_attach(g, None))
+    pr_shard_mc_bind(g)
+
+
+def torch_dist_multicast_setup(g, group=None) -> None:
+    """The NVLS team over torch.distributed: rank 0 creates and shares the
+    fabric handle, every rank attaches, then (after all attached) binds."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    h = pr_shard_mc_create(g) if rank == 0 else None
+    allh = [None]
+    if rank == 0:
+        allh = [h]
+    dist.broadcast_object_list(allh, src=0, group=group)
+    pr_shard_mc_attach(g, None if rank == 0 else allh[0])
+    dist.barrier(group=group)
+    pr_shard_mc_bind(g)
+    dist.barrier(group=group)
 
 
 def pr_shard_device_barrier(g, on: bool = True) -> None:

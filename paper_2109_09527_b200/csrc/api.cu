@@ -551,6 +551,10 @@ int pr_shard_set_peers(pr_graph* g, void* const* y0s, void* const* y1s, int32_t 
         set_error("pr_shard_set_peers: world %d != the shard's %d", world, g->shard_world);
         return PR_EINVAL;
     }
+    if (g->mc) {
+        set_error("pr_shard_set_peers: the multicast team is set (exclusive with peer buffers)");
+        return PR_ESTATE;
+    }
     for (int r = 0; r < world; ++r)
         if (r != g->shard_rank && (!y0s[r] || !y1s[r])) {
             set_error("pr_shard_set_peers: NULL buffer for rank %d", r);
@@ -559,14 +563,49 @@ int pr_shard_set_peers(pr_graph* g, void* const* y0s, void* const* y1s, int32_t 
     return set_peers(g, (double* const*)y0s, (double* const*)y1s, world);
 }
 
+static int mc_guard(const pr_graph* g, const char* fn) {
+    if (!g) {
+        set_error("%s: NULL graph", fn);
+        return PR_EINVAL;
+    }
+    if (g->shard_world < 1) {
+        set_error("%s: the graph is not sharded", fn);
+        return PR_ESTATE;
+    }
+    return PR_OK;
+}
+
+int pr_shard_mc_create(pr_graph* g, void* handle_out) {
+    g_err[0] = 0;
+    PR_TRY(mc_guard(g, "pr_shard_mc_create"));
+    return mc_create(g, handle_out);
+}
+
+int pr_shard_mc_attach(pr_graph* g, const void* handle) {
+    g_err[0] = 0;
+    PR_TRY(mc_guard(g, "pr_shard_mc_attach"));
+    return mc_attach(g, handle);
+}
+
+int pr_shard_mc_bind(pr_graph* g, void* stream) {
+    g_err[0] = 0;
+    PR_TRY(mc_guard(g, "pr_shard_mc_bind"));
+    Ctx ctx;
+    PR_TRY(make_ctx(ctx, stream));
+    const int rc = mc_bind(g, ctx);
+    if (rc != PR_OK) clear_multicast(g);
+    return rc;
+}
+
 int pr_shard_device_barrier(pr_graph* g, int32_t on) {
     g_err[0] = 0;
     if (!g) {
         set_error("pr_shard_device_barrier: NULL graph");
         return PR_EINVAL;
     }
-    if (on && (g->shard_world < 1 || (g->shard_world > 1 && !g->speer_flags))) {
-        set_error("pr_shard_device_barrier: needs the peer buffers (pr_shard_set_peers / pr_shard_open_ipc)");
+    if (on && (g->shard_world < 1 || (g->shard_world > 1 && !g->speer_flags && !(g->mc && g->mc->bound)))) {
+        set_error("pr_shard_device_barrier: needs the peer buffers (pr_shard_set_peers / pr_shard_open_ipc) or "
+                  "the multicast team (pr_shard_mc_*)");
         return PR_ESTATE;
     }
     if (on && g->shard_world > 65) {

@@ -86,6 +86,19 @@ struct DevState {
     int32_t peer_err;   // the device-side peer barrier timed out
 };
 
+// NVLS multicast team of the sharded contrib buffers (multicast.cu)
+struct McState {
+    unsigned long long mc = 0;   // CUmemGenericAllocationHandle of the multicast object
+    unsigned long long mem = 0;  // this rank's physical allocation bound to it
+    bool have_mc = false;
+    bool bound = false;
+    size_t seg = 0;          // bytes per parity segment (ny doubles + world flags, granularity-rounded)
+    size_t size = 0;         // 2 * seg
+    void* uva = nullptr;     // unicast mapping of mem (sy[0], sy[1] point into it)
+    void* mva = nullptr;     // multicast mapping (multimem.st replicates to every rank)
+    double* y[2] = {nullptr, nullptr};  // multicast addresses of the two parities
+};
+
 }  // namespace prgpu
 
 struct pr_graph {
@@ -140,6 +153,7 @@ struct pr_graph {
     unsigned long long** speer_flags = nullptr;  // [world-1] peers' arrival flags (after their sy[0])
     bool sdev_barrier = false;      // per-sweep synchronisation by the device-side peer barrier
     uint64_t bar_epoch = 0;         // epochs of that barrier so far (the same sequence on every rank)
+    prgpu::McState* mc = nullptr;   // NVLS multicast buffers (pr_shard_mc_*), exclusive with the IPC peers
     std::vector<void*> speer_ipc;   // IPC-opened peer bases to close
     // iteration buffers (allocated lazily by pr_run)
     double* x = nullptr;            // fp64[n] (used when the caller's ranks are on the host)
@@ -185,6 +199,10 @@ void clear_shard(pr_graph* g, cudaStream_t s);
 void clear_peers(pr_graph* g);
 int set_peers(pr_graph* g, double* const* y0s, double* const* y1s, int world);
 int device_barrier(pr_graph* g, Ctx& ctx);
+int mc_create(pr_graph* g, void* handle_out);
+int mc_attach(pr_graph* g, const void* handle);
+int mc_bind(pr_graph* g, Ctx& ctx);
+void clear_multicast(pr_graph* g);
 int barrier_selftest(int world, int epochs, Ctx& ctx, int* bad_out);
 int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, double* ranks, Ctx& ctx,
                 pr_exchange_fn exchange, void* exchange_ctx, int32_t* iters_out, double* delta_out);

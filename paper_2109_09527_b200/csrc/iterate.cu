@@ -79,6 +79,12 @@ struct AccumPolicy {
     __device__ __forceinline__ void emit_first(int64_t, double s) const { red_add_f64(sums + m_first, s); }
 };
 
+// NVLS: one store that lands in the same slot of every team member's buffer
+// (p is a multicast address, multicast.cu)
+__device__ __forceinline__ void st_mc_f64(double* p, double v) {
+    asm volatile("multimem.st.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 struct IterArgs {
     DevState* st;
     double* cta_partial;        // (L1, Linf) per CTA: gather / finalize CTAs, member CTAs, zero-in CTAs
@@ -93,6 +99,7 @@ struct IterArgs {
     double* const* peer_y = nullptr;
     int npeer = 0;
     int64_t shard_off = 0;
+    double* mc_out = nullptr;   // NVLS: multicast address of the chunk tail (replaces shard_out / peer_y)
 };
 
 // The stop test on a sweep's (L1, Linf): iteration count, delta log, done /
@@ -144,7 +151,10 @@ __device__ void global_finalize(const IterArgs& ia, double* red) {
             li = fmax(li, red[32 + w]);
         }
         DevState* st = ia.st;
-        if (ia.shard_out) {
+        if (ia.mc_out) {
+            st_mc_f64(ia.mc_out, l1);
+            st_mc_f64(ia.mc_out + 1, li);
+        } else if (ia.shard_out) {
             ia.shard_out[0] = l1;
             ia.shard_out[1] = li;
             for (int q = 0; q < ia.npeer; ++q) {
@@ -258,6 +268,7 @@ struct FinArgs {
     // the same slot of each peer's buffer (the all-gather fused into K-FINALIZE)
     double* const* peer_y = nullptr;
     int npeer = 0;
+    double* mc_y = nullptr;     // NVLS: contribs stored through this multicast address instead
     // delayed chain resolution (sync reduced mode without PR_CHAIN_EAGER):
     // hist[(t mod L) * nh + h] = x_t of chain source h (L = max_chain + 1
     // sweeps, slot 0 = x_0 = 1/n); chain member m at distance k takes
@@ -311,8 +322,12 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
                 xr[r] = xn;
                 const double yv = inf[u].x > 0 ? xn / (double)inf[u].x : 0.0;
                 if (inf[u].x > 0) {
-                    y[inf[u].y] = yv;
-                    for (int q = 0; q < f.npeer; ++q) f.peer_y[q][inf[u].y] = yv;
+                    if (f.mc_y) {
+                        st_mc_f64(f.mc_y + inf[u].y, yv);
+                    } else {
+                        y[inf[u].y] = yv;
+                        for (int q = 0; q < f.npeer; ++q) f.peer_y[q][inf[u].y] = yv;
+                    }
                 }
                 const double dl = fabs(xn - xo[u]);
                 l1 += dl;
@@ -394,7 +409,7 @@ __global__ void k_fill_f64(double* __restrict__ a, int64_t cnt, double v) {
 // sweep 2 on their Delta is exactly 0 and no kernel touches them.
 __global__ void __launch_bounds__(GT_NT) k_zero(const int32_t* __restrict__ zl, int64_t nz, double c, double* x,
                                                 double* y_out, const int32_t* __restrict__ od,
-                                                const int32_t* __restrict__ cidx, double* partial) {
+                                                const int32_t* __restrict__ cidx, double* partial, int mc = 0) {
     // grid-stride, 4 vertices per thread with all loads issued first (the
     // old x is read too: it is 1/n from k_init, but Delta_1 must be measured)
     __shared__ double red[64];
@@ -416,7 +431,12 @@ __global__ void __launch_bounds__(GT_NT) k_zero(const int32_t* __restrict__ zl, 
         for (int u = 0; u < 4; ++u)
             if (v[u] >= 0) {
                 x[v[u]] = c;
-                if (o[u] > 0) y_out[ci[u]] = c / (double)o[u];
+                if (o[u] > 0) {
+                    if (mc)
+                        st_mc_f64(y_out + ci[u], c / (double)o[u]);
+                    else
+                        y_out[ci[u]] = c / (double)o[u];
+                }
                 const double dl = fabs(c - xo[u]);
                 l1 += dl;
                 linf = fmax(linf, dl);
@@ -428,11 +448,16 @@ __global__ void __launch_bounds__(GT_NT) k_zero(const int32_t* __restrict__ zl, 
 // Sync mode: after sweep 1 also store the constant contribs of the in-degree-0
 // vertices into the other ping-pong buffer (read by sweep 3, 5, ...).
 __global__ void k_zero_y(const int32_t* __restrict__ zl, int64_t nz, double c, double* y,
-                         const int32_t* __restrict__ od, const int32_t* __restrict__ cidx) {
+                         const int32_t* __restrict__ od, const int32_t* __restrict__ cidx, int mc = 0) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = zl[i];
         const int32_t o = od[v];
-        if (o > 0) y[cidx[v]] = c / (double)o;
+        if (o > 0) {
+            if (mc)
+                st_mc_f64(y + cidx[v], c / (double)o);
+            else
+                y[cidx[v]] = c / (double)o;
+        }
     }
 }
 
@@ -1201,6 +1226,10 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
     const int world = g->shard_world, rank = g->shard_rank;
     const int64_t chunk = g->shard_chunk, H = g->shard_hot;
     const bool peers = g->speer_dev != nullptr && world > 1;
+    // NVLS multicast team (multicast.cu): every contrib / delta-pair store is
+    // ONE multimem store into all ranks' buffers; the exchange is a barrier only
+    const bool mcast = g->mc != nullptr && g->mc->bound;
+    const bool barrier_only = peers || mcast;
     const int64_t launches0 = ctx.launches;
     PR_TRY(reset_tickets(v, s));
     if (!g->x) PR_TRY(dalloc(&g->x, (size_t)n, s));
@@ -1238,10 +1267,10 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
     PR_LAUNCH(ctx, k_shard_combine, cgrid, 256, 0, ia0, g->sy[0], (const int32_t*)g->shot_src, H, world, chunk, 0);
     // peer buffers: no rank may store into another's buffers before that rank
     // has initialised them (sweep 1's stores would be overwritten)
-    const bool dev_bar = peers && g->sdev_barrier;
+    const bool dev_bar = barrier_only && g->sdev_barrier;
     if (dev_bar) {
         PR_TRY(device_barrier(g, ctx));
-    } else if (peers && exchange(exchange_ctx, nullptr, chunk, world, (void*)s) != 0) {
+    } else if (barrier_only && exchange(exchange_ctx, nullptr, chunk, world, (void*)s) != 0) {
         set_error("pr_run_sharded: the exchange callback failed before sweep 1");
         return PR_ECUDA;
     }
@@ -1263,9 +1292,12 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
         ia.peer_y = pout;
         ia.npeer = peers ? world - 1 : 0;
         ia.shard_off = H + (int64_t)rank * chunk + chunk - 2;
+        double* mc_out = mcast ? g->mc->y[(it + 1) & 1] : nullptr;  // multicast address of y_out
+        if (mcast) ia.mc_out = mc_out + ia.shard_off;
         if (it == 0 && zgrid > 0)
-            PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->szlist, nz, c, x, y_out,
-                      (const int32_t*)g->outdeg, (const int32_t*)g->scidx, zero_partial);
+            PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->szlist, nz, c, x,
+                      mcast ? mc_out : y_out, (const int32_t*)g->outdeg, (const int32_t*)g->scidx, zero_partial,
+                      mcast ? 1 : 0);
         PR_TRY(tmr.mark(it, 0, s));
         PR_TRY(launch_gather(ctx, g, v, y_in, gc));
         PR_TRY(tmr.mark(it, 1, s));
@@ -1273,9 +1305,16 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
         f.y_out = y_out;
         f.peer_y = pout;
         f.npeer = peers ? world - 1 : 0;
+        f.mc_y = mc_out;
         PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
         PR_TRY(tmr.mark(it, 2, s));
-        if (it == 0 && nz > 0) {
+        // multicast: the in-degree-0 contribs go to every rank's sweep-1 output
+        // (k_zero above) and, in sweep 2, to its other buffer (their sweep-2
+        // output; in sweep 1 every rank gathers from it)
+        if (mcast && it == 1 && nz > 0)
+            PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256, 0,
+                      (const int32_t*)g->szlist, nz, c, mc_out, (const int32_t*)g->outdeg, (const int32_t*)g->scidx, 1);
+        if (it == 0 && nz > 0 && !mcast) {
             const unsigned zg = (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8);
             PR_LAUNCH(ctx, k_zero_y, zg, 256, 0, (const int32_t*)g->szlist, nz, c, y_in, (const int32_t*)g->outdeg,
                       (const int32_t*)g->scidx);
@@ -1294,7 +1333,7 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
         // on the device when the device-side barrier is on: no host sync)
         if (dev_bar) {
             PR_TRY(device_barrier(g, ctx));
-        } else if (exchange(exchange_ctx, peers ? nullptr : y_out + H, chunk, world, (void*)s) != 0) {
+        } else if (exchange(exchange_ctx, barrier_only ? nullptr : y_out + H, chunk, world, (void*)s) != 0) {
             set_error("pr_run_sharded: the exchange callback failed at sweep %lld", (long long)it + 1);
             return PR_ECUDA;
         }

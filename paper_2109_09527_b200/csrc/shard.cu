@@ -170,6 +170,7 @@ void clear_peers(pr_graph* g) {
 }
 
 void clear_shard(pr_graph* g, cudaStream_t s) {
+    clear_multicast(g);  // (its buffers are sy[0], sy[1])
     free_view(g->shard, s);
     dfree(g->sowner, s);
     dfree(g->scidx, s);
@@ -378,9 +379,37 @@ __global__ void k_peer_barrier(unsigned long long* mine, unsigned long long* con
         if (r != rank) prank[q++] = r;
     if (!peer_barrier(mine, peers, prank, npeer, rank, epoch)) atomicExch(err, 1);
 }
+// NVLS form: ONE multimem store of the epoch into slot `rank` of every team
+// member's flags (the multicast address of the flags), then the same wait.
+__global__ void k_mc_barrier(unsigned long long* mine, unsigned long long* mc_flags, int rank, int world,
+                             unsigned long long epoch, int* err) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    __threadfence_system();
+    asm volatile("multimem.st.release.sys.global.u64 [%0], %1;" ::"l"(mc_flags + rank), "l"(epoch) : "memory");
+    const long long t0 = clock64();
+    for (int r = 0; r < world; ++r) {
+        if (r == rank) continue;
+        while (ld_acquire_sys_u64(mine + r) < epoch) {
+            if (clock64() - t0 > 40000000000ll) {
+                atomicExch(err, 1);
+                return;
+            }
+            __nanosleep(64);
+        }
+    }
+    __threadfence_system();
+}
 
 int device_barrier(pr_graph* g, Ctx& ctx) {
     const int world = g->shard_world;
+    if (world > 1 && g->mc && g->mc->bound) {
+        const int64_t ny = g->shard_hot + (int64_t)world * g->shard_chunk + 1;
+        g->bar_epoch += 1;
+        PR_LAUNCH(ctx, k_mc_barrier, 1, 32, 0, reinterpret_cast<unsigned long long*>(g->sy[0] + ny),
+                  reinterpret_cast<unsigned long long*>(g->mc->y[0] + ny), g->shard_rank, world,
+                  (unsigned long long)g->bar_epoch, &g->st->peer_err);
+        return PR_OK;
+    }
     if (world <= 1 || !g->speer_flags) return PR_OK;
     if (world > 65) {
         set_error("device peer barrier: world %d > 65", world);

@@ -548,3 +548,70 @@ def test_device_barrier_world1_and_validation(pr):
     finally:
         for g in graphs:
             g.close()
+
+
+# ------------------------------------------------------------ NVLS multicast --
+def _multicast_supported():
+    import ctypes
+    try:
+        cu = ctypes.CDLL("libcuda.so.1")
+        cu.cuInit(0)
+        dev = ctypes.c_int()
+        cu.cuDeviceGet(ctypes.byref(dev), 0)
+        v = ctypes.c_int(0)
+        cu.cuDeviceGetAttribute(ctypes.byref(v), 132, dev)   # CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED
+        return v.value == 1
+    except OSError:
+        return False
+
+
+@pytest.mark.parametrize("name", ["planted", "random", "in_star", "no_edges", "single"])
+@pytest.mark.parametrize("devbar", [False, True])
+def test_multicast_world1_is_sync(pr, name, devbar):
+    """The NVLS form of the fused exchange on a one-GPU team: every contrib,
+    delta pair and in-degree-0 contrib is stored with multimem.st through the
+    multicast address (the switch's replication to a team of one); the run is
+    bit-identical to the plain world-1 run (hence to pr_run)."""
+    if not _multicast_supported():
+        pytest.skip("no NVLS multicast on this device")
+    n, edges = GRAPHS[name]()
+    s, t = G.edges_to_arrays(edges)
+    with pr.Graph(n, dev(s), dev(t)) as g:
+        x0 = torch.empty(n, dtype=torch.float64, device="cuda")
+        ref = g.run(x0, D, 1e-12, 1000)
+        ref_log = g.delta_log()
+        g.shard(0, 1)
+        pr.shard_multicast_local(g.handle)
+        if devbar:
+            pr.pr_shard_device_barrier(g.handle, True)
+        calls = []
+        x = torch.empty(n, dtype=torch.float64, device="cuda")
+        out = g.run_sharded(x, lambda buf, *a: calls.append(buf), D, 1e-12, 1000)
+        assert out == ref
+        assert torch.equal(x, x0)
+        assert np.array_equal(g.delta_log(), ref_log)
+        assert all(b is None for b in calls)              # barrier-only exchange
+        if devbar:
+            assert not calls                             # no host call inside the sweep loop
+        again = g.run_sharded(x, lambda *a: None, D, 1e-12, 1000)   # a second run on the same team
+        assert again == ref and torch.equal(x, x0)
+        with pytest.raises(pr.PRError) as e:             # exclusive with the IPC peer buffers
+            g.set_peers([0], [0])
+        assert e.value.code == pr.PR_ESTATE
+
+
+def test_multicast_local_ingest_world1(pr):
+    if not _multicast_supported():
+        pytest.skip("no NVLS multicast on this device")
+    gen = graphgen.make_config(2)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        x0 = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+        ref = g.run(x0, gen.d, gen.tau, gen.max_iter)
+    g = pr.Graph.sharded(gen.n, dev(gen.src), dev(gen.dst), 0, 1, lambda *a: None)
+    try:
+        pr.shard_multicast_local(g.handle)
+        x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+        assert g.run_sharded(x, lambda *a: None, gen.d, gen.tau, gen.max_iter) == ref
+        assert torch.equal(x, x0)
+    finally:
+        g.close()
