@@ -355,3 +355,22 @@ def test_outdeg_split_sort_edge_cases(pr, n):
         rp, col, od = gpu_csr(pr, g, n, ref_g.E)
         assert np.array_equal(od, ref_g.outdeg)
         assert np.array_equal(rp, ref_g.row_ptr) and np.array_equal(col, ref_g.col_idx)
+
+
+def test_run_loop_batches_with_and_without_timing(pr):
+    """The sweep loop launches batches sized by a geometric fit of the
+    batch-end deltas: with or without PR_TIMING
+    (events every 4th sweep) the run is bit-identical, stops at the oracle's
+    sweep count, and synchronises the host only a handful of times."""
+    gen = graphgen.make_config(2)
+    ref = oracle.pagerank(oracle.build_csr(gen.n, gen.src, gen.dst), D, gen.tau, gen.max_iter)
+    with gpu_graph(pr, gen.n, gen.src, gen.dst) as g:
+        a = gpu_run(pr, g, gen.n, gen.tau)
+        sa = g.stats()
+        b = gpu_run(pr, g, gen.n, gen.tau, mode=pr.PR_TIMING)
+        sb = g.stats()
+    assert a[1] == b[1] and np.array_equal(a[3], b[3])
+    assert_iters(a[1], ref, gen.tau)
+    assert sb["timed_iterations"] >= a[1] // 4 - 1 and sb["gather_ms"] > 0
+    assert sa["timed_iterations"] == 0
+    assert sa["host_syncs"] <= 8 and sb["host_syncs"] <= 8
