@@ -269,6 +269,7 @@ struct FinArgs {
     double* const* peer_y = nullptr;
     int npeer = 0;
     double* mc_y = nullptr;     // NVLS: contribs stored through this multicast address instead
+    int vec = 0;                // rows two at a time with 16-byte loads (PRGPU_FIN_VEC)
     // delayed chain resolution (sync reduced mode without PR_CHAIN_EAGER):
     // hist[(t mod L) * nh + h] = x_t of chain source h (L = max_chain + 1
     // sweeps, slot 0 = x_0 = 1/n); chain member m at distance k takes
@@ -299,7 +300,44 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     double* __restrict__ xr = f.xr;
     double* __restrict__ y = f.y_out;
     uint32_t nfrozen = 0;
-    for (int64_t r0 = f.row0 + t0; r0 < f.nrows; r0 += FIN_U * T) {
+    int64_t rlo = f.row0;  // rows [rlo, nrows) left to the general loop below
+    if (f.vec && !f.fz && !f.mc_y && f.npeer == 0 && (f.row0 & 1) == 0) {
+        // two consecutive rows per 16-byte load of S, x and (outdeg, slot)
+        const double2* __restrict__ S2 = reinterpret_cast<const double2*>(sums);
+        double2* __restrict__ X2 = reinterpret_cast<double2*>(xr);
+        const int4* __restrict__ I2 = reinterpret_cast<const int4*>(f.rinfo);
+        const int64_t p_end = f.nrows >> 1;
+        for (int64_t p0 = (f.row0 >> 1) + t0; p0 < p_end; p0 += 2 * T) {
+            double2 sv[2], xv[2];
+            int4 iv[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int64_t p = p0 + u * T;
+                if (p < p_end) {
+                    sv[u] = __ldcs(S2 + p);
+                    xv[u] = X2[p];
+                    iv[u] = __ldg(I2 + p);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int64_t p = p0 + u * T;
+                if (p < p_end) {
+                    const double xa = __dadd_rn(f.c, __dmul_rn(f.d, sv[u].x));
+                    const double xb = __dadd_rn(f.c, __dmul_rn(f.d, sv[u].y));
+                    X2[p] = make_double2(xa, xb);
+                    if (iv[u].x > 0) y[iv[u].y] = xa / (double)iv[u].x;
+                    if (iv[u].z > 0) y[iv[u].w] = xb / (double)iv[u].z;
+                    const double da = fabs(xa - xv[u].x), db = fabs(xb - xv[u].y);
+                    l1 += da;
+                    l1 += db;
+                    linf = fmax(linf, fmax(da, db));
+                }
+            }
+        }
+        rlo = p_end << 1;  // the odd last row, if any
+    }
+    for (int64_t r0 = rlo + t0; r0 < f.nrows; r0 += FIN_U * T) {
         double S[FIN_U], xo[FIN_U];
         int2 inf[FIN_U];
         uint8_t fr[FIN_U];
@@ -1046,6 +1084,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     double* zero_partial = g->cta_partial + 2 * ggrid;
     const MemArgs ma{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, nm > 0 ? (nm + gc.grid - 1) / gc.grid : 0, g->ab};
     FinArgs fa{v.sums, v.nrows, v.rinfo, g->xr, g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, g->ab, nullptr, c, d};
+    fa.vec = env_int("PRGPU_FIN_VEC", 0);
     // delayed chain resolution (sync reduced, reading Q-C2): the last
     // max_chain + 1 values of every chain source, slot 0 = x_0 = 1/n
     if (reduced && nm > 0 && !async && !phased && !(mode & PR_CHAIN_EAGER) && g->n_hsrc > 0) {
