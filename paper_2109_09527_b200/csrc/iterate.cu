@@ -1084,7 +1084,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     double* zero_partial = g->cta_partial + 2 * ggrid;
     const MemArgs ma{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, nm > 0 ? (nm + gc.grid - 1) / gc.grid : 0, g->ab};
     FinArgs fa{v.sums, v.nrows, v.rinfo, g->xr, g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, g->ab, nullptr, c, d};
-    fa.vec = env_int("PRGPU_FIN_VEC", 0);
+    fa.vec = env_int("PRGPU_FIN_VEC", 1);
     // delayed chain resolution (sync reduced, reading Q-C2): the last
     // max_chain + 1 values of every chain source, slot 0 = x_0 = 1/n
     if (reduced && nm > 0 && !async && !phased && !(mode & PR_CHAIN_EAGER) && g->n_hsrc > 0) {

@@ -551,18 +551,22 @@ def test_device_barrier_world1_and_validation(pr):
 
 
 # ------------------------------------------------------------ NVLS multicast --
-def _multicast_supported():
-    import ctypes
-    try:
-        cu = ctypes.CDLL("libcuda.so.1")
-        cu.cuInit(0)
-        dev = ctypes.c_int()
-        cu.cuDeviceGet(ctypes.byref(dev), 0)
-        v = ctypes.c_int(0)
-        cu.cuDeviceGetAttribute(ctypes.byref(v), 132, dev)   # CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED
-        return v.value == 1
-    except OSError:
-        return False
+def _multicast_usable(pr):
+    """NVLS needs the device attribute AND a multicast object the driver lets
+    this process create (on the one-GPU slice of this pool cuMulticastCreate
+    returns CUDA_ERROR_INVALID_VALUE for every handle type and team size,
+    tools/probe_multicast.py, although the attribute reads 1)."""
+    n, edges = GRAPHS["random"]()
+    s_, t_ = G.edges_to_arrays(edges)
+    with pr.Graph(n, dev(s_), dev(t_)) as g:
+        g.shard(0, 1)
+        try:
+            pr.shard_multicast_local(g.handle)
+            return True
+        except pr.PRError as e:
+            if "cuMulticast" in str(e) or "driver entry point" in str(e):
+                return False
+            raise
 
 
 @pytest.mark.parametrize("name", ["planted", "random", "in_star", "no_edges", "single"])
@@ -572,8 +576,8 @@ def test_multicast_world1_is_sync(pr, name, devbar):
     delta pair and in-degree-0 contrib is stored with multimem.st through the
     multicast address (the switch's replication to a team of one); the run is
     bit-identical to the plain world-1 run (hence to pr_run)."""
-    if not _multicast_supported():
-        pytest.skip("no NVLS multicast on this device")
+    if not _multicast_usable(pr):
+        pytest.skip("NVLS multicast objects cannot be created on this device / slice")
     n, edges = GRAPHS[name]()
     s, t = G.edges_to_arrays(edges)
     with pr.Graph(n, dev(s), dev(t)) as g:
@@ -601,8 +605,8 @@ def test_multicast_world1_is_sync(pr, name, devbar):
 
 
 def test_multicast_local_ingest_world1(pr):
-    if not _multicast_supported():
-        pytest.skip("no NVLS multicast on this device")
+    if not _multicast_usable(pr):
+        pytest.skip("NVLS multicast objects cannot be created on this device / slice")
     gen = graphgen.make_config(2)
     with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
         x0 = torch.empty(gen.n, dtype=torch.float64, device="cuda")
