@@ -209,7 +209,7 @@ typedef struct {
     int64_t gather_edges;       /* edges one gather launch processes */
     int64_t scatter_members;    /* members one scatter launch processes (0 plain) */
     int64_t n_contrib;          /* vertices with outdeg > 0 (size of the contrib vector) */
-    int64_t n_tasks;            /* row-task engine tasks (0 until that engine is first used) */
+    int64_t n_tasks;            /* reserved: always 0 (the round-1 row-task engine was removed) */
     int32_t nosync_min_iters;   /* PR_MODE_NOSYNC: fewest local sweeps of any CTA */
     int32_t nosync_launches;    /* PR_MODE_NOSYNC: persistent launches (1 + relaunches) */
     int32_t nosync_median_iters;/* PR_MODE_NOSYNC: median local sweeps over the CTAs (the max

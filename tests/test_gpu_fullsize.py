@@ -3,7 +3,9 @@ configuration bench.py times (persistent gather grid, reduced and plain modes),
 plus the in-place async and the persistent No-Sync modes on both.
 
 A converged oracle run at these sizes takes ~10 min single-threaded (config 4:
-644 s measured, tests/golden/config_iters.json), so the checks are:
+644 s measured, tests/golden/config_iters.json), so this suite checks (and
+tests/test_gpu_fullsize_converged.py, slow, compares with CONVERGED oracle
+runs; its log is profiles/r2/fullsize_converged_parity.log):
   * integer outputs bit-exact against the oracle (full arrays, compared by hash);
   * the first 3 sweeps element by element against the oracle's first 3 sweeps
     (same arithmetic path, tau = 0);

@@ -29,5 +29,5 @@ stt = g.stats()
 ti = max(1, stt["timed_iterations"])
 print(gen.name, mode, "iters", it, "gather ms/launch", round(stt["gather_ms"] / ti, 4),
       "finalize/scatter ms/launch", round(stt["scatter_ms"] / ti, 4),
-      "tasks", stt["n_tasks"], "rows", stt["gather_rows"], "edges", stt["gather_edges"], "ncontrib", stt["n_contrib"])
+      "rows", stt["gather_rows"], "edges", stt["gather_edges"], "ncontrib", stt["n_contrib"])
 g.close()
