@@ -83,15 +83,19 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
                                  so the reduced sweep reproduces the plain (Jacobi) trajectory
                                  while still gathering no chain member.  The phased, async and
                                  No-Sync modes always resolve members eagerly (in place). */
-#define PR_MODE_PHASED   64u  /* in-place sweeps in K ordered phases (block Gauss-Seidel; Q-B):
-                                 one contrib buffer; phase k gathers a contiguous 1/K of the
-                                 edge stream and finalizes the rows ending in it, so it reads
-                                 the values phases 0..k-1 of the same sweep wrote (the
-                                 in-place reads of Alg.3 P:545-565 in a fixed order).
-                                 Deterministic.  K = PRGPU_PHASES (default: 8 when each phase
-                                 still has >= 24 edge steps of 256 per resident warp, fewer on
-                                 small graphs; one phase on a source-blocked view).  Exclusive
-                                 with ASYNC / NOSYNC / PERFORATE. */
+#define PR_MODE_PHASED   64u  /* block Gauss-Seidel in K ordered, ROW-ALIGNED phases (Q-B):
+                                 one contrib buffer; the rows of the view (vertex order) are
+                                 cut at b_k = the first row whose first edge e has
+                                 e * K >= k * E; phase k gathers its rows from the values
+                                 phases 0..k-1 of the same sweep wrote and updates them in
+                                 place (the in-place reads of Alg.3 P:545-565 in a fixed
+                                 order); members (eager, Q-C) and, in sweep 1, the in-degree-0
+                                 vertices after the last phase.  Deterministic; equals the
+                                 oracle's block Gauss-Seidel with the same K.  K = PRGPU_PHASES
+                                 (default: 8 when each phase still has >= 24 edge steps of
+                                 256 per resident warp, fewer on small graphs; one phase on a
+                                 source-blocked view).  Exclusive with ASYNC / NOSYNC /
+                                 PERFORATE. */
 
 /*
  * pr_graph_create -- build the in-edge CSR and out-degrees on the device
@@ -203,8 +207,7 @@ typedef struct {
     double  gather_ms;          /* PR_TIMING: summed CUDA-event time of the gather launches
                                    (K-GATHER; in-place modes: the whole fused sweep) */
     double  scatter_ms;         /* PR_TIMING: summed time of the launches after the gather:
-                                   K-FINALIZE in sync mode (rows + members), the member
-                                   scatter of the row-task engine, 0 in place */
+                                   K-FINALIZE in sync mode (rows + members), 0 in place */
     int64_t gather_rows;        /* rows one gather launch processes (in-degree > 0: all, or |R| reduced) */
     int64_t gather_edges;       /* edges one gather launch processes */
     int64_t scatter_members;    /* members one scatter launch processes (0 plain) */
@@ -226,10 +229,10 @@ int pr_get_run_stats(const pr_graph *g, pr_run_stats *out);
 
 /*
  * pr_get_phase_plan -- the phase plan of the last PR_MODE_PHASED run on the
- * plain (reduced = 0) or reduced view (Q-B): phase k gathers the view's edges
- * [edge_bounds[k], edge_bounds[k+1]) (view edge order: the view's rows in
- * vertex order, each row's in-edges in CSR order) and finalizes the view rows
- * [row_bounds[k], row_bounds[k+1]).  Host arrays of cap >= K+1 entries.
+ * plain (reduced = 0) or reduced view (Q-B): phase k gathers and updates the
+ * view rows [row_bounds[k], row_bounds[k+1]) (the view's rows in vertex order),
+ * whose in-edges are the view's edges [edge_bounds[k], edge_bounds[k+1]) (each
+ * row's in-edges in CSR order).  Host arrays of cap >= K+1 entries.
  * Returns K >= 1, or on error a negative value (-PR_EINVAL: bad arguments or
  * cap; -PR_ESTATE: no phased run on that view yet) with the message in
  * pr_last_error().
