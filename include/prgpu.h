@@ -52,7 +52,9 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
 
 /* pr_run mode bits */
 #define PR_MODE_SYNC      0u  /* synchronous pull, double-buffered contribs (Alg.1) */
-#define PR_MODE_ASYNC     1u  /* in-place No-Sync-style sweeps (Alg.3; Q-Y) */
+#define PR_MODE_ASYNC     1u  /* in-place No-Sync-style sweeps (Alg.3; Q-Y); on a
+                                 source-blocked view (contrib vector beyond L2) the Jacobi
+                                 schedule, a valid No-Sync schedule (Q-Y2) */
 #define PR_NORM_L1        0u  /* stop when sum_v |x_t(v)-x_{t-1}(v)| <= threshold (configs) */
 #define PR_NORM_LINF      2u  /* stop when max_v |x_t(v)-x_{t-1}(v)| <= threshold */
 #define PR_USE_REDUCTIONS 4u  /* compute one vertex per identical group, resolve chain
@@ -67,11 +69,15 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
                                  ||F(x) - x|| of the ORIGINAL system is certified by one
                                  synchronous gather and the kernel is relaunched if it is
                                  above threshold.  iterations = the largest number of local
-                                 sweeps of any CTA. */
+                                 sweeps of any CTA.  On a source-blocked view: launch-level
+                                 sweeps on the Jacobi schedule, then the same certificate
+                                 (Q-Y2). */
 #define PR_PERFORATE     32u  /* loop perforation (Barriers-Opt, Alg.5),
                                  synchronous plain mode only: a vertex whose change in a sweep
-                                 is 0 < |delta| < threshold * 1e-5 keeps its value from then on
-                                 and is no longer gathered (APPROXIMATE: the result is not the
+                                 is 0 < |delta| < threshold * 1e-5 gets Alg.5's sticky
+                                 threshold_check flag and keeps its value from the next sweep
+                                 on; flagged rows are compacted out of the gather at batch
+                                 ends (performance only) (APPROXIMATE: the result is not the
                                  fixed point; the stop test counts frozen vertices as 0). */
 #define PR_CHAIN_EAGER  128u  /* with PR_USE_REDUCTIONS in the synchronous mode: resolve chain
                                  members in the SAME sweep from their head's new value (reading
