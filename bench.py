@@ -268,8 +268,8 @@ def compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags):
     timed region: sync (Barriers, Alg.1), phased in-place sweeps (block
     Gauss-Seidel, deterministic; DESIGN.md Q-B), launch-level in-place async,
     persistent barrier-free No-Sync (Alg.3) -- the paper's Fig.7 comparison,
-    P:994 -- and loop perforation (Barriers-Opt, Alg.5; plain sync only,
-    approximate) with its work fraction and L1 distance to the exact plain
+    P:994 -- and loop perforation (Alg.5, approximate: Barriers-Opt on the
+    sync schedule, in place with async, No-Sync-Opt) with its work fraction and L1 distance to the exact plain
     result (the Figs.5-6 analogue)."""
     def timed(g, mode):
         best = None
@@ -304,12 +304,14 @@ def compare_modes(pr, torch, gen, n, src_d, dst_d, x_d, stream, flags):
     rc_, it_e, fd_ = g.run(x_d, gen.d, gen.tau, gen.max_iter, mode=0)
     x_exact = x_d.clone()
     work_exact = g.stats()["edges_gathered"]
-    ms_, it_, fd_, st_ = timed(g, pr.PR_PERFORATE)
-    modes["perforated_plain"] = {
-        "time_to_converge_ms": round(ms_, 3), "iterations": it_,
-        "work_fraction": round(st_["edges_gathered"] / max(1, work_exact), 4),
-        "frozen_rows": st_["frozen_rows"], "compactions": st_["compactions"],
-        "l1_vs_exact_plain": float((x_d - x_exact).abs().sum()), "exact_plain_iterations": it_e}
+    for name, md in (("perforated_plain", 0), ("perforated_async", pr.PR_MODE_ASYNC),
+                     ("perforated_nosync", pr.PR_MODE_NOSYNC)):
+        ms_, it_, fd_, st_ = timed(g, pr.PR_PERFORATE | md)
+        modes[name] = {
+            "time_to_converge_ms": round(ms_, 3), "iterations": it_,
+            "work_fraction": round(st_["edges_gathered"] / max(1, work_exact), 4),
+            "frozen_rows": st_["frozen_rows"], "compactions": st_["compactions"],
+            "l1_vs_exact_plain": float((x_d - x_exact).abs().sum()), "exact_plain_iterations": it_e}
     g.close()
     return modes
 

@@ -72,13 +72,19 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
                                  sweeps of any CTA.  On a source-blocked view: launch-level
                                  sweeps on the Jacobi schedule, then the same certificate
                                  (Q-Y2). */
-#define PR_PERFORATE     32u  /* loop perforation (Barriers-Opt, Alg.5),
-                                 synchronous plain mode only: a vertex whose change in a sweep
-                                 is 0 < |delta| < threshold * 1e-5 gets Alg.5's sticky
+#define PR_PERFORATE     32u  /* loop perforation (Alg.5), plain view
+                                 only: a vertex whose change in a sweep is
+                                 0 < |delta| < threshold * 1e-5 gets Alg.5's sticky
                                  threshold_check flag and keeps its value from the next sweep
                                  on; flagged rows are compacted out of the gather at batch
                                  ends (performance only) (APPROXIMATE: the result is not the
-                                 fixed point; the stop test counts frozen vertices as 0). */
+                                 fixed point; the stop test counts frozen vertices as 0).
+                                 Alone: synchronous sweeps (Barriers-Opt).  With
+                                 PR_MODE_ASYNC: in-place sweeps.  With PR_MODE_NOSYNC
+                                 (No-Sync-Opt): persistent barrier-free launches of <= 8
+                                 local sweeps per CTA with the CTA-level stop test, no
+                                 certificate (iterations = the sum over launches of the
+                                 largest local count; final delta = the published sum). */
 #define PR_CHAIN_EAGER  128u  /* with PR_USE_REDUCTIONS in the synchronous mode: resolve chain
                                  members in the SAME sweep from their head's new value (reading
                                  Q-C as first written; information crosses a chain in one sweep,
@@ -141,8 +147,8 @@ int pr_preprocess(pr_graph *g, uint32_t flags, void *stream);
  *   max_iter   >= 1; reaching it returns PR_NOT_CONVERGED with valid ranks
  *   mode       one of PR_MODE_SYNC (0) / PR_MODE_ASYNC / PR_MODE_NOSYNC /
  *              PR_MODE_PHASED, or'ed
- *              with PR_NORM_LINF, PR_USE_REDUCTIONS, PR_TIMING; PR_PERFORATE only
- *              with the plain synchronous mode
+ *              with PR_NORM_LINF, PR_USE_REDUCTIONS, PR_TIMING; PR_PERFORATE with
+ *              SYNC / ASYNC / NOSYNC on the plain view
  *   ranks      fp64[n] output in vertex-id order (host or device, caller-owned)
  *   iters_out  (host, nullable) number of update sweeps including the final
  *              one that met the stop test (Q-I); PR_MODE_NOSYNC: the

@@ -424,8 +424,8 @@ int pr_run(pr_graph* g, double d, double threshold, int32_t max_iter, void* stre
         set_error("pr_run: PR_MODE_PHASED is exclusive with PR_MODE_ASYNC / PR_MODE_NOSYNC / PR_PERFORATE");
         return PR_EINVAL;
     }
-    if ((mode & PR_PERFORATE) && (mode & (PR_MODE_ASYNC | PR_MODE_NOSYNC | PR_USE_REDUCTIONS))) {
-        set_error("pr_run: PR_PERFORATE is defined for the synchronous plain mode only");
+    if ((mode & PR_PERFORATE) && (mode & PR_USE_REDUCTIONS)) {
+        set_error("pr_run: PR_PERFORATE is defined for the plain view only (not with PR_USE_REDUCTIONS)");
         return PR_EINVAL;
     }
     if ((mode & PR_USE_REDUCTIONS) && !g->pre_done) {

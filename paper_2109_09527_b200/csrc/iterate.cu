@@ -286,6 +286,10 @@ struct FinArgs {
 // contrib store y[slot]; x is kept in row / member order (xr, xm) during the
 // sweeps and written back to vertex order once, by k_unpermute.
 constexpr int FIN_U = 4;
+#ifndef PRGPU_FIN_PAIRS
+#define PRGPU_FIN_PAIRS 2
+#endif
+constexpr int FIN_PAIRS = PRGPU_FIN_PAIRS;  // row pairs per thread and iteration of the 16-byte path
 
 __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     __shared__ double red[64];
@@ -307,11 +311,12 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
         double2* __restrict__ X2 = reinterpret_cast<double2*>(xr);
         const int4* __restrict__ I2 = reinterpret_cast<const int4*>(f.rinfo);
         const int64_t p_end = f.nrows >> 1;
-        for (int64_t p0 = (f.row0 >> 1) + t0; p0 < p_end; p0 += 2 * T) {
-            double2 sv[2], xv[2];
-            int4 iv[2];
+        constexpr int FP = FIN_PAIRS;
+        for (int64_t p0 = (f.row0 >> 1) + t0; p0 < p_end; p0 += FP * T) {
+            double2 sv[FP], xv[FP];
+            int4 iv[FP];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < FP; ++u) {
                 const int64_t p = p0 + u * T;
                 if (p < p_end) {
                     sv[u] = __ldcs(S2 + p);
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < FP; ++u) {
                 const int64_t p = p0 + u * T;
                 if (p < p_end) {
                     const double xa = __dadd_rn(f.c, __dmul_rn(f.d, sv[u].x));
@@ -548,6 +553,12 @@ struct InPlacePolicy {
     double xo_f;
     int2 inf[SE_V];
     double xo[SE_V];
+    // loop perforation in place (No-Sync-Opt, Alg.5; reading Q-P):
+    // fz[r] = sticky threshold_check flag of row r (nullptr: off)
+    uint8_t* fz;
+    double tau_f;
+    unsigned long long* nfz;  // flags set, counted per thread, added at the end
+    uint32_t nfrozen;
 
     __device__ __forceinline__ double load(int32_t u) const {
         if (u < hot_n) return hot[u];
@@ -567,12 +578,20 @@ struct InPlacePolicy {
             }
     }
     __device__ __forceinline__ void fin(int64_t r, double s, int2 q, double xold) {
+        if (fz && fz[r]) return;  // flagged: keeps x and its contrib, |delta| = 0
         const double xn = __dadd_rn(c, __dmul_rn(d, s));
         st_relaxed_f64(xr + r, xn);
         if (q.x > 0) st_relaxed_f64(y + q.y, xn / (double)q.x);
         const double dl = fabs(xn - xold);
         l1 += dl;
         linf = fmax(linf, dl);
+        if (fz && dl != 0.0 && dl < tau_f) {  // threshold_check <- True (Alg.5)
+            fz[r] = 1;
+            ++nfrozen;
+        }
+    }
+    __device__ __forceinline__ void flush_frozen() const {
+        if (nfrozen) atomicAdd(nfz, (unsigned long long)nfrozen);
     }
     __device__ __forceinline__ void emit(int64_t r, double s) { fin(r, s, __ldg(rinfo + r), ld_relaxed_f64(xr + r)); }
     __device__ __forceinline__ void emit_at(int j, int64_t r, double s) { fin(r, s, inf[j], xo[j]); }
@@ -628,6 +647,7 @@ __global__ void __launch_bounds__(SE_NT_IP, 1)
     p.linf = 0.0;
     stream_run(p, a);
     members_inplace(ma, p.xr, p.y, p.l1, p.linf);
+    if (p.fz) p.flush_frozen();
     partial_and_ticket(ia, p.l1, p.linf, red, blockIdx.x, &ia.st->ticket_gather, &flag);
 }
 
@@ -677,6 +697,7 @@ __global__ void __launch_bounds__(SE_NT_IP, 1) k_nosync_stream(InPlacePolicy p, 
         __syncthreads();
         if (flag) break;
     }
+    if (p.fz) p.flush_frozen();
 }
 
 // Certificate of an in-place result: ||F(x) - x|| of the ORIGINAL system, with
@@ -1038,8 +1059,8 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     const bool blocked_async = (mode & (PR_MODE_ASYNC | PR_MODE_NOSYNC)) && v.nseg > 0;
     const uint32_t mode_in = mode;
     if (blocked_async) mode &= ~(PR_MODE_ASYNC | PR_MODE_NOSYNC);
-    if (mode & PR_MODE_NOSYNC) return run_nosync(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     if (mode & PR_PERFORATE) return run_perforated(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
+    if (mode & PR_MODE_NOSYNC) return run_nosync(g, d, tau, max_iter, mode, ranks, ctx, iters_out, delta_out);
     cudaStream_t s = ctx.stream;
     const bool async = (mode & PR_MODE_ASYNC) != 0;
     const bool phased = (mode & PR_MODE_PHASED) != 0;
@@ -1531,6 +1552,11 @@ static int run_nosync(pr_graph* g, double d, double tau, int32_t max_iter, uint3
 // performance step, at the host sync after each batch of 8 sweeps the gathered
 // view is COMPACTED to the unflagged rows once >= 5 % of them are flagged, so
 // later sweeps stop streaming the frozen rows' edges.  Approximate by design.
+// With PR_MODE_ASYNC the sweeps are in place (k_stream_async, the flags in
+// InPlacePolicy); with PR_MODE_NOSYNC (No-Sync-Opt, Alg.5 with Alg.3's
+// barrier-free loop) each batch is ONE persistent k_nosync_stream launch of at
+// most 8 local sweeps per CTA that stops early on the CTA-level convergence
+// test, so the compaction still happens between launches.
 struct KeepGet {
     const uint8_t* fz;
     __device__ int64_t operator()(int64_t r) const { return fz[r] ? 0 : 1; }
@@ -1589,6 +1615,11 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
     cudaStream_t s = ctx.stream;
     const int64_t n = g->n;
     View& V = g->plain;
+    // schedule: synchronous sweeps (Barriers-Opt), in-place launch-level
+    // sweeps (ASYNC), or persistent barrier-free launches of at most
+    // PF_BATCH local sweeps each (No-Sync-Opt)
+    const bool nosync = (mode & PR_MODE_NOSYNC) != 0;
+    const bool inplace = nosync || (mode & PR_MODE_ASYNC) != 0;
     const int64_t launches0 = ctx.launches;
     RunBufs rb;
     PR_TRY(run_buffers(g, ctx, ranks, max_iter, &rb));
@@ -1599,18 +1630,30 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
         std::min<int64_t>(std::max<int64_t>((V.nrows + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
     const int64_t nz = g->nz;
     const int64_t zgrid = nz > 0 ? std::min<int64_t>((nz + GT_NT * 4 - 1) / (GT_NT * 4), cap4) : 0;
-    PR_TRY(ensure_partials(g, ctx, 2 * (fgrid_max + zgrid)));
+    GatherCfg gc_full;
+    PR_TRY(gather_config(ctx, V, g, inplace ? G_INPLACE : G_SYNC, &gc_full));
+    const int64_t pmax = std::max<int64_t>(fgrid_max, gc_full.grid);
+    PR_TRY(ensure_partials(g, ctx, 2 * (pmax + zgrid) + 2));
     uint8_t* fz = nullptr;
     unsigned long long* cnt = nullptr;
+    double* err = nullptr;    // No-Sync-Opt: (L1, Linf) each CTA last published
+    int32_t* lits = nullptr;  // No-Sync-Opt: local sweeps of each CTA in this launch
     TmpGuard tg_(ctx.stream);
     tg_.track(fz);
     tg_.track(cnt);
+    tg_.track(err);
+    tg_.track(lits);
     PR_TRY(dalloc(&fz, (size_t)std::max<int64_t>(V.nrows, 1), s));
     PR_TRY(dalloc(&cnt, 1, s));
     PR_CUDA(cudaMemsetAsync(fz, 0, (size_t)std::max<int64_t>(V.nrows, 1), s));
     PR_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), s));
+    if (nosync) {
+        PR_TRY(dalloc(&err, (size_t)(2 * gc_full.grid), s));
+        PR_TRY(dalloc(&lits, (size_t)gc_full.grid, s));
+    }
     PR_TRY(init_state(g, ctx, tau, max_iter, mode, x, g->cidx, g->y[0], V, 0));
     const unsigned fg = (unsigned)std::min<int64_t>((V.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+    const double tau_f = tau * 1e-5;  // "threshold*0.00001" (Alg.5; Q-P)
 
     ActiveView A;
     A.v = V;  // shallow: the plain view's arrays
@@ -1618,17 +1661,46 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
     A.is_full = true;
     int64_t edges_gathered = 0;
     int32_t compactions = 0;
-    int64_t launched = 0;
+    int64_t launched = 0;         // sweeps launched (No-Sync-Opt: the largest local count so far)
     int64_t flagged_active = 0;   // flagged rows still in the active view
     GatherCfg gc;
     int64_t fgrid = 0;
     auto setup = [&]() -> int {
-        PR_TRY(gather_config(ctx, A.v, g, G_SYNC, &gc));
+        PR_TRY(gather_config(ctx, A.v, g, inplace ? G_INPLACE : G_SYNC, &gc));
         fgrid = std::min<int64_t>(std::max<int64_t>((A.v.nrows + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
         return PR_OK;
     };
     PR_TRY(setup());
+    auto inplace_policy = [&]() {
+        InPlacePolicy ip{};
+        ip.y_in = g->y[0];
+        ip.y = g->y[0];
+        ip.hot_n = gc.hot_n;
+        ip.xr = A.xr;
+        ip.rinfo = A.v.rinfo;
+        ip.c = c;
+        ip.d = d;
+        ip.fz = fz;
+        ip.tau_f = tau_f;
+        ip.nfz = cnt;
+        return ip;
+    };
+    const MemArgs ma0{nullptr, nullptr, nullptr, nullptr, 0, 0, nullptr};
     auto sweep = [&](int64_t it, int) -> int {
+        if (inplace) {  // one contrib buffer, updated in place
+            const int64_t gg = gc.grid;
+            IterArgs ia{g->st, g->cta_partial, gg, 0, it == 0 ? zgrid : 0, g->delta_log};
+            if (it == 0 && zgrid > 0)  // in-degree-0 vertices before the first in-place sweep (Q-Z)
+                PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, c, x, g->y[0],
+                          (const int32_t*)g->outdeg, (const int32_t*)g->cidx, g->cta_partial + 2 * gg);
+            if (A.v.nspans > 0) {
+                PR_LAUNCH(ctx, k_stream_async, gc.grid, gc.nt, gc.smem, inplace_policy(), stream_args(A.v), ma0, ia);
+            } else {  // nothing left to gather: the reduction alone (delta 0)
+                FinArgs f{A.v.sums, 0, A.v.rinfo, A.xr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, g->y[0], c, d};
+                PR_LAUNCH_PDL(ctx, k_finalize, 1, GT_NT, 0, f, ia);
+            }
+            return PR_OK;
+        }
         IterArgs ia{g->st, g->cta_partial, fgrid, 0, it == 0 ? zgrid : 0, g->delta_log};
         const double* y_in = g->y[it & 1];
         double* y_out = g->y[(it + 1) & 1];
@@ -1638,7 +1710,7 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
         PR_TRY(launch_gather(ctx, g, A.v, y_in, gc));
         FinArgs f{A.v.sums, A.v.nrows, A.v.rinfo, A.xr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, y_out, c, d};
         f.fz = fz;
-        f.tau_f = tau * 1e-5;  // "threshold*0.00001" (Alg.5; Q-P)
+        f.tau_f = tau_f;
         f.y_other = (double*)y_in;
         f.nfz = cnt;
         PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
@@ -1648,23 +1720,84 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
                       (const int32_t*)g->cidx);
         return PR_OK;
     };
+    // No-Sync-Opt: one persistent launch of at most `cap` local sweeps per CTA
+    // over the active view, stopping early on the CTA-level convergence test
+    // (thread-level convergence) over the deltas the CTAs published
+    std::vector<int32_t> hit;
+    std::vector<double> herr, hlog;
+    double ns_delta[2] = {0.0, 0.0};
+    int ns_status = PR_NOT_CONVERGED;
+    int32_t ns_launches = 0;
+    auto nosync_launch = [&](int cap, int64_t* local_max, double* local_mean) -> int {
+        const int grid = gc.grid;
+        if (launched == 0 && zgrid > 0)
+            PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, c, x, g->y[0],
+                      (const int32_t*)g->outdeg, (const int32_t*)g->cidx, g->cta_partial);
+        PR_LAUNCH(ctx, k_fill_f64, 1, 256, 0, err, (int64_t)(2 * grid), 1e300);
+        PR_CUDA(cudaMemsetAsync(lits, 0, sizeof(int32_t) * (size_t)grid, s));
+        NoSyncArgs na{err, lits, (mode & PR_NORM_LINF) ? 1 : 0, tau, cap};
+        if (A.v.nspans > 0) {
+            PR_LAUNCH(ctx, k_nosync_stream, (unsigned)grid, gc.nt, gc.smem, inplace_policy(), stream_args(A.v), ma0,
+                      na);
+            ++ns_launches;
+        }
+        hit.resize(grid);
+        herr.resize(2 * grid);
+        PR_CUDA(cudaMemcpyAsync(hit.data(), lits, sizeof(int32_t) * (size_t)grid, cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaMemcpyAsync(herr.data(), err, sizeof(double) * 2 * (size_t)grid, cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        if (A.v.nspans == 0) {  // nothing left to gather: every delta is 0
+            *local_max = 1;
+            *local_mean = 1.0;
+            ns_delta[0] = ns_delta[1] = 0.0;
+        } else {
+            *local_max = *std::max_element(hit.begin(), hit.end());
+            *local_mean = 0.0;
+            for (int32_t h : hit) *local_mean += h;
+            *local_mean /= grid;
+            ns_delta[0] = ns_delta[1] = 0.0;
+            for (int b = 0; b < grid; ++b) {
+                ns_delta[0] += herr[2 * b];
+                ns_delta[1] = std::max(ns_delta[1], herr[2 * b + 1]);
+            }
+        }
+        hlog.push_back(ns_delta[0]);
+        hlog.push_back(ns_delta[1]);
+        if (((mode & PR_NORM_LINF) ? ns_delta[1] : ns_delta[0]) <= tau) ns_status = PR_OK;
+        return PR_OK;
+    };
     DevState* hs = g->st_host;
     int host_syncs = 0;
     int rc = PR_OK;
     while (true) {
         const int nb = (int)std::min<int64_t>(8, max_iter - launched);
-        for (int j = 0; j < nb && rc == PR_OK; ++j) rc = sweep(launched + j, j);
-        if (rc != PR_OK) break;
+        bool finished = false;
         unsigned long long flagged = 0;  // flags set since the last compaction (this view's rows)
-        PR_CUDA(cudaMemcpyAsync(hs, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-        PR_CUDA(cudaMemcpyAsync(&flagged, cnt, sizeof(flagged), cudaMemcpyDeviceToHost, s));
-        PR_CUDA(cudaStreamSynchronize(s));
-        ++host_syncs;
+        if (nosync) {
+            int64_t lmax = 0;
+            double lmean = 0.0;
+            rc = nosync_launch(nb, &lmax, &lmean);
+            if (rc != PR_OK) break;
+            PR_CUDA(cudaMemcpyAsync(&flagged, cnt, sizeof(flagged), cudaMemcpyDeviceToHost, s));
+            PR_CUDA(cudaStreamSynchronize(s));
+            ++host_syncs;
+            edges_gathered += (int64_t)((double)A.v.nedges * lmean + 0.5);  // spans are equal-sized: an estimate
+            launched += lmax;
+            finished = ns_status == PR_OK || launched >= max_iter;
+        } else {
+            for (int j = 0; j < nb && rc == PR_OK; ++j) rc = sweep(launched + j, j);
+            if (rc != PR_OK) break;
+            PR_CUDA(cudaMemcpyAsync(hs, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+            PR_CUDA(cudaMemcpyAsync(&flagged, cnt, sizeof(flagged), cudaMemcpyDeviceToHost, s));
+            PR_CUDA(cudaStreamSynchronize(s));
+            ++host_syncs;
+            const int64_t done_sweeps = std::min<int64_t>(hs->iters, launched + nb) - launched;
+            edges_gathered += A.v.nedges * std::max<int64_t>(done_sweeps, 0);
+            launched += nb;
+            finished = hs->done || launched >= max_iter;
+        }
         flagged_active = (int64_t)flagged;
-        const int64_t done_sweeps = std::min<int64_t>(hs->iters, launched + nb) - launched;
-        edges_gathered += A.v.nedges * std::max<int64_t>(done_sweeps, 0);
-        launched += nb;
-        if (hs->done || launched >= max_iter) break;
+        if (finished) break;
         if (flagged_active * 20 < A.v.nrows || flagged_active == 0) continue;  // compact once >= 5 % are flagged
         // ---- compaction (performance only): gather only the unflagged rows ----
         if (!A.is_full)
@@ -1719,9 +1852,23 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
         if (!rb.ranks_dev) PR_CUDA(cudaMemcpyAsync(ranks, x, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
     }
     const int64_t frozen = V.nrows - A.v.nrows + flagged_active;
+    int nlog = 0;
+    if (rc == PR_OK && nosync) {  // host-side state and log: the published deltas after each launch
+        hs->iters = (int32_t)std::min<int64_t>(launched, max_iter);
+        hs->status = ns_status;
+        hs->l1 = ns_delta[0];
+        hs->linf = ns_delta[1];
+        hs->done = 1;
+        PR_CUDA(cudaMemcpyAsync(g->st, hs, sizeof(DevState), cudaMemcpyHostToDevice, s));
+        nlog = std::min<int>((int)hlog.size() / 2, std::min(max_iter, 4096));
+        if (nlog > 0)
+            PR_CUDA(cudaMemcpyAsync(g->delta_log, hlog.data(), sizeof(double) * 2 * nlog, cudaMemcpyHostToDevice, s));
+    }
     free_active(A, s);
     dfree(fz, s);
     dfree(cnt, s);
+    dfree(err, s);
+    dfree(lits, s);
     PR_CUDA(cudaStreamSynchronize(s));
     if (rc != PR_OK) return rc;
     fill_stats(g, ctx, launches0, V, 0, host_syncs, 1);
@@ -1729,6 +1876,10 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
     rs.edges_gathered = edges_gathered;
     rs.frozen_rows = frozen;
     rs.compactions = compactions;
+    if (nosync) {
+        g->log_len = nlog;
+        rs.nosync_launches = ns_launches;
+    }
     if (iters_out) *iters_out = hs->iters;
     if (delta_out) *delta_out = (mode & PR_NORM_LINF) ? hs->linf : hs->l1;
     return hs->status;

@@ -1,5 +1,5 @@
-"""GPU tests of PR_PERFORATE: loop perforation (Barriers-Opt, Alg.5 P:670-707;
-SURVEY §8 f2).  Approximate by design: a vertex whose change falls to
+"""GPU tests of PR_PERFORATE: loop perforation (Barriers-Opt and, in place,
+No-Sync-Opt, Alg.5).  Approximate by design: a vertex whose change falls to
 0 < |delta| < tau * 1e-5 gets its sticky threshold_check flag and keeps its
 value from the next sweep on (reading Q-P); flagged rows are compacted out of
 the gather (a performance step only).  Pinned: element-wise parity with the
@@ -56,11 +56,48 @@ def test_perforation_saves_work_and_stays_close(pr, cfg, scale):
           f"of exact, L1 {l1:.3e} (exact {l1_exact:.3e})")
 
 
+@pytest.mark.parametrize("sched", ["async", "nosync"])
+@pytest.mark.parametrize("cfg,scale", [(4, 14), (4, 16), (2, None)])
+def test_perforation_in_place(pr, cfg, scale, sched):
+    """Perforation on the in-place schedules (with PR_MODE_ASYNC, and No-Sync-Opt
+    = Alg.5 with Alg.3's barrier-free loop).  Not deterministic, so pinned by
+    properties: the stop test holds, rows freeze and leave the gather, the work
+    is below the same schedule's unperforated run, and the result is as close to
+    x* as the synchronous perforated run's bound (the flag rule is the same)."""
+    mode = pr.PR_MODE_ASYNC if sched == "async" else pr.PR_MODE_NOSYNC
+    gen = graphgen.make_config(cfg, scale_override=scale) if scale else graphgen.make_config(cfg)
+    ref_g = oracle.build_csr(gen.n, gen.src, gen.dst)
+    tight = oracle.pagerank(ref_g, D, gen.tau / 100, 5000)
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
+        x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+        g.run(x, D, gen.tau, 1000)
+        l1_exact = np.abs(x.cpu().numpy() - tight.x).sum()
+        g.run(x, D, gen.tau, 1000, mode=pr.PR_MODE_ASYNC)
+        full_work = g.stats()["edges_gathered"] if sched == "async" else None
+        st, it_p, fd = g.run(x, D, gen.tau, 1000, mode=mode | pr.PR_PERFORATE)
+        xp = x.cpu().numpy()
+        s = g.stats()
+        log = g.delta_log()
+    assert st == pr.PR_OK and fd <= gen.tau
+    assert log[-1, 0] == fd
+    assert s["frozen_rows"] > 0
+    assert s["edges_gathered"] < s["gather_edges"] * it_p
+    if full_work is not None:
+        assert s["edges_gathered"] < full_work
+    if sched == "nosync":
+        assert s["nosync_launches"] >= 1 and len(log) == s["nosync_launches"]
+    l1 = np.abs(xp - tight.x).sum()
+    assert l1 <= max(1e-6, 1e4 * l1_exact), (l1, l1_exact)
+    assert np.isfinite(xp).all() and (xp > 0).all()
+    print(f"{gen.name} {sched}: sweeps {it_p}, frozen {s['frozen_rows']}, compactions {s['compactions']}, "
+          f"L1 {l1:.3e} (exact {l1_exact:.3e})")
+
+
 def test_perforation_mode_checks(pr):
     gen = graphgen.make_config(1)
     with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g:
         x = torch.empty(gen.n, dtype=torch.float64, device="cuda")
-        for bad in (pr.PR_PERFORATE | pr.PR_MODE_ASYNC, pr.PR_PERFORATE | pr.PR_MODE_NOSYNC):
+        for bad in (pr.PR_PERFORATE | pr.PR_MODE_ASYNC | pr.PR_MODE_NOSYNC, pr.PR_PERFORATE | pr.PR_MODE_PHASED):
             with pytest.raises(pr.PRError) as e:
                 pr.pr_run(g.handle, D, 1e-10, 10, x, mode=bad)
             assert e.value.code == pr.PR_EINVAL
@@ -82,3 +119,7 @@ def test_perforation_tiny_tau_is_exact_trajectory(pr):
         b = x.cpu().numpy()
         assert g.stats()["frozen_rows"] == 0
         assert np.array_equal(a, b)
+        for sched in (pr.PR_MODE_ASYNC, pr.PR_MODE_NOSYNC):   # no flag is ever set in place either
+            st, it, _ = g.run(x, D, 0.0, 30, mode=sched | pr.PR_PERFORATE)
+            assert st == pr.PR_NOT_CONVERGED and it == 30
+            assert g.stats()["frozen_rows"] == 0 and g.stats()["compactions"] == 0

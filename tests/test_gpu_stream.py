@@ -142,10 +142,11 @@ def test_blocked_rmat(pr, monkeypatch):
 
 @pytest.mark.parametrize("bits", [4, 8])
 def test_blocked_views_with_every_mode(pr, monkeypatch, bits):
-    """Source-blocked views: the in-place modes run the in-place blocked sweep
-    (rows finalized in their last segment's pass), No-Sync adds its
-    certificate (a blocked sync gather), perforation runs blocked first,
-    unblocked after compaction -- all must reach the oracle's fixed point."""
+    """Source-blocked views: the in-place modes run on the Jacobi schedule
+    (reading Q-Y2), No-Sync adds its certificate (a blocked sync gather),
+    perforation runs blocked first, unblocked after compaction -- all must
+    reach the oracle's fixed point (perforation: the oracle's perforated run;
+    with ASYNC / NOSYNC it is the same synchronous perforated run, Q-Y2)."""
     monkeypatch.setenv("PRGPU_SEG_BITS", str(bits))
     n, s, t = hub_graph(seed=11)
     ref_g = oracle.build_csr(n, s, t)
@@ -163,6 +164,9 @@ def test_blocked_views_with_every_mode(pr, monkeypatch, bits):
         ref_p = oracle.pagerank(ref_g, D, 1e-12, 1000, perforate=True)
         assert st == pr.PR_OK and abs(it - ref_p.iters) <= 1
         assert np.abs(x - ref_p.x).max() <= 1e-10 and np.abs(x - ref_p.x).sum() <= 1e-9
+        for extra in (pr.PR_MODE_ASYNC, pr.PR_MODE_NOSYNC):
+            st2, it2, _, x2 = gpu_run(pr, g, n, 1e-12, mode=pr.PR_PERFORATE | extra)
+            assert st2 == st and it2 == it and np.array_equal(x2, x)
 
 
 def test_perforation_can_freeze_everything(pr):
@@ -173,6 +177,7 @@ def test_perforation_can_freeze_everything(pr):
     ref_g = oracle.build_csr(n, s, t)
     ref = oracle.pagerank(ref_g, D, 1e-13, 5000)
     with pr.Graph(n, dev(s), dev(t)) as g:
-        st, it, fd, x = gpu_run(pr, g, n, 1e-13, max_iter=5000, mode=pr.PR_PERFORATE)
-        assert st == pr.PR_OK
-        assert np.abs(x - ref.x).max() <= 1e-12
+        for mode in (pr.PR_PERFORATE, pr.PR_PERFORATE | pr.PR_MODE_ASYNC, pr.PR_PERFORATE | pr.PR_MODE_NOSYNC):
+            st, it, fd, x = gpu_run(pr, g, n, 1e-13, max_iter=5000, mode=mode)
+            assert st == pr.PR_OK, mode
+            assert np.abs(x - ref.x).max() <= 1e-12, mode

@@ -78,7 +78,9 @@ for k in cfgs:
            "create_ms": round(sorted(cts)[1], 3), "preprocess_ms": round(sorted(pts)[1], 3)}
     for name, mode in (("plain", 0), ("reduced", pr.PR_USE_REDUCTIONS),
                        ("reduced_eager", pr.PR_USE_REDUCTIONS | pr.PR_CHAIN_EAGER), ("phased", pr.PR_MODE_PHASED),
-                       ("async", pr.PR_MODE_ASYNC), ("nosync", pr.PR_MODE_NOSYNC), ("perforated", pr.PR_PERFORATE)):
+                       ("async", pr.PR_MODE_ASYNC), ("nosync", pr.PR_MODE_NOSYNC), ("perforated", pr.PR_PERFORATE),
+                       ("perforated_async", pr.PR_PERFORATE | pr.PR_MODE_ASYNC),
+                       ("perforated_nosync", pr.PR_PERFORATE | pr.PR_MODE_NOSYNC)):
         (ms, it, rc), stt, gms, fms = timed_run(g, x, gen, mode)
         r = {"time_to_converge_ms": round(ms, 3), "iterations": it, "status": rc}
         if name in ("plain", "reduced"):
@@ -91,7 +93,7 @@ for k in cfgs:
             r.update(phases=stt["phases"])
         if name == "nosync":
             r.update(median_local_sweeps=stt["nosync_median_iters"], certified_residual=stt["residual"])
-        if name == "perforated":
+        if name.startswith("perforated"):
             r.update(frozen_rows=stt["frozen_rows"], edges_gathered=stt["edges_gathered"])
         rec[name] = r
     g.close()
