@@ -31,7 +31,8 @@ def graphs():
 
 
 MODES = [0, pr.PR_USE_REDUCTIONS, pr.PR_MODE_ASYNC, pr.PR_MODE_ASYNC | pr.PR_USE_REDUCTIONS, pr.PR_MODE_NOSYNC,
-         pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS, pr.PR_PERFORATE, pr.PR_NORM_LINF, pr.PR_MODE_PHASED,
+         pr.PR_MODE_NOSYNC | pr.PR_USE_REDUCTIONS, pr.PR_PERFORATE, pr.PR_PERFORATE | pr.PR_MODE_ASYNC,
+         pr.PR_PERFORATE | pr.PR_MODE_NOSYNC, pr.PR_NORM_LINF, pr.PR_MODE_PHASED,
          pr.PR_MODE_PHASED | pr.PR_USE_REDUCTIONS]
 
 env_sets = [{}, {"PRGPU_SEG_BITS": "5"}, {"PRGPU_SPAN": "1", "PRGPU_PHASES": "16"}, {"PRGPU_PHASES": "3"}]
