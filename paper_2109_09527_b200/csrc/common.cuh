@@ -169,6 +169,12 @@ __device__ __forceinline__ double ld_gather_f64(const double* ptr, uint64_t pol)
     return r;
 }
 
+__device__ __forceinline__ int32_t ld_hint_s32(const int32_t* ptr, uint64_t pol) {
+    int32_t r;
+    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+    return r;
+}
+
 // Two-tier gather: hot contribs (small index = high out-degree) stay in L1
 // (evict_last), cold ones bypass it (no_allocate) so they cannot evict the
 // hot lines.  One predicated load each, branch-free.

@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(SR_NT) k_src_runs(const uint64_t* __restrict__
 // Key i is kept iff it is not the sentinel and differs from key i-1.
 // Kept key i lands at p = its rank among kept keys: col[p] = src; and when it
 // starts row d = dst (dst of key i-1 differs, or i == 0), row_ptr[d'+1 .. d]
-// = p for the previous dst d' (rows in between have in-degree 0).  Reduce-
+// = p for the previous dst d' (rows in between have in-degree 0); the rows
+// after the last real key are closed by k_close_tail.  Reduce-
 // then-scan with UQ_G fixed chunks (deterministic); tiles are staged through
 // shared memory so global loads and the col stores are coalesced.
 constexpr int UQ_NT = 256;
@@ -177,9 +178,8 @@ __global__ void __launch_bounds__(UQ_NT) k_uniq_count(const uint64_t* __restrict
 }
 
 __global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict__ k, int64_t n, int64_t per_cta,
-                                                     uint64_t sentinel, int b, int64_t nv,
-                                                     const int64_t* __restrict__ partial,
-                                                     const int64_t* __restrict__ total, int32_t* __restrict__ col,
+                                                     uint64_t sentinel, int b,
+                                                     const int64_t* __restrict__ partial, int32_t* __restrict__ col,
                                                      int64_t* __restrict__ row_ptr, int32_t* __restrict__ od_dup) {
     // striped: in stripe j, thread t handles tile item j*UQ_NT + t (conflict-
     // free shared-memory reads, adjacent lanes write adjacent row_ptr
@@ -195,7 +195,6 @@ __global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict_
     const int64_t cb = (int64_t)blockIdx.x * per_cta;
     const int64_t ce = min(n, cb + per_cta);
     int64_t base = partial[blockIdx.x];
-    const int64_t E = *total;
     for (int64_t tb = cb; tb < ce; tb += UQ_TILE) {
         const int tn = (int)min((int64_t)UQ_TILE, ce - tb);
         for (int i = threadIdx.x; i < tn; i += UQ_NT) sk[i + 1] = k[tb + i];
@@ -256,18 +255,34 @@ __global__ void __launch_bounds__(UQ_NT) k_uniq_emit(const uint64_t* __restrict_
                 const int64_t p = base + q;
                 for (int64_t r = dp + 1; r <= d; ++r) row_ptr[r] = p;   // first edge of row d
             }
-            if (i < tn) {  // the last real key (kept or a duplicate) closes every later row
-                const uint64_t key = sk[i + 1];
-                if (key != sentinel &&
-                    (tb + i + 1 == n || (i + 1 < tn ? sk[i + 2] : k[tb + i + 1]) == sentinel))
-                    for (int64_t r = (int64_t)(key >> b) + 1; r <= nv; ++r) row_ptr[r] = E;
-            }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < tile_tot; i += UQ_NT) col[base + i] = so[i];
         base += tile_tot;
         __syncthreads();
     }
+}
+
+// Rows after the last real key's dst (the sentinels sort last) start at E:
+// row_ptr[d_last + 1 .. nv] = E.  The last real key is found by a binary
+// search for the first sentinel (no rows to close when every key is one).
+__global__ void k_close_tail(const uint64_t* __restrict__ k, int64_t n, uint64_t sentinel, int b, int64_t nv,
+                             const int64_t* __restrict__ total, int64_t* __restrict__ row_ptr) {
+    __shared__ int64_t first_row;
+    if (threadIdx.x == 0) {
+        int64_t lo = 0, hi = n;  // first index with k[i] == sentinel (keys sorted ascending)
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (k[mid] == sentinel) hi = mid;
+            else lo = mid + 1;
+        }
+        first_row = lo > 0 ? (int64_t)(k[lo - 1] >> b) + 1 : nv + 1;
+    }
+    __syncthreads();
+    const int64_t E = *total;
+    for (int64_t r = first_row + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= nv;
+         r += (int64_t)gridDim.x * blockDim.x)
+        row_ptr[r] = E;
 }
 
 int read_count(Ctx& ctx, const int64_t* dev, int64_t* host) {
@@ -359,8 +374,10 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
         PR_TRY(dalloc(&part, (size_t)G, s));
         PR_LAUNCH(ctx, k_uniq_count, (unsigned)G, UQ_NT, 0, sorted, mk, per, sentinel, part);
         PR_LAUNCH(ctx, (k_scan_partials<int64_t>), 1, 1024, 0, part, G, scratch);
-        PR_LAUNCH(ctx, k_uniq_emit, (unsigned)G, UQ_NT, 0, sorted, mk, per, sentinel, b, n, (const int64_t*)part,
-                  (const int64_t*)scratch, g->col, g->row_ptr, od_runs ? g->outdeg : nullptr);
+        PR_LAUNCH(ctx, k_uniq_emit, (unsigned)G, UQ_NT, 0, sorted, mk, per, sentinel, b, (const int64_t*)part,
+                  g->col, g->row_ptr, od_runs ? g->outdeg : nullptr);
+        PR_LAUNCH(ctx, k_close_tail, grid_for(ctx, n, 256), 256, 0, sorted, mk, sentinel, b, n,
+                  (const int64_t*)scratch, g->row_ptr);
         dfree(part, s);
         dfree(keys, s);
         dfree(keys_alt, s);
@@ -420,10 +437,35 @@ __global__ void k_set_cidx(const uint64_t* __restrict__ sorted, int64_t cnt, uin
         cidx[sorted[i] & vmask] = (int32_t)i;
 }
 
+// col (streamed once: evict-first loads and stores) through the cidx table
+// (random: kept in L2 with evict_last; 4 bytes x n, beside the 8E-byte stream)
 __global__ void k_map_col(const int32_t* __restrict__ col, int64_t E, const int32_t* __restrict__ cidx,
                           int32_t* __restrict__ out) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
-        out[e] = cidx[col[e]];
+    const uint64_t pol = policy_evict_last();
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t E4 = E >> 2;  // col and out are 16-byte aligned (pool allocations)
+    const int4* __restrict__ c4 = reinterpret_cast<const int4*>(col);
+    int4* __restrict__ o4 = reinterpret_cast<int4*>(out);
+    for (int64_t i = t0; i < E4; i += 2 * T) {
+        int4 a = __ldcs(c4 + i), b = make_int4(0, 0, 0, 0);
+        const bool two = i + T < E4;
+        if (two) b = __ldcs(c4 + i + T);
+        int4 ra, rb;
+        ra.x = ld_hint_s32(cidx + a.x, pol);
+        ra.y = ld_hint_s32(cidx + a.y, pol);
+        ra.z = ld_hint_s32(cidx + a.z, pol);
+        ra.w = ld_hint_s32(cidx + a.w, pol);
+        if (two) {
+            rb.x = ld_hint_s32(cidx + b.x, pol);
+            rb.y = ld_hint_s32(cidx + b.y, pol);
+            rb.z = ld_hint_s32(cidx + b.z, pol);
+            rb.w = ld_hint_s32(cidx + b.w, pol);
+        }
+        __stcs(o4 + i, ra);
+        if (two) __stcs(o4 + i + T, rb);
+    }
+    for (int64_t e = (E4 << 2) + t0; e < E; e += T) out[e] = cidx[col[e]];
 }
 
 struct ZeroInGet {

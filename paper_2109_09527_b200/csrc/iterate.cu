@@ -291,6 +291,22 @@ constexpr int FIN_U = 4;
 #endif
 constexpr int FIN_PAIRS = PRGPU_FIN_PAIRS;  // row pairs per thread and iteration of the 16-byte path
 
+// One new contrib: this buffer (and every peer's), or one multicast store.
+template <bool REMOTE>
+__device__ __forceinline__ void fin_store_y(const FinArgs& f, double* y, int32_t slot, double yv) {
+    if (!REMOTE) {
+        y[slot] = yv;
+    } else if (f.mc_y) {
+        st_mc_f64(f.mc_y + slot, yv);
+    } else {
+        y[slot] = yv;
+        for (int q = 0; q < f.npeer; ++q) f.peer_y[q][slot] = yv;
+    }
+}
+
+// REMOTE: the sharded sweep with peer buffers or a multicast team (every
+// contrib also stored remotely); the plain instance keeps fewer registers.
+template <bool REMOTE>
 __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     __shared__ double red[64];
     __shared__ int flag;
@@ -305,7 +321,7 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
     double* __restrict__ y = f.y_out;
     uint32_t nfrozen = 0;
     int64_t rlo = f.row0;  // rows [rlo, nrows) left to the general loop below
-    if (f.vec && !f.fz && !f.mc_y && f.npeer == 0 && (f.row0 & 1) == 0) {
+    if (f.vec && !f.fz && (f.row0 & 1) == 0) {
         // two consecutive rows per 16-byte load of S, x and (outdeg, slot)
         const double2* __restrict__ S2 = reinterpret_cast<const double2*>(sums);
         double2* __restrict__ X2 = reinterpret_cast<double2*>(xr);
@@ -331,8 +347,8 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
                     const double xa = __dadd_rn(f.c, __dmul_rn(f.d, sv[u].x));
                     const double xb = __dadd_rn(f.c, __dmul_rn(f.d, sv[u].y));
                     X2[p] = make_double2(xa, xb);
-                    if (iv[u].x > 0) y[iv[u].y] = xa / (double)iv[u].x;
-                    if (iv[u].z > 0) y[iv[u].w] = xb / (double)iv[u].z;
+                    if (iv[u].x > 0) fin_store_y<REMOTE>(f, y, iv[u].y, xa / (double)iv[u].x);
+                    if (iv[u].z > 0) fin_store_y<REMOTE>(f, y, iv[u].w, xb / (double)iv[u].z);
                     const double da = fabs(xa - xv[u].x), db = fabs(xb - xv[u].y);
                     l1 += da;
                     l1 += db;
@@ -364,14 +380,7 @@ __global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
                 const double xn = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
                 xr[r] = xn;
                 const double yv = inf[u].x > 0 ? xn / (double)inf[u].x : 0.0;
-                if (inf[u].x > 0) {
-                    if (f.mc_y) {
-                        st_mc_f64(f.mc_y + inf[u].y, yv);
-                    } else {
-                        y[inf[u].y] = yv;
-                        for (int q = 0; q < f.npeer; ++q) f.peer_y[q][inf[u].y] = yv;
-                    }
-                }
+                if (inf[u].x > 0) fin_store_y<REMOTE>(f, y, inf[u].y, yv);
                 const double dl = fabs(xn - xo[u]);
                 l1 += dl;
                 linf = fmax(linf, dl);
@@ -1158,7 +1167,7 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
                 if (it == 0 && zgrid > 0 && k == K - 1)
                     PR_LAUNCH(ctx, k_zero, (unsigned)zgrid, GT_NT, 0, (const int32_t*)g->zlist, nz, c, x, y_out,
                               (const int32_t*)g->outdeg, (const int32_t*)g->cidx, zero_partial);
-                PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid_k[k], GT_NT, 0, f, ia);
+                PR_LAUNCH_PDL(ctx, k_finalize<false>, (unsigned)fgrid_k[k], GT_NT, 0, f, ia);
             }
             PR_TRY(tmr.mark(it, 1, s));
         } else if (async) {
@@ -1173,14 +1182,14 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
             if (v.nspans > 0 || nm > 0)
                 PR_LAUNCH(ctx, k_stream_async, gc.grid, gc.nt, gc.smem, ip, stream_args(v), ma, ia);
             else  // nothing to gather: the zero-in partials still need their reduction
-                PR_LAUNCH_PDL(ctx, k_finalize, 1, GT_NT, 0, fa, ia);
+                PR_LAUNCH_PDL(ctx, k_finalize<false>, 1, GT_NT, 0, fa, ia);
             PR_TRY(tmr.mark(it, 1, s));
         } else {
             PR_TRY(launch_gather(ctx, g, v, y_in, gc));
             PR_TRY(tmr.mark(it, 1, s));
             FinArgs f = fa;
             f.y_out = y_out;
-            PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
+            PR_LAUNCH_PDL(ctx, k_finalize<false>, (unsigned)fgrid, GT_NT, 0, f, ia);
             if (it == 0 && nz > 0)
                 PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8),
                           256, 0, (const int32_t*)g->zlist, nz, c, (double*)y_in, (const int32_t*)g->outdeg,
@@ -1339,6 +1348,7 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
     ia_first.zero_ctas = zgrid;
     double* zero_partial = g->cta_partial + 2 * fgrid;
     const FinArgs fa{v.sums, v.nrows, v.rinfo, g->xr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, nullptr, c, d};
+    const int fin_vec = env_int("PRGPU_FIN_VEC", 1);
 
     SweepTimer tmr;
     tmr.on = timing;
@@ -1366,7 +1376,11 @@ int run_sharded(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mo
         f.peer_y = pout;
         f.npeer = peers ? world - 1 : 0;
         f.mc_y = mc_out;
-        PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
+        f.vec = fin_vec;  // as in the unsharded sync sweep: world 1 reproduces its Delta bit for bit
+        if (peers || mcast)
+            PR_LAUNCH_PDL(ctx, k_finalize<true>, (unsigned)fgrid, GT_NT, 0, f, ia);
+        else
+            PR_LAUNCH_PDL(ctx, k_finalize<false>, (unsigned)fgrid, GT_NT, 0, f, ia);
         PR_TRY(tmr.mark(it, 2, s));
         // multicast: the in-degree-0 contribs go to every rank's sweep-1 output
         // (k_zero above) and, in sweep 2, to its other buffer (their sweep-2
@@ -1697,7 +1711,7 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
                 PR_LAUNCH(ctx, k_stream_async, gc.grid, gc.nt, gc.smem, inplace_policy(), stream_args(A.v), ma0, ia);
             } else {  // nothing left to gather: the reduction alone (delta 0)
                 FinArgs f{A.v.sums, 0, A.v.rinfo, A.xr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, g->y[0], c, d};
-                PR_LAUNCH_PDL(ctx, k_finalize, 1, GT_NT, 0, f, ia);
+                PR_LAUNCH_PDL(ctx, k_finalize<false>, 1, GT_NT, 0, f, ia);
             }
             return PR_OK;
         }
@@ -1713,7 +1727,7 @@ static int run_perforated(pr_graph* g, double d, double tau, int32_t max_iter, u
         f.tau_f = tau_f;
         f.y_other = (double*)y_in;
         f.nfz = cnt;
-        PR_LAUNCH_PDL(ctx, k_finalize, (unsigned)fgrid, GT_NT, 0, f, ia);
+        PR_LAUNCH_PDL(ctx, k_finalize<false>, (unsigned)fgrid, GT_NT, 0, f, ia);
         if (it == 0 && nz > 0)
             PR_LAUNCH(ctx, k_zero_y, (unsigned)std::min<int64_t>((nz + 255) / 256, (int64_t)ctx.num_sms * 8), 256, 0,
                       (const int32_t*)g->zlist, nz, c, (double*)y_in, (const int32_t*)g->outdeg,

@@ -150,18 +150,19 @@ int device_scan(Ctx& ctx, int64_t n, Get get, Emit emit, T* total_dev) {
 // ------------------------------------------------------------ radix sort --
 // LSD radix sort, 8-bit digits, "reduce-then-scan" per pass with a fixed
 // number G of CTAs, each owning a contiguous chunk of the array (stable and
-// deterministic, no look-back).  Tiles of RS_TILE = 4096 keys per CTA step at
-// 2 CTAs/SM (measured best against 3072 / 6144 / 8192) keep the block
-// barriers per key low and each digit's run in a tile ~16 keys long, so the
-// write-out is coalesced.
+// deterministic, no look-back).  Tiles of RS_TILE = 3072 keys (256 threads x
+// 12) per CTA step at 3 CTAs/SM keep the block barriers per key low and each
+// digit's run in a tile ~12 keys long, so the write-out is coalesced
+// (R-MAT-24 create: 15.7 ms against 16.1 with 512 x 8 at 2 CTAs/SM, 17.0 with
+// 256 x 8 at 4, 16.7 with 384 x 8 at 2).
 #ifndef PRGPU_RS_NT
-#define PRGPU_RS_NT 512
+#define PRGPU_RS_NT 256
 #endif
 #ifndef PRGPU_RS_ROUNDS
-#define PRGPU_RS_ROUNDS 8
+#define PRGPU_RS_ROUNDS 12
 #endif
 #ifndef PRGPU_RS_MINB
-#define PRGPU_RS_MINB 2
+#define PRGPU_RS_MINB 3
 #endif
 constexpr int RS_NT = PRGPU_RS_NT;
 constexpr int RS_WARPS = RS_NT / 32;
@@ -221,10 +222,30 @@ static __global__ void __launch_bounds__(256) k_rs_dbase(const uint32_t* __restr
     if (threadIdx.x < RS_BINS) dbase[threadIdx.x] = ex;
 }
 
+// Lanes of the warp whose digit equals this lane's (bits 0..RS_BITS-1 of d):
+// one ballot per bit, each folded in with one LOP3 (peers &= ~(ballot ^ own
+// bit broadcast)) -- written in PTX so that ptxas emits 4 instructions per bit
+// (the C++ form compiled to a second, negated ballot per bit).
+__device__ __forceinline__ uint32_t rs_match_digit(uint32_t d, uint32_t peers) {
+#pragma unroll
+    for (int bit = 0; bit < RS_BITS; ++bit) {
+        uint32_t bb, m;
+        asm("{\n\t.reg .pred p;\n\t"
+            "and.b32 %1, %2, %3;\n\t"
+            "setp.ne.u32 p, %1, 0;\n\t"
+            "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+            "selp.b32 %1, -1, 0, p;\n\t}"
+            : "=r"(bb), "=&r"(m)
+            : "r"(d), "r"(1u << bit));
+        peers &= ~(bb ^ m);
+    }
+    return peers;
+}
+
 template <class K, bool HAS_V>
 struct RsSmem {
-    uint32_t base[RS_BINS];      // global start of each digit for the current tile
-    uint32_t toff[RS_BINS + 1];  // tile-local start of each digit
+    uint32_t base[RS_BINS];      // global start of each digit for the next tile
+    uint32_t adj[RS_BINS];       // global index of tile position i (digit d) = adj[d] + i
     uint32_t wc[RS_WARPS][RS_BINS + 1];
     uint32_t sw[33];
     alignas(16) K sk[RS_TILE];
@@ -240,7 +261,7 @@ struct RsSmem {
 // memory, then a coalesced write-out (consecutive threads write consecutive
 // addresses of one digit's run).
 template <class K, bool HAS_V>
-__global__ void __launch_bounds__(RS_NT, PRGPU_RS_MINB) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(RS_NT, HAS_V ? 2 : PRGPU_RS_MINB) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       int64_t n, int64_t per_cta, int shift, uint32_t dmask,
                                                       const uint32_t* __restrict__ offs, int64_t G,
@@ -276,16 +297,18 @@ __global__ void __launch_bounds__(RS_NT, PRGPU_RS_MINB) k_rs_scatter(const K* __
         fence_mbar_init();
         if (b < e) stage(b);
     }
+    for (int i = threadIdx.x; i < RS_WARPS * (RS_BINS + 1); i += RS_NT) (&sm.wc[0][0])[i] = 0;
     __syncthreads();
+    // Barriers per tile: staging consumed / ranked / (scan) / offsets ready /
+    // local sort done.  The write-out of tile t overlaps the next tile's
+    // staging wait; the wc counters are cleared during the write-out.
     uint32_t phase = 0;
     for (int64_t tb = b; tb < e; tb += RS_TILE) {
         const int tn = (int)min((int64_t)RS_TILE, e - tb);
-        for (int i = threadIdx.x; i < RS_WARPS * (RS_BINS + 1); i += RS_NT) (&sm.wc[0][0])[i] = 0;
         K k[RS_ROUNDS];
         uint32_t v[RS_ROUNDS];
         uint32_t dg[RS_ROUNDS];
         uint32_t pos[RS_ROUNDS];
-        const int64_t s = tb + (int64_t)warp * (32 * RS_ROUNDS);
         mbar_wait(&sm.bar, phase);
         phase ^= 1u;
 #pragma unroll
@@ -295,25 +318,24 @@ __global__ void __launch_bounds__(RS_NT, PRGPU_RS_MINB) k_rs_scatter(const K* __
             k[r] = valid ? sm.stk[li] : K(0);
             if (HAS_V) v[r] = valid ? sm.stv[li] : 0u;
         }
-        __syncthreads();  // staging buffer consumed (and wc cleared): prefetch the next tile
+        __syncthreads();  // staging consumed, wc cleared, previous write-out done: prefetch the next tile
         if (threadIdx.x == 0 && tb + RS_TILE < e) {
             fence_proxy_async_smem();
             stage(tb + RS_TILE);
         }
+        const int wl = warp * (32 * RS_ROUNDS) + lane;  // tile-local index of round 0
 #pragma unroll
         for (int r = 0; r < RS_ROUNDS; ++r) {
-            const bool valid = s + r * 32 + lane < e;
+            const bool valid = wl + r * 32 < tn;
             const uint32_t d = valid ? ((uint32_t)(k[r] >> shift) & dmask) : RS_BINS;
             dg[r] = d;
             // lanes with the same digit: 8 ballots (MATCH.ANY measured 1.6x slower here)
-            uint32_t peers = __ballot_sync(0xffffffffu, valid);
-            if (!valid) peers = ~peers;
-#pragma unroll
-            for (int bit = 0; bit < RS_BITS; ++bit) {
-                const bool on = (d >> bit) & 1u;
-                const uint32_t bb = __ballot_sync(0xffffffffu, on);
-                peers &= on ? bb : ~bb;
+            uint32_t peers = 0xffffffffu;
+            if (tn < RS_TILE) {  // ragged last tile: valid lanes never match invalid ones
+                peers = __ballot_sync(0xffffffffu, valid);
+                if (!valid) peers = ~peers;
             }
+            peers = rs_match_digit(d, peers);
             const uint32_t rank = __popc(peers & lt);
             pos[r] = sm.wc[warp][d] + rank;
             __syncwarp();
@@ -331,7 +353,8 @@ __global__ void __launch_bounds__(RS_NT, PRGPU_RS_MINB) k_rs_scatter(const K* __
             uint32_t tot;
             const uint32_t off = block_exclusive_sum(cnt, &tot, sm.sw);
             if (d < RS_BINS) {
-                sm.toff[d] = off;
+                sm.adj[d] = sm.base[d] - off;
+                sm.base[d] += cnt;  // advance past this tile (only thread d touches base[d])
                 uint32_t run = off;
 #pragma unroll
                 for (int w = 0; w < RS_WARPS; ++w) {
@@ -340,7 +363,6 @@ __global__ void __launch_bounds__(RS_NT, PRGPU_RS_MINB) k_rs_scatter(const K* __
                     run += c;
                 }
             }
-            if (d == 0) sm.toff[RS_BINS] = (uint32_t)tn;
         }
         __syncthreads();
 #pragma unroll
@@ -352,19 +374,24 @@ __global__ void __launch_bounds__(RS_NT, PRGPU_RS_MINB) k_rs_scatter(const K* __
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < tn; i += RS_NT) {
-            const K key = sm.sk[i];
-            const uint32_t d = (uint32_t)(key >> shift) & dmask;
-            const int64_t dst = (int64_t)sm.base[d] + (i - (int64_t)sm.toff[d]);
-            kout[dst] = key;
-            if (HAS_V) vout[dst] = sm.sv[i];
+        for (int i = threadIdx.x; i < RS_WARPS * (RS_BINS + 1); i += RS_NT) (&sm.wc[0][0])[i] = 0;
+        if (tn == RS_TILE) {
+#pragma unroll
+            for (int r = 0; r < RS_ROUNDS; ++r) {
+                const int i = threadIdx.x + r * RS_NT;
+                const K key = sm.sk[i];
+                const uint32_t dst = sm.adj[(uint32_t)(key >> shift) & dmask] + (uint32_t)i;
+                kout[dst] = key;
+                if (HAS_V) vout[dst] = sm.sv[i];
+            }
+        } else {
+            for (int i = threadIdx.x; i < tn; i += RS_NT) {
+                const K key = sm.sk[i];
+                const uint32_t dst = sm.adj[(uint32_t)(key >> shift) & dmask] + (uint32_t)i;
+                kout[dst] = key;
+                if (HAS_V) vout[dst] = sm.sv[i];
+            }
         }
-        __syncthreads();
-        if (threadIdx.x < RS_BINS) {  // advance the digit bases past this tile
-            const int d = threadIdx.x;
-            sm.base[d] += sm.toff[d + 1] - sm.toff[d];
-        }
-        __syncthreads();
     }
 }
 
