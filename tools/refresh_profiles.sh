@@ -11,3 +11,4 @@ timeout 1500 python tools/all_configs.py > gpurun_out/all_configs.json 2> gpurun
 timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; tail -c 300 gpurun_out/bench_reference.json
 timeout 600 python tools/shard_scaling.py 4 1 2 4 8 local > gpurun_out/shard_scaling_local.json 2> gpurun_out/shard_scaling_local.err
 PRGPU_PROFILE=2 timeout 300 python tools/profile_create_sharded.py 4 8 0 > gpurun_out/create_sharded_profile.log 2>&1
+PRGPU_PROFILE=2 timeout 300 python tools/time_create.py 4 2 > gpurun_out/create_profile.log 2>&1
