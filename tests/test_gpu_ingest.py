@@ -1,0 +1,154 @@
+"""GPU parity of the counting-form ingest (csr_count.cu) against the oracle's
+CSR (SPEC S:69-77 build_csr; §5.2) and against the sort-based
+ingest (PRGPU_INGEST=radix), bit for bit.
+
+The counting form sorts every destination bucket by one of four engines
+chosen by the bucket length L (thread <= 16, warp <= 512, CTA of 8 warps
+<= 4096, CTA of 32 warps <= 16384, device radix beyond); the graphs below put
+rows at and around every class boundary, with duplicates and self-loops in
+every class, sources in ascending, descending and random order, and rows
+whose sources are all one value.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import graphgen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+BOUNDARY_LENGTHS = [0, 1, 2, 3, 4, 5, 8, 9, 15, 16, 17, 31, 32, 33, 63, 64, 65, 128, 129, 255, 256, 257,
+                    511, 512, 513, 1000, 1024, 1025, 2048, 4095, 4096, 4097, 8192, 16383, 16384, 16385,
+                    20000, 40000]
+
+
+@pytest.fixture(scope="module")
+def pr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_09527_b200 as m
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+
+
+def csr_of(pr, n, src, dst, ingest=None):
+    old = os.environ.get("PRGPU_INGEST")
+    if ingest:
+        os.environ["PRGPU_INGEST"] = ingest
+    else:
+        os.environ.pop("PRGPU_INGEST", None)
+    try:
+        with pr.Graph(n, dev(src), dev(dst)) as g:
+            E = g.info()["E"]
+            rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+            col = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
+            od = torch.empty(n, dtype=torch.int32, device="cuda")
+            pr.pr_get_csr(g.handle, rp, col, od)
+            return E, rp.cpu().numpy(), col[:E].cpu().numpy(), od.cpu().numpy()
+    finally:
+        if old is None:
+            os.environ.pop("PRGPU_INGEST", None)
+        else:
+            os.environ["PRGPU_INGEST"] = old
+
+
+def check(pr, n, src, dst, radix_too=True):
+    ref = oracle.build_csr(n, src, dst)
+    E, rp, col, od = csr_of(pr, n, src, dst)
+    assert E == ref.E
+    assert np.array_equal(rp, ref.row_ptr)
+    assert np.array_equal(col, ref.col_idx)
+    assert np.array_equal(od, ref.outdeg)
+    if radix_too:
+        E2, rp2, col2, od2 = csr_of(pr, n, src, dst, "radix")
+        assert E2 == E and np.array_equal(rp2, rp) and np.array_equal(col2, col) and np.array_equal(od2, od)
+
+
+def class_graph(seed, n, lengths, order, dup_frac):
+    """Row v = 10 * i + 7 gets lengths[i] raw in-edges: sources in the given
+    order, a fraction dup_frac of them repeats of earlier ones, one self-loop
+    per row of length >= 3."""
+    rng = np.random.default_rng(seed)
+    src, dst = [], []
+    for i, L in enumerate(lengths):
+        v = 10 * i + 7
+        if L == 0:
+            continue
+        s = rng.integers(0, n, L)
+        k = int(L * dup_frac)
+        if k:
+            s[L - k:] = s[rng.integers(0, max(L - k, 1), k)]
+        if order == "asc":
+            s = np.sort(s)
+        elif order == "desc":
+            s = np.sort(s)[::-1]
+        if L >= 3:
+            s[L // 2] = v
+        src.append(s)
+        dst.append(np.full(L, v))
+    src = np.concatenate(src).astype(np.int32)
+    dst = np.concatenate(dst).astype(np.int32)
+    p = rng.permutation(len(src))  # edge order in the input is irrelevant
+    return src[p], dst[p]
+
+
+@pytest.mark.parametrize("order", ["random", "asc", "desc"])
+@pytest.mark.parametrize("dup_frac", [0.0, 0.3])
+def test_row_classes(pr, order, dup_frac):
+    n = 100_000
+    src, dst = class_graph(11, n, BOUNDARY_LENGTHS, order, dup_frac)
+    check(pr, n, src, dst)
+
+
+def test_single_source_rows(pr):
+    """Rows whose sources are one value (all but one entry duplicates), in
+    every class; and sources drawn from a handful of values."""
+    n = 50_000
+    src, dst = [], []
+    for i, L in enumerate(BOUNDARY_LENGTHS):
+        v = 10 * i + 3
+        src.append(np.full(L, (v * 7 + 1) % n))
+        dst.append(np.full(L, v))
+        src.append(np.arange(L) % 5 + 11)
+        dst.append(np.full(L, v + 1))
+    src = np.concatenate(src).astype(np.int32)
+    dst = np.concatenate(dst).astype(np.int32)
+    check(pr, n, src, dst)
+
+
+def test_many_hub_rows(pr):
+    """More rows past the CTA limit than one radix digit of row ranks (the
+    device-wide hub sort then spans two digits of ranks)."""
+    n = 4_000
+    rng = np.random.default_rng(5)
+    rows = 300
+    L = 16_400
+    dst = np.repeat(np.arange(rows, dtype=np.int32) * 13 % n, L)
+    src = rng.integers(0, n, rows * L).astype(np.int32)
+    check(pr, n, src, dst, radix_too=False)
+
+
+def test_self_loops_only_and_tiny(pr):
+    n = 10
+    s = np.arange(10, dtype=np.int32)
+    check(pr, n, s, s.copy())
+    check(pr, 2, np.array([0, 1, 0], np.int32), np.array([1, 0, 1], np.int32))
+
+
+def test_invalid_ids_counting_path(pr):
+    for s, t in (([0, 1, 7], [1, 2, 0]), ([0, 1, 2], [1, -3, 0]), ([0, 1, 2], [1, 2, 1 << 30])):
+        with pytest.raises(pr.PRError) as e:
+            pr.Graph(5, dev(np.array(s)), dev(np.array(t)))
+        assert e.value.code == pr.PR_EINVAL
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_configs_match_radix_path(pr, cfg):
+    g = graphgen.make_config(cfg)
+    check(pr, g.n, g.src, g.dst)
