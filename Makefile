@@ -3,7 +3,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -fvisibility=hidden --expt-relaxed-constexpr
 CSRC := paper_2109_09527_b200/csrc
-SRCS := $(CSRC)/api.cu $(CSRC)/ingest.cu $(CSRC)/preprocess.cu $(CSRC)/iterate.cu $(CSRC)/blocked.cu $(CSRC)/shard.cu $(CSRC)/multicast.cu $(CSRC)/csr_count.cu
+SRCS := $(CSRC)/api.cu $(CSRC)/ingest.cu $(CSRC)/preprocess.cu $(CSRC)/iterate.cu $(CSRC)/blocked.cu $(CSRC)/shard.cu $(CSRC)/multicast.cu
 HDRS := $(wildcard $(CSRC)/*.cuh $(CSRC)/*.h) include/prgpu.h
 LIB := paper_2109_09527_b200/libprgpu.so
 OBJS := $(SRCS:.cu=.o)

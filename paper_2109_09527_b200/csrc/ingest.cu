@@ -301,7 +301,6 @@ static unsigned grid_for(const Ctx& ctx, int64_t work, int nt) {
 
 int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank, int world) {
     const int64_t n = g->n, m = g->m_raw;
-    if (world == 1 && ingest_count_applies(n, m)) return ingest_count(g, src, dst, ctx);
     const int b = bits_for((uint64_t)(n - 1));
     cudaStream_t s = ctx.stream;
 

@@ -178,10 +178,6 @@ struct pr_graph {
 
 namespace prgpu {
 int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank = 0, int world = 1);
-// counting form of the ingest (csr_count.cu), used by ingest() for a
-// single-rank create unless PRGPU_INGEST=radix
-bool ingest_count_applies(int64_t n, int64_t m);
-int ingest_count(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx);
 int build_relabel(pr_graph* g, Ctx& ctx);
 int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx);
 int build_spans(View& v, Ctx& ctx, int64_t span_steps);
