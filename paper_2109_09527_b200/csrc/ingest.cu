@@ -407,9 +407,10 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
 
 // ---------------------------------------------------------------- relabel --
 // The gather reads contrib values y(u) = x(u)/outdeg(u) only for sources u
-// (outdeg > 0).  They are stored compactly, ordered by (outdeg desc, id asc),
-// so the hottest contribs share sectors and the vector is ~44 % of n on R-MAT
-// (DESIGN.md "Data layout").  cidx[v] = position, or -1 for dangling v.
+// (outdeg > 0).  They are stored compactly (~44 % of n on R-MAT; DESIGN.md
+// "Data layout"): the K hottest by (outdeg desc, id asc), so the hottest
+// contribs share sectors and fit the gather's on-chip tiers, then the rest in
+// row order (ColdGet below).  cidx[v] = position, or -1 for dangling v.
 struct NdGet {
     const int32_t* od;
     __device__ int64_t operator()(int64_t v) const { return od[v] > 0 ? 1 : 0; }
@@ -499,6 +500,27 @@ struct NonZeroEmit {
     }
 };
 
+// Slots [K, n_contrib) in row order (PRGPU_DEG_SLOTS): the sources that have
+// rows (in-degree > 0) by increasing id, then those of in-degree 0 -- so the
+// contrib stores of consecutive rows in K-FINALIZE land in consecutive slots.
+struct ColdGet {
+    const int32_t* cidx;
+    const int64_t* rp;
+    int64_t K;
+    int rows;  // 1: sources with rows, 0: sources of in-degree 0
+    __device__ int64_t operator()(int64_t v) const {
+        return (cidx[v] >= K && (int)(rp[v + 1] > rp[v]) == rows) ? 1 : 0;
+    }
+};
+struct ColdEmit {
+    int32_t* cidx;
+    int64_t K;
+    const int64_t* base;  // slots already taken by the first group (device), or null
+    __device__ void operator()(int64_t v, int64_t pos, int64_t f) const {
+        if (f) cidx[v] = (int32_t)(K + (base ? *base : 0) + pos);
+    }
+};
+
 int build_relabel(pr_graph* g, Ctx& ctx) {
     cudaStream_t s = ctx.stream;
     const int64_t n = g->n;
@@ -539,6 +561,22 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
     if (cnt > 0)
         PR_LAUNCH(ctx, k_set_cidx, grid_for(ctx, cnt, 256), 256, 0, sorted, cnt,
                   b ? ((1ull << b) - 1) : 0ull, g->cidx);
+    // only the K = 2^20 hottest keep the degree order (the gather's shared-
+    // memory and L1 tiers and the sharded hot copies use slots < 32768; the
+    // rest of the first 2^20 keeps the gather's L2 locality): R-MAT-24 reduced
+    // K-FINALIZE 0.091 -> 0.076 ms, K-GATHER unchanged (K = 32K / 128K / 512K
+    // / 1M / 2M / 4M / all: step 105.65 / 105.86 / 105.37 / 105.34 / 105.54 /
+    // 106.04 / 106.63 ms, profiles/r2/ab_degslots.txt).  PRGPU_DEG_SLOTS=k
+    // sets K (k <= 0: every slot in degree order).
+    const char* ds = getenv("PRGPU_DEG_SLOTS");
+    const int64_t kds = ds ? atoll(ds) : (int64_t)1 << 20;
+    const int64_t K = kds <= 0 ? cnt : std::max<int64_t>(kds, 32768);
+    if (by_degree && K < cnt) {
+        PR_TRY((device_scan<int64_t>(ctx, n, ColdGet{g->cidx, g->row_ptr, K, 1}, ColdEmit{g->cidx, K, nullptr},
+                                     scratch + 1)));
+        PR_TRY((device_scan<int64_t>(ctx, n, ColdGet{g->cidx, g->row_ptr, K, 0},
+                                     ColdEmit{g->cidx, K, (const int64_t*)(scratch + 1)}, (int64_t*)nullptr)));
+    }
     // zero in-degree vertices (written once, in sweep 1) and the plain view:
     // the rows of in-degree > 0 (identity view when there are no empty rows)
     View& v = g->plain;
