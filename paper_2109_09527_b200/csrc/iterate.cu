@@ -35,10 +35,11 @@ struct StreamPolicy {
         if (HOT && u < hot_n) return hot[u];
         return ld_gather_tiered_f64(y_in + u, u < SE_L1_TIER, pol_last);
     }
-    __device__ __forceinline__ void emit(int64_t r, double s) const { sums[r] = s; }
+    __device__ __forceinline__ void st_sum(int64_t r, double s) const { sums[r] = s; }
+    __device__ __forceinline__ void emit(int64_t r, double s) const { st_sum(r, s); }
     __device__ __forceinline__ void prep(int64_t, uint32_t) {}
-    __device__ __forceinline__ void emit_at(int, int64_t r, double s) const { sums[r] = s; }
-    __device__ __forceinline__ void emit_first(int64_t r, double s) const { sums[r] = s; }
+    __device__ __forceinline__ void emit_at(int, int64_t r, double s) const { st_sum(r, s); }
+    __device__ __forceinline__ void emit_first(int64_t r, double s) const { st_sum(r, s); }
 };
 
 __device__ __forceinline__ void red_add_f64(double* p, double v) {
@@ -285,7 +286,16 @@ struct FinArgs {
 // loads are all issued before any store.  Every access is coalesced except the
 // contrib store y[slot]; x is kept in row / member order (xr, xm) during the
 // sweeps and written back to vertex order once, by k_unpermute.
-constexpr int FIN_U = 4;
+// FIN_U = 2 with 4 CTAs/SM (64 registers, no spills): R-MAT-24 reduced 0.0762
+// -> 0.0723 ms against FIN_U = 4 at 73 registers / 3 CTAs/SM (FIN_U = 8: 0.0845;
+// 4 pairs / thread: 0.085; profiles/r2/ab_fin.txt)
+#ifndef PRGPU_FIN_U
+#define PRGPU_FIN_U 2
+#endif
+#ifndef PRGPU_FIN_MINB
+#define PRGPU_FIN_MINB 4
+#endif
+constexpr int FIN_U = PRGPU_FIN_U;
 #ifndef PRGPU_FIN_PAIRS
 #define PRGPU_FIN_PAIRS 2
 #endif
@@ -307,7 +317,7 @@ __device__ __forceinline__ void fin_store_y(const FinArgs& f, double* y, int32_t
 // REMOTE: the sharded sweep with peer buffers or a multicast team (every
 // contrib also stored remotely); the plain instance keeps fewer registers.
 template <bool REMOTE>
-__global__ void __launch_bounds__(GT_NT) k_finalize(FinArgs f, IterArgs ia) {
+__global__ void __launch_bounds__(GT_NT, PRGPU_FIN_MINB) k_finalize(FinArgs f, IterArgs ia) {
     __shared__ double red[64];
     __shared__ int flag;
     pdl_wait();

@@ -374,3 +374,14 @@ def test_run_loop_batches_with_and_without_timing(pr):
     assert sb["timed_iterations"] >= a[1] // 4 - 1 and sb["gather_ms"] > 0
     assert sa["timed_iterations"] == 0
     assert sa["host_syncs"] <= 8 and sb["host_syncs"] <= 8
+
+
+@pytest.mark.parametrize("k", ["32768", "0"])
+def test_cold_slots_in_row_order(pr, k, monkeypatch):
+    """Contrib slots past the K hottest in row order (DESIGN §5, PRGPU_DEG_SLOTS;
+    k = 0: every slot by out-degree): a graph with more than 32768 sources,
+    so that with K = 32768 most rows' slots follow the row order; every mode's
+    result must match the oracle as with any other slot order."""
+    monkeypatch.setenv("PRGPU_DEG_SLOTS", k)
+    src, dst = graphgen.rmat(17, 8 << 17, seed=31)
+    check_all(pr, 1 << 17, src, dst, tau=1e-11)
