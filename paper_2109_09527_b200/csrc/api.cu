@@ -320,7 +320,7 @@ static int create_graph(const char* fn, int64_t n, int64_t m, const int32_t* src
             }
             pt.mark("allreduce");
         }
-        if ((rc = build_relabel(g, ctx)) != PR_OK) break;
+        if ((rc = build_relabel(g, ctx, !(world > 1 || allreduce))) != PR_OK) break;
         pt.mark("relabel");
         if (world > 1 || allreduce) {
             g->shard_only = true;

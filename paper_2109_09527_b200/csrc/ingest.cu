@@ -521,7 +521,7 @@ struct ColdEmit {
     }
 };
 
-int build_relabel(pr_graph* g, Ctx& ctx) {
+int build_relabel(pr_graph* g, Ctx& ctx, bool cold_rows) {
     cudaStream_t s = ctx.stream;
     const int64_t n = g->n;
     int64_t* scratch = nullptr;
@@ -571,7 +571,7 @@ int build_relabel(pr_graph* g, Ctx& ctx) {
     const char* ds = getenv("PRGPU_DEG_SLOTS");
     const int64_t kds = ds ? atoll(ds) : (int64_t)1 << 20;
     const int64_t K = kds <= 0 ? cnt : std::max<int64_t>(kds, 32768);
-    if (by_degree && K < cnt) {
+    if (by_degree && cold_rows && K < cnt) {
         PR_TRY((device_scan<int64_t>(ctx, n, ColdGet{g->cidx, g->row_ptr, K, 1}, ColdEmit{g->cidx, K, nullptr},
                                      scratch + 1)));
         PR_TRY((device_scan<int64_t>(ctx, n, ColdGet{g->cidx, g->row_ptr, K, 0},

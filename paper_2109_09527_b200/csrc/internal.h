@@ -178,7 +178,10 @@ struct pr_graph {
 
 namespace prgpu {
 int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank = 0, int world = 1);
-int build_relabel(pr_graph* g, Ctx& ctx);
+// cold_rows: slots past the 2^20 hottest in row order (this rank holds every
+// row); false for a per-rank sharded create, whose slots must come out the
+// same on every rank from the all-reduced out-degrees alone
+int build_relabel(pr_graph* g, Ctx& ctx, bool cold_rows);
 int build_view_stream(View& v, Ctx& ctx, int32_t pad_slot, const int32_t* outdeg, const int32_t* cidx);
 int build_spans(View& v, Ctx& ctx, int64_t span_steps);
 void free_spans(View& v, cudaStream_t s);
