@@ -63,20 +63,6 @@ __device__ __forceinline__ uint32_t ld_stream_u8(const uint8_t* p) {
     return r;
 }
 
-#ifndef PRGPU_SE_INTERIOR
-#define PRGPU_SE_INTERIOR 1
-#endif
-
-// Sum over the warp by an xor butterfly: every lane ends with the same value
-// (each level adds the same two operands in every lane of a pair, and IEEE
-// addition is commutative), so the result is warp-uniform and deterministic.
-template <class T>
-__device__ __forceinline__ T warp_allsum(T x) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    return x;
-}
-
 // Lane 0 of some warp: hand the piece `val` of boundary row b (from span
 // `span`) to the ticket protocol; the last of the b_s1 - b_s0 + 1 pieces sums
 // them in span order and finalizes the row.
@@ -127,12 +113,6 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
     int4 c1 = ld_stream_v4(a.col + sb * SE_STEP + (int64_t)lane * SE_V + 4, pol_stream);
     uint32_t fn = ld_stream_u8(a.flags8 + sb * 32 + lane);
     int32_t Rn = a.step_row[sb];
-    // Interior steps (no row starts in any lane: the middle of a long row)
-    // skip the segmented scan: each lane adds its SE_V gathers to lacc, and the
-    // lanes' sums are folded into carry (butterfly, identical in every lane)
-    // at the next step with a row start or at the span's end.
-    T lacc = T(0);
-    bool pend = false;  // warp-uniform: lacc holds interior sums not yet folded
     for (int64_t s = sb; s < se; ++s) {
         T v[SE_V];
         v[0] = p.load(c0.x);
@@ -152,21 +132,6 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
             fn = ld_stream_u8(a.flags8 + (s + 1) * 32 + lane);
             Rn = a.step_row[s + 1];
         }
-#if PRGPU_SE_INTERIOR
-        if (!__any_sync(0xffffffffu, f)) {
-            T r = v[0];
-#pragma unroll
-            for (int j = 1; j < SE_V; ++j) r += v[j];
-            lacc += r;
-            pend = true;
-            continue;
-        }
-        if (pend) {
-            carry += warp_allsum(lacc);
-            lacc = T(0);
-            pend = false;
-        }
-#endif
         // row starts: warp-exclusive rank of this lane's first start and the
         // step's total, from ballots of the bit planes of the per-lane count
         // (nf <= 8: 4 planes; no shuffles on the MIO pipe)
@@ -228,7 +193,6 @@ __device__ __forceinline__ void stream_span(P& p, const StreamArgs& a, int64_t s
         }
         if (nst > 0) first_closure = false;
     }
-    if (pend) carry += warp_allsum(lacc);
     if (lane == 0) {
         if (first_closure) {
             stream_piece(p, a, bin, span, carry, false);  // a middle piece of a long row
