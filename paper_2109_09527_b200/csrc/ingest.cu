@@ -562,7 +562,7 @@ int build_relabel(pr_graph* g, Ctx& ctx, bool cold_rows) {
         PR_LAUNCH(ctx, k_set_cidx, grid_for(ctx, cnt, 256), 256, 0, sorted, cnt,
                   b ? ((1ull << b) - 1) : 0ull, g->cidx);
     // only the K = 2^20 hottest keep the degree order (the gather's shared-
-    // memory and L1 tiers and the sharded hot copies use slots < 32768; the
+    // memory and L1 tiers and the sharded hot copies use slots < SE_L1_TIER; the
     // rest of the first 2^20 keeps the gather's L2 locality): R-MAT-24 reduced
     // K-FINALIZE 0.091 -> 0.076 ms, K-GATHER unchanged (K = 32K / 128K / 512K
     // / 1M / 2M / 4M / all: step 105.65 / 105.86 / 105.37 / 105.34 / 105.54 /
@@ -570,7 +570,7 @@ int build_relabel(pr_graph* g, Ctx& ctx, bool cold_rows) {
     // sets K (k <= 0: every slot in degree order).
     const char* ds = getenv("PRGPU_DEG_SLOTS");
     const int64_t kds = ds ? atoll(ds) : (int64_t)1 << 20;
-    const int64_t K = kds <= 0 ? cnt : std::max<int64_t>(kds, 32768);
+    const int64_t K = kds <= 0 ? cnt : std::max<int64_t>(kds, SE_L1_TIER);
     if (by_degree && cold_rows && K < cnt) {
         PR_TRY((device_scan<int64_t>(ctx, n, ColdGet{g->cidx, g->row_ptr, K, 1}, ColdEmit{g->cidx, K, nullptr},
                                      scratch + 1)));

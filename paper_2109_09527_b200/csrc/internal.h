@@ -17,13 +17,23 @@ constexpr int SE_NT_IP = 512;               // in-place (async / No-Sync) stream
 // Contribs [0, hot_n) (the highest out-degrees) are copied into shared memory
 // by every CTA at the start of a synchronous sweep; [hot_n, SE_L1_TIER) are
 // gathered with L1::evict_last, the rest with L1::no_allocate.
-constexpr int SE_HOT_MAX = 16384;           // 128 KB of fp64
+// R-MAT-24 K-GATHER by (smem tier, L1 tier) slots: (12K, 32K) 0.777, (16K, 32K)
+// 0.770, (18K, 34K) 0.774, (20K, 32K) 0.768, (20K, 36K) 0.767, (20K, 40K) 0.782,
+// (22K, 40K) 0.824 ms -- past ~20K the L1 left over is too small for the
+// misses in flight (profiles/r2/ab_tiers.txt)
+#ifndef PRGPU_SE_HOT_MAX
+#define PRGPU_SE_HOT_MAX 20480
+#endif
+constexpr int SE_HOT_MAX = PRGPU_SE_HOT_MAX;  // 160 KB of fp64
 // In-place sweeps read the hot tier as a snapshot taken at the start of the
 // (local) sweep, so a larger tier makes sweeps faster but fresher values rarer:
 // R-MAT-24 async, hot 0 / 2K / 8K / 16K: 61 / 68 / 73 / 78 sweeps, 109 / 78 / 80 / 82 ms.
 constexpr int SE_HOT_IP = 2048;
 constexpr int SE_MAX_PHASES = 64;   // PR_MODE_PHASED: most phases per sweep
-constexpr int SE_L1_TIER = 32768;
+#ifndef PRGPU_SE_L1_TIER
+#define PRGPU_SE_L1_TIER 36864
+#endif
+constexpr int SE_L1_TIER = PRGPU_SE_L1_TIER;
 inline int64_t stream_pad(int64_t E) { return ((E > 0 ? E : 1) + SE_STEP - 1) / SE_STEP * SE_STEP; }
 // Threads per CTA of the row-parallel kernels (K-FINALIZE, K-ZERO, ...).
 constexpr int GT_NT = 256;

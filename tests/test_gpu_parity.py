@@ -379,8 +379,8 @@ def test_run_loop_batches_with_and_without_timing(pr):
 @pytest.mark.parametrize("k", ["32768", "0"])
 def test_cold_slots_in_row_order(pr, k, monkeypatch):
     """Contrib slots past the K hottest in row order (DESIGN §5, PRGPU_DEG_SLOTS;
-    k = 0: every slot by out-degree): a graph with more than 32768 sources,
-    so that with K = 32768 most rows' slots follow the row order; every mode's
+    k = 0: every slot by out-degree; K is raised to the L1 tier, 36864): a
+    graph of 64K sources, so that most rows' slots follow the row order; every mode's
     result must match the oracle as with any other slot order."""
     monkeypatch.setenv("PRGPU_DEG_SLOTS", k)
     src, dst = graphgen.rmat(17, 8 << 17, seed=31)
