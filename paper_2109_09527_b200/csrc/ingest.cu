@@ -319,7 +319,12 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
     bool od_runs = false;  // outdeg counted from the src runs of the partial sort
     const uint64_t sentinel = b > 0 ? ((2 * b >= 64) ? ~0ull : ((1ull << (2 * b)) - 1)) : 0ull;
 
-    // pack, sort by (dst, src), deduplicate + CSR (row_ptr, col_idx) in one pass
+    // pack, sort by (dst, src), deduplicate + CSR (row_ptr, col_idx) in one pass.
+    // Single rank with 16-byte aligned edge arrays: the pack runs inside the
+    // first radix pass (RsPack; R-MAT-24: no 2 GB key write + read-back).
+    RsPack pack;
+    const bool fuse_pack = world == 1 && mk > 1 && ((((uintptr_t)src) | ((uintptr_t)dst)) & 15) == 0 &&
+                           !(getenv("PRGPU_PACK") && getenv("PRGPU_PACK")[0] == '0');
     PR_TRY(dalloc(&g->row_ptr, (size_t)n + 1, s));
     PR_CUDA(cudaMemsetAsync(g->row_ptr, 0, sizeof(int64_t) * (size_t)(n + 1), s));  // E == 0: all rows empty
     if (mk > 0) {
@@ -336,6 +341,13 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
             }
             mk = h2[0];
             PR_CUDA(cudaMemsetAsync(scratch, 0, sizeof(int64_t), s));
+        } else if (fuse_pack) {
+            pack.src = src;  // the first radix pass forms the keys itself
+            pack.dst = dst;
+            pack.n = n;
+            pack.b = b;
+            pack.sentinel = sentinel;
+            pack.err = (int*)(scratch + 1);
         } else {
             PR_LAUNCH(ctx, k_pack, grid_for(ctx, mk, 256), 256, 0, src, dst, mk, n, b, sentinel, keys,
                       (int*)(scratch + 1), rank, world);
@@ -352,7 +364,8 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
         const uint64_t* sorted = nullptr;
         if (od_runs) {
             bool a1 = false, a2 = false;
-            PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, b, &a1)));
+            PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, b, &a1,
+                                                fuse_pack ? &pack : nullptr)));
             uint64_t* cur = a1 ? keys_alt : keys;
             uint64_t* oth = a1 ? keys : keys_alt;
             PR_LAUNCH(ctx, k_src_runs, grid_for(ctx, (mk + SR_IPT - 1) / SR_IPT, SR_NT), SR_NT, 0, (const uint64_t*)cur,
@@ -361,7 +374,8 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
             sorted = a2 ? oth : cur;
         } else {
             bool alt = false;
-            PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, 2 * b, &alt)));
+            PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, 2 * b, &alt,
+                                                fuse_pack ? &pack : nullptr)));
             sorted = alt ? keys_alt : keys;
         }
         int uq_occ = 0;  // every CTA of the emit pass resident (fixed chunks: no second wave)

@@ -172,19 +172,47 @@ constexpr int RS_BITS = 8;
 constexpr int RS_BINS = 1 << RS_BITS;
 static_assert(RS_NT >= RS_BINS, "one thread per digit in the tile scan");
 
+// Pack fused into the first radix pass (ingest, single rank): the pass reads
+// the raw edge arrays and forms key = dst << b | src itself (self-loops and
+// invalid ids -> sentinel, which sorts last; the histogram pass flags invalid
+// ids in *err), so the packed key array is never written and read back.
+struct RsPack {
+    const int32_t* src = nullptr;  // null: the pass reads keys
+    const int32_t* dst = nullptr;
+    int64_t n = 0;                 // vertices
+    int b = 0;
+    uint64_t sentinel = 0;
+    int* err = nullptr;
+};
+__device__ __forceinline__ uint64_t rs_pack_key(const RsPack& pk, int32_t s, int32_t t, bool* bad) {
+    *bad = s < 0 || (int64_t)s >= pk.n || t < 0 || (int64_t)t >= pk.n;
+    return (*bad || s == t) ? pk.sentinel : (((uint64_t)(uint32_t)t << pk.b) | (uint32_t)s);
+}
+
 template <class K>
 __global__ void __launch_bounds__(RS_NT) k_rs_hist(const K* __restrict__ keys, int64_t n, int64_t per_cta,
                                                    int shift, uint32_t dmask, uint32_t* __restrict__ hist,
-                                                   int64_t G) {
+                                                   int64_t G, RsPack pk) {
     __shared__ uint32_t cnt[RS_WARPS][RS_BINS];
     for (int i = threadIdx.x; i < RS_WARPS * RS_BINS; i += RS_NT) (&cnt[0][0])[i] = 0;
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     const int64_t b = (int64_t)blockIdx.x * per_cta;
     const int64_t e = min(n, b + per_cta);
-    for (int64_t i = b + threadIdx.x; i < e; i += RS_NT) {
-        uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
-        atomicAdd(&cnt[warp][d], 1u);
+    if (pk.src) {
+        bool any_bad = false;
+        for (int64_t i = b + threadIdx.x; i < e; i += RS_NT) {
+            bool bad;
+            const uint64_t key = rs_pack_key(pk, __ldg(pk.src + i), __ldg(pk.dst + i), &bad);
+            any_bad |= bad;
+            atomicAdd(&cnt[warp][(uint32_t)(key >> shift) & dmask], 1u);
+        }
+        if (any_bad) atomicOr(pk.err, 1);
+    } else {
+        for (int64_t i = b + threadIdx.x; i < e; i += RS_NT) {
+            uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+            atomicAdd(&cnt[warp][d], 1u);
+        }
     }
     __syncthreads();
     for (int d = threadIdx.x; d < RS_BINS; d += RS_NT) {
@@ -260,12 +288,12 @@ struct RsSmem {
 // ranking (match_any), tile-local digit offsets, a local sort into shared
 // memory, then a coalesced write-out (consecutive threads write consecutive
 // addresses of one digit's run).
-template <class K, bool HAS_V>
+template <class K, bool HAS_V, bool PACK = false>
 __global__ void __launch_bounds__(RS_NT, HAS_V ? 2 : PRGPU_RS_MINB) k_rs_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       int64_t n, int64_t per_cta, int shift, uint32_t dmask,
                                                       const uint32_t* __restrict__ offs, int64_t G,
-                                                      const uint32_t* __restrict__ dbase) {
+                                                      const uint32_t* __restrict__ dbase, RsPack pk) {
     extern __shared__ __align__(16) unsigned char rs_raw[];
     RsSmem<K, HAS_V>& sm = *reinterpret_cast<RsSmem<K, HAS_V>*>(rs_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -274,8 +302,31 @@ __global__ void __launch_bounds__(RS_NT, HAS_V ? 2 : PRGPU_RS_MINB) k_rs_scatter
     const int64_t b = (int64_t)blockIdx.x * per_cta;
     const int64_t e = min(n, b + per_cta);
     // stage tile [tb, tb + tn) (16-byte rounded; allocations carry >= 64 B of slack)
+    // pack form: src tile at stk (as int32), dst tile RS_TILE int32 further; the
+    // last, partial tile of the array is read with plain loads instead (user
+    // buffers carry no slack for a 16-byte rounded copy)
+    int32_t* const ps = reinterpret_cast<int32_t*>(sm.stk);
+    int32_t* const pd = ps + RS_TILE;
+    static_assert(sizeof(K) != 8 || sizeof(K) * RS_TILE >= 2 * sizeof(int32_t) * RS_TILE, "pack staging fits the key tile");
     auto stage = [&](int64_t tb) {
         const int tn = (int)min((int64_t)RS_TILE, e - tb);
+        if (PACK) {
+            if (tn < RS_TILE) return;
+            const uint32_t pb = (uint32_t)(RS_TILE * sizeof(int32_t));
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&sm.bar)), "r"(2 * pb)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(ps)),
+                "l"(pk.src + tb), "r"(pb), "r"(smem_addr(&sm.bar))
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(pd)),
+                "l"(pk.dst + tb), "r"(pb), "r"(smem_addr(&sm.bar))
+                : "memory");
+            return;
+        }
         const uint32_t kb = ((uint32_t)(tn * sizeof(K)) + 15u) & ~15u;
         const uint32_t vb = HAS_V ? (((uint32_t)(tn * 4) + 15u) & ~15u) : 0u;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&sm.bar)), "r"(kb + vb)
@@ -309,14 +360,33 @@ __global__ void __launch_bounds__(RS_NT, HAS_V ? 2 : PRGPU_RS_MINB) k_rs_scatter
         uint32_t v[RS_ROUNDS];
         uint32_t dg[RS_ROUNDS];
         uint32_t pos[RS_ROUNDS];
-        mbar_wait(&sm.bar, phase);
-        phase ^= 1u;
+        if (PACK) {
+            bool dummy;
+            if (tn == RS_TILE) {
+                mbar_wait(&sm.bar, phase);
+                phase ^= 1u;
 #pragma unroll
-        for (int r = 0; r < RS_ROUNDS; ++r) {
-            const int li = warp * (32 * RS_ROUNDS) + r * 32 + lane;
-            const bool valid = li < tn;
-            k[r] = valid ? sm.stk[li] : K(0);
-            if (HAS_V) v[r] = valid ? sm.stv[li] : 0u;
+                for (int r = 0; r < RS_ROUNDS; ++r) {
+                    const int li = warp * (32 * RS_ROUNDS) + r * 32 + lane;
+                    k[r] = (K)rs_pack_key(pk, ps[li], pd[li], &dummy);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < RS_ROUNDS; ++r) {
+                    const int li = warp * (32 * RS_ROUNDS) + r * 32 + lane;
+                    k[r] = li < tn ? (K)rs_pack_key(pk, __ldg(pk.src + tb + li), __ldg(pk.dst + tb + li), &dummy) : K(0);
+                }
+            }
+        } else {
+            mbar_wait(&sm.bar, phase);
+            phase ^= 1u;
+#pragma unroll
+            for (int r = 0; r < RS_ROUNDS; ++r) {
+                const int li = warp * (32 * RS_ROUNDS) + r * 32 + lane;
+                const bool valid = li < tn;
+                k[r] = valid ? sm.stk[li] : K(0);
+                if (HAS_V) v[r] = valid ? sm.stv[li] : 0u;
+            }
         }
         __syncthreads();  // staging consumed, wc cleared, previous write-out done: prefetch the next tile
         if (threadIdx.x == 0 && tb + RS_TILE < e) {
@@ -398,10 +468,16 @@ __global__ void __launch_bounds__(RS_NT, HAS_V ? 2 : PRGPU_RS_MINB) k_rs_scatter
 // Stable LSD radix sort of keys[0..n) on bits [begin_bit, end_bit), carrying
 // optional uint32 values.  Uses keys_alt / vals_alt as ping-pong buffers.  On
 // return *in_alt tells which buffer holds the sorted result.
+// pack (optional, 64-bit keys without values): the first pass forms the keys
+// from pack.src / pack.dst instead of reading keys (whose contents are ignored)
 template <class K, bool HAS_V>
 int radix_sort(Ctx& ctx, K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_alt, int64_t n,
-               int begin_bit, int end_bit, bool* in_alt) {
+               int begin_bit, int end_bit, bool* in_alt, const RsPack* pack = nullptr) {
     *in_alt = false;
+    if (pack && (HAS_V || sizeof(K) != 8)) {
+        set_error("radix_sort: the fused pack needs 64-bit keys without values");
+        return PR_EINVAL;
+    }
     if (n <= 1 || end_bit <= begin_bit) return PR_OK;
     if (n > (int64_t)UINT32_MAX) {
         set_error("radix_sort: %lld keys exceed the 32-bit digit offsets", (long long)n);
@@ -409,6 +485,9 @@ int radix_sort(Ctx& ctx, K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_al
     }
     const size_t smem = sizeof(RsSmem<K, HAS_V>);
     PR_CUDA(cudaFuncSetAttribute(k_rs_scatter<K, HAS_V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (pack)
+        PR_CUDA(cudaFuncSetAttribute(k_rs_scatter<K, HAS_V, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
     int per_sm = 0;
     PR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_rs_scatter<K, HAS_V>, RS_NT, smem));
     if (per_sm < 1) per_sm = 1;
@@ -432,12 +511,19 @@ int radix_sort(Ctx& ctx, K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_al
         // ordered by exactly [begin_bit, end_bit) (stable for everything else)
         const int nb = end_bit - shift < RS_BITS ? end_bit - shift : RS_BITS;
         const uint32_t dmask = (1u << nb) - 1u;
-        PR_LAUNCH(ctx, (k_rs_hist<K>), (unsigned)G, RS_NT, 0, (const K*)kin, n, per, shift, dmask, hist, G);
+        RsPack pk;
+        if (pack && shift == begin_bit) pk = *pack;
+        PR_LAUNCH(ctx, (k_rs_hist<K>), (unsigned)G, RS_NT, 0, (const K*)kin, n, per, shift, dmask, hist, G, pk);
         PR_LAUNCH(ctx, k_rs_digit_scan, RS_BINS, 256, 0, hist, G, dtot);
         PR_LAUNCH(ctx, k_rs_dbase, 1, 256, 0, (const uint32_t*)dtot, dbase);
-        PR_LAUNCH(ctx, (k_rs_scatter<K, HAS_V>), (unsigned)G, RS_NT, smem, (const K*)kin,
-                  (const uint32_t*)vin, kout, vout, n, per, shift, dmask, (const uint32_t*)hist, G,
-                  (const uint32_t*)dbase);
+        if (pk.src)
+            PR_LAUNCH(ctx, (k_rs_scatter<K, HAS_V, true>), (unsigned)G, RS_NT, smem, (const K*)kin,
+                      (const uint32_t*)vin, kout, vout, n, per, shift, dmask, (const uint32_t*)hist, G,
+                      (const uint32_t*)dbase, pk);
+        else
+            PR_LAUNCH(ctx, (k_rs_scatter<K, HAS_V>), (unsigned)G, RS_NT, smem, (const K*)kin,
+                      (const uint32_t*)vin, kout, vout, n, per, shift, dmask, (const uint32_t*)hist, G,
+                      (const uint32_t*)dbase, pk);
         K* tk = kin; kin = kout; kout = tk;
         uint32_t* tv = vin; vin = vout; vout = tv;
         alt = !alt;

@@ -127,3 +127,50 @@ def test_invalid_ids(pr):
         with pytest.raises(pr.PRError) as e:
             pr.Graph(5, dev(np.array(s)), dev(np.array(t)))
         assert e.value.code == pr.PR_EINVAL
+
+
+@pytest.mark.parametrize("m", [2, 3072 * 4, 3072 * 5 + 17, 100_003])
+def test_pack_fused_first_pass(pr, m, monkeypatch):
+    """The pack fused into the first radix pass (aligned edge arrays) against
+    the separate pack kernel (PRGPU_PACK=0) and the oracle: whole tiles, a
+    ragged last tile (plain loads instead of the bulk copy), two edges."""
+    n = 5000
+    rng = np.random.default_rng(m)
+    src = rng.integers(0, n, m).astype(np.int32)
+    dst = rng.integers(0, n, m).astype(np.int32)
+    src[::7] = dst[::7]  # self-loops
+    check(pr, n, src, dst)
+    monkeypatch.setenv("PRGPU_PACK", "0")
+    check(pr, n, src, dst)
+
+
+def test_unaligned_edge_arrays(pr):
+    """Edge arrays that are not 16-byte aligned take the separate pack kernel."""
+    n, m = 3000, 20_001
+    rng = np.random.default_rng(9)
+    s_all = torch.from_numpy(rng.integers(0, n, m + 1).astype(np.int32)).cuda()
+    t_all = torch.from_numpy(rng.integers(0, n, m + 1).astype(np.int32)).cuda()
+    s, t = s_all[1:], t_all[1:]
+    assert s.data_ptr() % 16 != 0
+    ref = oracle.build_csr(n, s.cpu().numpy(), t.cpu().numpy())
+    with pr.Graph(n, s, t) as g:
+        assert g.info()["E"] == ref.E
+        rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        col = torch.empty(max(ref.E, 1), dtype=torch.int32, device="cuda")
+        od = torch.empty(n, dtype=torch.int32, device="cuda")
+        pr.pr_get_csr(g.handle, rp, col, od)
+        assert np.array_equal(rp.cpu().numpy(), ref.row_ptr)
+        assert np.array_equal(col[:ref.E].cpu().numpy(), ref.col_idx)
+        assert np.array_equal(od.cpu().numpy(), ref.outdeg)
+
+
+@pytest.mark.parametrize("where", [5, 3072 * 2 + 100])
+def test_invalid_id_in_full_and_ragged_tiles(pr, where):
+    n, m = 1000, 3072 * 2 + 200
+    rng = np.random.default_rng(where)
+    src = rng.integers(0, n, m).astype(np.int32)
+    dst = rng.integers(0, n, m).astype(np.int32)
+    dst[where] = n
+    with pytest.raises(pr.PRError) as e:
+        pr.Graph(n, dev(src), dev(dst))
+    assert e.value.code == pr.PR_EINVAL
