@@ -735,6 +735,11 @@ void pr_destroy(pr_graph* g) {
     dfree(g->mem_srow, s);
     dfree(g->mem_info, s);
     dfree(g->mem_h, s);
+    dfree(g->fold_rinfo, s);
+    dfree(g->fold_w, s);
+    dfree(g->fold_list, s);
+    g->fold_n = 0;
+    g->fold_ready = false;
     dfree(g->xr, s);
     dfree(g->xm, s);
     dfree(g->x, s);

@@ -176,6 +176,16 @@ struct pr_graph {
     double* ab = nullptr;           // chain alpha/beta [2 * (max_chain+1)]
     double* hist = nullptr;         // [(max_chain+1) * n_hsrc] last values of the chain sources (ring)
     int64_t hist_cap = 0;
+    // identical members folded into their source row (sync reduced sweeps,
+    // iterate.cu build_fold): rinfo of the reduced view with FOLD_FLAG on the
+    // rows that have identical members, their multiplicity 1 + #members, and
+    // the members that still need per-sweep work (chain members, and identical
+    // members with out-degree > 0: their contrib)
+    int2* fold_rinfo = nullptr;
+    int32_t* fold_w = nullptr;
+    int32_t* fold_list = nullptr;
+    int64_t fold_n = 0;
+    bool fold_ready = false;
     double* delta_log = nullptr;    // [2 * log_cap]
     int32_t log_cap = 0;
     int32_t log_len = 0;            // entries of delta_log written by the last pr_run

@@ -279,7 +279,18 @@ struct FinArgs {
     const int32_t* mh = nullptr;
     int64_t nh = 0;
     int L = 1;
+    // identical members folded into their source row (build_fold): rinfo.x
+    // carries FOLD_FLAG on rows with identical members, whose |delta| then
+    // counts fold_w[r] = 1 + #members times (x_t(m) = x_t(rep) exactly, so
+    // |x_t(m) - x_{t-1}(m)| is the row's own); the member loop visits only
+    // fold_list (chain members; identical members with outdeg > 0 store their
+    // contrib and nothing else); k_unpermute takes their x from the row
+    int fold = 0;
+    const int32_t* fold_w = nullptr;
+    const int32_t* fold_list = nullptr;
 };
+constexpr int32_t FOLD_FLAG = 1 << 30;
+constexpr int32_t FOLD_MASK = FOLD_FLAG - 1;
 
 // Rows are visited grid-stride (all CTAs sweep the row space together, which
 // keeps the TLB working set small) in batches of FIN_U rows per thread whose
@@ -357,12 +368,19 @@ __global__ void __launch_bounds__(GT_NT, PRGPU_FIN_MINB) k_finalize(FinArgs f, I
                     const double xa = __dadd_rn(f.c, __dmul_rn(f.d, sv[u].x));
                     const double xb = __dadd_rn(f.c, __dmul_rn(f.d, sv[u].y));
                     X2[p] = make_double2(xa, xb);
-                    if (iv[u].x > 0) fin_store_y<REMOTE>(f, y, iv[u].y, xa / (double)iv[u].x);
-                    if (iv[u].z > 0) fin_store_y<REMOTE>(f, y, iv[u].w, xb / (double)iv[u].z);
+                    const int32_t oa = f.fold ? (iv[u].x & FOLD_MASK) : iv[u].x;
+                    const int32_t ob = f.fold ? (iv[u].z & FOLD_MASK) : iv[u].z;
+                    if (oa > 0) fin_store_y<REMOTE>(f, y, iv[u].y, xa / (double)oa);
+                    if (ob > 0) fin_store_y<REMOTE>(f, y, iv[u].w, xb / (double)ob);
                     const double da = fabs(xa - xv[u].x), db = fabs(xb - xv[u].y);
-                    l1 += da;
-                    l1 += db;
                     linf = fmax(linf, fmax(da, db));
+                    if (f.fold && ((iv[u].x | iv[u].z) & FOLD_FLAG)) {
+                        l1 += (iv[u].x & FOLD_FLAG) ? da * (double)__ldg(f.fold_w + 2 * p) : da;
+                        l1 += (iv[u].z & FOLD_FLAG) ? db * (double)__ldg(f.fold_w + 2 * p + 1) : db;
+                    } else {
+                        l1 += da;
+                        l1 += db;
+                    }
                 }
             }
         }
@@ -389,10 +407,11 @@ __global__ void __launch_bounds__(GT_NT, PRGPU_FIN_MINB) k_finalize(FinArgs f, I
             if (r < f.nrows && !fr[u]) {
                 const double xn = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
                 xr[r] = xn;
-                const double yv = inf[u].x > 0 ? xn / (double)inf[u].x : 0.0;
-                if (inf[u].x > 0) fin_store_y<REMOTE>(f, y, inf[u].y, yv);
+                const int32_t od = f.fold ? (inf[u].x & FOLD_MASK) : inf[u].x;
+                const double yv = od > 0 ? xn / (double)od : 0.0;
+                if (od > 0) fin_store_y<REMOTE>(f, y, inf[u].y, yv);
                 const double dl = fabs(xn - xo[u]);
-                l1 += dl;
+                l1 += (f.fold && (inf[u].x & FOLD_FLAG)) ? dl * (double)__ldg(f.fold_w + r) : dl;
                 linf = fmax(linf, dl);
                 if (f.fz && dl != 0.0 && dl < f.tau_f) {  // threshold_check <- True (Alg.5)
                     f.fz[r] = 1;
@@ -408,25 +427,32 @@ __global__ void __launch_bounds__(GT_NT, PRGPU_FIN_MINB) k_finalize(FinArgs f, I
     }
     double* __restrict__ xm = f.xm;
     const int t_sw = f.hist ? ia.st->iters + 1 : 0;  // this sweep's number (delayed chains)
-    for (int64_t i0 = t0; i0 < f.nm; i0 += FIN_U * T) {
+    for (int64_t j0 = t0; j0 < f.nm; j0 += FIN_U * T) {
         double S[FIN_U], xo[FIN_U];
         int32_t k[FIN_U];
         int2 inf[FIN_U];
+        int64_t mi[FIN_U];
 #pragma unroll
         for (int u = 0; u < FIN_U; ++u) {
-            const int64_t i = i0 + u * T;
-            if (i < f.nm) {
+            const int64_t j = j0 + u * T;
+            if (j < f.nm) {
+                const int64_t i = f.fold ? (int64_t)__ldg(f.fold_list + j) : j;
+                mi[u] = i;
                 k[u] = __ldg(f.mk + i);
                 S[u] = sums[__ldg(f.msrow + i)];
-                xo[u] = xm[i];
+                if (!(f.fold && k[u] == 0)) xo[u] = xm[i];
                 inf[u] = __ldg(f.minfo + i);
             }
         }
 #pragma unroll
         for (int u = 0; u < FIN_U; ++u) {
-            const int64_t i = i0 + u * T;
-            if (i < f.nm) {
+            const int64_t i = mi[u];
+            if (j0 + u * T < f.nm) {
                 const double xs = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
+                if (f.fold && k[u] == 0) {  // folded identical member: its contrib only
+                    if (inf[u].x > 0) y[inf[u].y] = xs / (double)inf[u].x;
+                    continue;
+                }
                 int j = k[u];
                 double xsrc = xs;
                 if (f.hist && j > 0) {  // delayed: the source's value j sweeps ago (Eq.(1) along the chain)
@@ -452,12 +478,36 @@ __global__ void __launch_bounds__(GT_NT, PRGPU_FIN_MINB) k_finalize(FinArgs f, I
 }
 
 // x in vertex order from the row / member ordered state.
+// (mk, msrow given: the sweeps folded the identical members (k = 0) into their
+// source row, whose x they take)
 __global__ void k_unpermute(const double* __restrict__ xr, const int32_t* __restrict__ vid, int64_t nrows,
                             const double* __restrict__ xm, const int32_t* __restrict__ mvid, int64_t nm,
-                            double* __restrict__ x) {
+                            double* __restrict__ x, const int32_t* __restrict__ mk = nullptr,
+                            const int32_t* __restrict__ msrow = nullptr) {
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += T) x[vid ? vid[r] : r] = xr[r];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += T) x[mvid[i]] = xm[i];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += T)
+        x[mvid[i]] = (mk && mk[i] == 0) ? xr[msrow[i]] : xm[i];
+}
+
+// build_fold: multiplicity of every row with identical members, flagged rinfo,
+// and the members that keep per-sweep work
+__global__ void k_fold_count(const int32_t* __restrict__ mk, const int32_t* __restrict__ msrow, int64_t nm,
+                             int32_t* __restrict__ w) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += (int64_t)gridDim.x * blockDim.x)
+        if (mk[i] == 0) atomicAdd(w + msrow[i], 1);
+}
+__global__ void k_fold_rows(const int2* __restrict__ rinfo, int64_t nrows, int32_t* __restrict__ w,
+                            int2* __restrict__ out) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        int2 ri = rinfo[r];
+        const int32_t c = w[r];
+        if (c > 0) {
+            ri.x |= FOLD_FLAG;
+            w[r] = c + 1;
+        }
+        out[r] = ri;
+    }
 }
 
 __global__ void k_fill_f64(double* __restrict__ a, int64_t cnt, double v) {
@@ -827,6 +877,42 @@ static int launch_gather(Ctx& ctx, pr_graph* g, const View& v, const double* y_i
     return PR_OK;
 }
 
+// Identical members folded into their source row (FinArgs::fold): tables
+// built once per preprocess, on the first sync reduced run that uses them.
+struct FoldKeepGet {
+    const int32_t* mk;
+    const int2* minfo;
+    __device__ int64_t operator()(int64_t i) const { return (mk[i] > 0 || minfo[i].x > 0) ? 1 : 0; }
+};
+struct FoldKeepEmit {
+    int32_t* list;
+    __device__ void operator()(int64_t i, int64_t pos, int64_t f) const {
+        if (f) list[pos] = (int32_t)i;
+    }
+};
+static int build_fold(pr_graph* g, Ctx& ctx, const View& v) {
+    if (g->fold_ready) return PR_OK;
+    cudaStream_t s = ctx.stream;
+    const int64_t nm = g->n_members;
+    int64_t* cnt = nullptr;
+    TmpGuard tg_(s);
+    tg_.track(cnt);
+    PR_TRY(dalloc(&g->fold_w, (size_t)v.nrows, s));
+    PR_CUDA(cudaMemsetAsync(g->fold_w, 0, sizeof(int32_t) * (size_t)v.nrows, s));
+    PR_TRY(dalloc(&g->fold_rinfo, (size_t)v.nrows, s));
+    PR_TRY(dalloc(&g->fold_list, (size_t)nm, s));
+    PR_TRY(dalloc(&cnt, 1, s));
+    const unsigned gm = (unsigned)std::min<int64_t>((nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+    const unsigned gr = (unsigned)std::min<int64_t>((v.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+    PR_LAUNCH(ctx, k_fold_count, gm, 256, 0, (const int32_t*)g->mem_k, (const int32_t*)g->mem_srow, nm, g->fold_w);
+    PR_LAUNCH(ctx, k_fold_rows, gr, 256, 0, (const int2*)v.rinfo, v.nrows, g->fold_w, g->fold_rinfo);
+    PR_TRY((device_scan<int64_t>(ctx, nm, FoldKeepGet{g->mem_k, g->mem_info}, FoldKeepEmit{g->fold_list}, cnt)));
+    PR_CUDA(cudaMemcpyAsync(&g->fold_n, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
+    g->fold_ready = true;
+    return PR_OK;
+}
+
 // PR_MODE_PHASED: K row-aligned phases (build_phase_view; reading Q-B).
 static int phase_plan(pr_graph* g, bool reduced, Ctx& ctx, int* K_out) {
     View& v = reduced ? g->reduced : g->plain;
@@ -1125,6 +1211,17 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     const MemArgs ma{g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, nm > 0 ? (nm + gc.grid - 1) / gc.grid : 0, g->ab};
     FinArgs fa{v.sums, v.nrows, v.rinfo, g->xr, g->mem_srow, g->mem_k, g->mem_info, g->xm, nm, g->ab, nullptr, c, d};
     fa.vec = env_int("PRGPU_FIN_VEC", 1);
+    // identical members folded into their source row (sync reduced sweeps; the
+    // flag bit needs out-degrees < 2^30, i.e. n <= 2^30)
+    const bool fold = reduced && nm > 0 && !async && !phased && n <= ((int64_t)1 << 30) && env_int("PRGPU_FOLD", 1);
+    if (fold) {
+        PR_TRY(build_fold(g, ctx, v));
+        fa.fold = 1;
+        fa.rinfo = g->fold_rinfo;
+        fa.fold_w = g->fold_w;
+        fa.fold_list = g->fold_list;
+        fa.nm = g->fold_n;
+    }
     // delayed chain resolution (sync reduced, reading Q-C2): the last
     // max_chain + 1 values of every chain source, slot 0 = x_0 = 1/n
     if (reduced && nm > 0 && !async && !phased && !(mode & PR_CHAIN_EAGER) && g->n_hsrc > 0) {
@@ -1212,7 +1309,8 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     PR_TRY(sweep_loop(g, ctx, max_iter, tau, sweep, [&](int64_t) { return tmr.harvest(g->st_host->iters); }, ls));
     const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
     PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
-              (const double*)g->xm, (const int32_t*)g->mem_vid, nm, x);
+              (const double*)g->xm, (const int32_t*)g->mem_vid, nm, x, fold ? (const int32_t*)g->mem_k : nullptr,
+              fold ? (const int32_t*)g->mem_srow : nullptr);
     if (!rb.ranks_dev) {
         PR_CUDA(cudaMemcpyAsync(ranks, x, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
         PR_CUDA(cudaStreamSynchronize(s));

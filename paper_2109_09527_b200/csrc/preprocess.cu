@@ -362,6 +362,11 @@ static void clear_reductions(pr_graph* g, cudaStream_t s) {
     dfree(g->mem_srow, s);
     dfree(g->mem_info, s);
     dfree(g->mem_h, s);
+    dfree(g->fold_rinfo, s);
+    dfree(g->fold_w, s);
+    dfree(g->fold_list, s);
+    g->fold_n = 0;
+    g->fold_ready = false;
     g->n_hsrc = 0;
     dfree(g->xm, s);
     free_view(g->reduced, s);
