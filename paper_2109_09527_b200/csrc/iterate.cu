@@ -1188,11 +1188,12 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     // K-FINALIZE: fixed grid per phase, so each CTA's rows and members (and
     // hence its Delta partial) are a fixed set (deterministic)
     int64_t fgrid_k[SE_MAX_PHASES], foff_k[SE_MAX_PHASES];
+    const int64_t fin_cap = (int64_t)ctx.num_sms * env_int("PRGPU_FIN_CTAS_PER_SM", 8);
     int64_t fgrid = 0;
     for (int k = 0; k < K; ++k) {
         const int64_t rows = phased ? v.phase_rb[k + 1] - v.phase_rb[k] : v.nrows;
         const int64_t work = rows + (k == K - 1 ? nm : 0);
-        fgrid_k[k] = std::min<int64_t>(std::max<int64_t>((work + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), cap4 * 2);
+        fgrid_k[k] = std::min<int64_t>(std::max<int64_t>((work + GT_NT * FIN_U - 1) / (GT_NT * FIN_U), 1), fin_cap);
         foff_k[k] = fgrid;
         fgrid += fgrid_k[k];
     }

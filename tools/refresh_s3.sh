@@ -1,8 +1,14 @@
-mkdir -p gpurun_out/s3
-timeout 1400 python -m pytest tests -m gpu -q -x > gpurun_out/s3/pytest_gpu.log 2>&1; tail -2 gpurun_out/s3/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/s3/smoke.log 2>&1; tail -1 gpurun_out/s3/smoke.log
-timeout 500 python bench.py > gpurun_out/s3/bench.json 2> gpurun_out/s3/bench.err; tail -c 300 gpurun_out/s3/bench.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s3/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-modes --no-plain > gpurun_out/s3/ncu_bench.log 2>&1; tail -c 100 gpurun_out/s3/ncu_bench.log
-timeout 600 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"k_stream|k_finalize" -s 20 -c 2 -o gpurun_out/s3/stream_rmat24_reduced_warm python tools/step_once.py 4 reduced > gpurun_out/s3/ncu_stream.log 2>&1; tail -1 gpurun_out/s3/ncu_stream.log
-timeout 1500 python tools/all_configs.py > gpurun_out/s3/all_configs.json 2> gpurun_out/s3/all_configs.err; tail -c 200 gpurun_out/s3/all_configs.err
-PRGPU_PROFILE=2 timeout 300 python tools/time_create.py 4 2 > gpurun_out/s3/create_profile.log 2>&1; tail -1 gpurun_out/s3/create_profile.log
+# Round-2 session-3 evidence refresh on the GPU box (gpurun): full GPU suite,
+# smoke, bench line, bench launch list, warm ncu capture of the sweep kernels,
+# all five configs, create profile, and the full-size converged parity run.
+# Usage: bash tools/refresh_s3.sh [outdir=gpurun_out/s3]
+O=${1:-gpurun_out/s3}
+mkdir -p $O
+timeout 1400 python -m pytest tests -m gpu -q -x > $O/pytest_gpu.log 2>&1; tail -2 $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
+timeout 500 python bench.py > $O/bench.json 2> $O/bench.err; tail -c 300 $O/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-modes --no-plain > $O/ncu_bench.log 2>&1; tail -c 100 $O/ncu_bench.log
+timeout 600 ncu --set full --cache-control none --clock-control none --import-source on -k regex:"k_stream|k_finalize" -s 20 -c 2 -o $O/stream_rmat24_reduced_warm python tools/step_once.py 4 reduced > $O/ncu_stream.log 2>&1; tail -1 $O/ncu_stream.log
+timeout 1500 python tools/all_configs.py > $O/all_configs.json 2> $O/all_configs.err; tail -c 200 $O/all_configs.err
+PRGPU_PROFILE=2 timeout 300 python tools/time_create.py 4 2 > $O/create_profile.log 2>&1; tail -1 $O/create_profile.log
+PRGPU_FULL=1 timeout 1800 python -m pytest tests/test_gpu_fullsize_converged.py -q -s > $O/fullsize_converged_parity.log 2>&1; tail -2 $O/fullsize_converged_parity.log
