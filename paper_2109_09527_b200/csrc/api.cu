@@ -154,6 +154,15 @@ static void pinned_state_free(DevState* p) {
     cudaFreeHost(p);
 }
 
+static bool is_pinned_host_ptr(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 static bool is_device_ptr(const void* p) {
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -284,7 +293,11 @@ static int create_graph(const char* fn, int64_t n, int64_t m, const int32_t* src
         if ((rc = dalloc(&g->st, 1, ctx.stream)) != PR_OK) break;
         const int32_t* s = src;
         const int32_t* t = dst;
-        if (m > 0 && !is_device_ptr(src)) {  // host edge list: copy in (e2e path)
+        // pinned host edge list, one rank: copied in chunks inside the ingest,
+        // overlapped with the sorting of the chunks already in
+        const bool host_chunked = m > 0 && world == 1 && !allreduce && is_pinned_host_ptr(src) &&
+                                  is_pinned_host_ptr(dst) && ingest_chunked_applies(n, m);
+        if (m > 0 && !host_chunked && !is_device_ptr(src)) {  // host edge list: copy in (e2e path)
             if ((rc = dalloc(&dsrc, (size_t)m, ctx.stream)) != PR_OK) break;
             if (cudaMemcpyAsync(dsrc, src, sizeof(int32_t) * (size_t)m, cudaMemcpyDefault, ctx.stream) != cudaSuccess) {
                 set_error("copy of src failed");
@@ -293,7 +306,7 @@ static int create_graph(const char* fn, int64_t n, int64_t m, const int32_t* src
             }
             s = dsrc;
         }
-        if (m > 0 && !is_device_ptr(dst)) {
+        if (m > 0 && !host_chunked && !is_device_ptr(dst)) {
             if ((rc = dalloc(&ddst, (size_t)m, ctx.stream)) != PR_OK) break;
             if (cudaMemcpyAsync(ddst, dst, sizeof(int32_t) * (size_t)m, cudaMemcpyDefault, ctx.stream) != cudaSuccess) {
                 set_error("copy of dst failed");
@@ -304,7 +317,7 @@ static int create_graph(const char* fn, int64_t n, int64_t m, const int32_t* src
         }
         pt0.mark("setup");
         PhaseTimer pt(ctx.stream, "create");
-        if ((rc = ingest(g, s, t, ctx, rank, world)) != PR_OK) break;
+        if ((rc = ingest(g, s, t, ctx, rank, world, host_chunked)) != PR_OK) break;
         pt.mark("ingest");
         dfree(dsrc, ctx.stream);
         dfree(ddst, ctx.stream);

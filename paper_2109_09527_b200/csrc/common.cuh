@@ -105,6 +105,8 @@ void dfree(T*& p, cudaStream_t s) {
     p = nullptr;
 }
 
+// (track() keeps the ADDRESS of the pointer variable: declare the variable in
+// the guard's own scope, never in an inner block that ends before the guard.)
 // Frees the device temporaries registered with track() when the scope ends,
 // early error returns included; a pointer already released with dfree (and so
 // set to nullptr) is skipped.  Graph-owned buffers are never tracked: on error

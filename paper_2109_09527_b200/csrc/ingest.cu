@@ -299,7 +299,21 @@ static unsigned grid_for(const Ctx& ctx, int64_t work, int nt) {
     return (unsigned)g;
 }
 
-int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank, int world) {
+// Host edge arrays (pinned, single rank): the copy in runs in CH_K chunks on a
+// copy stream; each chunk is sorted as soon as it has arrived (pack fused into
+// its first pass, the src runs counted per chunk) and merged into the sorted
+// prefix of the chunks before it (merge path), so only the last chunk's sort
+// and one merge follow the last byte over PCIe.
+// chunks: R-MAT-24 e2e step 141.2 / 138.6 / 137.1 / 143.0 ms for 4 / 8 / 16 / 32
+// (the ladder's merges grow with the chunk count; the tail shrinks with it)
+constexpr int CH_K = 32;  // most chunks (PRGPU_CHUNKS, default 16)
+constexpr int64_t CH_MIN = (int64_t)1 << 22;
+bool ingest_chunked_applies(int64_t n, int64_t m) {
+    const char* e = getenv("PRGPU_CHUNKED");
+    return n > 1 && m >= CH_MIN && !(e && e[0] == '0');
+}
+
+int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank, int world, bool host_src) {
     const int64_t n = g->n, m = g->m_raw;
     const int b = bits_for((uint64_t)(n - 1));
     cudaStream_t s = ctx.stream;
@@ -307,10 +321,16 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
     uint64_t* keys = nullptr;
     uint64_t* keys_alt = nullptr;
     int64_t* scratch = nullptr;  // [0] = E, [1] = error flag
+    uint64_t* keys_m = nullptr;  // host_src: the third buffer of the merge ladder
+    int32_t* dsrc = nullptr;     // host_src: device copies of the edge arrays
+    int32_t* ddst = nullptr;
     TmpGuard tg_(ctx.stream);
     tg_.track(keys);
     tg_.track(keys_alt);
     tg_.track(scratch);
+    tg_.track(keys_m);
+    tg_.track(dsrc);
+    tg_.track(ddst);
 
     PR_TRY(dalloc(&scratch, 2, s));
     PR_CUDA(cudaMemsetAsync(scratch, 0, 2 * sizeof(int64_t), s));
@@ -341,6 +361,8 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
             }
             mk = h2[0];
             PR_CUDA(cudaMemsetAsync(scratch, 0, sizeof(int64_t), s));
+        } else if (host_src) {
+            // keys formed chunk by chunk below, from the device copies of the chunks
         } else if (fuse_pack) {
             pack.src = src;  // the first radix pass forms the keys itself
             pack.dst = dst;
@@ -362,7 +384,80 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
         // when splitting costs no extra radix pass; else one sort and atomics
         od_runs = b >= 8 && 2 * ((b + RS_BITS - 1) / RS_BITS) == (2 * b + RS_BITS - 1) / RS_BITS;
         const uint64_t* sorted = nullptr;
-        if (od_runs) {
+        if (host_src) {
+            PR_TRY(dalloc(&dsrc, (size_t)mk, s));
+            PR_TRY(dalloc(&ddst, (size_t)mk, s));
+            PR_TRY(dalloc(&keys_m, (size_t)mk, s));
+            const int kreq = std::min(CH_K, std::max(1, getenv("PRGPU_CHUNKS") ? atoi(getenv("PRGPU_CHUNKS")) : 16));
+            int64_t C = (mk + kreq - 1) / kreq;
+            C = (C + RS_TILE - 1) / RS_TILE * RS_TILE;
+            const int K = (int)std::max<int64_t>(1, mk / C);  // the last chunk takes the remainder: len in [C, 2C)
+            cudaStream_t cs = nullptr;
+            cudaEvent_t ev[CH_K + 1] = {};
+            struct StreamEvents {  // released on every exit (after the work queued on them)
+                cudaStream_t* cs;
+                cudaEvent_t* ev;
+                ~StreamEvents() {
+                    for (int i = 0; i <= CH_K; ++i)
+                        if (ev[i]) cudaEventDestroy(ev[i]);
+                    if (*cs) cudaStreamDestroy(*cs);
+                }
+            } se_{&cs, ev};
+            PR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            for (int i = 0; i <= CH_K; ++i) PR_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+            PR_CUDA(cudaEventRecord(ev[CH_K], s));  // the copy buffers exist on the copy stream
+            PR_CUDA(cudaStreamWaitEvent(cs, ev[CH_K], 0));
+            auto off_of = [&](int i) { return i < K ? (int64_t)i * C : mk; };
+            for (int i = 0; i < K; ++i) {
+                const int64_t off = off_of(i), len = off_of(i + 1) - off;
+                PR_CUDA(cudaMemcpyAsync(dsrc + off, src + off, sizeof(int32_t) * (size_t)len, cudaMemcpyHostToDevice, cs));
+                PR_CUDA(cudaMemcpyAsync(ddst + off, dst + off, sizeof(int32_t) * (size_t)len, cudaMemcpyHostToDevice, cs));
+                PR_CUDA(cudaEventRecord(ev[i], cs));
+            }
+            uint64_t* R = nullptr;        // the buffer the sorted chunks land in (same parity for all)
+            uint64_t* P = nullptr;        // the radix ping-pong partner
+            const uint64_t* acc = nullptr;
+            for (int i = 0; i < K; ++i) {
+                const int64_t off = off_of(i), len = off_of(i + 1) - off;
+                PR_CUDA(cudaStreamWaitEvent(s, ev[i], 0));
+                RsPack pk;
+                pk.src = dsrc + off;
+                pk.dst = ddst + off;
+                pk.n = n;
+                pk.b = b;
+                pk.sentinel = sentinel;
+                pk.err = (int*)(scratch + 1);
+                const uint64_t* res = nullptr;
+                if (od_runs) {
+                    bool a1 = false, a2 = false;
+                    PR_TRY((radix_sort<uint64_t, false>(ctx, keys + off, keys_alt + off, nullptr, nullptr, len, 0, b,
+                                                        &a1, &pk)));
+                    uint64_t* cur = (a1 ? keys_alt : keys) + off;
+                    uint64_t* oth = (a1 ? keys : keys_alt) + off;
+                    PR_LAUNCH(ctx, k_src_runs, grid_for(ctx, (len + SR_IPT - 1) / SR_IPT, SR_NT), SR_NT, 0,
+                              (const uint64_t*)cur, len, b, sentinel, n, g->outdeg);
+                    PR_TRY((radix_sort<uint64_t, false>(ctx, cur, oth, nullptr, nullptr, len, b, 2 * b, &a2)));
+                    res = a2 ? oth : cur;
+                } else {
+                    bool alt = false;
+                    PR_TRY((radix_sort<uint64_t, false>(ctx, keys + off, keys_alt + off, nullptr, nullptr, len, 0,
+                                                        2 * b, &alt, &pk)));
+                    res = (alt ? keys_alt : keys) + off;
+                }
+                if (i == 0) {
+                    R = const_cast<uint64_t*>(res);
+                    P = R == keys ? keys_alt : keys;
+                    acc = R;
+                    continue;
+                }
+                // acc = sorted [0, off); merge with chunk i into P, M, P, ... (never
+                // into R, whose next chunks are still to come)
+                uint64_t* out = (i & 1) ? P : keys_m;
+                PR_TRY(merge_u64(ctx, acc, off, res, len, out));
+                acc = out;
+            }
+            sorted = acc;
+        } else if (od_runs) {
             bool a1 = false, a2 = false;
             PR_TRY((radix_sort<uint64_t, false>(ctx, keys, keys_alt, nullptr, nullptr, mk, 0, b, &a1,
                                                 fuse_pack ? &pack : nullptr)));

@@ -197,7 +197,11 @@ struct pr_graph {
 };
 
 namespace prgpu {
-int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank = 0, int world = 1);
+// host_src: src / dst are pinned host arrays (single rank, m >= 2^22): copied
+// in chunks that are sorted and merged while the rest is still in flight
+int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int rank = 0, int world = 1,
+           bool host_src = false);
+bool ingest_chunked_applies(int64_t n, int64_t m);
 // cold_rows: slots past the 2^20 hottest in row order (this rank holds every
 // row); false for a per-rank sharded create, whose slots must come out the
 // same on every rank from the all-reduced out-degrees alone

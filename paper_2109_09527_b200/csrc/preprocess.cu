@@ -509,8 +509,12 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
 
     // members (scatter list) and the computed set R (reduced gather view)
     int64_t* cnt = nullptr;
+    int32_t* mark = nullptr;  // chain sources' history index (below); declared here, where the guard lives
+    int32_t* idx = nullptr;
     TmpGuard tg_(ctx.stream);
     tg_.track(cnt);
+    tg_.track(mark);
+    tg_.track(idx);
     PR_TRY(dalloc(&cnt, 3, s));
     PR_CUDA(cudaMemsetAsync(cnt, 0, 3 * sizeof(int64_t), s));
     PR_LAUNCH(ctx, k_max_chain, grid_of(ctx, n), 256, 0, (const int32_t*)g->chain_k, n, (int*)(cnt + 2));
@@ -564,10 +568,6 @@ int preprocess(pr_graph* g, uint32_t flags, Ctx& ctx) {
         PR_LAUNCH(ctx, k_rinfo, grid_of(ctx, g->n_members), 256, 0, (const int32_t*)g->mem_vid, g->n_members,
                   (const int32_t*)g->outdeg, (const int32_t*)g->cidx, g->mem_info);
         if (g->max_chain > 0) {
-            int32_t* mark = nullptr;
-            int32_t* idx = nullptr;
-            tg_.track(mark);
-            tg_.track(idx);
             PR_TRY(dalloc(&mark, (size_t)std::max<int64_t>(R.nrows, 1), s));
             PR_TRY(dalloc(&idx, (size_t)std::max<int64_t>(R.nrows, 1), s));
             PR_CUDA(cudaMemsetAsync(mark, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(R.nrows, 1), s));

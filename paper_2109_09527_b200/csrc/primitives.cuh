@@ -533,6 +533,71 @@ int radix_sort(Ctx& ctx, K* keys, K* keys_alt, uint32_t* vals, uint32_t* vals_al
     return PR_OK;
 }
 
+// ----------------------------------------------------------------- merge --
+// C = the stable merge of sorted A[0, na) and B[0, nb) (merge path: ties take
+// A first).  k_merge_part finds, for every tile boundary t*MG_TILE of C, the
+// number of A elements before it (one binary search per boundary, all in
+// parallel); each CTA then merges its tile's A and B slices from shared memory
+// (a binary search per thread for its own diagonal, VT outputs each) and
+// writes the tile out coalesced.  Used by the chunked host ingest (ingest.cu).
+constexpr int MG_NT = 256, MG_VT = 8, MG_TILE = MG_NT * MG_VT;
+static __global__ void k_merge_part(const uint64_t* __restrict__ A, int64_t na, const uint64_t* __restrict__ B, int64_t nb,
+                             int64_t ntiles, int64_t* __restrict__ part) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > ntiles) return;
+    const int64_t diag = min(t * MG_TILE, na + nb);
+    int64_t lo = max((int64_t)0, diag - nb), hi = min(diag, na);
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (A[mid] <= B[diag - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    part[t] = lo;
+}
+static __global__ void __launch_bounds__(MG_NT) k_merge_tile(const uint64_t* __restrict__ A, int64_t na,
+                                                      const uint64_t* __restrict__ B, int64_t nb,
+                                                      const int64_t* __restrict__ part, uint64_t* __restrict__ C) {
+    __shared__ uint64_t sk[MG_TILE];
+    __shared__ uint64_t so[MG_TILE];
+    const int64_t t = blockIdx.x;
+    const int64_t d0 = t * MG_TILE, d1 = min(d0 + MG_TILE, na + nb);
+    const int64_t i0 = part[t], i1 = part[t + 1];
+    const int64_t j0 = d0 - i0, j1 = d1 - i1;
+    const int la = (int)(i1 - i0), lb = (int)(j1 - j0), ln = la + lb;
+    for (int k = threadIdx.x; k < la; k += MG_NT) sk[k] = A[i0 + k];
+    for (int k = threadIdx.x; k < lb; k += MG_NT) sk[la + k] = B[j0 + k];
+    __syncthreads();
+    const int dd = min((int)threadIdx.x * MG_VT, ln);
+    int lo = max(0, dd - lb), hi = min(dd, la);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sk[mid] <= sk[la + dd - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    int ia = lo, ib = dd - lo;
+#pragma unroll
+    for (int v = 0; v < MG_VT; ++v) {
+        const int o = dd + v;
+        if (o < ln) {
+            const bool takeA = ib >= lb || (ia < la && sk[ia] <= sk[la + ib]);
+            so[o] = takeA ? sk[ia++] : sk[la + ib++];
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < ln; k += MG_NT) C[d0 + k] = so[k];
+}
+inline int merge_u64(Ctx& ctx, const uint64_t* A, int64_t na, const uint64_t* B, int64_t nb, uint64_t* C) {
+    const int64_t n = na + nb;
+    if (n == 0) return PR_OK;
+    const int64_t ntiles = (n + MG_TILE - 1) / MG_TILE;
+    int64_t* part = nullptr;
+    PR_TRY(dalloc(&part, (size_t)ntiles + 1, ctx.stream));
+    PR_LAUNCH(ctx, k_merge_part, (unsigned)((ntiles + 1 + 255) / 256), 256, 0, A, na, B, nb, ntiles, part);
+    PR_LAUNCH(ctx, k_merge_tile, (unsigned)ntiles, MG_NT, 0, A, na, B, nb, (const int64_t*)part, C);
+    dfree(part, ctx.stream);
+    return PR_OK;
+}
+
 inline int bits_for(uint64_t maxval) {  // number of bits to represent values <= maxval
     int b = 0;
     while (b < 64 && (maxval >> b) != 0) ++b;

@@ -174,3 +174,65 @@ def test_invalid_id_in_full_and_ragged_tiles(pr, where):
     with pytest.raises(pr.PRError) as e:
         pr.Graph(n, dev(src), dev(dst))
     assert e.value.code == pr.PR_EINVAL
+
+
+def csr_from(pr, n, s, t):
+    with pr.Graph(n, s, t) as g:
+        E = g.info()["E"]
+        rp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        col = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
+        od = torch.empty(n, dtype=torch.int32, device="cuda")
+        pr.pr_get_csr(g.handle, rp, col, od)
+        return E, rp.cpu().numpy(), col[:E].cpu().numpy(), od.cpu().numpy()
+
+
+@pytest.mark.parametrize("m,n", [((1 << 22) + 12345, 1 << 20), (3 * (1 << 22) + 7, 50_000)])
+def test_host_pinned_chunked_ingest(pr, m, n, monkeypatch):
+    """Pinned host edge arrays take the chunked ingest (copy in CH_K chunks,
+    each sorted on arrival and merged into the sorted prefix): the CSR equals
+    the oracle's and the one-shot host copy's (PRGPU_CHUNKED=0)."""
+    rng = np.random.default_rng(m)
+    src = rng.integers(0, n, m).astype(np.int32)
+    dst = rng.integers(0, n, m).astype(np.int32)
+    idx = np.arange(0, m - 1, 5)                     # duplicates (some straddle chunk boundaries)
+    src[idx] = src[idx + 1]
+    dst[idx] = dst[idx + 1]
+    dst[::11] = src[::11]                            # self-loops
+    ref = oracle.build_csr(n, src, dst)
+    s_h = torch.from_numpy(src).pin_memory()
+    t_h = torch.from_numpy(dst).pin_memory()
+    E, rp, col, od = csr_from(pr, n, s_h, t_h)
+    assert E == ref.E
+    assert np.array_equal(rp, ref.row_ptr)
+    assert np.array_equal(col, ref.col_idx)
+    assert np.array_equal(od, ref.outdeg)
+    monkeypatch.setenv("PRGPU_CHUNKED", "0")
+    E2, rp2, col2, od2 = csr_from(pr, n, s_h, t_h)
+    assert E2 == E and np.array_equal(rp2, rp) and np.array_equal(col2, col) and np.array_equal(od2, od)
+
+
+def test_host_pinned_chunked_rmat_run(pr):
+    """R-MAT scale 20 from pinned host buffers: CSR and the reduced run match
+    the device-buffer create."""
+    import graphgen
+    gen = graphgen.make_config(2)
+    x1 = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+    x2 = torch.empty(gen.n, dtype=torch.float64, device="cuda")
+    with pr.Graph(gen.n, dev(gen.src), dev(gen.dst)) as g1, \
+            pr.Graph(gen.n, torch.from_numpy(gen.src).pin_memory(), torch.from_numpy(gen.dst).pin_memory()) as g2:
+        for g in (g1, g2):
+            g.preprocess()
+        r1 = g1.run(x1, gen.d, gen.tau, gen.max_iter, mode=pr.PR_USE_REDUCTIONS)
+        r2 = g2.run(x2, gen.d, gen.tau, gen.max_iter, mode=pr.PR_USE_REDUCTIONS)
+        assert r1 == r2 and torch.equal(x1, x2)
+
+
+def test_host_pinned_invalid_id_last_chunk(pr):
+    n, m = 1000, (1 << 22) + 100
+    rng = np.random.default_rng(3)
+    src = rng.integers(0, n, m).astype(np.int32)
+    dst = rng.integers(0, n, m).astype(np.int32)
+    dst[m - 3] = n + 5
+    with pytest.raises(pr.PRError) as e:
+        pr.Graph(n, torch.from_numpy(src).pin_memory(), torch.from_numpy(dst).pin_memory())
+    assert e.value.code == pr.PR_EINVAL
