@@ -397,7 +397,11 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
             struct StreamEvents {  // released on every exit (after the work queued on them)
                 cudaStream_t* cs;
                 cudaEvent_t* ev;
+                bool joined = false;  // the compute stream waits for every chunk copy
                 ~StreamEvents() {
+                    // early error exit: copies may still be landing in buffers the
+                    // guard is about to free on the compute stream
+                    if (!joined && *cs) cudaStreamSynchronize(*cs);
                     for (int i = 0; i <= CH_K; ++i)
                         if (ev[i]) cudaEventDestroy(ev[i]);
                     if (*cs) cudaStreamDestroy(*cs);
@@ -456,6 +460,7 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
                 PR_TRY(merge_u64(ctx, acc, off, res, len, out));
                 acc = out;
             }
+            se_.joined = true;
             sorted = acc;
         } else if (od_runs) {
             bool a1 = false, a2 = false;
