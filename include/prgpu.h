@@ -116,7 +116,11 @@ typedef struct pr_graph pr_graph;     /* opaque; owned by the library */
  *   n      number of vertices, 1 <= n <= 2^31-1 (dense 0-based ids, Q-V)
  *   m      number of raw edges, 0 <= m <= 2^31-1
  *   src,dst  int32[m] raw edge list (src -> dst); duplicates and self-loops
- *          allowed (removed here).  Host or device memory; read only.
+ *          allowed (removed here).  Host or device memory; read only.  Pinned
+ *          host arrays with m >= 2^22 are copied in chunks on a stream of the
+ *          library's own, each chunk sorted while the next ones are in
+ *          flight; the call returns after the last copy (the caller may then
+ *          reuse the arrays).
  *   out    receives the new graph (NULL on failure)
  * Result: row_ptr int64[n+1], col_idx int32[E] (sources of each row sorted
  * ascending), outdeg int32[n], all bit-exact functions of the edge set.
