@@ -385,3 +385,32 @@ def test_cold_slots_in_row_order(pr, k, monkeypatch):
     monkeypatch.setenv("PRGPU_DEG_SLOTS", k)
     src, dst = graphgen.rmat(17, 8 << 17, seed=31)
     check_all(pr, 1 << 17, src, dst, tau=1e-11)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_chain_relation_at_exit(pr, seed):
+    """at exit every chain member v with predecessor p (its only
+    in-neighbour, out-degree 1) satisfies x(v) = c + d * x(p) to 1e-14
+    relative in the eager reduced mode (x_t(v) = alpha_k + beta_k * x_t(src),
+    the same-sweep chain, Q-C), and to the convergence error in the delayed
+    mode (x_t(v) = c + d * x_{t-1}(p): the plain trajectory, Q-C2);
+    identical members equal their representative exactly."""
+    n, edges = G.planted_graph(seed, n_base=200, chains=(2, 9, 16, 5))
+    s, t = G.edges_to_arrays(edges)
+    ref_g = oracle.build_csr(n, s, t)
+    c = (1 - D) / n
+    with gpu_graph(pr, n, s, t) as g:
+        g.preprocess(pr.PR_PRE_IDENTICAL | pr.PR_PRE_CHAIN)
+        rep, cs, ck = gpu_reductions(pr, g, n)
+        members = np.nonzero(ck > 0)[0]
+        assert len(members) > 0
+        pred = ref_g.col_idx[ref_g.row_ptr[members]]
+        assert np.all(np.diff(ref_g.row_ptr)[members] == 1) and np.all(ref_g.outdeg[pred] == 1)
+        tau = 1e-13
+        _, _, _, xe = gpu_run(pr, g, n, tau, mode=pr.PR_USE_REDUCTIONS | pr.PR_CHAIN_EAGER)
+        rel = np.abs(xe[members] - (c + D * xe[pred])) / xe[members]
+        assert rel.max() <= 1e-14, rel.max()
+        _, _, _, xd = gpu_run(pr, g, n, tau, mode=pr.PR_USE_REDUCTIONS)
+        assert np.abs(xd[members] - (c + D * xd[pred])).max() <= 10 * tau
+        ident = np.nonzero(rep != np.arange(n))[0]
+        assert np.array_equal(xe[ident], xe[rep[ident]]) and np.array_equal(xd[ident], xd[rep[ident]])
