@@ -381,8 +381,11 @@ int ingest(pr_graph* g, const int32_t* src, const int32_t* dst, Ctx& ctx, int ra
         PR_TRY(dalloc(&g->outdeg, (size_t)n, s));
         PR_CUDA(cudaMemsetAsync(g->outdeg, 0, sizeof(int32_t) * (size_t)n, s));
         // sort the src bits, count the src runs (outdeg), then the dst bits --
-        // when splitting costs no extra radix pass; else one sort and atomics
-        od_runs = b >= 8 && 2 * ((b + RS_BITS - 1) / RS_BITS) == (2 * b + RS_BITS - 1) / RS_BITS;
+        // also when the split costs one more pass (b not a multiple of 8): a
+        // radix pass is ~5 ms per 1e9 keys, per-edge atomics over the
+        // deduplicated sources ~27 ms (config 5, b = 26: create 117 -> 98 ms);
+        // b < 8 or PRGPU_OD_RUNS=0: one sort, then per-edge atomics
+        od_runs = b >= 8 && !(getenv("PRGPU_OD_RUNS") && getenv("PRGPU_OD_RUNS")[0] == '0');
         const uint64_t* sorted = nullptr;
         if (host_src) {
             PR_TRY(dalloc(&dsrc, (size_t)mk, s));
