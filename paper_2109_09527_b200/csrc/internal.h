@@ -183,8 +183,10 @@ struct pr_graph {
     // members with out-degree > 0: their contrib)
     int2* fold_rinfo = nullptr;
     int32_t* fold_w = nullptr;
-    int32_t* fold_list = nullptr;
+    int32_t* fold_list = nullptr;   // chain members
     int64_t fold_n = 0;
+    int4* fold_rec = nullptr;       // identical members with a contrib: (source row, outdeg, slot, -)
+    int64_t fold_nrec = 0;
     bool fold_ready = false;
     double* delta_log = nullptr;    // [2 * log_cap]
     int32_t log_cap = 0;

@@ -283,11 +283,14 @@ struct FinArgs {
     // carries FOLD_FLAG on rows with identical members, whose |delta| then
     // counts fold_w[r] = 1 + #members times (x_t(m) = x_t(rep) exactly, so
     // |x_t(m) - x_{t-1}(m)| is the row's own); the member loop visits only
-    // fold_list (chain members; identical members with outdeg > 0 store their
-    // contrib and nothing else); k_unpermute takes their x from the row
+    // fold_list (chain members) and the packed fold_rec records (identical
+    // members with outdeg > 0: their contrib and nothing else, one record load
+    // then the source row's S); k_unpermute takes their x from the row
     int fold = 0;
     const int32_t* fold_w = nullptr;
-    const int32_t* fold_list = nullptr;
+    const int32_t* fold_list = nullptr;  // the chain members (nm of them)
+    const int4* fold_rec = nullptr;      // identical members with a contrib: (source row, outdeg, slot, -)
+    int64_t nrec = 0;
 };
 constexpr int32_t FOLD_FLAG = 1 << 30;
 constexpr int32_t FOLD_MASK = FOLD_FLAG - 1;
@@ -424,6 +427,21 @@ __global__ void __launch_bounds__(GT_NT, PRGPU_FIN_MINB) k_finalize(FinArgs f, I
     if (f.fz) {
         nfrozen = warp_sum(nfrozen);
         if ((threadIdx.x & 31) == 0 && nfrozen) atomicAdd(f.nfz, (unsigned long long)nfrozen);
+    }
+    if (f.fold) {  // folded identical members with a contrib: y = (c + d*S(source row)) / outdeg
+        for (int64_t j0 = t0; j0 < f.nrec; j0 += FIN_U * T) {
+            int4 rc[FIN_U];
+            double S[FIN_U];
+#pragma unroll
+            for (int u = 0; u < FIN_U; ++u)
+                if (j0 + u * T < f.nrec) rc[u] = __ldg(f.fold_rec + j0 + u * T);
+#pragma unroll
+            for (int u = 0; u < FIN_U; ++u)
+                if (j0 + u * T < f.nrec) S[u] = sums[rc[u].x];
+#pragma unroll
+            for (int u = 0; u < FIN_U; ++u)
+                if (j0 + u * T < f.nrec) y[rc[u].z] = __dadd_rn(f.c, __dmul_rn(f.d, S[u])) / (double)rc[u].y;
+        }
     }
     double* __restrict__ xm = f.xm;
     const int t_sw = f.hist ? ia.st->iters + 1 : 0;  // this sweep's number (delayed chains)
@@ -879,15 +897,27 @@ static int launch_gather(Ctx& ctx, pr_graph* g, const View& v, const double* y_i
 
 // Identical members folded into their source row (FinArgs::fold): tables
 // built once per preprocess, on the first sync reduced run that uses them.
-struct FoldKeepGet {
+struct FoldChainGet {
     const int32_t* mk;
-    const int2* minfo;
-    __device__ int64_t operator()(int64_t i) const { return (mk[i] > 0 || minfo[i].x > 0) ? 1 : 0; }
+    __device__ int64_t operator()(int64_t i) const { return mk[i] > 0 ? 1 : 0; }
 };
-struct FoldKeepEmit {
+struct FoldChainEmit {
     int32_t* list;
     __device__ void operator()(int64_t i, int64_t pos, int64_t f) const {
         if (f) list[pos] = (int32_t)i;
+    }
+};
+struct FoldRecGet {
+    const int32_t* mk;
+    const int2* minfo;
+    __device__ int64_t operator()(int64_t i) const { return (mk[i] == 0 && minfo[i].x > 0) ? 1 : 0; }
+};
+struct FoldRecEmit {
+    const int32_t* msrow;
+    const int2* minfo;
+    int4* rec;
+    __device__ void operator()(int64_t i, int64_t pos, int64_t f) const {
+        if (f) rec[pos] = make_int4(msrow[i], minfo[i].x, minfo[i].y, 0);
     }
 };
 static int build_fold(pr_graph* g, Ctx& ctx, const View& v) {
@@ -901,14 +931,20 @@ static int build_fold(pr_graph* g, Ctx& ctx, const View& v) {
     PR_CUDA(cudaMemsetAsync(g->fold_w, 0, sizeof(int32_t) * (size_t)v.nrows, s));
     PR_TRY(dalloc(&g->fold_rinfo, (size_t)v.nrows, s));
     PR_TRY(dalloc(&g->fold_list, (size_t)nm, s));
-    PR_TRY(dalloc(&cnt, 1, s));
+    PR_TRY(dalloc(&cnt, 2, s));
     const unsigned gm = (unsigned)std::min<int64_t>((nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
     const unsigned gr = (unsigned)std::min<int64_t>((v.nrows + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
     PR_LAUNCH(ctx, k_fold_count, gm, 256, 0, (const int32_t*)g->mem_k, (const int32_t*)g->mem_srow, nm, g->fold_w);
     PR_LAUNCH(ctx, k_fold_rows, gr, 256, 0, (const int2*)v.rinfo, v.nrows, g->fold_w, g->fold_rinfo);
-    PR_TRY((device_scan<int64_t>(ctx, nm, FoldKeepGet{g->mem_k, g->mem_info}, FoldKeepEmit{g->fold_list}, cnt)));
-    PR_CUDA(cudaMemcpyAsync(&g->fold_n, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    PR_TRY(dalloc(&g->fold_rec, (size_t)nm, s));
+    PR_TRY((device_scan<int64_t>(ctx, nm, FoldChainGet{g->mem_k}, FoldChainEmit{g->fold_list}, cnt)));
+    PR_TRY((device_scan<int64_t>(ctx, nm, FoldRecGet{g->mem_k, g->mem_info},
+                                 FoldRecEmit{g->mem_srow, g->mem_info, g->fold_rec}, cnt + 1)));
+    int64_t hc[2];
+    PR_CUDA(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
     PR_CUDA(cudaStreamSynchronize(s));
+    g->fold_n = hc[0];
+    g->fold_nrec = hc[1];
     g->fold_ready = true;
     return PR_OK;
 }
@@ -1222,6 +1258,8 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         fa.fold_w = g->fold_w;
         fa.fold_list = g->fold_list;
         fa.nm = g->fold_n;
+        fa.fold_rec = g->fold_rec;
+        fa.nrec = g->fold_nrec;
     }
     // delayed chain resolution (sync reduced, reading Q-C2): the last
     // max_chain + 1 values of every chain source, slot 0 = x_0 = 1/n

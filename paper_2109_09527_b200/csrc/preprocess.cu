@@ -365,7 +365,9 @@ static void clear_reductions(pr_graph* g, cudaStream_t s) {
     dfree(g->fold_rinfo, s);
     dfree(g->fold_w, s);
     dfree(g->fold_list, s);
+    dfree(g->fold_rec, s);
     g->fold_n = 0;
+    g->fold_nrec = 0;
     g->fold_ready = false;
     g->n_hsrc = 0;
     dfree(g->xm, s);
