@@ -751,6 +751,8 @@ void pr_destroy(pr_graph* g) {
     dfree(g->fold_rinfo, s);
     dfree(g->fold_w, s);
     dfree(g->fold_list, s);
+    dfree(g->fold_crec, s);
+    dfree(g->fold_xc, s);
     dfree(g->fold_rec, s);
     g->fold_n = 0;
     g->fold_nrec = 0;

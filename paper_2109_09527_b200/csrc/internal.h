@@ -185,6 +185,8 @@ struct pr_graph {
     int32_t* fold_w = nullptr;
     int32_t* fold_list = nullptr;   // chain members
     int64_t fold_n = 0;
+    int4* fold_crec = nullptr;      // chain members in fold_list order: (source row, hist index or -1, slot, k)
+    double* fold_xc = nullptr;      // x of the chain members in fold_list order (during a run)
     int4* fold_rec = nullptr;       // identical members with a contrib: (source row, outdeg, slot, -)
     int64_t fold_nrec = 0;
     bool fold_ready = false;

@@ -291,6 +291,8 @@ struct FinArgs {
     const int32_t* fold_list = nullptr;  // the chain members (nm of them)
     const int4* fold_rec = nullptr;      // identical members with a contrib: (source row, outdeg, slot, -)
     int64_t nrec = 0;
+    const int4* fold_crec = nullptr;     // the chain members: (source row, hist index, slot, k), list order
+    double* xc = nullptr;                // x of the chain members, list order
 };
 constexpr int32_t FOLD_FLAG = 1 << 30;
 constexpr int32_t FOLD_MASK = FOLD_FLAG - 1;
@@ -313,7 +315,10 @@ constexpr int FIN_U = PRGPU_FIN_U;
 #ifndef PRGPU_FIN_PAIRS
 #define PRGPU_FIN_PAIRS 2
 #endif
-constexpr int FIN_PAIRS = PRGPU_FIN_PAIRS;  // row pairs per thread and iteration of the 16-byte path
+constexpr int FIN_PAIRS = PRGPU_FIN_PAIRS;
+// (the folded rows' Delta weights loaded with the row data, 8 B per row pair,
+// instead of after the flag test measured the same: R-MAT-24 reduced 0.0681
+// vs 0.0680 ms, profiles/r2/ab_fin_chainrec.jsonl)  // row pairs per thread and iteration of the 16-byte path
 
 // One new contrib: this buffer (and every peer's), or one multicast store.
 template <bool REMOTE>
@@ -445,7 +450,59 @@ __global__ void __launch_bounds__(GT_NT, PRGPU_FIN_MINB) k_finalize(FinArgs f, I
     }
     double* __restrict__ xm = f.xm;
     const int t_sw = f.hist ? ia.st->iters + 1 : 0;  // this sweep's number (delayed chains)
-    for (int64_t j0 = t0; j0 < f.nm; j0 += FIN_U * T) {
+    if (f.fold_crec) {
+        // folded sweep: the chain members from their packed records (list
+        // order, x in xc), every operand one level below the record: delayed,
+        // only the distance-1 member (the writer of its source's history)
+        // needs S of the source row; the value it resolves from is the
+        // history slot of the sweep j = min(k, t) ago (never this sweep's)
+        for (int64_t j0 = t0; j0 < f.nm; j0 += FIN_U * T) {
+            int4 rc[FIN_U];
+            double S[FIN_U], xo[FIN_U], hx[FIN_U];
+#pragma unroll
+            for (int u = 0; u < FIN_U; ++u) {
+                const int64_t j = j0 + u * T;
+                if (j < f.nm) {
+                    rc[u] = __ldg(f.fold_crec + j);
+                    xo[u] = f.xc[j];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < FIN_U; ++u) {
+                if (j0 + u * T < f.nm) {
+                    if (f.hist) {
+                        const int jj = min(rc[u].w, t_sw);
+                        hx[u] = f.hist[(int64_t)((t_sw - jj) % f.L) * f.nh + rc[u].y];
+                        if (rc[u].w == 1) S[u] = sums[rc[u].x];
+                    } else {
+                        S[u] = sums[rc[u].x];
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < FIN_U; ++u) {
+                const int64_t jl = j0 + u * T;
+                if (jl < f.nm) {
+                    int j = rc[u].w;
+                    double xsrc;
+                    if (f.hist) {
+                        if (j == 1) f.hist[(int64_t)(t_sw % f.L) * f.nh + rc[u].y] = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
+                        j = min(j, t_sw);
+                        xsrc = hx[u];
+                    } else {
+                        xsrc = __dadd_rn(f.c, __dmul_rn(f.d, S[u]));
+                    }
+                    const double xn = __dadd_rn(f.ab[2 * j], __dmul_rn(f.ab[2 * j + 1], xsrc));
+                    f.xc[jl] = xn;
+                    y[rc[u].z] = xn;  // out-degree 1: xn / 1
+                    const double dl = fabs(xn - xo[u]);
+                    l1 += dl;
+                    linf = fmax(linf, dl);
+                }
+            }
+        }
+    }
+    for (int64_t j0 = t0; j0 < (f.fold_crec ? 0 : f.nm); j0 += FIN_U * T) {
         double S[FIN_U], xo[FIN_U];
         int32_t k[FIN_U];
         int2 inf[FIN_U];
@@ -498,14 +555,21 @@ __global__ void __launch_bounds__(GT_NT, PRGPU_FIN_MINB) k_finalize(FinArgs f, I
 // x in vertex order from the row / member ordered state.
 // (mk, msrow given: the sweeps folded the identical members (k = 0) into their
 // source row, whose x they take)
+// (clist, xc given: the chain members' x is xc in clist order)
 __global__ void k_unpermute(const double* __restrict__ xr, const int32_t* __restrict__ vid, int64_t nrows,
                             const double* __restrict__ xm, const int32_t* __restrict__ mvid, int64_t nm,
                             double* __restrict__ x, const int32_t* __restrict__ mk = nullptr,
-                            const int32_t* __restrict__ msrow = nullptr) {
+                            const int32_t* __restrict__ msrow = nullptr, const int32_t* __restrict__ clist = nullptr,
+                            const double* __restrict__ xc = nullptr, int64_t nc = 0) {
     const int64_t T = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += T) x[vid ? vid[r] : r] = xr[r];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += T)
-        x[mvid[i]] = (mk && mk[i] == 0) ? xr[msrow[i]] : xm[i];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nm; i += T) {
+        if (mk && mk[i] == 0)
+            x[mvid[i]] = xr[msrow[i]];
+        else if (!xc)
+            x[mvid[i]] = xm[i];
+    }
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nc; j += T) x[mvid[clist[j]]] = xc[j];
 }
 
 // build_fold: multiplicity of every row with identical members, flagged rinfo,
@@ -525,6 +589,19 @@ __global__ void k_fold_rows(const int2* __restrict__ rinfo, int64_t nrows, int32
             w[r] = c + 1;
         }
         out[r] = ri;
+    }
+}
+
+// One 16-byte record per chain member in fold_list order, so the member loop
+// of K-FINALIZE issues one coalesced load instead of a list load followed by
+// five dependent ones.  A chain member has out-degree 1 by definition
+// (preprocess.cu: chain(v) <=> indeg 1 and outdeg 1), so its contrib is its x.
+__global__ void k_fold_crec(const int32_t* __restrict__ list, int64_t nc, const int32_t* __restrict__ msrow,
+                            const int32_t* __restrict__ mh, const int2* __restrict__ minfo,
+                            const int32_t* __restrict__ mk, int4* __restrict__ rec) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nc; j += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = list[j];
+        rec[j] = make_int4(msrow[i], mh ? mh[i] : -1, minfo[i].y, mk[i]);
     }
 }
 
@@ -945,6 +1022,13 @@ static int build_fold(pr_graph* g, Ctx& ctx, const View& v) {
     PR_CUDA(cudaStreamSynchronize(s));
     g->fold_n = hc[0];
     g->fold_nrec = hc[1];
+    if (g->fold_n > 0) {
+        PR_TRY(dalloc(&g->fold_crec, (size_t)g->fold_n, s));
+        PR_TRY(dalloc(&g->fold_xc, (size_t)g->fold_n, s));
+        const unsigned gc = (unsigned)std::min<int64_t>((g->fold_n + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
+        PR_LAUNCH(ctx, k_fold_crec, gc, 256, 0, (const int32_t*)g->fold_list, g->fold_n, (const int32_t*)g->mem_srow,
+                  (const int32_t*)g->mem_h, (const int2*)g->mem_info, (const int32_t*)g->mem_k, g->fold_crec);
+    }
     g->fold_ready = true;
     return PR_OK;
 }
@@ -1260,6 +1344,12 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
         fa.nm = g->fold_n;
         fa.fold_rec = g->fold_rec;
         fa.nrec = g->fold_nrec;
+        if (g->fold_n > 0) {
+            fa.fold_crec = g->fold_crec;
+            fa.xc = g->fold_xc;
+            PR_LAUNCH(ctx, k_fill_f64, (unsigned)std::min<int64_t>((g->fold_n + 255) / 256, (int64_t)ctx.num_sms * 16),
+                      256, 0, g->fold_xc, g->fold_n, 1.0 / (double)n);
+        }
     }
     // delayed chain resolution (sync reduced, reading Q-C2): the last
     // max_chain + 1 values of every chain source, slot 0 = x_0 = 1/n
@@ -1349,7 +1439,8 @@ int run(pr_graph* g, double d, double tau, int32_t max_iter, uint32_t mode, doub
     const unsigned ug = (unsigned)std::min<int64_t>((v.nrows + nm + 255) / 256 + 1, (int64_t)ctx.num_sms * 16);
     PR_LAUNCH(ctx, k_unpermute, ug, 256, 0, (const double*)g->xr, (const int32_t*)v.vid, v.nrows,
               (const double*)g->xm, (const int32_t*)g->mem_vid, nm, x, fold ? (const int32_t*)g->mem_k : nullptr,
-              fold ? (const int32_t*)g->mem_srow : nullptr);
+              fold ? (const int32_t*)g->mem_srow : nullptr, fa.fold_crec ? (const int32_t*)g->fold_list : nullptr,
+              (const double*)fa.xc, fa.fold_crec ? g->fold_n : 0);
     if (!rb.ranks_dev) {
         PR_CUDA(cudaMemcpyAsync(ranks, x, sizeof(double) * (size_t)n, cudaMemcpyDefault, s));
         PR_CUDA(cudaStreamSynchronize(s));

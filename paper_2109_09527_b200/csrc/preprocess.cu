@@ -365,6 +365,8 @@ static void clear_reductions(pr_graph* g, cudaStream_t s) {
     dfree(g->fold_rinfo, s);
     dfree(g->fold_w, s);
     dfree(g->fold_list, s);
+    dfree(g->fold_crec, s);
+    dfree(g->fold_xc, s);
     dfree(g->fold_rec, s);
     g->fold_n = 0;
     g->fold_nrec = 0;
