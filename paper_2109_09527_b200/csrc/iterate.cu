@@ -318,7 +318,10 @@ constexpr int FIN_U = PRGPU_FIN_U;
 constexpr int FIN_PAIRS = PRGPU_FIN_PAIRS;
 // (the folded rows' Delta weights loaded with the row data, 8 B per row pair,
 // instead of after the flag test measured the same: R-MAT-24 reduced 0.0681
-// vs 0.0680 ms, profiles/r2/ab_fin_chainrec.jsonl)  // row pairs per thread and iteration of the 16-byte path
+// vs 0.0680 ms, profiles/r2/ab_fin_chainrec.jsonl; the thread's first 1 / 2
+// folded-member records and their S loaded during the rows loop spill at 64
+// registers and measured slower: 0.0717 / 0.0754 vs 0.0679 ms,
+// profiles/r2/ab_fin_recpre.jsonl)  // row pairs per thread and iteration of the 16-byte path
 
 // One new contrib: this buffer (and every peer's), or one multicast store.
 template <bool REMOTE>
