@@ -365,3 +365,125 @@ extern "C" int ceiling_tma(const int32_t* col, int64_t E, const double* y, int64
     cudaEventDestroy(b);
     return (int)cudaGetLastError();
 }
+
+// Hybrid: are the LDG path (L1TEX) and the TMA path independent routes to L2?
+// Warps [0, 32 - nT) of each 1024-thread CTA gather chunks [0, nA) with
+// ld.global.nc.L1::no_allocate; warps [32 - nT, 32) gather chunks [nA, nch)
+// with TMA gather4 (S stages per warp), concurrently.  If the two paths do not
+// share the limiter, the pass takes max(t_ldg(nA), t_tma(nch - nA)).
+template <int S>
+__global__ void __launch_bounds__(1024) k_hybrid(const __grid_constant__ CUtensorMap tm, const int32_t* __restrict__ col,
+                                                 int64_t E, const double* __restrict__ y, int nT, int64_t nA,
+                                                 double* out) {
+    extern __shared__ __align__(128) unsigned char sm_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int nL = 32 - nT;
+    const int64_t nch = E / 128;
+    double acc = 0.0;
+    if (wib < nL) {
+        const int64_t lw = (int64_t)blockIdx.x * nL + wib, nlw = (int64_t)gridDim.x * nL;
+        for (int64_t c = lw; c < nA; c += nlw) {
+            const int4 q = ldg_stream(reinterpret_cast<const int4*>(col + c * 128) + lane);
+            acc += ldg_na(y + q.x) + ldg_na(y + q.y) + ldg_na(y + q.z) + ldg_na(y + q.w);
+        }
+    } else {
+        const int tw = wib - nL;
+        double* buf = reinterpret_cast<double*>(sm_raw) + (size_t)tw * S * 512;
+        uint64_t* bar = reinterpret_cast<uint64_t*>(sm_raw + (size_t)nT * S * 4096) + tw * S;
+        const int64_t gw = (int64_t)blockIdx.x * nT + tw, ngw = (int64_t)gridDim.x * nT;
+        if (lane == 0)
+            for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(bar + s)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
+        int4 ix[S];
+        auto issue = [&](int s, int64_t c) {
+            ix[s] = reinterpret_cast<const int4*>(col + c * 128)[lane];
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 2048;" ::"r"(sa(bar + s)) : "memory");
+            __syncwarp();
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(sa(buf + s * 512 + lane * 16)),
+                "l"(&tm), "r"(sa(bar + s)), "r"(0), "r"(ix[s].x >> 1), "r"(ix[s].y >> 1), "r"(ix[s].z >> 1),
+                "r"(ix[s].w >> 1)
+                : "memory");
+        };
+        int64_t c = nA + gw;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (c + s * ngw < nch) issue(s, c + s * ngw);
+        uint32_t ph = 0;
+        for (; c < nch; c += S * ngw) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int64_t cc = c + s * ngw;
+                if (cc >= nch) break;
+                asm volatile(
+                    "{\n\t.reg .pred P;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra W_%=;\n\t}" ::"r"(
+                        sa(bar + s)),
+                    "r"(ph)
+                    : "memory");
+                const double* b = buf + s * 512 + lane * 16;
+                acc += b[ix[s].x & 1] + b[2 + (ix[s].y & 1)] + b[4 + (ix[s].z & 1)] + b[6 + (ix[s].w & 1)];
+                __syncwarp();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                const int64_t nx = cc + S * ngw;
+                if (nx < nch) issue(s, nx);
+            }
+            ph ^= 1;
+        }
+    }
+    out[(int64_t)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+extern "C" int ceiling_hybrid(const int32_t* col, int64_t E, const double* y, int64_t nsrc, int nT, int stages,
+                              double frac_tma, int reps, double* out, float* ms_out) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess || !enc)
+        return -100;
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {2, (cuuint64_t)((nsrc + 1) / 2)};
+    cuuint64_t strides[1] = {16};
+    cuuint32_t box[2] = {2, 1};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)y, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return -200 - (int)r;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t nch = E / 128;
+    const int64_t nA = nT == 0 ? nch : (nT == 32 ? 0 : (int64_t)((1.0 - frac_tma) * (double)nch));
+    size_t smem = (size_t)(nT > 0 ? nT : 1) * stages * 4096 + (size_t)(nT > 0 ? nT : 1) * stages * 8;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto launch = [&]() {
+#define L(S)                                                                                               \
+    if (stages == S) {                                                                                     \
+        cudaFuncSetAttribute(k_hybrid<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+        k_hybrid<S><<<sms, 1024, smem>>>(tm, col, E, y, nT, nA, out);                                      \
+    }
+        L(1) L(2) L(3) L(4)
+#undef L
+    };
+    launch();
+    {
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            fprintf(stderr, "hybrid kernel: %s\n", cudaGetErrorString(e));
+            return -300;
+        }
+    }
+    cudaEventRecord(a);
+    for (int i = 0; i < reps; ++i) launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    *ms_out = ms / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return (int)cudaGetLastError();
+}

@@ -108,7 +108,34 @@ def run_cluster(colv, HL, HD, cl, tier=0, label="skewed + cluster DSMEM tier"):
           f"{ms.value:.4f} ms  {gps:7.1f} G gathers/s  {gps * 1e9 / (sms * clk):.3f} gathers/SM/cycle@1965MHz", flush=True)
 
 
+lib.ceiling_hybrid.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
+                               ctypes.POINTER(ctypes.c_float)]
+
+
+def run_hybrid(colv, nT, stages, frac, label):
+    ms = ctypes.c_float()
+    out.zero_()
+    E128 = colv.numel() // 128 * 128
+    rc = lib.ceiling_hybrid(colv.data_ptr(), E128, y.data_ptr(), nsrc, nT, stages, frac, 10, out.data_ptr(),
+                            ctypes.byref(ms))
+    assert rc == 0, rc
+    gps = E128 / (ms.value * 1e-3) / 1e9
+    print(f"{label:38s} tma_warps={nT:2d} stages={stages} tma_frac={frac:.2f}: {ms.value:.4f} ms  {gps:7.1f} G gathers/s  "
+          f"{gps * 1e9 / (sms * clk):.3f} gathers/SM/cycle@1965MHz", flush=True)
+
+
 print(f"{gen.name}: n={n} E={E} sources={nsrc}")
+if which == "hybrid":
+    u = torch.randint(0, nsrc, (E,), dtype=torch.int32, device=dev)
+    run_hybrid(u, 0, 2, 0.0, "uniform, LDG warps only (32)")
+    run_hybrid(u, 32, 1, 1.0, "uniform, TMA warps only (32)")
+    for nT in (4, 8, 12, 16):
+        for frac in (0.15, 0.25, 0.35, 0.45):
+            run_hybrid(u, nT, 2, frac, "uniform, hybrid")
+    run_hybrid(u, 8, 3, 0.3, "uniform, hybrid")
+    run_hybrid(u, 8, 4, 0.3, "uniform, hybrid")
+    sys.exit(0)
 if which == "cluster":
     run(col, 16384, 4, 1, "skewed + hot smem + L1 tier (current)", threads=1024, tier=32768)
     for cl, HL, HD, tier in ((1, 16384, 0, 32768), (2, 16384, 12288, 0), (2, 16384, 12288, 65536),
