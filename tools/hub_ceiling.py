@@ -3,7 +3,10 @@ config into the rows with in-degree >= T (hub part: grouped by the 16K-slot
 slice of their contrib slot, gathered from a shared-memory copy of the slice,
 tools/hub_ceiling.cu) and the rest (the flat tiered gather of
 tools/gather_ceiling.cu), and times both against the flat gather of all edges.
-Usage: python tools/hub_ceiling.py [config=4] [T=256,1024]"""
+Usage: python tools/hub_ceiling.py [config=4] [T=256,1024] [tiers=k1,k2,...]
+With `tiers=`: instead of hub rows, the edges of ALL rows whose slot lies in tiers 2..k+1
+(slots [16K, 16K*(k+1)): the sources just past the shared-memory tier) form the slice part.
+A T of 0 skips the hub-row variants."""
 import ctypes
 import os
 import subprocess
@@ -80,8 +83,16 @@ allcol = slot.to(torch.int32).contiguous()
 t_all = flat(allcol)
 print(f"{gen.name}: E={E} flat tiered gather of all edges {t_all:.4f} ms", flush=True)
 SL, U = 16384, 32
-for T in Ts:
-    hubm = indeg[rows] >= T
+tiers = []
+for a in sys.argv[3:]:
+    if a.startswith("tiers="):
+        tiers = [int(k) for k in a[6:].split(",")]
+variants = [("T", T) for T in Ts if T > 0] + [("tiers", k) for k in tiers]
+for kind, T in variants:
+    if kind == "T":
+        hubm = indeg[rows] >= T
+    else:
+        hubm = (slot >= SL) & (slot < SL * (1 + T))
     rest = allcol[~hubm].contiguous()
     hs = slot[hubm]
     q = hs // SL
@@ -108,6 +119,6 @@ for T in Ts:
                          ctypes.byref(ms))
         best = min(best, ms.value)
     t_rest = flat(rest)
-    print(f"T={T}: hub edges {hs.numel() / E:.3f} of E (padded {tot / max(1, hs.numel()):.3f}x, {nunits} units), "
+    print(f"{kind}={T}: hub edges {hs.numel() / E:.3f} of E (padded {tot / max(1, hs.numel()):.3f}x, {nunits} units), "
           f"hub part {best:.4f} ms (rc {rc}), rest {rest.numel() / E:.3f} of E {t_rest:.4f} ms, "
           f"sum {best + t_rest:.4f} ms vs flat {t_all:.4f} ms", flush=True)
